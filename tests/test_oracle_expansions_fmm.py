@@ -1,0 +1,216 @@
+"""Pins for the oracle's expansions (O5) and the whole evaluation pass.
+
+Operators (representation P:436-440): closed forms (single charge at
+the centre, the M2L series of a unit charge about 4, log 5 after an M2M shift,
+[1,1] -> [2,1] under L2L), exact translation identities (M2M of a P2M equals
+the P2M about the new centre; two L2L shifts equal one), and agreement of the
+truncated far field with the direct sum for well-separated sets.
+
+Whole pass: error against the O(N^2) direct sum within the paper's a-priori
+law const * theta^{p+1}/(1-theta)^2, its decay slope in p,
+ordering in theta, BASELINE's empirical gate (<= 1e-6 at p = 17, theta = 0.5)
+and independence of the input order.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _g():
+    with open(os.path.join(GOLD, "expansion_closed_forms.json")) as f:
+        return json.load(f)
+
+
+def _nerr(a, b):
+    return np.abs(a - b).max() / np.abs(b).max()
+
+
+def test_p2m_single_source_at_centre(orc):
+    m = complex(*_g()["p2m_centre"]["m"])
+    a = orc.p2m(np.array([0.3 + 0.2j]), np.array([m]), 0.3 + 0.2j, 12)
+    assert a[0] == m and np.all(a[1:] == 0)
+
+
+def test_p2m_general_term(orc):
+    # a_k = -m (z - c)^k / k for one source: a wrong sign / index / 1/k fails this
+    a = orc.p2m(np.array([0.5 + 0.25j]), np.array([2.0 - 1.0j]), 0.0, 6)
+    w = 0.5 + 0.25j
+    for k in range(1, 7):
+        assert a[k] == pytest.approx(-(2.0 - 1.0j) * w ** k / k, rel=1e-15)
+
+
+def test_m2m_log5_closed_form(orc):
+    g = _g()["m2m_log5"]
+    p = 40
+    a = orc.p2m(np.array([0j]), np.array([1.0 + 0j]), complex(*g["c"]), p)
+    b = orc.m2m(a, complex(*g["c"]), complex(*g["cparent"]), p)
+    phi, dphi = orc.m2p(b, complex(*g["cparent"]), p, np.array([complex(*g["z"])]))
+    assert phi[0].real == pytest.approx(g["phi"], abs=1e-14)
+    assert dphi[0] == pytest.approx(1 / 5.0, abs=1e-14)
+
+
+def test_m2m_translation_identity(orc):
+    """M2M of a P2M about c equals the P2M about c' (exact shift)."""
+    rng = np.random.default_rng(1)
+    z = 0.1 * (rng.random(50) - 0.5) + 0.1j * (rng.random(50) - 0.5)
+    m = rng.random(50) - 0.5 + 1j * (rng.random(50) - 0.5)
+    c, cp = 0.01 - 0.02j, 0.13 + 0.07j
+    for p in (5, 17, 30):
+        a = orc.p2m(z, m, c, p)
+        b = orc.m2m(a, c, cp, p)
+        ref = orc.p2m(z, m, cp, p)
+        scale = np.array([0.25 ** k for k in range(p + 1)])   # |z - c'|^k scale
+        assert np.abs((b - ref) / scale).max() <= 1e-13 * np.abs(ref / scale).max()
+
+
+def test_m2l_unit_charge_closed_form(orc):
+    g = _g()["m2l_unit_charge"]
+    p = 20
+    a = np.zeros(p + 1, complex)
+    a[0] = 1.0
+    b = orc.m2l(a, complex(*g["cs"]), complex(*g["ct"]), p)
+    assert b[0] == pytest.approx(g["b0"], abs=1e-15)
+    for l in range(1, p + 1):
+        assert b[l] == pytest.approx((-1) ** (l + 1) / (l * 4.0 ** l), rel=1e-14)
+
+
+def test_m2l_dipole_terms_closed_form(orc):
+    # a_k (z - c_s)^-k about c_t: a_1 / (w - z0) = -a_1/z0 * sum_l (w/z0)^l
+    p = 12
+    a = np.zeros(p + 1, complex)
+    a[1] = 1.0
+    cs, ct = 0.0, 3.0 + 1.0j
+    z0 = cs - ct
+    b = orc.m2l(a, cs, ct, p)
+    for l in range(p + 1):
+        assert b[l] == pytest.approx(-1.0 / z0 ** (l + 1), rel=1e-14)
+
+
+def test_l2l_closed_form_and_composition(orc):
+    g = _g()["l2l_linear"]
+    b = np.array([complex(*v) for v in g["b"]])
+    d = orc.l2l(b, complex(*g["c"]), complex(*g["cnew"]), 1)
+    np.testing.assert_array_equal(d, np.array([complex(*v) for v in g["d"]]))
+    rng = np.random.default_rng(2)
+    b = rng.random(10) + 1j * rng.random(10)
+    one = orc.l2l(b, 0.0, 0.3 - 0.2j, 9)
+    two = orc.l2l(orc.l2l(b, 0.0, 0.1 + 0.1j, 9), 0.1 + 0.1j, 0.3 - 0.2j, 9)
+    assert np.abs(one - two).max() <= 1e-13 * np.abs(one).max()
+
+
+def test_l2p_against_power_sum(orc):
+    rng = np.random.default_rng(4)
+    b = rng.random(8) + 1j * rng.random(8)
+    c = 0.2 + 0.1j
+    z = np.array([0.25 + 0.05j, 0.1 + 0.2j])
+    phi, dphi = orc.l2p(b, c, 7, z)
+    for i, zi in enumerate(z):
+        w = zi - c
+        assert phi[i] == pytest.approx(sum(b[l] * w ** l for l in range(8)), rel=1e-14)
+        assert dphi[i] == pytest.approx(sum(l * b[l] * w ** (l - 1) for l in range(1, 8)), rel=1e-14)
+
+
+@pytest.mark.parametrize("theta", [0.3, 0.5, 0.7])
+def test_p2m_m2l_l2p_vs_direct_within_bound(orc, theta):
+    """One well-separated pair exactly at the criterion boundary (equal radii
+    rho, d = rho (1+theta)/theta): the far-to-local approximation error decays
+    like theta^{p+1}."""
+    rng = np.random.default_rng(7)
+    rho = 1.0
+    d = rho * (1 + theta) / theta
+    errs = []
+    ps = list(range(4, 25, 4))
+    for p in ps:
+        e = 0.0
+        for trial in range(5):
+            u = rng.random(30) * 2 * np.pi
+            s = rho * np.sqrt(rng.random(30))
+            zs = s * np.exp(1j * u)
+            ms = rng.random(30) - 0.5 + 0j
+            t = rho * np.sqrt(rng.random(20)) * np.exp(1j * rng.random(20) * 2 * np.pi) + d
+            a = orc.p2m(zs, ms, 0.0, p)
+            b = orc.m2l(a, 0.0, d, p)
+            phi, dphi = orc.l2p(b, d, p, t)
+            ref = np.array([np.sum(ms / (ti - zs)) for ti in t])
+            e = max(e, np.abs(dphi - ref).max() / np.abs(ms).sum())
+        errs.append(e)
+    # decays geometrically with ratio <= theta (1 + 0.2)
+    slope = np.polyfit(ps, np.log(errs), 1)[0]
+    assert slope <= math.log(theta * 1.2)
+
+
+# ------------------------------------------------------------------ whole pass
+
+@pytest.fixture(scope="module")
+def c1(orc):
+    z, m = W.make_config("C1")
+    L = orc.nlevels(len(z), 35)
+    phi_d, dphi_d = orc.direct(z, m)
+    return z, m, L, phi_d, dphi_d
+
+
+def test_fmm_C1_within_gate(orc, c1):
+    """BASELINE gate: <= 1e-6 normwise on Re Phi (real m) at p=17, theta=0.5, and
+    within the a-priori law const*theta^{p+1}/(1-theta)^2 (constant 1)."""
+    z, m, L, phi_d, dphi_d = c1
+    assert L == 2
+    phi, dphi = orc.plan(z, 0.5, L).eval(m, 17)
+    e_phi = _nerr(phi.real, phi_d.real)
+    e_dphi = _nerr(dphi, dphi_d)
+    assert e_phi <= 1e-6
+    assert e_phi <= orc.error_bound(0.5, 17)
+    assert e_dphi <= orc.error_bound(0.5, 17)
+
+
+def test_fmm_error_slope_and_theta_order(orc):
+    z, m = W.make("uniform", 4000, "real", seed=21)
+    L = 3
+    phi_d, dphi_d = orc.direct(z, m)
+    res = {}
+    for theta in (0.3, 0.5, 0.7):
+        P = orc.plan(z, theta, L)
+        res[theta] = []
+        for p in range(6, 19, 2):
+            phi, dphi = P.eval(m, p)
+            res[theta].append(max(_nerr(phi.real, phi_d.real), _nerr(dphi, dphi_d)))
+    ps = np.arange(6, 19, 2)
+    slope = np.polyfit(ps, np.log10(res[0.5]), 1)[0]
+    # decays at least as fast as theta^p, within +0.12
+    assert slope <= math.log10(0.5) + 0.12
+    # smaller theta -> smaller error at fixed p
+    for k in range(len(ps)):
+        assert res[0.3][k] < res[0.5][k] < res[0.7][k]
+
+
+def test_fmm_complex_strengths_dphi(orc):
+    # complex unit-modulus m (C2 recipe): only dPhi is branch-free vs the direct sum
+    z, m = W.make("uniform", 3000, "phase", seed=23)
+    L = orc.nlevels(3000, 35)
+    phi_d, dphi_d = orc.direct(z, m)
+    _, dphi = orc.plan(z, 0.5, L).eval(m, 17)
+    assert _nerr(dphi, dphi_d) <= 1e-6
+
+
+def test_fmm_input_order_invariance(orc):
+    z, m = W.make("clusters", 2000, "real", seed=25)
+    L = 2
+    phi, dphi = orc.plan(z, 0.5, L).eval(m, 12)
+    perm = np.random.default_rng(0).permutation(2000)
+    phi2, dphi2 = orc.plan(z[perm], 0.5, L).eval(m[perm], 12)
+    # different tie order only, so results agree to rounding
+    assert _nerr(phi2, phi[perm]) < 1e-13 and _nerr(dphi2, dphi[perm]) < 1e-13
+
+
+def test_fmm_root_only_is_direct_sum(orc):
+    """L = 0: the root is strong to itself, everything is P2P."""
+    z, m = W.make("uniform", 60, "phase", seed=27)
+    phi, dphi = orc.plan(z, 0.5, 0).eval(m, 5)
+    phi_d, dphi_d = orc.direct(z, m)
+    assert _nerr(phi, phi_d) < 1e-14 and _nerr(dphi, dphi_d) < 1e-14
