@@ -1,0 +1,350 @@
+"""Benchmark: FMM evaluated points/s on B200 (BASELINE.json metric) + roofline + CPU oracle.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl fmm2d|reference]
+
+One step = one pass of the whole hot path (rows A0-A11) over one
+synthetic instance: fmm2d_build (validate, median-split tree, discs, theta-criterion
+lists) + fmm2d_eval (P2M, M2M, M2L, L2L, L2P + P2P, input order) for Phi and Phi'.
+Inputs (z, m) are resident in HBM before the timed region; every instance is larger
+than L2 (C5: 1.6 GB of positions), so no extra L2 flush is needed.
+
+value      = N * steps * n_gpus / max-over-ranks device time (points/s, whole job)
+e2e        = the same through the C ABI with HOST buffers (pinned): H2D of z and m,
+             D2H of Phi and Phi' inside the timed region
+roofline   = the dominant kernel (P2P+L2P, k_near): algorithmic FP64 flops per launch
+             (ordered pairs x 105 flop) / its CUDA-event time vs the
+             measured FP64 peak
+cpu_baseline = the oracle (oracle/, plain C++, OpenMP) on a bounded sample of the same
+             workload: the C5 recipe at N = 390,625 (same leaf occupancy, L = 7)
+
+--impl reference runs the oracle itself (the reference arm for this tier) on rank 0.
+Multi-GPU (torchrun, N > 1): each rank evaluates its own independent seeded instance of
+the config ("replicas", weak scaling, no data-path collective) -- see DESIGN.md section 8.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+METRIC = "FMM evaluated points/sec at 1/2/4/8 B200 (θ=0.5, p=17) and % FP64 roofline"
+P2P_FLOPS_PER_PAIR = 105.0        # SURVEY 8(d) working estimate (algorithmic, per ordered pair)
+M2L_FLOPS_PER_PAIR = 1450.0       # SURVEY 8(d), p = 17
+NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def fp64_peak():
+    """(TFLOP/s, source).  MEASURED_PEAKS.json if it has an FP64 entry, else our own
+    DFMA microbenchmark result profiles/fp64_peak.json, else the nominal figure."""
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        for k in ("fp64_tflops", "fp64_tflops_sustained"):
+            if k in mp:
+                return float(mp[k]), "MEASURED_PEAKS.json:" + k
+    except Exception:
+        pass
+    try:
+        fp = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        return float(fp["dfma_tflops"]), "profiles/fp64_peak.json (DFMA microbenchmark, measured)"
+    except Exception:
+        pass
+    return NOMINAL_FP64_TFLOPS, "nominal 148 SM x 64 DFMA x 2 x 1.965 GHz"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([s.strip() for s in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline(cfg, seconds_hint=True):
+    """Oracle (plain C++ + OpenMP) on a bounded sample of the same workload."""
+    import oracle
+    n = 390_625 if cfg.n >= 390_625 else cfg.n          # C5 recipe, L = 7, occupancy 23.8
+    z, m = W.make(cfg.dist, n, cfg.strengths, seed=W.SEED_BASE + 77)
+    L = oracle.nlevels(n, cfg.leaf_target)
+    t0 = time.perf_counter()
+    P = oracle.plan(z, cfg.theta, L)
+    P.eval(m, cfg.p)
+    dt = time.perf_counter() - t0
+    cores = _env_int("OMP_NUM_THREADS", os.cpu_count() or 1)
+    return {"value": n / dt, "unit": "points/s", "cores": cores, "kind": "oracle",
+            "sample": f"{cfg.dist} N={n} (L={L}, same leaf occupancy as {cfg.name}), theta={cfg.theta}, "
+                      f"p={cfg.p}: one build+eval pass, {dt:.2f} s"}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import oracle
+    n = 390_625 if cfg.n >= 390_625 else cfg.n
+    z, m = W.make(cfg.dist, n, cfg.strengths, seed=W.SEED_BASE + 77)
+    L = oracle.nlevels(n, cfg.leaf_target)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        P = oracle.plan(z, cfg.theta, L)
+        P.eval(m, cfg.p)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    T = float(np.sum(times))
+    value = n * len(times) / T
+    cores = _env_int("OMP_NUM_THREADS", os.cpu_count() or 1)
+    line = {"metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{cfg.name} recipe at N={n} (bounded CPU sample)", "n": n, "theta": cfg.theta,
+                       "p": cfg.p, "leaf_target": cfg.leaf_target, "levels": L + 1},
+            "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{cfg.dist} N={n}, one oracle build+eval per step"},
+            "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--n", type=int, default=None, help="override N (same recipe)")
+    ap.add_argument("--impl", default="fmm2d", choices=["fmm2d", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = W.CONFIGS[args.config]
+    if args.n:
+        cfg = W.Config(cfg.name, args.n, cfg.dist, cfg.strengths, cfg.theta, cfg.p, cfg.leaf_target)
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local_rank = _env_int("LOCAL_RANK", 0)
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1006_2269_b200 import Fmm2d
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # inputs resident in HBM (each rank: its own independent seeded instance)
+    z_np, m_np = W.make(cfg.dist, cfg.n, cfg.strengths, seed=W.SEED_BASE + 4 + 1000 * rank)
+    z = torch.from_numpy(z_np).to(dev)
+    m = torch.from_numpy(m_np).to(dev)
+    real = cfg.strengths == "real"
+    phi = torch.empty(cfg.n, dtype=torch.complex128, device=dev)
+    dphi = torch.empty(cfg.n, dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        plan = Fmm2d(z, theta=cfg.theta, p=cfg.p, leaf_target=cfg.leaf_target, real_strengths=real,
+                     stream=stream)
+        plan.eval(m, phi, dphi)
+        return plan
+
+    # warm-up
+    last = None
+    for _ in range(args.warmup):
+        if last is not None:
+            last.close()
+        last = step()
+    torch.cuda.synchronize()
+    info = last.stats() if last is not None else {}
+    if last is not None:
+        last.close()
+    L = int(info.get("L", 0))
+
+    # timed region
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    plans = []
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            p_ = step()
+            plans.append(p_)
+            if len(plans) > 1:
+                plans.pop(0).close()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    st = plans[-1].stats()
+    for p_ in plans:
+        p_.close()
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = cfg.n * world * args.steps / (ms_max / 1e3)
+
+    # per-phase breakdown + roofline of the dominant kernel (k_near) on one extra pass
+    phase = phase_times(z, m, phi, dphi, cfg, real, stream)
+    peak, peak_src = fp64_peak()
+    pairs = st.get("p2p_pairs", 0.0)
+    near_ms = phase["near_ms"]
+    achieved = pairs * P2P_FLOPS_PER_PAIR / (near_ms / 1e3) / 1e12
+    roof = {"bound": "alu", "kernel": "k_near (P2P+L2P)", "achieved": achieved, "peak": peak,
+            "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+            "flops_per_launch": pairs * P2P_FLOPS_PER_PAIR, "pairs_per_launch": pairs,
+            "peak_source": peak_src,
+            "flop_convention": f"{P2P_FLOPS_PER_PAIR:.0f} FP64 flop per ordered P2P pair (SURVEY 8(d))"}
+    weak_pairs = st.get("weak_pairs", 0.0)
+    m2l_tf = weak_pairs * M2L_FLOPS_PER_PAIR / (phase["m2l_ms"] / 1e3) / 1e12 if phase["m2l_ms"] > 0 else 0.0
+
+    # end to end through the C ABI with host (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = end_to_end(z_np, m_np, cfg, real, stream, args)
+        if world > 1:
+            t = torch.tensor([e2e["ms"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["ms"] = float(t.item())
+        e2e = {"value": cfg.n * world / (e2e["ms"] / 1e3), "unit": "points/s",
+               "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]}
+
+    launches_per_step = phase["launches"]
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{cfg.name}: {cfg.dist} N={cfg.n} ({'replicas' if world > 1 else 'single'})",
+                           "n": cfg.n, "theta": cfg.theta, "p": cfg.p, "leaf_target": cfg.leaf_target,
+                           "levels": L + 1, "strengths": cfg.strengths,
+                           "step": "fmm2d_build + fmm2d_eval (rows A0-A11)",
+                           "l2": "inputs larger than L2 (no flush needed)",
+                           "parallelism": f"replicas{world}" if world > 1 else "single"},
+                "phases_ms": phase, "eval_only_points_per_s": cfg.n / (phase["eval_ms"] / 1e3),
+                "m2l_tflops": m2l_tf,
+                "roofline": roof, "gpu_launches": launches_per_step * args.steps,
+                "clocks": clk.summary(), "e2e": e2e,
+                "stats": {"weak_pairs": weak_pairs, "p2p_pairs": pairs, "min_leaf": st.get("min_leaf"),
+                          "max_leaf": st.get("max_leaf")}}
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def phase_times(z, m, phi, dphi, cfg, real, stream):
+    """Device time of each phase of one extra pass (CUDA events on the launching stream)
+    and the number of this library's kernel launches in one pass."""
+    import torch
+    from paper_1006_2269_b200 import Fmm2d
+    from paper_1006_2269_b200.fmm2d import launch_count
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    n0 = launch_count()
+    ev[0].record(stream)
+    plan = Fmm2d(z, theta=cfg.theta, p=cfg.p, leaf_target=cfg.leaf_target, real_strengths=real, stream=stream)
+    ev[1].record(stream)
+    pt = plan.eval_timed(m, phi, dphi)
+    launches = launch_count() - n0
+    build_ms = ev[0].elapsed_time(ev[1])
+    plan.close()
+    return {"build_ms": build_ms, "launches": launches, **pt}
+
+
+def end_to_end(z_np, m_np, cfg, real, stream, args):
+    """Build + eval through the C ABI with host pinned buffers; copies inside the timing."""
+    import torch
+    from paper_1006_2269_b200 import Fmm2d
+    zh = torch.from_numpy(z_np).pin_memory()
+    mh = torch.from_numpy(m_np).pin_memory()
+    ph = torch.empty(cfg.n, dtype=torch.complex128).pin_memory()
+    dh = torch.empty(cfg.n, dtype=torch.complex128).pin_memory()
+    for _ in range(1):
+        Fmm2d(zh, theta=cfg.theta, p=cfg.p, leaf_target=cfg.leaf_target, real_strengths=real,
+              stream=stream).eval(mh, ph, dh)
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 3))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        plan = Fmm2d(zh, theta=cfg.theta, p=cfg.p, leaf_target=cfg.leaf_target, real_strengths=real,
+                     stream=stream)
+        plan.eval(mh, ph, dh)
+        plan.close()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return {"ms": e0.elapsed_time(e1) / steps, "h2d": 16 * cfg.n * 2, "d2h": 16 * cfg.n * 2}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,142 @@
+/*
+ * fmm2d.h -- C ABI of libfmm2d.so, the B200-native (sm_100a) evaluation pass of
+ * the asymmetric adaptive 2D fast multipole method of
+ *   S. Engblom, "On well-separated sets and fast multipole methods",
+ *   arXiv 1006.2269  (cited as P:<line> of its text).
+ *
+ * What it computes (Eq. 1, with the log kernel):
+ *     Phi(z_i)  = sum_{j != i} m_j * Log(z_i - z_j)
+ *     Phi'(z_i) = sum_{j != i} m_j / (z_i - z_j)
+ * at every source z_i, by the paper's FMM: a balanced 4-ary tree of median
+ * splits, theta-criterion connectivity (Criterion 1, P:115-123;
+ * rule P:343-353), upward P2M/M2M, M2L along the weak lists, downward L2L,
+ * and L2P + direct P2P along the strong leaf lists.  Readings of
+ * points the paper leaves open are DESIGN.md section 2 (R1..R22).
+ *
+ * Conventions for every entry point:
+ *   - Complex arrays are interleaved float64 pairs (re, im), length 2*n doubles,
+ *     in INPUT order (index j of z, m, phi, dphi refers to the same source).
+ *   - Pointers are CUDA device pointers on opt.stream unless FMM2D_HOST_PTRS is set
+ *     in opt.flags, in which case they are host pointers (pinned memory gives the
+ *     fastest copies) and the call returns after the results are in host memory.
+ *   - Return 0 on success, a negative FMM2D_E* code on error; nothing aborts or
+ *     exits.  On error the outputs are unspecified and an existing plan is unchanged.
+ *   - There is no CPU fallback: every numeric step runs in the library's CUDA kernels.
+ */
+#ifndef FMM2D_H
+#define FMM2D_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define FMM2D_API __attribute__((visibility("default")))
+#else
+#define FMM2D_API
+#endif
+
+#define FMM2D_PMAX 32            /* largest supported truncation order p          */
+#define FMM2D_ABI_VERSION 1
+
+/* error codes */
+#define FMM2D_OK          0
+#define FMM2D_EINVAL     -1      /* theta outside (0,1), p outside 1..PMAX, n < 1,
+                                    n >= 2^31, forced nlevels with n < 4^L, NULL args */
+#define FMM2D_ENONFINITE -2      /* a coordinate is NaN or +-inf                        */
+#define FMM2D_ENOMEM     -3      /* device or host allocation failed                    */
+#define FMM2D_ECUDA      -4      /* a CUDA runtime / kernel error                       */
+#define FMM2D_ENCCL      -5      /* a NCCL error (multi-rank builds)                    */
+#define FMM2D_ENOTSUP    -6      /* unsupported option combination                      */
+
+/* opt.flags */
+#define FMM2D_HOST_PTRS       0x1  /* z, m, phi, dphi are host pointers               */
+#define FMM2D_REAL_STRENGTHS  0x2  /* caller promises Im m_j == 0 (kernel may skip it) */
+
+typedef struct fmm2d_plan fmm2d_plan;   /* opaque; owns all device memory */
+
+typedef struct {
+    double theta;        /* Criterion 1 parameter, (0,1) exclusive; rejected (not
+                            clamped) otherwise.                              */
+    int    p;            /* truncation order: multipole a_0..a_p, local b_0..b_p
+                            (DESIGN R1); 1..FMM2D_PMAX.                              */
+    int    leaf_target;  /* used when nlevels < 0: L = min L >= 0 with
+                            n <= 2*leaf_target*4^L (DESIGN R4).          */
+    int    nlevels;      /* >= 0 forces L (requires n >= 4^L); < 0 = automatic.     */
+    int    flags;        /* FMM2D_HOST_PTRS | FMM2D_REAL_STRENGTHS                   */
+    int    device;       /* CUDA device ordinal                                      */
+    void*  stream;       /* cudaStream_t for every kernel and copy (NULL = legacy
+                            default stream)                                          */
+    int    nranks;       /* 1 for one GPU                                            */
+    int    rank;         /* 0 for one GPU                                            */
+    const void* nccl_id; /* 128-byte ncclUniqueId for nranks > 1, else NULL          */
+} fmm2d_options;
+
+/* Fill *opt with defaults: theta 0.5, p 17, leaf_target 40, nlevels -1, flags 0,
+ * device 0, stream NULL, nranks 1, rank 0, nccl_id NULL (P:426-430 defaults). */
+FMM2D_API int fmm2d_default_options(fmm2d_options* opt);
+
+/* Build the plan for n source positions z (A0-A3 of DESIGN.md: validate, median-split
+ * tree P:333-341, box discs, theta-criterion lists P:343-353) and allocate the
+ * expansions for order opt->p.  z: n complex positions (interleaved), read during
+ * the call only.  Synchronous: returns after the plan is complete (the list sizes
+ * are read back to size the allocations).  *out receives the new plan (NULL on
+ * error).  Errors: EINVAL, ENONFINITE, ENOMEM, ECUDA. */
+FMM2D_API int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan** out);
+
+/* One evaluation pass for strengths m (A4-A11: P2M, M2M, M2L on every level's weak
+ * lists, L2L, L2P + P2P on the strong leaf lists).
+ * m:    n complex strengths in input order (read only).
+ * phi:  n complex outputs Phi(z_i) in input order, or NULL to skip.
+ * dphi: n complex outputs Phi'(z_i) in input order, or NULL to skip.
+ * Device pointers: asynchronous on the plan's stream (the caller synchronises).
+ * FMM2D_HOST_PTRS: synchronous.  Errors: EINVAL, ECUDA. */
+FMM2D_API int fmm2d_eval(fmm2d_plan* plan, const double* m, double* phi, double* dphi);
+
+/* fmm2d_eval, then synchronise and report the device time of each phase in
+ * ms_out[0..7] (CUDA events on the plan's stream): 0 strength gather, 1 P2M+M2M,
+ * 2 M2L (all levels), 3 L2L, 4 L2P+P2P+output, 5 total, 6..7 reserved.
+ * Same arguments and errors as fmm2d_eval; ms_out may not be NULL. */
+FMM2D_API int fmm2d_eval_timed(fmm2d_plan* plan, const double* m, double* phi, double* dphi,
+                               double* ms_out);
+
+/* Number of kernels this library has launched since it was loaded (all plans and
+ * threads; CUB's internal launches are not counted). */
+FMM2D_API int64_t fmm2d_launch_count(void);
+
+/* Free the plan and all its device memory.  NULL-safe. */
+FMM2D_API void fmm2d_free(fmm2d_plan* plan);
+
+/* Static string for an error code. */
+FMM2D_API const char* fmm2d_strerror(int code);
+
+/* Detail of the last CUDA failure seen by this thread ("" if none): the CUDA error
+ * string, the failing call and its source location.  Thread-local storage. */
+FMM2D_API const char* fmm2d_last_error_detail(void);
+
+/* Plan facts: n, L, p, theta-independent sizes.  Any out pointer may be NULL. */
+FMM2D_API int fmm2d_plan_info(const fmm2d_plan* plan, int64_t* n, int* nlevels, int* p,
+                    int64_t* weak_pairs, int64_t* strong_leaf_pairs);
+
+/* ---- test / diagnostic exports (copy plan data to HOST memory dst) ----------
+ * what:                                 level   dst layout                      */
+#define FMM2D_EXPORT_PERM        1  /* -      uint32[n]: leaf position -> input index */
+#define FMM2D_EXPORT_OFFSETS     2  /* l      int64[4^l+1]: box ranges in leaf order  */
+#define FMM2D_EXPORT_DISCS       3  /* l      double[3*4^l]: cx[], cy[], r[]          */
+#define FMM2D_EXPORT_STRONG      4  /* l      int64[4^l+1] offsets then uint32[] idx  */
+#define FMM2D_EXPORT_WEAK        5  /* l      int64[4^l+1] offsets then uint32[] idx  */
+#define FMM2D_EXPORT_MPOLE       6  /* l      complex128[4^l][p+1] (after an eval)    */
+#define FMM2D_EXPORT_LOCAL       7  /* l      complex128[4^l][p+1] (after an eval)    */
+#define FMM2D_EXPORT_STATS       8  /* -      double[16]: see fmm2d_api.cu            */
+/* If dst is NULL, *bytes receives the required size.  Otherwise *bytes must hold
+ * the capacity of dst; on success it receives the bytes written.  Synchronises the
+ * plan's stream.  Errors: EINVAL (bad what/level/capacity), ECUDA. */
+FMM2D_API int fmm2d_export(const fmm2d_plan* plan, int what, int level, void* dst, size_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMM2D_H */

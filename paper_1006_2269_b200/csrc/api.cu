@@ -1,0 +1,363 @@
+// api.cu -- the C ABI of libfmm2d.so (include/fmm2d.h): plan life cycle and the
+// orchestration of the build (A0-A3) and evaluation (A4-A11) passes on one stream.
+//
+// Paper order: mesh first, then connectivity, then upward shifts,
+// far-to-local shifts along the weak pattern, downward shifts, and the direct
+// near field at the finest level.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "fmm2d_internal.cuh"
+
+static thread_local char g_last_err[512] = "";
+
+void fmm2d_set_last_cuda_error(cudaError_t e, const char* what, const char* file, int line)
+{
+    snprintf(g_last_err, sizeof(g_last_err), "%s: %s (%s:%d)", cudaGetErrorString(e), what, file, line);
+}
+
+namespace fmm2d {
+
+static std::atomic<int64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+int dev_alloc(fmm2d_plan* P, void** ptr, size_t bytes)
+{
+    *ptr = nullptr;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(ptr, bytes, P->stream);
+    if (e != cudaSuccess) {
+        fmm2d_set_last_cuda_error(e, "cudaMallocAsync", __FILE__, __LINE__);
+        *ptr = nullptr;
+        return FMM2D_ENOMEM;
+    }
+    P->allocs.push_back(*ptr);
+    return 0;
+}
+
+}  // namespace fmm2d
+
+using namespace fmm2d;
+
+extern "C" {
+
+const char* fmm2d_last_error_detail(void) { return g_last_err; }
+
+int fmm2d_default_options(fmm2d_options* opt)
+{
+    if (!opt) return FMM2D_EINVAL;
+    memset(opt, 0, sizeof(*opt));
+    opt->theta = 0.5;
+    opt->p = 17;
+    opt->leaf_target = 40;
+    opt->nlevels = -1;
+    opt->flags = 0;
+    opt->device = 0;
+    opt->stream = nullptr;
+    opt->nranks = 1;
+    opt->rank = 0;
+    opt->nccl_id = nullptr;
+    return 0;
+}
+
+const char* fmm2d_strerror(int code)
+{
+    switch (code) {
+        case FMM2D_OK: return "ok";
+        case FMM2D_EINVAL: return "invalid argument";
+        case FMM2D_ENONFINITE: return "non-finite coordinate";
+        case FMM2D_ENOMEM: return "out of memory";
+        case FMM2D_ECUDA: return "CUDA error";
+        case FMM2D_ENCCL: return "NCCL error";
+        case FMM2D_ENOTSUP: return "unsupported option";
+        default: return "unknown error";
+    }
+}
+
+void fmm2d_free(fmm2d_plan* P)
+{
+    if (!P) return;
+    cudaSetDevice(P->device);
+    for (void* p : P->allocs) cudaFreeAsync(p, P->stream);
+    cudaStreamSynchronize(P->stream);
+    delete P;
+}
+
+// DESIGN R4: L = min L >= 0 with n <= 2 * leaf_target * 4^L.
+static int depth_rule(int64_t n, int leaf_target)
+{
+    int L = 0;
+    int64_t cap = 2 * (int64_t)leaf_target;
+    while (n > cap && L < FMM2D_MAXL) { cap *= 4; ++L; }
+    return L;
+}
+
+int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan** out)
+{
+    if (!out) return FMM2D_EINVAL;
+    *out = nullptr;
+    if (!z || !opt) return FMM2D_EINVAL;
+    if (!(opt->theta > 0.0 && opt->theta < 1.0)) return FMM2D_EINVAL;        // P:119, not clamped
+    if (opt->p < 1 || opt->p > FMM2D_PMAX) return FMM2D_EINVAL;
+    if (n < 1 || n >= ((int64_t)1 << 31)) return FMM2D_EINVAL;
+    if (opt->nranks != 1 || opt->rank != 0) return FMM2D_ENOTSUP;
+    int L;
+    if (opt->nlevels >= 0) {
+        L = opt->nlevels;
+        if (L > FMM2D_MAXL || n < nboxes(L)) return FMM2D_EINVAL;           // DESIGN R12
+    } else {
+        if (opt->leaf_target < 1) return FMM2D_EINVAL;
+        L = depth_rule(n, opt->leaf_target);
+        while (L > 0 && n < nboxes(L)) --L;
+    }
+    if (cudaSetDevice(opt->device) != cudaSuccess) return FMM2D_ECUDA;
+    fmm2d_plan* P = new (std::nothrow) fmm2d_plan();
+    if (!P) return FMM2D_ENOMEM;
+    P->n = n;
+    P->L = L;
+    P->p = opt->p;
+    P->theta = opt->theta;
+    P->flags = opt->flags;
+    P->device = opt->device;
+    P->stream = (cudaStream_t)opt->stream;
+    P->base.resize(L + 2);
+    for (int l = 0; l <= L + 1; ++l) P->base[l] = level_base(l);
+    P->nbox_total = P->base[L + 1];
+
+    auto body = [&]() -> int {
+        cudaEvent_t e0, e1, e2;
+        FMM2D_CUDA_TRY(cudaEventCreate(&e0));
+        FMM2D_CUDA_TRY(cudaEventCreate(&e1));
+        FMM2D_CUDA_TRY(cudaEventCreate(&e2));
+        FMM2D_CUDA_TRY(cudaEventRecord(e0, P->stream));
+        // keep freed pool memory for the next build/eval (no OS round trips)
+        {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, P->device) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        }
+        FMM2D_TRY(upload_binomials(P->p));
+        const int64_t nb = P->nbox_total;
+        const int P1 = P->p + 1;
+        FMM2D_TRY(dev_alloc(P, (void**)&P->perm, sizeof(uint32_t) * n));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->src, sizeof(double4) * n));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->cx, sizeof(double) * nb));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->cy, sizeof(double) * nb));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->r, sizeof(double) * nb));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->mpole, sizeof(double2) * nb * P1));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->local, sizeof(double2) * nb * P1));
+        const double2* zd = (const double2*)z;
+        double2* zstage = nullptr;
+        if (P->flags & FMM2D_HOST_PTRS) {
+            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&zstage, sizeof(double2) * n, P->stream));
+            FMM2D_CUDA_TRY(cudaMemcpyAsync(zstage, z, sizeof(double2) * n, cudaMemcpyHostToDevice, P->stream));
+            zd = zstage;
+        }
+        int rc = build_tree(P, zd);
+        if (zstage) cudaFreeAsync(zstage, P->stream);
+        if (rc) return rc;
+        FMM2D_CUDA_TRY(cudaEventRecord(e1, P->stream));
+        FMM2D_TRY(build_lists(P));
+        FMM2D_CUDA_TRY(cudaEventRecord(e2, P->stream));
+        FMM2D_CUDA_TRY(cudaEventSynchronize(e2));
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, e0, e1);
+        cudaEventElapsedTime(&b, e1, e2);
+        P->stats.t_tree_ms = a;
+        P->stats.t_lists_ms = b;
+        P->stats.t_build_ms = a + b;
+        // P2P pair count (ordered, including i == j exclusions already removed)
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaEventDestroy(e2);
+        return 0;
+    };
+    int rc = body();
+    if (rc) {
+        fmm2d_free(P);
+        return rc;
+    }
+    *out = P;
+    return 0;
+}
+
+static int eval_impl(fmm2d_plan* P, const double* m, double* phi, double* dphi, cudaEvent_t* ev)
+{
+    if (!P || !m) return FMM2D_EINVAL;
+    FMM2D_CUDA_TRY(cudaSetDevice(P->device));
+    const int64_t n = P->n;
+    const bool host = (P->flags & FMM2D_HOST_PTRS) != 0;
+    const double2* md = (const double2*)m;
+    double2* phid = (double2*)phi;
+    double2* dphid = (double2*)dphi;
+    if (host) {
+        if (!P->mstage) {
+            FMM2D_TRY(dev_alloc(P, (void**)&P->mstage, sizeof(double2) * n));
+            FMM2D_TRY(dev_alloc(P, (void**)&P->phistage, sizeof(double2) * n));
+            FMM2D_TRY(dev_alloc(P, (void**)&P->dphistage, sizeof(double2) * n));
+        }
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(P->mstage, m, sizeof(double2) * n, cudaMemcpyHostToDevice, P->stream));
+        md = P->mstage;
+        phid = phi ? P->phistage : nullptr;
+        dphid = dphi ? P->dphistage : nullptr;
+    }
+    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[0], P->stream));
+    FMM2D_TRY(gather_strengths(P, md));
+    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[1], P->stream));
+    FMM2D_TRY(run_upward(P));
+    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[2], P->stream));
+    FMM2D_TRY(run_m2l(P));
+    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[3], P->stream));
+    FMM2D_TRY(run_downward(P));
+    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[4], P->stream));
+    FMM2D_TRY(run_near(P, phid, dphid));
+    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[5], P->stream));
+    if (host) {
+        if (phi) FMM2D_CUDA_TRY(cudaMemcpyAsync(phi, phid, sizeof(double2) * n, cudaMemcpyDeviceToHost, P->stream));
+        if (dphi) FMM2D_CUDA_TRY(cudaMemcpyAsync(dphi, dphid, sizeof(double2) * n, cudaMemcpyDeviceToHost, P->stream));
+        FMM2D_CUDA_TRY(cudaStreamSynchronize(P->stream));
+    }
+    return 0;
+}
+
+int fmm2d_eval(fmm2d_plan* P, const double* m, double* phi, double* dphi)
+{
+    return eval_impl(P, m, phi, dphi, nullptr);
+}
+
+int fmm2d_eval_timed(fmm2d_plan* P, const double* m, double* phi, double* dphi, double* ms_out)
+{
+    if (!P || !m || !ms_out) return FMM2D_EINVAL;
+    FMM2D_CUDA_TRY(cudaSetDevice(P->device));
+    cudaEvent_t ev[6];
+    for (int i = 0; i < 6; ++i) FMM2D_CUDA_TRY(cudaEventCreate(&ev[i]));
+    int rc = eval_impl(P, m, phi, dphi, ev);
+    if (rc == 0) {
+        cudaError_t e = cudaEventSynchronize(ev[5]);
+        if (e != cudaSuccess) {
+            fmm2d_set_last_cuda_error(e, "cudaEventSynchronize", __FILE__, __LINE__);
+            rc = FMM2D_ECUDA;
+        }
+    }
+    if (rc == 0) {
+        for (int i = 0; i < 5; ++i) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+            ms_out[i] = t;
+        }
+        float t = 0.f;
+        cudaEventElapsedTime(&t, ev[0], ev[5]);
+        ms_out[5] = t;
+        ms_out[6] = ms_out[7] = 0.0;
+    }
+    for (int i = 0; i < 6; ++i) cudaEventDestroy(ev[i]);
+    return rc;
+}
+
+int64_t fmm2d_launch_count(void) { return launch_count(); }
+
+int fmm2d_plan_info(const fmm2d_plan* P, int64_t* n, int* nlevels, int* p, int64_t* weak_pairs,
+                    int64_t* strong_leaf_pairs)
+{
+    if (!P) return FMM2D_EINVAL;
+    if (n) *n = P->n;
+    if (nlevels) *nlevels = P->L;
+    if (p) *p = P->p;
+    if (weak_pairs) *weak_pairs = P->stats.weak_pairs;
+    if (strong_leaf_pairs) *strong_leaf_pairs = P->stats.strong_leaf_pairs;
+    return 0;
+}
+
+static int copy_out(const void* dsrc, void* dst, size_t bytes, size_t* cap, size_t* off, cudaStream_t st)
+{
+    if (*off + bytes > *cap) return FMM2D_EINVAL;
+    if (bytes) FMM2D_CUDA_TRY(cudaMemcpyAsync((char*)dst + *off, dsrc, bytes, cudaMemcpyDeviceToHost, st));
+    *off += bytes;
+    return 0;
+}
+
+/* STATS layout (double[16]): 0 n, 1 L, 2 p, 3 theta, 4 weak pairs (all levels),
+ * 5 strong leaf pairs, 6 min leaf size, 7 max leaf size, 8 t_build_ms, 9 t_tree_ms,
+ * 10 t_lists_ms, 11 number of boxes (all levels), 12 kernel launches of this library
+ * since it was loaded (all plans), 13 ordered P2P pairs (j != i) of one eval, 14..15 reserved. */
+int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* bytes)
+{
+    if (!P || !bytes) return FMM2D_EINVAL;
+    if (cudaSetDevice(P->device) != cudaSuccess) return FMM2D_ECUDA;
+    const bool per_level = (what == FMM2D_EXPORT_OFFSETS || what == FMM2D_EXPORT_DISCS ||
+                            what == FMM2D_EXPORT_STRONG || what == FMM2D_EXPORT_WEAK ||
+                            what == FMM2D_EXPORT_MPOLE || what == FMM2D_EXPORT_LOCAL);
+    if (per_level && (level < 0 || level > P->L)) return FMM2D_EINVAL;
+    const int64_t nb = per_level ? nboxes(level) : 0;
+    size_t need = 0;
+    switch (what) {
+        case FMM2D_EXPORT_PERM: need = sizeof(uint32_t) * P->n; break;
+        case FMM2D_EXPORT_OFFSETS: need = sizeof(int64_t) * (nb + 1); break;
+        case FMM2D_EXPORT_DISCS: need = sizeof(double) * 3 * nb; break;
+        case FMM2D_EXPORT_STRONG:
+            need = sizeof(int64_t) * (nb + 1) + sizeof(uint32_t) * P->strong[level].total; break;
+        case FMM2D_EXPORT_WEAK:
+            need = sizeof(int64_t) * (nb + 1) + sizeof(uint32_t) * P->weak[level].total; break;
+        case FMM2D_EXPORT_MPOLE:
+        case FMM2D_EXPORT_LOCAL: need = sizeof(double2) * nb * (P->p + 1); break;
+        case FMM2D_EXPORT_STATS: need = sizeof(double) * 16; break;
+        default: return FMM2D_EINVAL;
+    }
+    if (!dst) {
+        *bytes = need;
+        return 0;
+    }
+    if (*bytes < need) return FMM2D_EINVAL;
+    size_t off = 0, cap = *bytes;
+    cudaStream_t st = P->stream;
+    switch (what) {
+        case FMM2D_EXPORT_PERM: FMM2D_TRY(copy_out(P->perm, dst, need, &cap, &off, st)); break;
+        case FMM2D_EXPORT_OFFSETS: {
+            int64_t* o = (int64_t*)dst;
+            for (int64_t b = 0; b <= nb; ++b) o[b] = P->h_boff[P->obase[level] + b];
+            off = need;
+            break;
+        }
+        case FMM2D_EXPORT_DISCS:
+            FMM2D_TRY(copy_out(P->cx + P->base[level], dst, sizeof(double) * nb, &cap, &off, st));
+            FMM2D_TRY(copy_out(P->cy + P->base[level], dst, sizeof(double) * nb, &cap, &off, st));
+            FMM2D_TRY(copy_out(P->r + P->base[level], dst, sizeof(double) * nb, &cap, &off, st));
+            break;
+        case FMM2D_EXPORT_STRONG:
+        case FMM2D_EXPORT_WEAK: {
+            const Csr& C = (what == FMM2D_EXPORT_STRONG) ? P->strong[level] : P->weak[level];
+            FMM2D_TRY(copy_out(C.off, dst, sizeof(int64_t) * (nb + 1), &cap, &off, st));
+            FMM2D_TRY(copy_out(C.idx, dst, sizeof(uint32_t) * C.total, &cap, &off, st));
+            break;
+        }
+        case FMM2D_EXPORT_MPOLE:
+        case FMM2D_EXPORT_LOCAL: {
+            const double2* E = (what == FMM2D_EXPORT_MPOLE) ? P->mpole : P->local;
+            FMM2D_TRY(copy_out(E + P->base[level] * (P->p + 1), dst, need, &cap, &off, st));
+            break;
+        }
+        case FMM2D_EXPORT_STATS: {
+            double* s = (double*)dst;
+            for (int i = 0; i < 16; ++i) s[i] = 0.0;
+            s[0] = (double)P->n; s[1] = P->L; s[2] = P->p; s[3] = P->theta;
+            s[4] = (double)P->stats.weak_pairs; s[5] = (double)P->stats.strong_leaf_pairs;
+            s[6] = P->stats.min_leaf; s[7] = P->stats.max_leaf;
+            s[8] = P->stats.t_build_ms; s[9] = P->stats.t_tree_ms; s[10] = P->stats.t_lists_ms;
+            s[11] = (double)P->nbox_total;
+            s[12] = (double)launch_count();
+            s[13] = (double)P->stats.p2p_pairs;
+            off = need;
+            break;
+        }
+    }
+    FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+    *bytes = off;
+    return 0;
+}
+
+}  // extern "C"

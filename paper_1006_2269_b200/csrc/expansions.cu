@@ -1,0 +1,350 @@
+// expansions.cu -- A4-A8: P2M, M2M, M2L and L2L as sm_100a FP64 kernels.
+//
+// Paper: "In the downward/upward phases the expansions are shifted as usual
+// according to parent/child relations.  The critical far-to-local shift follows
+// the weak connectivity pattern", in "the classical complex
+// polynomial/multipole representation".  Forms:
+//   P2M  a_0 = sum m_j,  a_k = -sum m_j (z_j - c)^k / k
+//   M2M  b_l = -a_0 z0^l / l + sum_{k=1..l} a_k z0^{l-k} C(l-1,k-1),  z0 = c - c'
+//   M2L  b_0 = a_0 Log(c_t - c_s) + sum_k (-1)^k a_k z0^-k
+//        b_l = z0^-l ( sum_k C(l+k-1,k-1) (-1)^k a_k z0^-k  -  a_0 / l ),  z0 = c_s - c_t
+//   L2L  d_k = sum_{l>=k} b_l C(l,k) h^{l-k},  h = c' - c  (Horner/Taylor shift)
+// M2L is organised as the paper's "constant transition matrices with pre- and
+// post-scaling according to the local geometry": pre-scale
+// alpha_k = a_k (-1/z0)^k, apply the constant (p+1) x p matrix C(l+k-1,k-1)
+// (held in __constant__ memory, a warp-uniform operand of every DFMA), post-scale
+// by z0^-l -- fused per pair in registers (no HBM staging: 2.25 flop/B would be
+// below the machine balance).  Every kernel is templated on p so the coefficient
+// vectors live in registers.
+#include "fmm2d_internal.cuh"
+
+namespace fmm2d {
+
+__constant__ double c_m2l[(FMM2D_PMAX + 1) * (FMM2D_PMAX + 1)];   // [l][k] = C(l+k-1, k-1)
+__constant__ double c_pas[(FMM2D_PMAX + 1) * (FMM2D_PMAX + 1)];   // [a][b] = C(a, b)
+
+// exact binomials in 64-bit integers (C(63,31) < 2^64), correctly rounded to double
+static uint64_t binom_u64(int a, int b)
+{
+    if (b < 0 || b > a) return 0;
+    if (b > a - b) b = a - b;
+    unsigned __int128 v = 1;
+    for (int i = 1; i <= b; ++i) v = v * (unsigned __int128)(a - b + i) / (unsigned __int128)i;
+    return (uint64_t)v;
+}
+
+int upload_binomials(int p)
+{
+    static int uploaded_for_device = -1;
+    int dev = 0;
+    FMM2D_CUDA_TRY(cudaGetDevice(&dev));
+    if (uploaded_for_device == dev) return 0;
+    (void)p;
+    const int S = FMM2D_PMAX + 1;
+    std::vector<double> m2l(S * S, 0.0), pas(S * S, 0.0);
+    for (int l = 0; l <= FMM2D_PMAX; ++l)
+        for (int k = 1; k <= FMM2D_PMAX; ++k) m2l[l * S + k] = (double)binom_u64(l + k - 1, k - 1);
+    for (int a = 0; a <= FMM2D_PMAX; ++a)
+        for (int b = 0; b <= a; ++b) pas[a * S + b] = (double)binom_u64(a, b);
+    FMM2D_CUDA_TRY(cudaMemcpyToSymbol(c_m2l, m2l.data(), sizeof(double) * S * S));
+    FMM2D_CUDA_TRY(cudaMemcpyToSymbol(c_pas, pas.data(), sizeof(double) * S * S));
+    uploaded_for_device = dev;
+    return 0;
+}
+
+namespace {
+
+constexpr int S1 = FMM2D_PMAX + 1;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b)
+{
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
+// ---------------------------------------------------------------- P2M (A4)
+template <int P>
+__global__ void __launch_bounds__(128) k_p2m(int64_t nleaf, const uint32_t* __restrict__ off,
+                                             const double4* __restrict__ src, const double* __restrict__ cx,
+                                             const double* __restrict__ cy, double2* __restrict__ mp)
+{
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nleaf) return;
+    double2 a[P + 1];
+#pragma unroll
+    for (int k = 0; k <= P; ++k) a[k] = make_double2(0.0, 0.0);
+    const double c0 = cx[b], c1 = cy[b];
+    for (uint32_t j = off[b]; j < off[b + 1]; ++j) {
+        double4 s = src[j];
+        double2 w = make_double2(s.x - c0, s.y - c1);
+        double2 m = make_double2(s.z, s.w);
+        a[0] = cadd(a[0], m);
+        double2 wk = m;                                 // m w^k, k = 1..P
+#pragma unroll
+        for (int k = 1; k <= P; ++k) {
+            wk = cmul(wk, w);
+            a[k] = csub(a[k], cscale(wk, 1.0 / k));
+        }
+    }
+    double2* out = mp + b * (P + 1);
+#pragma unroll
+    for (int k = 0; k <= P; ++k) out[k] = a[k];
+}
+
+// ---------------------------------------------------------------- M2M (A5)
+template <int P>
+__global__ void __launch_bounds__(128) k_m2m(int64_t nb, const double* __restrict__ cxp,
+                                             const double* __restrict__ cyp, const double* __restrict__ cxc,
+                                             const double* __restrict__ cyc, const double2* __restrict__ mc,
+                                             double2* __restrict__ mpar)
+{
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    double2 acc[P + 1];
+#pragma unroll
+    for (int k = 0; k <= P; ++k) acc[k] = make_double2(0.0, 0.0);
+    const double px = cxp[b], py = cyp[b];
+    for (int q = 0; q < 4; ++q) {
+        int64_t c = 4 * b + q;
+        const double2* A = mc + c * (P + 1);
+        double2 a[P + 1];
+#pragma unroll
+        for (int k = 0; k <= P; ++k) a[k] = A[k];
+        double2 z0 = make_double2(cxc[c] - px, cyc[c] - py);
+        acc[0] = cadd(acc[0], a[0]);
+        double2 zl = make_double2(1.0, 0.0);
+#pragma unroll
+        for (int l = 1; l <= P; ++l) {
+            zl = cmul(zl, z0);                          // z0^l
+            // Horner in z0: sum_{k=1..l} C(l-1,k-1) a_k z0^{l-k}
+            double2 t = cscale(a[1], c_pas[(l - 1) * S1 + 0]);
+#pragma unroll
+            for (int k = 2; k <= l; ++k) t = cadd(cmul(t, z0), cscale(a[k], c_pas[(l - 1) * S1 + (k - 1)]));
+            t = csub(t, cscale(cmul(a[0], zl), 1.0 / l));
+            acc[l] = cadd(acc[l], t);
+        }
+    }
+    double2* out = mpar + b * (P + 1);
+#pragma unroll
+    for (int k = 0; k <= P; ++k) out[k] = acc[k];
+}
+
+// ---------------------------------------------------------------- M2L (A6/A7)
+struct M2LArgs {
+    const int64_t* woff[FMM2D_MAXL + 1];
+    const uint32_t* widx[FMM2D_MAXL + 1];
+    int64_t base[FMM2D_MAXL + 2];
+    int L;
+    const double* cx;
+    const double* cy;
+    const double2* mpole;
+    double2* local;
+};
+
+// One thread computes output coefficients l in [L0, L1) of one target box.
+template <int P, int L0, int L1>
+__device__ __forceinline__ void m2l_target(const M2LArgs& A, int64_t g, int lev)
+{
+    int64_t b = g - A.base[lev];
+    const int64_t* off = A.woff[lev];
+    const uint32_t* idx = A.widx[lev];
+    const double ctx = A.cx[g], cty = A.cy[g];
+    double2 acc[L1 - L0];
+#pragma unroll
+    for (int l = 0; l < L1 - L0; ++l) acc[l] = make_double2(0.0, 0.0);
+    const int64_t q0 = off[b], q1 = off[b + 1];
+    for (int64_t q = q0; q < q1; ++q) {
+        const int64_t s = A.base[lev] + idx[q];
+        const double csx = A.cx[s], csy = A.cy[s];
+        const double2* M = A.mpole + s * (P + 1);
+        // z0 = c_s - c_t and 1/z0
+        const double dx = csx - ctx, dy = csy - cty;
+        const double r2 = dx * dx + dy * dy;
+        const double ir2 = 1.0 / r2;
+        const double2 iz = make_double2(dx * ir2, -dy * ir2);
+        const double2 w = make_double2(-iz.x, -iz.y);
+        // pre-scale: alpha_k = a_k (-1/z0)^k
+        double2 al[P + 1];
+        double2 wk = w;
+#pragma unroll
+        for (int k = 1; k <= P; ++k) {
+            al[k] = cmul(M[k], wk);
+            if (k < P) wk = cmul(wk, w);
+        }
+        const double2 a0 = M[0];
+        double2 izl = make_double2(1.0, 0.0);
+#pragma unroll
+        for (int l = 0; l < L1; ++l) {
+            if (l >= 1) izl = cmul(izl, iz);            // z0^-l
+            if (l < L0) continue;
+            double2 beta = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int k = 1; k <= P; ++k) {
+                const double c = c_m2l[l * S1 + k];
+                beta.x = fma(c, al[k].x, beta.x);
+                beta.y = fma(c, al[k].y, beta.y);
+            }
+            if (l == 0) {
+                // a_0 Log(c_t - c_s), componentwise difference (DESIGN R2)
+                const double tx = ctx - csx, ty = cty - csy;
+                const double2 lg = make_double2(0.5 * log(r2), atan2(ty, tx));
+                acc[0] = cadd(acc[0], cadd(cmul(a0, lg), beta));
+            } else {
+                const double2 t = csub(beta, cscale(a0, 1.0 / l));
+                acc[l - L0] = cadd(acc[l - L0], cmul(t, izl));
+            }
+        }
+    }
+    double2* out = A.local + g * (P + 1);
+#pragma unroll
+    for (int l = L0; l < L1; ++l) out[l] = acc[l - L0];
+}
+
+// threads: NS consecutive warps share 32 target boxes; warp-uniform part index.
+template <int P, int NS>
+__global__ void __launch_bounds__(128) k_m2l(M2LArgs A, int64_t g0, int64_t g1)
+{
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int lane = threadIdx.x & 31;
+    int64_t warp = t >> 5;
+    int part = (int)(warp % NS);
+    int64_t g = g0 + (warp / NS) * 32 + lane;
+    if (g >= g1) return;
+    int lev = 1;
+    while (lev < A.L && g >= A.base[lev + 1]) ++lev;
+    constexpr int H = (NS == 1) ? (P + 1) : (P + 2) / 2;
+    if constexpr (NS == 1) {
+        m2l_target<P, 0, H>(A, g, lev);
+    } else {
+        if (part == 0) m2l_target<P, 0, H>(A, g, lev);
+        else           m2l_target<P, H, P + 1>(A, g, lev);
+    }
+}
+
+// ---------------------------------------------------------------- L2L (A8)
+template <int P>
+__global__ void __launch_bounds__(128) k_l2l(int64_t nb, const double* __restrict__ cxp,
+                                             const double* __restrict__ cyp, const double* __restrict__ cxc,
+                                             const double* __restrict__ cyc, const double2* __restrict__ lpar,
+                                             double2* __restrict__ lch)
+{
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nb) return;
+    int64_t b = c >> 2;
+    const double2* B = lpar + b * (P + 1);
+    double2 d[P + 1];
+#pragma unroll
+    for (int k = 0; k <= P; ++k) d[k] = B[k];
+    const double2 h = make_double2(cxc[c] - cxp[b], cyc[c] - cyp[b]);
+    // Taylor shift: d_k = sum_{l>=k} b_l C(l,k) h^{l-k}
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+#pragma unroll
+        for (int j = P - 1; j >= i; --j) d[j] = cadd(d[j], cmul(h, d[j + 1]));
+    }
+    double2* out = lch + c * (P + 1);
+#pragma unroll
+    for (int k = 0; k <= P; ++k) out[k] = cadd(out[k], d[k]);
+}
+
+inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+
+template <int P>
+int upward_p(fmm2d_plan* Pl)
+{
+    cudaStream_t st = Pl->stream;
+    const int L = Pl->L;
+    int64_t nl = nboxes(L);
+    k_p2m<P><<<grid_for(nl, 128), 128, 0, st>>>(nl, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
+                                               Pl->cy + Pl->base[L], Pl->mpole + Pl->base[L] * (P + 1)); fmm2d::note_launch();
+    FMM2D_CUDA_TRY(cudaGetLastError());
+    for (int l = L - 1; l >= 0; --l) {
+        int64_t nb = nboxes(l);
+        k_m2m<P><<<grid_for(nb, 128), 128, 0, st>>>(
+            nb, Pl->cx + Pl->base[l], Pl->cy + Pl->base[l], Pl->cx + Pl->base[l + 1], Pl->cy + Pl->base[l + 1],
+            Pl->mpole + Pl->base[l + 1] * (P + 1), Pl->mpole + Pl->base[l] * (P + 1)); fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    }
+    return 0;
+}
+
+template <int P>
+constexpr int m2l_split() { return P <= 20 ? 1 : 2; }
+
+template <int P>
+int m2l_p(fmm2d_plan* Pl)
+{
+    cudaStream_t st = Pl->stream;
+    const int L = Pl->L;
+    if (L < 1) {
+        FMM2D_CUDA_TRY(cudaMemsetAsync(Pl->local, 0, sizeof(double2) * (P + 1), st));
+        return 0;
+    }
+    M2LArgs A;
+    for (int l = 0; l <= L; ++l) {
+        A.woff[l] = Pl->weak[l].off;
+        A.widx[l] = Pl->weak[l].idx;
+    }
+    for (int l = 0; l <= L + 1; ++l) A.base[l] = Pl->base[l];
+    A.L = L;
+    A.cx = Pl->cx;
+    A.cy = Pl->cy;
+    A.mpole = Pl->mpole;
+    A.local = Pl->local;
+    // level-0 local is zero (no M2L at the root)
+    FMM2D_CUDA_TRY(cudaMemsetAsync(Pl->local, 0, sizeof(double2) * (P + 1), st));
+    constexpr int NS = m2l_split<P>();
+    int64_t g0 = Pl->base[1], g1 = Pl->base[L + 1];
+    int64_t nthreads = ((g1 - g0 + 31) / 32) * 32 * NS;
+    k_m2l<P, NS><<<grid_for(nthreads, 128), 128, 0, st>>>(A, g0, g1); fmm2d::note_launch();
+    FMM2D_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+template <int P>
+int downward_p(fmm2d_plan* Pl)
+{
+    cudaStream_t st = Pl->stream;
+    for (int l = 2; l <= Pl->L; ++l) {
+        int64_t nb = nboxes(l);
+        k_l2l<P><<<grid_for(nb, 128), 128, 0, st>>>(
+            nb, Pl->cx + Pl->base[l - 1], Pl->cy + Pl->base[l - 1], Pl->cx + Pl->base[l], Pl->cy + Pl->base[l],
+            Pl->local + Pl->base[l - 1] * (P + 1), Pl->local + Pl->base[l] * (P + 1)); fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    }
+    return 0;
+}
+
+}  // namespace
+
+#define FMM2D_P_CASES(F)                                                                      \
+    case 1: return F<1>(P); case 2: return F<2>(P); case 3: return F<3>(P);                   \
+    case 4: return F<4>(P); case 5: return F<5>(P); case 6: return F<6>(P);                   \
+    case 7: return F<7>(P); case 8: return F<8>(P); case 9: return F<9>(P);                   \
+    case 10: return F<10>(P); case 11: return F<11>(P); case 12: return F<12>(P);             \
+    case 13: return F<13>(P); case 14: return F<14>(P); case 15: return F<15>(P);             \
+    case 16: return F<16>(P); case 17: return F<17>(P); case 18: return F<18>(P);             \
+    case 19: return F<19>(P); case 20: return F<20>(P); case 21: return F<21>(P);             \
+    case 22: return F<22>(P); case 23: return F<23>(P); case 24: return F<24>(P);             \
+    case 25: return F<25>(P); case 26: return F<26>(P); case 27: return F<27>(P);             \
+    case 28: return F<28>(P); case 29: return F<29>(P); case 30: return F<30>(P);             \
+    case 31: return F<31>(P); case 32: return F<32>(P);
+
+int run_upward(fmm2d_plan* P)
+{
+    switch (P->p) { FMM2D_P_CASES(upward_p) default: return FMM2D_EINVAL; }
+}
+
+int run_m2l(fmm2d_plan* P)
+{
+    switch (P->p) { FMM2D_P_CASES(m2l_p) default: return FMM2D_EINVAL; }
+}
+
+int run_downward(fmm2d_plan* P)
+{
+    switch (P->p) { FMM2D_P_CASES(downward_p) default: return FMM2D_EINVAL; }
+}
+
+}  // namespace fmm2d

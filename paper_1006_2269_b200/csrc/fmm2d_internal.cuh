@@ -1,0 +1,116 @@
+// fmm2d_internal.cuh -- plan layout and shared device helpers of libfmm2d.so.
+//
+// Product code (sm_100a).  Shares nothing with oracle/ (see DESIGN.md section 3).
+// Layout in HBM:
+//   boxes of all levels are numbered globally, level l occupying
+//   [base[l], base[l] + 4^l) with base[l] = (4^l - 1)/3;
+//   per-box SoA discs cx, cy, r (f64); expansions box-major double2[box][p+1];
+//   leaf-ordered sources double4 {x, y, Re m, Im m} (32 B, one 256-bit row each);
+//   lists per level as CSR (int64 offsets over the level's boxes, uint32 level-local ids).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <vector>
+
+#include "../../include/fmm2d.h"
+
+#define FMM2D_MAXL 15
+
+namespace fmm2d {
+
+static inline int64_t nboxes(int l) { return (int64_t)1 << (2 * l); }
+static inline int64_t level_base(int l) { return (nboxes(l) - 1) / 3; }
+
+struct Csr {
+    int64_t* off = nullptr;   // device, 4^l + 1
+    uint32_t* idx = nullptr;  // device, off[4^l] entries (level-local box ids)
+    int64_t total = 0;
+};
+
+// tree record: position, input index, current box id (24 B)
+struct Rec {
+    double x, y;
+    uint32_t idx, box;
+};
+
+struct Stats {
+    double t_build_ms = 0, t_tree_ms = 0, t_lists_ms = 0;
+    int64_t weak_pairs = 0, strong_leaf_pairs = 0, p2p_pairs = 0;
+    int max_leaf = 0, min_leaf = 0;
+};
+
+}  // namespace fmm2d
+
+struct fmm2d_plan {
+    int64_t n = 0;
+    int L = 0, p = 0, flags = 0, device = 0;
+    double theta = 0.5;
+    cudaStream_t stream = nullptr;
+    int64_t nbox_total = 0;
+    std::vector<int64_t> base;          // base[l], l = 0..L+1
+    // offsets of every level (uint32, n < 2^31), concatenated: level l at obase[l]
+    uint32_t* boff = nullptr;
+    std::vector<int64_t> obase;
+    std::vector<uint32_t> h_boff;       // host copy
+    // tree outputs
+    uint32_t* perm = nullptr;           // [n] leaf position -> input index
+    double4* src = nullptr;             // [n] leaf-ordered {x, y, Re m, Im m}
+    double *cx = nullptr, *cy = nullptr, *r = nullptr;   // [nbox_total]
+    // connectivity
+    std::vector<fmm2d::Csr> strong, weak;   // per level
+    // expansions
+    double2* mpole = nullptr;           // [nbox_total][p+1]
+    double2* local = nullptr;           // [nbox_total][p+1]
+    // staging for FMM2D_HOST_PTRS
+    double2* mstage = nullptr;
+    double2* phistage = nullptr;
+    double2* dphistage = nullptr;
+    fmm2d::Stats stats;
+    std::vector<void*> allocs;          // everything to free
+};
+
+// ---------------------------------------------------------------- helpers
+namespace fmm2d {
+
+int dev_alloc(fmm2d_plan* P, void** ptr, size_t bytes);
+
+// build steps (tree.cu, lists.cu)
+int build_tree(fmm2d_plan* P, const double2* z_dev);
+int build_lists(fmm2d_plan* P);
+// eval steps (expansions.cu, near.cu)
+int run_upward(fmm2d_plan* P);
+int run_m2l(fmm2d_plan* P);
+int run_downward(fmm2d_plan* P);
+int run_near(fmm2d_plan* P, double2* phi, double2* dphi);
+int gather_strengths(fmm2d_plan* P, const double2* m);
+int upload_binomials(int p);
+// count of this library's own kernel launches (reported by bench.py as gpu_launches)
+void note_launch();
+int64_t launch_count();
+
+}  // namespace fmm2d
+
+#define FMM2D_CUDA_TRY(expr)                                  \
+    do {                                                      \
+        cudaError_t _e = (expr);                              \
+        if (_e != cudaSuccess) {                              \
+            fmm2d_set_last_cuda_error(_e, #expr, __FILE__, __LINE__); \
+            return (_e == cudaErrorMemoryAllocation) ? FMM2D_ENOMEM : FMM2D_ECUDA; \
+        }                                                     \
+    } while (0)
+
+#define FMM2D_TRY(expr)                                       \
+    do {                                                      \
+        int _rc = (expr);                                     \
+        if (_rc) return _rc;                                  \
+    } while (0)
+
+void fmm2d_set_last_cuda_error(cudaError_t e, const char* what, const char* file, int line);
+
+// IEEE round-to-nearest helpers with no FMA contraction (DESIGN R11)
+__device__ __forceinline__ double rn_dist(double x, double y, double cx, double cy)
+{
+    double dx = __dsub_rn(x, cx);
+    double dy = __dsub_rn(y, cy);
+    return __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+}

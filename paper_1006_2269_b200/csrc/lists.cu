@@ -1,0 +1,187 @@
+// lists.cu -- A3: connectivity from the theta-criterion.
+//
+// Paper: "For each box b, the strong connections S(p) of its parent box
+// p are examined; all children of a box in S(p) that satisfy the theta-criterion
+// with respect to b become weakly coupled to b -- the rest remain strongly coupled.
+// This simple rule together with the fact that a box is always strongly connected
+// to itself recursively defines the connectivity for the whole tree.  The resulting
+// topology is conveniently stored in sparse matrices with sparsity patterns known
+// before each level is to be examined."
+// Criterion 1: well separated iff R + theta r <= theta d (readings
+// R9-R11: d > 0 required, non-strict, no FMA, exact operation order).
+//
+// GPU formulation: one warp per box; the candidate list (children of the parent's
+// strong list, in ascending order) is walked 32 at a time, each lane evaluates the
+// predicate, and ballot/popc compaction writes weak and strong entries in candidate
+// order (so lists come out ascending, R13).  Count pass -> scan -> fill pass.
+#include <cub/cub.cuh>
+
+#include "fmm2d_internal.cuh"
+
+namespace fmm2d {
+
+namespace {
+
+__device__ __forceinline__ bool well_separated(double cbx, double cby, double rb, double ccx, double ccy,
+                                               double rc, double theta)
+{
+    double dx = __dsub_rn(cbx, ccx);
+    double dy = __dsub_rn(cby, ccy);
+    double d = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+    double R = fmax(rb, rc);
+    double r = fmin(rb, rc);
+    return (d > 0.0) && (__dadd_rn(R, __dmul_rn(theta, r)) <= __dmul_rn(theta, d));
+}
+
+template <bool FILL>
+__global__ void k_lists(int64_t nb, const double* __restrict__ cx, const double* __restrict__ cy,
+                        const double* __restrict__ r, double theta, const int64_t* __restrict__ poff,
+                        const uint32_t* __restrict__ pidx, int64_t* __restrict__ wcnt,
+                        int64_t* __restrict__ scnt, const int64_t* __restrict__ woff,
+                        const int64_t* __restrict__ soff, uint32_t* __restrict__ widx,
+                        uint32_t* __restrict__ sidx)
+{
+    int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (b >= nb) return;
+    int64_t par = b >> 2;
+    int64_t o0 = poff[par];
+    int64_t ncand = 4 * (poff[par + 1] - o0);
+    double bx = cx[b], by = cy[b], br = r[b];
+    int64_t nw = 0, ns = 0;
+    int64_t wbase = FILL ? woff[b] : 0, sbase = FILL ? soff[b] : 0;
+    unsigned lt = (1u << lane) - 1u;
+    for (int64_t t0 = 0; t0 < ncand; t0 += 32) {
+        int64_t t = t0 + lane;
+        bool valid = t < ncand;
+        uint32_t c = 0;
+        bool ws = false;
+        if (valid) {
+            c = 4u * pidx[o0 + (t >> 2)] + (uint32_t)(t & 3);
+            ws = (c != (uint32_t)b) && well_separated(bx, by, br, cx[c], cy[c], r[c], theta);
+        }
+        unsigned wm = __ballot_sync(0xffffffffu, valid && ws);
+        unsigned sm = __ballot_sync(0xffffffffu, valid && !ws);
+        if (FILL && valid) {
+            if (ws) widx[wbase + nw + __popc(wm & lt)] = c;
+            else    sidx[sbase + ns + __popc(sm & lt)] = c;
+        }
+        nw += __popc(wm);
+        ns += __popc(sm);
+    }
+    if (!FILL && lane == 0) {
+        wcnt[b] = nw;
+        scnt[b] = ns;
+    }
+}
+
+// ordered P2P pairs (j != i) of one evaluation: sum_t n_t * sum_{s in S(t)} n_s - N
+__global__ void k_pair_count(int64_t nb, const uint32_t* __restrict__ off, const int64_t* __restrict__ soff,
+                             const uint32_t* __restrict__ sidx, unsigned long long* __restrict__ total)
+{
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long v = 0;
+    if (t < nb) {
+        unsigned long long ns = 0;
+        for (int64_t q = soff[t]; q < soff[t + 1]; ++q) {
+            uint32_t s = sidx[q];
+            ns += off[s + 1] - off[s];
+        }
+        unsigned long long nt = off[t + 1] - off[t];
+        v = nt * ns - nt;
+    }
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(total, v);
+}
+
+inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+
+}  // namespace
+
+int build_lists(fmm2d_plan* P)
+{
+    const int L = P->L;
+    cudaStream_t st = P->stream;
+    P->strong.assign(L + 1, Csr());
+    P->weak.assign(L + 1, Csr());
+    // level 0: S(root) = {root}, no weak pairs
+    {
+        int64_t h_off[2] = {0, 1}, h_woff[2] = {0, 0};
+        uint32_t zero = 0;
+        FMM2D_TRY(dev_alloc(P, (void**)&P->strong[0].off, sizeof(h_off)));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->strong[0].idx, sizeof(uint32_t)));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->weak[0].off, sizeof(h_woff)));
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(P->strong[0].off, h_off, sizeof(h_off), cudaMemcpyHostToDevice, st));
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(P->strong[0].idx, &zero, sizeof(zero), cudaMemcpyHostToDevice, st));
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(P->weak[0].off, h_woff, sizeof(h_woff), cudaMemcpyHostToDevice, st));
+        FMM2D_CUDA_TRY(cudaStreamSynchronize(st));   // host sources go out of scope
+        P->strong[0].total = 1;
+        P->weak[0].total = 0;
+    }
+    if (L == 0) {
+        P->stats.strong_leaf_pairs = 1;
+        P->stats.p2p_pairs = P->n * (P->n - 1);
+        return 0;
+    }
+    int64_t nbmax = nboxes(L);
+    int64_t *cnt_w = nullptr, *cnt_s = nullptr;
+    void* scratch = nullptr;
+    size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)(nbmax + 1), st);
+    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt_w, sizeof(int64_t) * (nbmax + 1), st));
+    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt_s, sizeof(int64_t) * (nbmax + 1), st));
+    FMM2D_CUDA_TRY(cudaMallocAsync(&scratch, scan_bytes, st));
+    auto body = [&]() -> int {
+        for (int l = 1; l <= L; ++l) {
+            int64_t nb = nboxes(l);
+            Csr& W = P->weak[l];
+            Csr& S = P->strong[l];
+            const Csr& PS = P->strong[l - 1];
+            const double* cx = P->cx + P->base[l];
+            const double* cy = P->cy + P->base[l];
+            const double* r = P->r + P->base[l];
+            FMM2D_TRY(dev_alloc(P, (void**)&W.off, sizeof(int64_t) * (nb + 1)));
+            FMM2D_TRY(dev_alloc(P, (void**)&S.off, sizeof(int64_t) * (nb + 1)));
+            FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_w + nb, 0, sizeof(int64_t), st));
+            FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_s + nb, 0, sizeof(int64_t), st));
+            unsigned grid = grid_for(nb * 32, 256);
+            k_lists<false><<<grid, 256, 0, st>>>(nb, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w, cnt_s,
+                                                 nullptr, nullptr, nullptr, nullptr); fmm2d::note_launch();
+            FMM2D_CUDA_TRY(cudaGetLastError());
+            size_t sb = scan_bytes;
+            FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, cnt_w, W.off, (int)(nb + 1), st));
+            sb = scan_bytes;
+            FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, cnt_s, S.off, (int)(nb + 1), st));
+            int64_t tot[2];
+            FMM2D_CUDA_TRY(cudaMemcpyAsync(&tot[0], W.off + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            FMM2D_CUDA_TRY(cudaMemcpyAsync(&tot[1], S.off + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+            W.total = tot[0];
+            S.total = tot[1];
+            FMM2D_TRY(dev_alloc(P, (void**)&W.idx, sizeof(uint32_t) * std::max<int64_t>(W.total, 1)));
+            FMM2D_TRY(dev_alloc(P, (void**)&S.idx, sizeof(uint32_t) * std::max<int64_t>(S.total, 1)));
+            k_lists<true><<<grid, 256, 0, st>>>(nb, cx, cy, r, P->theta, PS.off, PS.idx, nullptr, nullptr,
+                                                W.off, S.off, W.idx, S.idx); fmm2d::note_launch();
+            FMM2D_CUDA_TRY(cudaGetLastError());
+            P->stats.weak_pairs += W.total;
+        }
+        P->stats.strong_leaf_pairs = P->strong[L].total;
+        unsigned long long* d_tot = (unsigned long long*)cnt_w;   // reuse scratch
+        FMM2D_CUDA_TRY(cudaMemsetAsync(d_tot, 0, sizeof(unsigned long long), st));
+        k_pair_count<<<grid_for(nbmax, 256), 256, 0, st>>>(nbmax, P->boff + P->obase[L], P->strong[L].off,
+                                                           P->strong[L].idx, d_tot); fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+        unsigned long long h_tot = 0;
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_tot, d_tot, sizeof(h_tot), cudaMemcpyDeviceToHost, st));
+        FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+        P->stats.p2p_pairs = (int64_t)h_tot;
+        return 0;
+    };
+    int rc = body();
+    cudaFreeAsync(cnt_w, st);
+    cudaFreeAsync(cnt_s, st);
+    cudaFreeAsync(scratch, st);
+    return rc;
+}
+
+}  // namespace fmm2d

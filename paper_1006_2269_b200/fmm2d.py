@@ -1,0 +1,245 @@
+"""Thin Python binding of libfmm2d.so (include/fmm2d.h): argument marshalling only.
+
+Every step of the evaluation pass runs in the library's CUDA kernels; there is no
+CPU fallback.  If the library is missing or no CUDA device is present the calls
+raise.  PyTorch supplies device memory and streams.
+
+    from paper_1006_2269_b200 import Fmm2d
+    plan = Fmm2d(z, theta=0.5, p=17, leaf_target=40)     # z: complex128 (cuda tensor or numpy)
+    phi, dphi = plan.eval(m)                             # Phi(z_i), Phi'(z_i) in input order
+
+Method: S. Engblom, arXiv 1006.2269 -- Phi(z_i) = sum_{j!=i} m_j Log(z_i - z_j)
+ by the asymmetric adaptive FMM.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfmm2d.so")
+
+PMAX = 32
+HOST_PTRS = 0x1
+REAL_STRENGTHS = 0x2
+
+EXPORT_PERM, EXPORT_OFFSETS, EXPORT_DISCS, EXPORT_STRONG, EXPORT_WEAK, EXPORT_MPOLE, EXPORT_LOCAL, \
+    EXPORT_STATS = range(1, 9)
+
+# every symbol include/fmm2d.h declares
+SYMBOLS = ["fmm2d_default_options", "fmm2d_build", "fmm2d_eval", "fmm2d_eval_timed", "fmm2d_launch_count",
+           "fmm2d_free", "fmm2d_strerror", "fmm2d_last_error_detail", "fmm2d_plan_info", "fmm2d_export"]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("theta", ctypes.c_double), ("p", ctypes.c_int), ("leaf_target", ctypes.c_int),
+                ("nlevels", ctypes.c_int), ("flags", ctypes.c_int), ("device", ctypes.c_int),
+                ("stream", ctypes.c_void_p), ("nranks", ctypes.c_int), ("rank", ctypes.c_int),
+                ("nccl_id", ctypes.c_void_p)]
+
+
+class FmmError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        self.code = code
+        L = _lib
+        msg = L.fmm2d_strerror(code).decode() if L else str(code)
+        detail = L.fmm2d_last_error_detail().decode() if L else ""
+        super().__init__(f"{what}: {msg} ({code}) {detail}".strip())
+
+
+_lib = None
+
+
+def lib():
+    """Load libfmm2d.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        vp = ctypes.c_void_p
+        L.fmm2d_default_options.argtypes = [ctypes.POINTER(Options)]
+        L.fmm2d_build.argtypes = [vp, ctypes.c_int64, ctypes.POINTER(Options), ctypes.POINTER(vp)]
+        L.fmm2d_eval.argtypes = [vp, vp, vp, vp]
+        L.fmm2d_eval_timed.argtypes = [vp, vp, vp, vp, ctypes.POINTER(ctypes.c_double)]
+        L.fmm2d_launch_count.argtypes = []
+        L.fmm2d_launch_count.restype = ctypes.c_int64
+        L.fmm2d_free.argtypes = [vp]
+        L.fmm2d_free.restype = None
+        L.fmm2d_strerror.argtypes = [ctypes.c_int]
+        L.fmm2d_strerror.restype = ctypes.c_char_p
+        L.fmm2d_last_error_detail.argtypes = []
+        L.fmm2d_last_error_detail.restype = ctypes.c_char_p
+        L.fmm2d_plan_info.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int),
+                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64),
+                                      ctypes.POINTER(ctypes.c_int64)]
+        L.fmm2d_export.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_size_t)]
+        _lib = L
+    return _lib
+
+
+def launch_count() -> int:
+    """Kernels launched by libfmm2d.so since it was loaded (CUB internals excluded)."""
+    return int(lib().fmm2d_launch_count())
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise FmmError(rc, what)
+
+
+def _ptr_of(a, host: bool):
+    """(pointer, keepalive) of a complex128 array: torch tensor (cuda or pinned cpu) or numpy."""
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.dtype != torch.complex128 or not a.is_contiguous():
+                raise TypeError("expected a contiguous complex128 tensor")
+            if host == a.is_cuda:
+                raise TypeError("device/host pointer kind does not match the plan's flags")
+            return a.data_ptr(), a
+    except ImportError:
+        pass
+    if not host:
+        raise TypeError("device plans need CUDA tensors")
+    arr = np.ascontiguousarray(a, dtype=np.complex128)
+    return arr.ctypes.data, arr
+
+
+class Fmm2d:
+    """A built plan (tree, discs, theta-criterion lists, expansion storage) for fixed
+    positions z; ``eval(m)`` runs one evaluation pass.
+
+    z: complex128 CUDA tensor (device plan) or host array (numpy / CPU tensor; the
+    plan then uses FMM2D_HOST_PTRS and host inputs/outputs)."""
+
+    def __init__(self, z, theta: float = 0.5, p: int = 17, leaf_target: int = 40, nlevels: int = -1,
+                 real_strengths: bool = False, device: int | None = None, stream=None):
+        L = lib()
+        import torch
+        host = not (isinstance(z, torch.Tensor) and z.is_cuda)
+        if device is None:
+            device = z.device.index if (not host and z.device.index is not None) else torch.cuda.current_device()
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.device = device
+        self.stream = stream
+        self.host = host
+        opt = Options()
+        L.fmm2d_default_options(ctypes.byref(opt))
+        opt.theta = float(theta)
+        opt.p = int(p)
+        opt.leaf_target = int(leaf_target)
+        opt.nlevels = int(nlevels)
+        opt.flags = (HOST_PTRS if host else 0) | (REAL_STRENGTHS if real_strengths else 0)
+        opt.device = int(device)
+        opt.stream = ctypes.c_void_p(stream.cuda_stream)
+        self._opt = opt
+        zp, keep = _ptr_of(z, host)
+        self.n = int(keep.shape[0])
+        h = ctypes.c_void_p()
+        _check(L.fmm2d_build(ctypes.c_void_p(zp), self.n, ctypes.byref(opt), ctypes.byref(h)), "fmm2d_build")
+        self._h = h
+        n = ctypes.c_int64()
+        nl = ctypes.c_int()
+        pp = ctypes.c_int()
+        wp = ctypes.c_int64()
+        sp = ctypes.c_int64()
+        _check(L.fmm2d_plan_info(h, ctypes.byref(n), ctypes.byref(nl), ctypes.byref(pp), ctypes.byref(wp),
+                                 ctypes.byref(sp)), "fmm2d_plan_info")
+        self.L = nl.value
+        self.p = pp.value
+        self.theta = float(theta)
+        self.weak_pairs = wp.value
+        self.strong_leaf_pairs = sp.value
+
+    # -- evaluation -------------------------------------------------------
+    def eval(self, m, phi=None, dphi=None, want_phi: bool = True, want_dphi: bool = True):
+        """Phi(z_i), Phi'(z_i) in input order.  Device plans: complex128 CUDA tensors,
+        asynchronous on the plan's stream.  Host plans: numpy/pinned arrays, synchronous."""
+        import torch
+        if self._h is None:
+            raise RuntimeError("plan freed")
+        mp, mkeep = _ptr_of(m, self.host)
+        if self.host:
+            if want_phi and phi is None:
+                phi = torch.empty(self.n, dtype=torch.complex128, pin_memory=torch.cuda.is_available())
+            if want_dphi and dphi is None:
+                dphi = torch.empty(self.n, dtype=torch.complex128, pin_memory=torch.cuda.is_available())
+        else:
+            dev = torch.device("cuda", self.device)
+            if want_phi and phi is None:
+                phi = torch.empty(self.n, dtype=torch.complex128, device=dev)
+            if want_dphi and dphi is None:
+                dphi = torch.empty(self.n, dtype=torch.complex128, device=dev)
+        pp = _ptr_of(phi, self.host)[0] if phi is not None else None
+        dp = _ptr_of(dphi, self.host)[0] if dphi is not None else None
+        _check(lib().fmm2d_eval(self._h, ctypes.c_void_p(mp), ctypes.c_void_p(pp), ctypes.c_void_p(dp)),
+               "fmm2d_eval")
+        return phi, dphi
+
+    def eval_timed(self, m, phi, dphi) -> dict:
+        """eval into preallocated outputs, synchronise, return per-phase device ms."""
+        t = (ctypes.c_double * 8)()
+        mp = _ptr_of(m, self.host)[0]
+        pp = _ptr_of(phi, self.host)[0] if phi is not None else None
+        dp = _ptr_of(dphi, self.host)[0] if dphi is not None else None
+        _check(lib().fmm2d_eval_timed(self._h, ctypes.c_void_p(mp), ctypes.c_void_p(pp), ctypes.c_void_p(dp), t),
+               "fmm2d_eval_timed")
+        return {"gather_ms": t[0], "upward_ms": t[1], "m2l_ms": t[2], "downward_ms": t[3], "near_ms": t[4],
+                "eval_ms": t[5]}
+
+    # -- exports (tests / diagnostics) -------------------------------------
+    def _export(self, what: int, level: int = 0) -> bytes:
+        L = lib()
+        nbytes = ctypes.c_size_t(0)
+        _check(L.fmm2d_export(self._h, what, level, None, ctypes.byref(nbytes)), "fmm2d_export(size)")
+        buf = (ctypes.c_char * max(nbytes.value, 1))()
+        _check(L.fmm2d_export(self._h, what, level, buf, ctypes.byref(nbytes)), "fmm2d_export")
+        return bytes(buf)[: nbytes.value]
+
+    def perm(self) -> np.ndarray:
+        return np.frombuffer(self._export(EXPORT_PERM), np.uint32).copy()
+
+    def offsets(self, level: int) -> np.ndarray:
+        return np.frombuffer(self._export(EXPORT_OFFSETS, level), np.int64).copy()
+
+    def discs(self, level: int):
+        a = np.frombuffer(self._export(EXPORT_DISCS, level), np.float64).reshape(3, -1)
+        return a[0].copy(), a[1].copy(), a[2].copy()
+
+    def list(self, level: int, kind: str):
+        raw = self._export(EXPORT_WEAK if kind == "weak" else EXPORT_STRONG, level)
+        nb = 4 ** level
+        off = np.frombuffer(raw[: 8 * (nb + 1)], np.int64).copy()
+        idx = np.frombuffer(raw[8 * (nb + 1):], np.uint32).copy()
+        return off, idx
+
+    def expansions(self, level: int, kind: str) -> np.ndarray:
+        raw = self._export(EXPORT_LOCAL if kind == "local" else EXPORT_MPOLE, level)
+        return np.frombuffer(raw, np.complex128).reshape(4 ** level, self.p + 1).copy()
+
+    def stats(self) -> dict:
+        s = np.frombuffer(self._export(EXPORT_STATS), np.float64)
+        keys = ["n", "L", "p", "theta", "weak_pairs", "strong_leaf_pairs", "min_leaf", "max_leaf",
+                "t_build_ms", "t_tree_ms", "t_lists_ms", "nboxes", "launches", "p2p_pairs"]
+        return {k: float(v) for k, v in zip(keys, s)}
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().fmm2d_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -1,0 +1,75 @@
+"""The C-ABI library loads and exports every symbol include/fmm2d.h declares; host-side
+validation (no GPU needed) rejects bad arguments with the documented codes."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "fmm2d.h")).read()
+    return sorted(set(re.findall(r"FMM2D_API\s+[\w\s\*]*?\b(fmm2d_\w+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    import paper_1006_2269_b200 as F
+    L = F.lib()
+    names = _declared()
+    assert len(names) >= 8
+    assert sorted(F.SYMBOLS) == names
+    for s in names:
+        assert hasattr(L, s), s
+
+
+def test_exports_are_only_the_abi():
+    import subprocess
+    import paper_1006_2269_b200 as F
+    out = subprocess.run(["nm", "-D", "--defined-only", F.LIB_PATH], capture_output=True, text=True).stdout
+    funcs = sorted(l.split()[-1] for l in out.splitlines() if " T " in l)
+    assert funcs == _declared()
+
+
+def test_default_options_and_strerror():
+    import paper_1006_2269_b200 as F
+    L = F.lib()
+    o = F.fmm2d.Options()
+    assert L.fmm2d_default_options(ctypes.byref(o)) == 0
+    assert (o.theta, o.p, o.leaf_target, o.nlevels, o.nranks, o.rank) == (0.5, 17, 40, -1, 1, 0)
+    assert L.fmm2d_strerror(-1) == b"invalid argument"
+    assert L.fmm2d_strerror(-2) == b"non-finite coordinate"
+    assert L.fmm2d_default_options(None) == -1
+
+
+@pytest.mark.parametrize("field,value", [("theta", 0.0), ("theta", 1.0), ("theta", -0.1), ("theta", float("nan")),
+                                         ("p", 0), ("p", 33), ("leaf_target", 0), ("nlevels", 3)])
+def test_build_rejects_invalid_options_without_gpu(field, value):
+    import paper_1006_2269_b200 as F
+    L = F.lib()
+    o = F.fmm2d.Options()
+    L.fmm2d_default_options(ctypes.byref(o))
+    setattr(o, field, value)
+    z = np.zeros(10, np.complex128)        # n = 10 < 4^3 for the nlevels case
+    h = ctypes.c_void_p()
+    rc = L.fmm2d_build(ctypes.c_void_p(z.ctypes.data), 10, ctypes.byref(o), ctypes.byref(h))
+    assert rc == -1 and not h.value
+
+
+def test_build_rejects_bad_sizes_and_nulls():
+    import paper_1006_2269_b200 as F
+    L = F.lib()
+    o = F.fmm2d.Options()
+    L.fmm2d_default_options(ctypes.byref(o))
+    z = np.zeros(4, np.complex128)
+    h = ctypes.c_void_p()
+    assert L.fmm2d_build(ctypes.c_void_p(z.ctypes.data), 0, ctypes.byref(o), ctypes.byref(h)) == -1
+    assert L.fmm2d_build(ctypes.c_void_p(z.ctypes.data), 1 << 31, ctypes.byref(o), ctypes.byref(h)) == -1
+    assert L.fmm2d_build(None, 4, ctypes.byref(o), ctypes.byref(h)) == -1
+    assert L.fmm2d_build(ctypes.c_void_p(z.ctypes.data), 4, None, ctypes.byref(h)) == -1
+    assert L.fmm2d_eval(None, None, None, None) == -1
+    L.fmm2d_free(None)                     # NULL-safe
+    o.nranks = 2                           # multi-rank builds are not in this ABI version
+    assert L.fmm2d_build(ctypes.c_void_p(z.ctypes.data), 4, ctypes.byref(o), ctypes.byref(h)) == -6

@@ -1,0 +1,202 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE north_star):
+  - permutation, box offsets, discs (centre, radius) and the strong / weak CSR
+    lists of every level: bit-exact;
+  - Phi and Phi' (complex, FMM branch R2): normwise max-abs error / max-abs
+    <= 1e-12 against the oracle FMM on the same inputs;
+  - Re Phi (real m) and Phi' against the direct sum within BJ's 1e-6 gate.
+Sizes span several tiles and ragged leaves; full-size configurations are
+checked on sampled outputs (tests/test_gpu_fullsize.py).
+"""
+import numpy as np
+import pytest
+import torch
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def _nerr(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def _gpu_plan(z, theta, p, L, real=False):
+    from paper_1006_2269_b200 import Fmm2d
+    zt = torch.from_numpy(z).cuda()
+    return Fmm2d(zt, theta=theta, p=p, nlevels=L, real_strengths=real)
+
+
+def _gpu_eval(plan, m):
+    phi, dphi = plan.eval(torch.from_numpy(m).cuda())
+    torch.cuda.synchronize()
+    return phi.cpu().numpy(), dphi.cpu().numpy()
+
+
+def _check_structure(gp, op, L):
+    assert gp.L == op.L == L
+    np.testing.assert_array_equal(gp.perm(), op.perm())
+    for l in range(L + 1):
+        np.testing.assert_array_equal(gp.offsets(l), op.offsets(l))
+        gcx, gcy, gr = gp.discs(l)
+        ocx, ocy, orr = op.discs(l)
+        np.testing.assert_array_equal(gcx, ocx)
+        np.testing.assert_array_equal(gcy, ocy)
+        np.testing.assert_array_equal(gr, orr)
+        for kind in ("strong", "weak"):
+            go, gi = gp.list(l, kind)
+            oo, oi = op.list(l, kind)
+            np.testing.assert_array_equal(go, oo, err_msg=f"{kind} offsets level {l}")
+            np.testing.assert_array_equal(gi, oi, err_msg=f"{kind} idx level {l}")
+
+
+STRUCT_CASES = [
+    ("C1", lambda: W.make_config("C1"), 0.5, None),
+    ("C2", lambda: W.make_config("C2"), 0.5, None),
+    ("C2-theta.3", lambda: W.make_config("C2"), 0.3, None),
+    ("C2-theta.7", lambda: W.make_config("C2"), 0.7, None),
+    ("C3-200k", lambda: W.make_config("C3", n=200_000), 0.5, None),
+    ("C4-200k", lambda: W.make_config("C4", n=200_000), 0.5, None),
+    ("lattice-ties", lambda: (W.lattice(6, 4, h=0.5, shuffle_seed=2), None), 0.5, 4),
+    ("ragged-7777", lambda: W.make("uniform", 7777, seed=3), 0.5, 3),
+]
+
+
+@pytest.mark.parametrize("name,mk,theta,L", STRUCT_CASES, ids=[c[0] for c in STRUCT_CASES])
+def test_tree_and_lists_bit_exact(orc, name, mk, theta, L):
+    z, _ = mk()
+    if L is None:
+        L = orc.nlevels(len(z), 35)
+    gp = _gpu_plan(z, theta, 17, L)
+    op = orc.plan(z, theta, L)
+    _check_structure(gp, op, L)
+
+
+def test_tree_adversarial_ties_dups_negzero(orc):
+    rng = np.random.default_rng(9)
+    n = 5000
+    x = np.round(rng.random(n) * 20) / 20          # heavy ties in x and y
+    y = np.round(rng.random(n) * 20) / 20
+    x[:50] = -0.0                                  # -0 mixed with +0
+    y[50:100] = 0.0
+    x[100:400] = 0.25                              # 300 duplicates
+    y[100:400] = 0.75
+    z = x + 1j * y
+    for L in (2, 4):
+        gp = _gpu_plan(z, 0.5, 8, L)
+        op = orc.plan(z, 0.5, L)
+        _check_structure(gp, op, L)
+
+
+def test_tree_tiny_and_forced_levels(orc):
+    for n, L in ((1, 0), (3, 0), (4, 1), (17, 2), (64, 3)):
+        z, _ = W.make("uniform", n, seed=n)
+        gp = _gpu_plan(z, 0.5, 4, L)
+        op = orc.plan(z, 0.5, L)
+        _check_structure(gp, op, L)
+
+
+EVAL_CASES = [
+    ("C1", "C1", None, 0.5, 17),
+    ("C2-t.5-p17", "C2", None, 0.5, 17),
+    ("C2-t.3-p8", "C2", None, 0.3, 8),
+    ("C2-t.7-p30", "C2", None, 0.7, 30),
+    ("C3-100k", "C3", 100_000, 0.5, 17),
+    ("C4-100k", "C4", 100_000, 0.5, 17),
+]
+
+
+@pytest.mark.parametrize("name,cfg,n,theta,p", EVAL_CASES, ids=[c[0] for c in EVAL_CASES])
+def test_eval_matches_oracle(orc, name, cfg, n, theta, p):
+    z, m = W.make_config(cfg, n=n)
+    L = orc.nlevels(len(z), 35)
+    gp = _gpu_plan(z, theta, p, L)
+    op = orc.plan(z, theta, L)
+    phi_o, dphi_o = op.eval(m, p)
+    phi_g, dphi_g = _gpu_eval(gp, m)
+    assert np.isfinite(phi_g).all() and np.isfinite(dphi_g).all()
+    e1, e2 = _nerr(phi_g, phi_o), _nerr(dphi_g, dphi_o)
+    assert e1 <= TOL and e2 <= TOL, (e1, e2)
+
+
+def test_eval_real_strength_flag_matches(orc):
+    z, m = W.make_config("C1")
+    L = 2
+    a = _gpu_eval(_gpu_plan(z, 0.5, 17, L, real=True), m)
+    b = _gpu_eval(_gpu_plan(z, 0.5, 17, L, real=False), m)
+    op = orc.plan(z, 0.5, L)
+    phi_o, dphi_o = op.eval(m, 17)
+    assert _nerr(a[0], phi_o) <= TOL and _nerr(a[1], dphi_o) <= TOL
+    assert _nerr(a[0], b[0]) <= TOL
+
+
+def test_expansions_per_level_match_oracle(orc):
+    """Diagnostic parity of every multipole and local expansion (locate any error)."""
+    z, m = W.make_config("C2", n=20_000)
+    L = orc.nlevels(len(z), 35)
+    gp = _gpu_plan(z, 0.5, 17, L)
+    op = orc.plan(z, 0.5, L)
+    op.eval(m, 17)
+    _gpu_eval(gp, m)
+    for l in range(L + 1):
+        for kind in ("mpole", "local"):
+            g = gp.expansions(l, kind)
+            o = op.expansions(l, kind)
+            if l == 0 and kind == "local":
+                assert np.all(g == 0) and np.all(o == 0)
+                continue
+            # coefficient-wise normwise error, scaled per coefficient index
+            for k in range(18):
+                den = np.abs(o[:, k]).max()
+                if den > 0:
+                    assert np.abs(g[:, k] - o[:, k]).max() <= 1e-12 * den, (l, kind, k)
+
+
+def test_eval_vs_direct_sum_gate(orc):
+    z, m = W.make_config("C1")
+    gp = _gpu_plan(z, 0.5, 17, 2)
+    phi_g, dphi_g = _gpu_eval(gp, m)
+    phi_d, dphi_d = orc.direct(z, m)
+    assert _nerr(phi_g.real, phi_d.real) <= 1e-6
+    assert _nerr(dphi_g, dphi_d) <= orc.error_bound(0.5, 17)
+
+
+def test_eval_root_only_equals_direct(orc):
+    z, m = W.make("uniform", 300, "phase", seed=31)       # L = 0: pure P2P, > 128 targets
+    phi_g, dphi_g = _gpu_eval(_gpu_plan(z, 0.5, 5, 0), m)
+    phi_d, dphi_d = orc.direct(z, m)
+    assert _nerr(phi_g, phi_d) <= 1e-13 and _nerr(dphi_g, dphi_d) <= 1e-13
+
+
+def test_host_pointer_path_equals_device_path():
+    from paper_1006_2269_b200 import Fmm2d
+    z, m = W.make_config("C1")
+    dev = _gpu_eval(_gpu_plan(z, 0.5, 17, 2), m)
+    hp = Fmm2d(z, theta=0.5, p=17, nlevels=2)           # numpy -> FMM2D_HOST_PTRS
+    phi, dphi = hp.eval(m)
+    np.testing.assert_array_equal(phi.numpy(), dev[0])
+    np.testing.assert_array_equal(dphi.numpy(), dev[1])
+
+
+def test_eval_deterministic_and_reusable():
+    z, m = W.make_config("C2", n=30_000)
+    gp = _gpu_plan(z, 0.5, 17, 5)
+    a = _gpu_eval(gp, m)
+    b = _gpu_eval(gp, m)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+    m2 = np.ascontiguousarray(m[::-1])
+    c = _gpu_eval(gp, m2)                                  # new strengths, same plan
+    assert not np.array_equal(c[0], a[0])
+
+
+def test_nonfinite_rejected():
+    from paper_1006_2269_b200 import Fmm2d, FmmError
+    z = np.zeros(100, np.complex128) + np.arange(100)
+    z[7] = complex(np.inf, 0)
+    with pytest.raises(FmmError) as e:
+        Fmm2d(torch.from_numpy(z).cuda(), nlevels=1)
+    assert e.value.code == -2
