@@ -70,30 +70,65 @@ def fp64_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled during the timed region, in-process through NVML
+    (pynvml; spawning nvidia-smi every 200 ms stalled the CUDA driver and inflated the
+    timed steps).  Falls back to nvidia-smi only if NVML cannot be loaded."""
 
-    def __init__(self, device: int):
+    REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap")]
+
+    def __init__(self, device: int, period: float = 0.1):
         self.device = device
-        self.samples = []
+        self.period = period
+        self.samples = []           # (sm_mhz, max_mhz, [reasons])
+        self.source = None
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_index(self):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            ids = [v.strip() for v in vis.split(",") if v.strip()]
+            if self.device < len(ids) and ids[self.device].isdigit():
+                return int(ids[self.device])
+        return self.device
+
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self._nvml_index())
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            masks = [(name, getattr(N, attr)) for name, attr in self.REASONS]
+
+            def sample():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                return (float(sm), float(mx), [name for name, m in masks if r & m])
+            self.source = "nvml"
+        except Exception:
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+
+            def sample():
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip().split(",")
+                v = [s.strip() for s in out]
+                return (float(v[0]), float(v[1]),
+                        [self.REASONS[i][0] for i in range(4) if v[2 + i].lower() == "active"])
+            self.source = "nvidia-smi"
 
         def run():
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([s.strip() for s in out.split(",")])
+                    self.samples.append(sample())
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(self.period)
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
@@ -106,14 +141,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        sm = [s[0] for s in self.samples]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted({r for s in self.samples for r in s[2]}), "samples": len(self.samples),
+                "source": self.source}
 
 
 def cpu_baseline(cfg, seconds_hint=True):
@@ -231,21 +263,21 @@ def main():
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    plans = []
+    plan = None
     with ClockSampler(local_rank) as clk:
         e0.record(stream)
+        h0 = time.perf_counter()
         for _ in range(args.steps):
-            p_ = step()
-            plans.append(p_)
-            if len(plans) > 1:
-                plans.pop(0).close()
+            if plan is not None:
+                plan.close()          # each step: free the previous plan, build + evaluate anew
+            plan = step()
         e1.record(stream)
         torch.cuda.synchronize()
+    host_ms = (time.perf_counter() - h0) * 1e3
     barrier()
     ms = e0.elapsed_time(e1)
-    st = plans[-1].stats()
-    for p_ in plans:
-        p_.close()
+    st = plan.stats()
+    plan.close()
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -288,7 +320,7 @@ def main():
                            "step": "fmm2d_build + fmm2d_eval (rows A0-A11)",
                            "l2": "inputs larger than L2 (no flush needed)",
                            "parallelism": f"replicas{world}" if world > 1 else "single"},
-                "phases_ms": phase, "eval_only_points_per_s": cfg.n / (phase["eval_ms"] / 1e3),
+                "phases_ms": phase, "host_ms_per_step": host_ms / args.steps, "eval_only_points_per_s": cfg.n / (phase["eval_ms"] / 1e3),
                 "m2l_tflops": m2l_tf,
                 "roofline": roof, "gpu_launches": launches_per_step * args.steps,
                 "clocks": clk.summary(), "e2e": e2e,

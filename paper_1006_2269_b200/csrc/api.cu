@@ -142,6 +142,7 @@ int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan
             }
         }
         FMM2D_TRY(upload_binomials(P->p));
+        FMM2D_TRY(prepare_near(P));
         const int64_t nb = P->nbox_total;
         const int P1 = P->p + 1;
         FMM2D_TRY(dev_alloc(P, (void**)&P->perm, sizeof(uint32_t) * n));
@@ -318,8 +319,12 @@ int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* by
     switch (what) {
         case FMM2D_EXPORT_PERM: FMM2D_TRY(copy_out(P->perm, dst, need, &cap, &off, st)); break;
         case FMM2D_EXPORT_OFFSETS: {
+            std::vector<uint32_t> h(nb + 1);
+            FMM2D_CUDA_TRY(cudaMemcpyAsync(h.data(), P->boff + P->obase[level], sizeof(uint32_t) * (nb + 1),
+                                           cudaMemcpyDeviceToHost, st));
+            FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
             int64_t* o = (int64_t*)dst;
-            for (int64_t b = 0; b <= nb; ++b) o[b] = P->h_boff[P->obase[level] + b];
+            for (int64_t b = 0; b <= nb; ++b) o[b] = h[b];
             off = need;
             break;
         }

@@ -214,12 +214,20 @@ __global__ void __launch_bounds__(128) k_m2l(M2LArgs A, int64_t g0, int64_t g1)
     if (g >= g1) return;
     int lev = 1;
     while (lev < A.L && g >= A.base[lev + 1]) ++lev;
-    constexpr int H = (NS == 1) ? (P + 1) : (P + 2) / 2;
+    // part q computes coefficients [q H, min((q+1) H, P+1)), H = ceil((P+1)/NS)
+    constexpr int H = (P + NS) / NS;
+    constexpr int E1 = (2 * H < P + 1) ? 2 * H : P + 1;
+    constexpr int E2 = (3 * H < P + 1) ? 3 * H : P + 1;
     if constexpr (NS == 1) {
-        m2l_target<P, 0, H>(A, g, lev);
-    } else {
+        m2l_target<P, 0, P + 1>(A, g, lev);
+    } else if constexpr (NS == 2) {
         if (part == 0) m2l_target<P, 0, H>(A, g, lev);
         else           m2l_target<P, H, P + 1>(A, g, lev);
+    } else {
+        static_assert(NS == 3, "M2L split into 1..3 parts");
+        if (part == 0)      m2l_target<P, 0, H>(A, g, lev);
+        else if (part == 1) m2l_target<P, H, E1>(A, g, lev);
+        else                m2l_target<P, E1, E2>(A, g, lev);
     }
 }
 
@@ -271,7 +279,7 @@ int upward_p(fmm2d_plan* Pl)
 }
 
 template <int P>
-constexpr int m2l_split() { return P <= 20 ? 1 : 2; }
+constexpr int m2l_split() { return P <= 20 ? 1 : (P <= 26 ? 2 : 3); }
 
 template <int P>
 int m2l_p(fmm2d_plan* Pl)

@@ -51,7 +51,6 @@ struct fmm2d_plan {
     // offsets of every level (uint32, n < 2^31), concatenated: level l at obase[l]
     uint32_t* boff = nullptr;
     std::vector<int64_t> obase;
-    std::vector<uint32_t> h_boff;       // host copy
     // tree outputs
     uint32_t* perm = nullptr;           // [n] leaf position -> input index
     double4* src = nullptr;             // [n] leaf-ordered {x, y, Re m, Im m}
@@ -65,6 +64,7 @@ struct fmm2d_plan {
     double2* mstage = nullptr;
     double2* phistage = nullptr;
     double2* dphistage = nullptr;
+    const void* tables = nullptr;       // fastmath tables (device, shared per device)
     fmm2d::Stats stats;
     std::vector<void*> allocs;          // everything to free
 };
@@ -82,6 +82,7 @@ int run_upward(fmm2d_plan* P);
 int run_m2l(fmm2d_plan* P);
 int run_downward(fmm2d_plan* P);
 int run_near(fmm2d_plan* P, double2* phi, double2* dphi);
+int prepare_near(fmm2d_plan* P);
 int gather_strengths(fmm2d_plan* P, const double2* m);
 int upload_binomials(int p);
 // count of this library's own kernel launches (reported by bench.py as gpu_launches)

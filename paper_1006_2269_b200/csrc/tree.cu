@@ -10,9 +10,13 @@
 // A split along x takes the first ceil(n/2) of the x-list (trivially partitioned)
 // and stably partitions the y-list by "(x, idx) < the first x-high record": one
 // flag pass, one device-wide scan, one scatter.  Stability keeps both lists sorted,
-// so the y-split is the same step with the axes swapped.  Box sizes are a pure
-// function of N, so all offsets are computed on the host.  The presort is two
-// stable radix sorts of orderable 64-bit keys (ties leave in index order).
+// so the y-split is the same step with the axes swapped.  The list that is only
+// trivially split is never rewritten: its records keep the id of the previous
+// (half-)level and every reader refines it from the record's position and the
+// offsets ("stale id + refine").  Box sizes are a pure function of N, so all
+// offsets come from a tiny per-level kernel.  The presort is two stable radix sorts
+// of orderable 64-bit keys (ties leave in index order); the sorted key itself gives
+// the sort coordinate back, only the other coordinate is gathered.
 #include <cub/cub.cuh>
 
 #include "fmm2d_internal.cuh"
@@ -25,6 +29,11 @@ __device__ __forceinline__ uint64_t orderable(double v)
 {
     uint64_t u = (uint64_t)__double_as_longlong(v);
     return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double from_orderable(uint64_t k)
+{
+    uint64_t u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+    return __longlong_as_double((long long)u);
 }
 
 // A0: validate, map -0 -> +0 (x + 0.0), order keys, identity indices.
@@ -44,18 +53,48 @@ __global__ void k_canon(const double2* __restrict__ z, int64_t n, double* __rest
     iota[i] = (uint32_t)i;
 }
 
-__global__ void k_make_recs(const uint32_t* __restrict__ order, const double* __restrict__ xs,
-                            const double* __restrict__ ys, int64_t n, Rec* __restrict__ out)
+// records of one presorted list: the sort coordinate from the key, the other gathered
+__global__ void k_make_recs(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ order,
+                            const double* __restrict__ other, int axis, int64_t n, Rec* __restrict__ out)
 {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     uint32_t i = order[k];
+    double c = from_orderable(keys[k]), o = other[i];
     Rec r;
-    r.x = xs[i];
-    r.y = ys[i];
+    r.x = axis ? o : c;
+    r.y = axis ? c : o;
     r.idx = i;
     r.box = 0;
     out[k] = r;
+}
+
+// offsets of level 0
+__global__ void k_root_off(uint32_t* __restrict__ O, uint32_t n)
+{
+    O[0] = 0;
+    O[1] = n;
+}
+
+// offsets of half-level l+1/2 (H) and level l+1 (C) from level l (O), DESIGN R5:
+// a box of size s splits into x-halves (ceil(s/2), floor(s/2)), each into (ceil, floor).
+__global__ void k_child_off(const uint32_t* __restrict__ O, int64_t nb, uint32_t* __restrict__ H,
+                            uint32_t* __restrict__ C)
+{
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    uint32_t s = O[b], sz = O[b + 1] - s;
+    uint32_t h0 = sz - sz / 2, h1 = sz / 2;
+    H[2 * b] = s;
+    H[2 * b + 1] = s + h0;
+    C[4 * b] = s;
+    C[4 * b + 1] = s + (h0 - h0 / 2);
+    C[4 * b + 2] = s + h0;
+    C[4 * b + 3] = s + h0 + (h1 - h1 / 2);
+    if (b == nb - 1) {
+        H[2 * nb] = O[nb];
+        C[4 * nb] = O[nb];
+    }
 }
 
 // (coord, idx) < (coord', idx') on axis 0 = x, 1 = y  (DESIGN R6)
@@ -65,16 +104,22 @@ __device__ __forceinline__ bool rec_less(const Rec& a, const Rec& b, int axis)
     return (ca < cb) || (ca == cb && a.idx < b.idx);
 }
 
+// parent segment of position k: the record's (stale) id, refined by one split if needed
+__device__ __forceinline__ uint32_t parent_of(uint32_t box, int64_t k, const uint32_t* __restrict__ refine)
+{
+    return refine ? 2 * box + ((uint32_t)k >= refine[2 * box + 1] ? 1u : 0u) : box;
+}
+
 // Split step, part 1: flag = 1 if the record belongs to the high side of its parent
-// segment p (= rec.box).  The high side of p starts at sub_off[2p+1] in split_list.
+// segment p.  The high side of p starts at sub_off[2p+1] in split_list.
 __global__ void k_flag(const Rec* __restrict__ list, const Rec* __restrict__ split_list,
-                       const uint32_t* __restrict__ par_off, const uint32_t* __restrict__ sub_off,
-                       int axis, int64_t n, uint32_t* __restrict__ flag)
+                       const uint32_t* __restrict__ refine, const uint32_t* __restrict__ par_off,
+                       const uint32_t* __restrict__ sub_off, int axis, int64_t n, uint32_t* __restrict__ flag)
 {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     Rec r = list[k];
-    uint32_t p = r.box;
+    uint32_t p = parent_of(r.box, k, refine);
     uint32_t sp = sub_off[2 * p + 1];
     uint32_t f = 0;
     if (sp < par_off[p + 1]) {
@@ -84,30 +129,22 @@ __global__ void k_flag(const Rec* __restrict__ list, const Rec* __restrict__ spl
     flag[k] = f;
 }
 
-// Split step, part 2: stable scatter inside each parent segment; new box = 2p + side.
+// Split step, part 2: stable scatter inside each parent segment; new id = 2p + side.
 __global__ void k_scatter(const Rec* __restrict__ list, const uint32_t* __restrict__ flag,
-                          const uint32_t* __restrict__ pos, const uint32_t* __restrict__ par_off,
-                          const uint32_t* __restrict__ sub_off, int64_t n, Rec* __restrict__ out)
+                          const uint32_t* __restrict__ pos, const uint32_t* __restrict__ refine,
+                          const uint32_t* __restrict__ par_off, const uint32_t* __restrict__ sub_off, int64_t n,
+                          Rec* __restrict__ out)
 {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     Rec r = list[k];
-    uint32_t p = r.box;
+    uint32_t p = parent_of(r.box, k, refine);
     uint32_t s = par_off[p];
     uint32_t hi_before = pos[k] - pos[s];
     uint32_t f = flag[k];
     uint32_t dst = f ? sub_off[2 * p + 1] + hi_before : (uint32_t)k - hi_before;
     r.box = 2 * p + f;
     out[dst] = r;
-}
-
-// The list sorted along the split axis is already partitioned: just relabel.
-__global__ void k_relabel(Rec* __restrict__ list, const uint32_t* __restrict__ sub_off, int64_t n)
-{
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    uint32_t p = list[k].box;
-    list[k].box = 2 * p + ((uint32_t)k >= sub_off[2 * p + 1] ? 1u : 0u);
 }
 
 // A2 (part 1): tight bounding box from the segment endpoints of both sorted lists;
@@ -125,79 +162,75 @@ __global__ void k_bbox(const Rec* __restrict__ xl, const Rec* __restrict__ yl,
     r[b] = 0.0;
 }
 
-// Final order: perm and the leaf-ordered source rows {x, y, 0, 0}.
-__global__ void k_finish(const Rec* __restrict__ yl, int64_t n, uint32_t* __restrict__ perm,
-                         double4* __restrict__ src)
+// Final order + A2 (part 2) for every level in one pass.  The final y-list is the
+// leaf order (leaves ascending, (y, idx) inside, R13): write perm and the source
+// rows, then r(box) = exact max distance (correctly rounded sqrt, no FMA) for the
+// box of every level containing the point: a block-wide max when the whole block
+// lies in one box (upper levels), else a segmented warp max; one atomicMax on the
+// bit pattern per segment (non-negative doubles order like their uint64 bits).
+constexpr int FIN_T = 256;
+struct RadArgs {
+    const double* cx[FMM2D_MAXL + 1];
+    const double* cy[FMM2D_MAXL + 1];
+    double* r[FMM2D_MAXL + 1];
+};
+__global__ void __launch_bounds__(FIN_T) k_finish(const Rec* __restrict__ yl, int64_t n, int L,
+                                                  const uint32_t* __restrict__ offL, uint32_t* __restrict__ perm,
+                                                  double4* __restrict__ src, RadArgs A)
 {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    Rec r = yl[k];
-    perm[k] = r.idx;
-    src[k] = make_double4(r.x, r.y, 0.0, 0.0);
-}
-
-// A2 (part 2): r = exact max distance (correctly rounded sqrt, no FMA).  One warp per
-// (box, chunk of up to 32*ITEMS points); warp max, then atomicMax on the bit pattern
-// (non-negative doubles order like their uint64 bits).
-constexpr int RAD_ITEMS = 32;
-__global__ void k_radius(const double4* __restrict__ src, const uint32_t* __restrict__ off,
-                         int64_t nb, int chunks_per_box, const double* __restrict__ cx,
-                         const double* __restrict__ cy, double* __restrict__ r)
-{
-    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    int64_t b = w / chunks_per_box;
-    if (b >= nb) return;
-    int ch = (int)(w - b * chunks_per_box);
-    uint32_t s = off[b], e = off[b + 1];
-    uint32_t cs = s + (uint32_t)ch * (32 * RAD_ITEMS);
-    if (cs >= e) return;
-    uint32_t ce = min(e, cs + 32 * RAD_ITEMS);
-    double c0 = cx[b], c1 = cy[b];
-    double m = 0.0;
-    for (uint32_t k = cs + lane; k < ce; k += 32) {
-        double4 v = src[k];
-        m = fmax(m, rn_dist(v.x, v.y, c0, c1));
+    __shared__ uint32_t sleaf[FIN_T];
+    __shared__ double wmax[FIN_T / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t k0 = (int64_t)blockIdx.x * FIN_T;
+    const int64_t k = k0 + tid;
+    const int nvalid = (int)((n - k0) < FIN_T ? (n - k0) : FIN_T);
+    const bool valid = k < n;
+    double x = 0.0, y = 0.0;
+    uint32_t leaf = 0;
+    if (valid) {
+        Rec r = yl[k];
+        leaf = (L > 0) ? parent_of(r.box, k, offL) : 0u;
+        x = r.x;
+        y = r.y;
+        perm[k] = r.idx;
+        src[k] = make_double4(x, y, 0.0, 0.0);
     }
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0)
-        atomicMax((unsigned long long*)(r + b), (unsigned long long)__double_as_longlong(m));
+    sleaf[tid] = leaf;
+    __syncthreads();
+    const uint32_t lf0 = sleaf[0], lf1 = sleaf[nvalid - 1];
+    for (int l = L; l >= 0; --l) {
+        const int sh = 2 * (L - l);
+        const uint32_t box = leaf >> sh;
+        double d = 0.0;
+        if (valid) d = rn_dist(x, y, A.cx[l][box], A.cy[l][box]);
+        if ((lf0 >> sh) == (lf1 >> sh)) {                 // block-uniform (warp-uniform too)
+            for (int o = 16; o; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+            if (lane == 0) wmax[warp] = d;
+            __syncthreads();
+            if (tid == 0) {
+                double m = wmax[0];
+                for (int w = 1; w < FIN_T / 32; ++w) m = fmax(m, wmax[w]);
+                atomicMax((unsigned long long*)(A.r[l] + (lf0 >> sh)), (unsigned long long)__double_as_longlong(m));
+            }
+            __syncthreads();
+        } else {
+            // segmented max over lanes [lane, end of my box's run) (runs are contiguous)
+            for (int o = 1; o < 32; o <<= 1) {
+                const double dv = __shfl_down_sync(0xffffffffu, d, o);
+                const uint32_t bv = __shfl_down_sync(0xffffffffu, box, o);
+                const bool vv = __shfl_down_sync(0xffffffffu, valid ? 1 : 0, o) != 0;
+                if (lane + o < 32 && vv && bv == box) d = fmax(d, dv);
+            }
+            const uint32_t bprev = __shfl_up_sync(0xffffffffu, box, 1);
+            if (valid && (lane == 0 || bprev != box))
+                atomicMax((unsigned long long*)(A.r[l] + box), (unsigned long long)__double_as_longlong(d));
+        }
+    }
 }
 
 inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
 }  // namespace
-
-// Host: offsets of every level and half-level, a pure function of n (DESIGN R5):
-// a box of size s splits into x-halves (ceil(s/2), floor(s/2)), each half into
-// (ceil(h/2), floor(h/2)).
-static void host_offsets(int64_t n, int L, std::vector<std::vector<uint32_t>>& lev,
-                         std::vector<std::vector<uint32_t>>& half)
-{
-    lev.assign(L + 1, {});
-    half.assign(L, {});
-    lev[0] = {0u, (uint32_t)n};
-    for (int l = 0; l < L; ++l) {
-        const auto& o = lev[l];
-        int64_t nb = nboxes(l);
-        auto& h = half[l];
-        auto& c = lev[l + 1];
-        h.resize(2 * nb + 1);
-        c.resize(4 * nb + 1);
-        for (int64_t b = 0; b < nb; ++b) {
-            uint32_t s = o[b], sz = o[b + 1] - o[b];
-            uint32_t h0 = sz - sz / 2, h1 = sz / 2;
-            h[2 * b] = s;
-            h[2 * b + 1] = s + h0;
-            c[4 * b] = s;
-            c[4 * b + 1] = s + (h0 - h0 / 2);
-            c[4 * b + 2] = s + h0;
-            c[4 * b + 3] = s + h0 + (h1 - h1 / 2);
-        }
-        h[2 * nb] = (uint32_t)n;
-        c[4 * nb] = (uint32_t)n;
-    }
-}
 
 int build_tree(fmm2d_plan* P, const double2* z)
 {
@@ -206,30 +239,23 @@ int build_tree(fmm2d_plan* P, const double2* z)
     cudaStream_t st = P->stream;
     const int BS = 256;
 
-    // ---- offsets (host) -> device: level l at obase[l]; half-levels after them
-    std::vector<std::vector<uint32_t>> lev, half;
-    host_offsets(n, L, lev, half);
+    // ---- offsets: level l at obase[l] (4^l + 1), half-level l+1/2 at hbase[l] (2 4^l + 1)
     P->obase.assign(L + 1, 0);
     std::vector<int64_t> hbase(L, 0);
     int64_t tot = 0;
-    for (int l = 0; l <= L; ++l) { P->obase[l] = tot; tot += (int64_t)lev[l].size(); }
-    for (int l = 0; l < L; ++l) { hbase[l] = tot; tot += (int64_t)half[l].size(); }
-    P->h_boff.resize(tot);
-    for (int l = 0; l <= L; ++l) std::copy(lev[l].begin(), lev[l].end(), P->h_boff.begin() + P->obase[l]);
-    for (int l = 0; l < L; ++l) std::copy(half[l].begin(), half[l].end(), P->h_boff.begin() + hbase[l]);
+    for (int l = 0; l <= L; ++l) { P->obase[l] = tot; tot += nboxes(l) + 1; }
+    for (int l = 0; l < L; ++l) { hbase[l] = tot; tot += 2 * nboxes(l) + 1; }
     FMM2D_TRY(dev_alloc(P, (void**)&P->boff, sizeof(uint32_t) * tot));
-    FMM2D_CUDA_TRY(cudaMemcpyAsync(P->boff, P->h_boff.data(), sizeof(uint32_t) * tot,
-                                   cudaMemcpyHostToDevice, st));
-    {
-        uint32_t mn = UINT32_MAX, mx = 0;
-        const auto& o = lev[L];
-        for (size_t b = 0; b + 1 < o.size(); ++b) {
-            mn = std::min(mn, o[b + 1] - o[b]);
-            mx = std::max(mx, o[b + 1] - o[b]);
-        }
-        P->stats.min_leaf = (int)mn;
-        P->stats.max_leaf = (int)mx;
+    k_root_off<<<1, 1, 0, st>>>(P->boff + P->obase[0], (uint32_t)n);
+    fmm2d::note_launch();
+    for (int l = 0; l < L; ++l) {
+        k_child_off<<<grid_for(nboxes(l), BS), BS, 0, st>>>(P->boff + P->obase[l], nboxes(l), P->boff + hbase[l],
+                                                           P->boff + P->obase[l + 1]);
+        fmm2d::note_launch();
     }
+    // leaf sizes are floor(n / 4^L) or ceil(n / 4^L) (DESIGN R5)
+    P->stats.min_leaf = (int)(n / nboxes(L));
+    P->stats.max_leaf = (int)((n + nboxes(L) - 1) / nboxes(L));
 
     // ---- scratch
     double *xs, *ys;
@@ -275,7 +301,8 @@ int build_tree(fmm2d_plan* P, const double2* z)
 
     auto body = [&]() -> int {
         FMM2D_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
-        k_canon<<<grid_for(n, BS), BS, 0, st>>>(z, n, xs, ys, kx, ky, iota, bad); fmm2d::note_launch();
+        k_canon<<<grid_for(n, BS), BS, 0, st>>>(z, n, xs, ys, kx, ky, iota, bad);
+        fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
         int h_bad = 0;
         FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -284,51 +311,53 @@ int build_tree(fmm2d_plan* P, const double2* z)
         // presort (stable LSD radix: ties stay in index order)
         size_t sb = cub_bytes;
         FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, kx, ksort, iota, ord, (int)n, 0, 64, st));
-        k_make_recs<<<grid_for(n, BS), BS, 0, st>>>(ord, xs, ys, n, xl); fmm2d::note_launch();
+        k_make_recs<<<grid_for(n, BS), BS, 0, st>>>(ksort, ord, ys, 0, n, xl);
+        fmm2d::note_launch();
         sb = cub_bytes;
         FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, ky, ksort, iota, ord, (int)n, 0, 64, st));
-        k_make_recs<<<grid_for(n, BS), BS, 0, st>>>(ord, xs, ys, n, yl); fmm2d::note_launch();
+        k_make_recs<<<grid_for(n, BS), BS, 0, st>>>(ksort, ord, xs, 1, n, yl);
+        fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
-        // level 0 bbox
         k_bbox<<<1, 32, 0, st>>>(xl, yl, P->boff + P->obase[0], 1, P->cx + P->base[0], P->cy + P->base[0],
-                                 P->r + P->base[0]); fmm2d::note_launch();
+                                 P->r + P->base[0]);
+        fmm2d::note_launch();
         for (int l = 0; l < L; ++l) {
             const uint32_t* O = P->boff + P->obase[l];
             const uint32_t* H = P->boff + hbase[l];
             const uint32_t* C = P->boff + P->obase[l + 1];
-            // x-split: y-list partitioned by (x, idx) against the x-list's first high record
-            k_flag<<<grid_for(n, BS), BS, 0, st>>>(yl, xl, O, H, 0, n, flag); fmm2d::note_launch();
+            // x-split: the y-list (ids: half-level l-1/2, refined by O) is partitioned by
+            // (x, idx) against the x-list's first high record
+            const uint32_t* yref = (l == 0) ? nullptr : O;
+            k_flag<<<grid_for(n, BS), BS, 0, st>>>(yl, xl, yref, O, H, 0, n, flag);
+            fmm2d::note_launch();
             sb = cub_bytes;
             FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, flag, pos, (int)n, st));
-            k_scatter<<<grid_for(n, BS), BS, 0, st>>>(yl, flag, pos, O, H, n, tmp); fmm2d::note_launch();
+            k_scatter<<<grid_for(n, BS), BS, 0, st>>>(yl, flag, pos, yref, O, H, n, tmp);
+            fmm2d::note_launch();
             std::swap(yl, tmp);
-            k_relabel<<<grid_for(n, BS), BS, 0, st>>>(xl, H, n); fmm2d::note_launch();
-            // y-split of each half: x-list partitioned by (y, idx) against the y-list
-            k_flag<<<grid_for(n, BS), BS, 0, st>>>(xl, yl, H, C, 1, n, flag); fmm2d::note_launch();
+            // y-split of each half: the x-list (ids: level l, refined by H) is partitioned
+            // by (y, idx) against the y-list's first high record
+            k_flag<<<grid_for(n, BS), BS, 0, st>>>(xl, yl, H, H, C, 1, n, flag);
+            fmm2d::note_launch();
             sb = cub_bytes;
             FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, flag, pos, (int)n, st));
-            k_scatter<<<grid_for(n, BS), BS, 0, st>>>(xl, flag, pos, H, C, n, tmp); fmm2d::note_launch();
+            k_scatter<<<grid_for(n, BS), BS, 0, st>>>(xl, flag, pos, H, H, C, n, tmp);
+            fmm2d::note_launch();
             std::swap(xl, tmp);
-            k_relabel<<<grid_for(n, BS), BS, 0, st>>>(yl, C, n); fmm2d::note_launch();
             int64_t nb = nboxes(l + 1);
-            k_bbox<<<grid_for(nb, BS), BS, 0, st>>>(xl, yl, C, nb, P->cx + P->base[l + 1],
-                                                    P->cy + P->base[l + 1], P->r + P->base[l + 1]); fmm2d::note_launch();
+            k_bbox<<<grid_for(nb, BS), BS, 0, st>>>(xl, yl, C, nb, P->cx + P->base[l + 1], P->cy + P->base[l + 1],
+                                                    P->r + P->base[l + 1]);
+            fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
         }
-        // leaf order = the final y-list (leaves in index order, (y, idx) inside, R13)
-        k_finish<<<grid_for(n, BS), BS, 0, st>>>(yl, n, P->perm, P->src); fmm2d::note_launch();
+        RadArgs A;
         for (int l = 0; l <= L; ++l) {
-            int64_t nb = nboxes(l);
-            uint32_t maxsz = 0;
-            const auto& o = lev[l];
-            for (int64_t b = 0; b < std::min<int64_t>(nb, 2); ++b) maxsz = std::max(maxsz, o[b + 1] - o[b]);
-            maxsz = (uint32_t)((n + nb - 1) / nb);
-            int cpb = (int)((maxsz + 32 * RAD_ITEMS - 1) / (32 * RAD_ITEMS));
-            int64_t warps = nb * cpb;
-            k_radius<<<grid_for(warps * 32, BS), BS, 0, st>>>(P->src, P->boff + P->obase[l], nb, cpb,
-                                                              P->cx + P->base[l], P->cy + P->base[l],
-                                                              P->r + P->base[l]); fmm2d::note_launch();
+            A.cx[l] = P->cx + P->base[l];
+            A.cy[l] = P->cy + P->base[l];
+            A.r[l] = P->r + P->base[l];
         }
+        k_finish<<<grid_for(n, FIN_T), FIN_T, 0, st>>>(yl, n, L, P->boff + P->obase[L], P->perm, P->src, A);
+        fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
         return 0;
     };

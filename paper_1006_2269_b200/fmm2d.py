@@ -19,7 +19,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfmm2d.so")
+# FMM2D_LIB selects an alternative build of the same library (tuning experiments only)
+LIB_PATH = os.environ.get("FMM2D_LIB") or os.path.join(_HERE, "libfmm2d.so")
 
 PMAX = 32
 HOST_PTRS = 0x1

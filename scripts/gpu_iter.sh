@@ -1,0 +1,10 @@
+# tests + bench + ncu capture of k_near on a 4M-point instance
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log | cut -c1-1200
+SMALL="python bench.py --n 4000000 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+$SMALL > gpurun_out/plain_small.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:'k_near' -s 1 -c 1 \
+    --metrics sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum \
+    -o gpurun_out/prof_iter $SMALL > gpurun_out/ncu_full.log 2>&1
+tail -1 gpurun_out/ncu_full.log

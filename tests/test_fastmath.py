@@ -1,0 +1,21 @@
+"""Accuracy of the product's table-driven FP64 log|z| and Arg z (fastmath.cuh), built
+for the host and compared with long double over 4e6 random arguments spanning 2^+-60
+and the axes / diagonal.  (The device build differs only in the MUFU reciprocal
+estimate, which one cubic Newton step makes irrelevant; GPU parity tests cover it.)"""
+import json
+import os
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_fastmath_ulps(tmp_path):
+    exe = tmp_path / "test_fastmath"
+    subprocess.check_call(["g++", "-O2", "-ffp-contract=off", "-o", str(exe),
+                           os.path.join(ROOT, "tools", "test_fastmath.cpp")])
+    r = json.loads(subprocess.check_output([str(exe)]).decode())
+    assert r["n"] > 3_000_000
+    assert r["log_max_ulp"] <= 2.0
+    assert r["log_max_abs"] <= 1e-14          # |log|dz|| up to ~42 here: < 1 ulp
+    assert r["arg_max_ulp"] <= 2.0
+    assert r["log0_is_neg_inf"] == 1 and r["arg_pi"] == 1 and r["arg_zero"] == 1
