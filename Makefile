@@ -10,7 +10,7 @@ ORACLE    := oracle/liboracle_fmm2d.so
 
 all: $(LIB) $(ORACLE)
 
-build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/fmm2d_internal.cuh include/fmm2d.h
+build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh) include/fmm2d.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 

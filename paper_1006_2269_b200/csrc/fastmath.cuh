@@ -139,13 +139,12 @@ FM_HD double log_pos(double r2, const double2* __restrict__ tab)
 FM_HD double arg(double dx, double dy, const double2* __restrict__ tab)
 {
     const int64_t bx = as_bits(dx), by = as_bits(dy);
-    const int64_t bax = bx & 0x7FFFFFFFFFFFFFFFll, bay = by & 0x7FFFFFFFFFFFFFFFll;
-    const double ax = from_bits(bax);
-    const double ay = from_bits(bay);
-    const bool swap = bay > bax;          // non-negative doubles order like their bits (ALU, not FP64)
-    const double mn = swap ? ax : ay;
-    const double mx = swap ? ay : ax;
-    const double q0 = mn * rcp_approx(mx);
+    const bool swap = fabs(dy) > fabs(dx);    // one DSETP with |.| operand modifiers
+    // select the signed values; |.| is applied as an operand modifier by the consumers
+    const double mns = swap ? dx : dy;
+    const double mxs = swap ? dy : dx;
+    const double mn = fabs(mns), mx = fabs(mxs);
+    const double q0 = fabs(mns * rcp_approx(mxs));
     // round q0 to a multiple of 2^-8 with the 1.5*2^44 magic number; j = the rounded q0 * 256
     const double y = q0 + kC[15];
     const int jr = (int)as_bits(y) & (2 * ATAN_N - 1);   // 0..256 (any value for mx == 0)

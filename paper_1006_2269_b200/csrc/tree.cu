@@ -110,41 +110,105 @@ __device__ __forceinline__ uint32_t parent_of(uint32_t box, int64_t k, const uin
     return refine ? 2 * box + ((uint32_t)k >= refine[2 * box + 1] ? 1u : 0u) : box;
 }
 
-// Split step, part 1: flag = 1 if the record belongs to the high side of its parent
-// segment p.  The high side of p starts at sub_off[2p+1] in split_list.
-__global__ void k_flag(const Rec* __restrict__ list, const Rec* __restrict__ split_list,
-                       const uint32_t* __restrict__ refine, const uint32_t* __restrict__ par_off,
-                       const uint32_t* __restrict__ sub_off, int axis, int64_t n, uint32_t* __restrict__ flag)
+// Per parent segment p: number of high-side records (the split rule fixes it).
+__global__ void k_high_sizes(const uint32_t* __restrict__ par_off, const uint32_t* __restrict__ sub_off,
+                             int64_t np, uint32_t* __restrict__ hs)
 {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    Rec r = list[k];
-    uint32_t p = parent_of(r.box, k, refine);
-    uint32_t sp = sub_off[2 * p + 1];
-    uint32_t f = 0;
-    if (sp < par_off[p + 1]) {
-        Rec s = split_list[sp];
-        f = rec_less(r, s, axis) ? 0u : 1u;
-    }
-    flag[k] = f;
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < np) hs[p] = par_off[p + 1] - sub_off[2 * p + 1];
 }
 
-// Split step, part 2: stable scatter inside each parent segment; new id = 2p + side.
-__global__ void k_scatter(const Rec* __restrict__ list, const uint32_t* __restrict__ flag,
-                          const uint32_t* __restrict__ pos, const uint32_t* __restrict__ refine,
-                          const uint32_t* __restrict__ par_off, const uint32_t* __restrict__ sub_off, int64_t n,
-                          Rec* __restrict__ out)
+// One split step in a single pass (replaces flag -> device scan -> scatter):
+//   flag  = record is on the high side of its parent segment p, i.e.
+//           (coord, idx) >= the first high record split_list[sub_off[2p+1]];
+//   G(k)  = number of high records before position k over the whole list, from a
+//           block scan + decoupled look-back across tiles (tile ids taken in launch
+//           order from a counter, so predecessors always make progress);
+//   dst   = stable position inside p: high -> sub_off[2p+1] + (G(k) - Gp[p]),
+//           low -> k - (G(k) - Gp[p]), where Gp[p] = high records before segment p
+//           (exclusive scan of k_high_sizes, a function of the offsets only).
+constexpr int PT = 256, PI = 4, PTILE = PT * PI;
+constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_MASK = 3ull << 62;
+
+__global__ void __launch_bounds__(PT) k_partition(const Rec* __restrict__ list, const Rec* __restrict__ split_list,
+                                                  const uint32_t* __restrict__ refine,
+                                                  const uint32_t* __restrict__ par_off,
+                                                  const uint32_t* __restrict__ sub_off,
+                                                  const uint32_t* __restrict__ Gp, int axis, int64_t n,
+                                                  Rec* __restrict__ out, unsigned long long* __restrict__ tstate,
+                                                  unsigned int* __restrict__ ticket)
 {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    Rec r = list[k];
-    uint32_t p = parent_of(r.box, k, refine);
-    uint32_t s = par_off[p];
-    uint32_t hi_before = pos[k] - pos[s];
-    uint32_t f = flag[k];
-    uint32_t dst = f ? sub_off[2 * p + 1] + hi_before : (uint32_t)k - hi_before;
-    r.box = 2 * p + f;
-    out[dst] = r;
+    typedef cub::BlockScan<uint32_t, PT> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ uint32_t s_tile, s_prefix;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t k0 = (int64_t)tile * PTILE + (int64_t)tid * PI;
+    Rec r[PI];
+    uint32_t par[PI], f[PI];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int u = 0; u < PI; ++u) {
+        const int64_t k = k0 + u;
+        f[u] = 0;
+        par[u] = 0;
+        if (k < n) {
+            r[u] = list[k];
+            const uint32_t p = parent_of(r[u].box, k, refine);
+            par[u] = p;
+            const uint32_t sp = sub_off[2 * p + 1];
+            if (sp < par_off[p + 1]) f[u] = rec_less(r[u], split_list[sp], axis) ? 0u : 1u;
+        }
+        cnt += f[u];
+    }
+    uint32_t excl, agg;
+    Scan(scan_tmp).ExclusiveSum(cnt, excl, agg);
+    // decoupled look-back (warp 0)
+    if (tid < 32) {
+        uint32_t prefix = 0;
+        if (tile == 0) {
+            if (tid == 0) atomicExch(&tstate[0], ST_PRE | agg);
+        } else {
+            if (tid == 0) atomicExch(&tstate[tile], ST_AGG | agg);
+            int64_t j = (int64_t)tile - 1 - tid;
+            for (;;) {
+                unsigned long long s = 0;
+                if (j >= 0) {
+                    do {
+                        s = *((volatile unsigned long long*)&tstate[j]);
+                    } while ((s & ST_MASK) == 0);
+                } else {
+                    s = ST_PRE;                     // before tile 0: inclusive prefix 0
+                }
+                const unsigned pre = __ballot_sync(0xffffffffu, (s & ST_MASK) == ST_PRE);
+                const int first = pre ? __ffs(pre) - 1 : 32;    // nearest tile with a prefix
+                uint32_t v = (tid <= first) ? (uint32_t)(s & ~ST_MASK) : 0u;
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                prefix += v;
+                if (pre) break;
+                j -= 32;
+            }
+            if (tid == 0) atomicExch(&tstate[tile], ST_PRE | (prefix + agg));
+        }
+        if (tid == 0) s_prefix = prefix;
+    }
+    __syncthreads();
+    uint32_t g = s_prefix + excl;             // G(k) for the first item of this thread
+#pragma unroll
+    for (int u = 0; u < PI; ++u) {
+        const int64_t k = k0 + u;
+        if (k < n) {
+            const uint32_t p = par[u];
+            const uint32_t hb = g - Gp[p];    // highs before k inside p
+            const uint32_t dst = f[u] ? sub_off[2 * p + 1] + hb : (uint32_t)k - hb;
+            Rec o = r[u];
+            o.box = 2 * p + f[u];
+            out[dst] = o;
+        }
+        g += f[u];
+    }
 }
 
 // A2 (part 1): tight bounding box from the segment endpoints of both sorted lists;
@@ -260,14 +324,18 @@ int build_tree(fmm2d_plan* P, const double2* z)
     // ---- scratch
     double *xs, *ys;
     uint64_t *kx, *ky, *ksort;
-    uint32_t *iota, *ord, *flag, *pos;
+    uint32_t *iota, *ord, *hs, *Gp;
     Rec *xl, *yl, *tmp;
     int* bad;
+    unsigned long long* tstate;
+    unsigned int* ticket;
     void* scratch = nullptr;
     size_t sort_bytes = 0, scan_bytes = 0;
+    const int64_t npmax = (L > 0) ? 2 * nboxes(L - 1) : 1;        // parents of the widest step
+    const int64_t ntiles = (n + PTILE - 1) / PTILE;
     cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr,
                                     (uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 64, st);
-    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)npmax, st);
     size_t cub_bytes = std::max(sort_bytes, scan_bytes);
     std::vector<void*> tmp_ptrs;
     auto talloc = [&](void** p, size_t b) -> int {
@@ -289,8 +357,10 @@ int build_tree(fmm2d_plan* P, const double2* z)
         if ((rc = talloc((void**)&ksort, 8 * n))) break;
         if ((rc = talloc((void**)&iota, 4 * n))) break;
         if ((rc = talloc((void**)&ord, 4 * n))) break;
-        if ((rc = talloc((void**)&flag, 4 * n))) break;
-        if ((rc = talloc((void**)&pos, 4 * n))) break;
+        if ((rc = talloc((void**)&hs, 4 * npmax))) break;
+        if ((rc = talloc((void**)&Gp, 4 * npmax))) break;
+        if ((rc = talloc((void**)&tstate, 8 * ntiles))) break;
+        if ((rc = talloc((void**)&ticket, 4))) break;
         if ((rc = talloc((void**)&xl, sizeof(Rec) * n))) break;
         if ((rc = talloc((void**)&yl, sizeof(Rec) * n))) break;
         if ((rc = talloc((void**)&tmp, sizeof(Rec) * n))) break;
@@ -321,6 +391,22 @@ int build_tree(fmm2d_plan* P, const double2* z)
         k_bbox<<<1, 32, 0, st>>>(xl, yl, P->boff + P->obase[0], 1, P->cx + P->base[0], P->cy + P->base[0],
                                  P->r + P->base[0]);
         fmm2d::note_launch();
+        // one split step: partition `list` inside the parent segments (par_off) into the
+        // sub-segments sub_off, comparing against `split` on `axis`
+        auto split_step = [&](const Rec* list, const Rec* split, const uint32_t* refine, const uint32_t* par_off,
+                              const uint32_t* sub_off, int64_t np, int axis, Rec* out) -> int {
+            k_high_sizes<<<grid_for(np, BS), BS, 0, st>>>(par_off, sub_off, np, hs);
+            fmm2d::note_launch();
+            size_t b2 = cub_bytes;
+            FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, b2, hs, Gp, (int)np, st));
+            FMM2D_CUDA_TRY(cudaMemsetAsync(tstate, 0, 8 * ntiles, st));
+            FMM2D_CUDA_TRY(cudaMemsetAsync(ticket, 0, 4, st));
+            k_partition<<<(unsigned)ntiles, PT, 0, st>>>(list, split, refine, par_off, sub_off, Gp, axis, n, out,
+                                                        tstate, ticket);
+            fmm2d::note_launch();
+            FMM2D_CUDA_TRY(cudaGetLastError());
+            return 0;
+        };
         for (int l = 0; l < L; ++l) {
             const uint32_t* O = P->boff + P->obase[l];
             const uint32_t* H = P->boff + hbase[l];
@@ -328,21 +414,11 @@ int build_tree(fmm2d_plan* P, const double2* z)
             // x-split: the y-list (ids: half-level l-1/2, refined by O) is partitioned by
             // (x, idx) against the x-list's first high record
             const uint32_t* yref = (l == 0) ? nullptr : O;
-            k_flag<<<grid_for(n, BS), BS, 0, st>>>(yl, xl, yref, O, H, 0, n, flag);
-            fmm2d::note_launch();
-            sb = cub_bytes;
-            FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, flag, pos, (int)n, st));
-            k_scatter<<<grid_for(n, BS), BS, 0, st>>>(yl, flag, pos, yref, O, H, n, tmp);
-            fmm2d::note_launch();
+            FMM2D_TRY(split_step(yl, xl, yref, O, H, nboxes(l), 0, tmp));
             std::swap(yl, tmp);
             // y-split of each half: the x-list (ids: level l, refined by H) is partitioned
             // by (y, idx) against the y-list's first high record
-            k_flag<<<grid_for(n, BS), BS, 0, st>>>(xl, yl, H, H, C, 1, n, flag);
-            fmm2d::note_launch();
-            sb = cub_bytes;
-            FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, flag, pos, (int)n, st));
-            k_scatter<<<grid_for(n, BS), BS, 0, st>>>(xl, flag, pos, H, H, C, n, tmp);
-            fmm2d::note_launch();
+            FMM2D_TRY(split_step(xl, yl, H, H, C, 2 * nboxes(l), 1, tmp));
             std::swap(xl, tmp);
             int64_t nb = nboxes(l + 1);
             k_bbox<<<grid_for(nb, BS), BS, 0, st>>>(xl, yl, C, nb, P->cx + P->base[l + 1], P->cy + P->base[l + 1],
