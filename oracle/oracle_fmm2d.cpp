@@ -48,7 +48,8 @@ int oracle_direct(const double* z, const double* m, int64_t n,
 {
     if (n < 1) return -1;
     int64_t nt = targets ? ntargets : n;
-#pragma omp parallel for schedule(dynamic, 16)
+    /* one target per work item: sampled direct sums have few targets and long rows */
+#pragma omp parallel for schedule(dynamic, 1)
     for (int64_t t = 0; t < nt; ++t) {
         int64_t i = targets ? targets[t] : t;
         cplxl s(0.0L, 0.0L), ds(0.0L, 0.0L);

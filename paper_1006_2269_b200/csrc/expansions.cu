@@ -186,15 +186,17 @@ __device__ __forceinline__ void m2l_target(const M2LArgs& A, int64_t g, int lev)
                 beta.x = fma(c, al[k].x, beta.x);
                 beta.y = fma(c, al[k].y, beta.y);
             }
+            double2 v;
             if (l == 0) {
                 // a_0 Log(c_t - c_s), componentwise difference (DESIGN R2)
                 const double tx = ctx - csx, ty = cty - csy;
                 const double2 lg = make_double2(0.5 * log(r2), atan2(ty, tx));
-                acc[0] = cadd(acc[0], cadd(cmul(a0, lg), beta));
+                v = cadd(cmul(a0, lg), beta);
             } else {
                 const double2 t = csub(beta, cscale(a0, 1.0 / l));
-                acc[l - L0] = cadd(acc[l - L0], cmul(t, izl));
+                v = cmul(t, izl);
             }
+            acc[l - L0] = cadd(acc[l - L0], v);
         }
     }
     double2* out = A.local + g * (P + 1);
@@ -202,9 +204,16 @@ __device__ __forceinline__ void m2l_target(const M2LArgs& A, int64_t g, int lev)
     for (int l = L0; l < L1; ++l) out[l] = acc[l - L0];
 }
 
+#ifndef FMM2D_M2L_MINB
+#define FMM2D_M2L_MINB 2
+#endif
+constexpr int M2L_T = 128;
+
 // threads: NS consecutive warps share 32 target boxes; warp-uniform part index.
+// (Tried and measured slower at p = 17 on B200: accumulators in shared memory, and a
+// k-outer contraction with beta in registers.)
 template <int P, int NS>
-__global__ void __launch_bounds__(128) k_m2l(M2LArgs A, int64_t g0, int64_t g1)
+__global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l(M2LArgs A, int64_t g0, int64_t g1)
 {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int lane = threadIdx.x & 31;
@@ -306,7 +315,7 @@ int m2l_p(fmm2d_plan* Pl)
     constexpr int NS = m2l_split<P>();
     int64_t g0 = Pl->base[1], g1 = Pl->base[L + 1];
     int64_t nthreads = ((g1 - g0 + 31) / 32) * 32 * NS;
-    k_m2l<P, NS><<<grid_for(nthreads, 128), 128, 0, st>>>(A, g0, g1); fmm2d::note_launch();
+    k_m2l<P, NS><<<grid_for(nthreads, M2L_T), M2L_T, 0, st>>>(A, g0, g1); fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -108,10 +108,12 @@ int64_t launch_count();
 
 void fmm2d_set_last_cuda_error(cudaError_t e, const char* what, const char* file, int line);
 
-// IEEE round-to-nearest helpers with no FMA contraction (DESIGN R11)
-__device__ __forceinline__ double rn_dist(double x, double y, double cx, double cy)
+// IEEE round-to-nearest helpers with no FMA contraction (DESIGN R11).  The squared
+// distance is what the radius pass maximises: sqrt_rn is monotone, so
+// sqrt_rn(max d^2) == max sqrt_rn(d^2) bit for bit (the oracle's order).
+__device__ __forceinline__ double rn_dist2(double x, double y, double cx, double cy)
 {
     double dx = __dsub_rn(x, cx);
     double dy = __dsub_rn(y, cy);
-    return __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+    return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
 }

@@ -141,11 +141,23 @@ __global__ void __launch_bounds__(PT) k_partition(const Rec* __restrict__ list, 
     typedef cub::BlockScan<uint32_t, PT> Scan;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ uint32_t s_tile, s_prefix;
+    __shared__ __align__(16) Rec stage[PTILE];
     const int tid = threadIdx.x;
     if (tid == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
     const int64_t k0 = (int64_t)tile * PTILE + (int64_t)tid * PI;
+    // stage the tile through shared memory with coalesced 16-byte loads (all independent)
+    const int64_t kt = (int64_t)tile * PTILE;
+    const int nrec = (int)((n - kt) < PTILE ? (n - kt) : PTILE);
+    {
+        const uint4* g = reinterpret_cast<const uint4*>(list + kt);
+        uint4* s = reinterpret_cast<uint4*>(stage);
+        const int nvec = (nrec * (int)sizeof(Rec)) / 16;            // whole vectors
+        for (int v = tid; v < nvec; v += PT) s[v] = g[v];
+        if (tid == 0 && (nrec * (int)sizeof(Rec)) % 16) stage[nrec - 1] = list[kt + nrec - 1];
+    }
+    __syncthreads();
     Rec r[PI];
     uint32_t par[PI], f[PI];
     uint32_t cnt = 0;
@@ -155,7 +167,7 @@ __global__ void __launch_bounds__(PT) k_partition(const Rec* __restrict__ list, 
         f[u] = 0;
         par[u] = 0;
         if (k < n) {
-            r[u] = list[k];
+            r[u] = stage[tid * PI + u];
             const uint32_t p = parent_of(r[u].box, k, refine);
             par[u] = p;
             const uint32_t sp = sub_off[2 * p + 1];
@@ -266,7 +278,7 @@ __global__ void __launch_bounds__(FIN_T) k_finish(const Rec* __restrict__ yl, in
         const int sh = 2 * (L - l);
         const uint32_t box = leaf >> sh;
         double d = 0.0;
-        if (valid) d = rn_dist(x, y, A.cx[l][box], A.cy[l][box]);
+        if (valid) d = rn_dist2(x, y, A.cx[l][box], A.cy[l][box]);     // squared; sqrt below
         if ((lf0 >> sh) == (lf1 >> sh)) {                 // block-uniform (warp-uniform too)
             for (int o = 16; o; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
             if (lane == 0) wmax[warp] = d;
@@ -290,6 +302,13 @@ __global__ void __launch_bounds__(FIN_T) k_finish(const Rec* __restrict__ yl, in
                 atomicMax((unsigned long long*)(A.r[l] + box), (unsigned long long)__double_as_longlong(d));
         }
     }
+}
+
+// r = sqrt_rn(max squared distance), every box of every level
+__global__ void k_sqrt(double* __restrict__ r, int64_t nb)
+{
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nb) r[b] = __dsqrt_rn(r[b]);
 }
 
 inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
@@ -433,6 +452,8 @@ int build_tree(fmm2d_plan* P, const double2* z)
             A.r[l] = P->r + P->base[l];
         }
         k_finish<<<grid_for(n, FIN_T), FIN_T, 0, st>>>(yl, n, L, P->boff + P->obase[L], P->perm, P->src, A);
+        fmm2d::note_launch();
+        k_sqrt<<<grid_for(P->nbox_total, BS), BS, 0, st>>>(P->r, P->nbox_total);
         fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
         return 0;
