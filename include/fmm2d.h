@@ -55,6 +55,11 @@ extern "C" {
 /* opt.flags */
 #define FMM2D_HOST_PTRS       0x1  /* z, m, phi, dphi are host pointers               */
 #define FMM2D_REAL_STRENGTHS  0x2  /* caller promises Im m_j == 0 (kernel may skip it) */
+#define FMM2D_SYMMETRIC_P2P   0x4  /* evaluate each unordered pair of distinct near leaves
+                                      once, feeding both directions (same results up to
+                                      rounding; needs a slot buffer; leaves <= 64 points).
+                                      Default: every ordered pair separately (measured
+                                      faster on B200)            */
 
 typedef struct fmm2d_plan fmm2d_plan;   /* opaque; owns all device memory */
 

@@ -164,6 +164,7 @@ int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan
         if (rc) return rc;
         FMM2D_CUDA_TRY(cudaEventRecord(e1, P->stream));
         FMM2D_TRY(build_lists(P));
+        FMM2D_TRY(prepare_near_sym(P));
         FMM2D_CUDA_TRY(cudaEventRecord(e2, P->stream));
         FMM2D_CUDA_TRY(cudaEventSynchronize(e2));
         float a = 0, b = 0;

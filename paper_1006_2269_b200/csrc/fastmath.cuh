@@ -135,6 +135,16 @@ FM_HD double log_pos(double r2, const double2* __restrict__ tab)
     return (r2 == 0.0) ? -HUGE_VAL : r;
 }
 
+// a = atan(mn/mx) in [0, pi/4] placed in its octant: (swap, neg) -> a, pi/2 - a, pi - a,
+// pi/2 + a == base +- a (one rounding), then the sign bit (dy = +0 keeps 0 / pi).
+FM_HD double octant_fix(double a, bool swap, bool neg, int64_t signbit)
+{
+    const double base = swap ? kC[10] : (neg ? kC[12] : 0.0);
+    const double sa = from_bits(as_bits(a) ^ ((int64_t)(swap != neg) << 63));
+    const double res = base + sa;                           // >= 0
+    return from_bits(as_bits(res) | signbit);
+}
+
 // principal Arg(dx + i dy) = atan2(dy, dx) in (-pi, pi]; dy = +0 gives 0 or pi.
 FM_HD double arg(double dx, double dy, const double2* __restrict__ tab)
 {
@@ -159,13 +169,34 @@ FM_HD double arg(double dx, double dy, const double2* __restrict__ tab)
     const double at = fma_(p * t2, t, t);
     const double2 T = tab[j];
     const double a = T.x + (at + T.y);                    // atan(mn/mx) in [0, pi/4]
-    // octant: (swap, dx<0) -> a, pi/2 - a, pi - a, pi/2 + a  ==  base +- a (one rounding)
-    const bool neg = bx < 0;
-    const double base = swap ? kC[10] : (neg ? kC[12] : 0.0);
-    const double sa = from_bits(as_bits(a) ^ ((int64_t)(swap != neg) << 63));
-    const double res = base + sa;                           // >= 0
-    // copy the sign of dy (dy = +0 keeps 0 / pi)
-    return from_bits(as_bits(res) | (by & (int64_t)0x8000000000000000ull));
+    return octant_fix(a, swap, bx < 0, by & (int64_t)0x8000000000000000ull);
+}
+
+// Arg(dz) and Arg(-dz), the latter of the componentwise difference z_j - z_i (zeros stay
+// +0, DESIGN R2): the same reduced angle, mirrored octant (-dx < 0 iff dx > 0) and sign
+// (-dy < 0 iff dy > 0).  Used by the symmetric near-field kernel.
+FM_HD void arg_pair(double dx, double dy, const double2* __restrict__ tab, double& th, double& thn)
+{
+    const int64_t bx = as_bits(dx), by = as_bits(dy);
+    const bool swap = fabs(dy) > fabs(dx);
+    const double mns = swap ? dx : dy;
+    const double mxs = swap ? dy : dx;
+    const double mn = fabs(mns), mx = fabs(mxs);
+    const double q0 = fabs(mns * rcp_approx(mxs));
+    const double y = q0 + kC[15];
+    const int jr = (int)as_bits(y) & (2 * ATAN_N - 1);
+    const int j = jr < ATAN_N ? jr : ATAN_N;
+    const double c = y - kC[15];
+    const double num = fma_(-c, mx, mn);
+    const double den = fma_(c, mn, mx);
+    const double t = num * rcp(den);
+    const double t2 = t * t;
+    const double p = fma_(kC[6], t2, kC[7]);
+    const double at = fma_(p * t2, t, t);
+    const double2 T = tab[j];
+    const double a = T.x + (at + T.y);
+    th = octant_fix(a, swap, bx < 0, by & (int64_t)0x8000000000000000ull);
+    thn = octant_fix(a, swap, bx > 0, by > 0 ? (int64_t)0x8000000000000000ull : 0);
 }
 
 // host: fill the tables (long double evaluation, rounded once to double)

@@ -65,6 +65,14 @@ struct fmm2d_plan {
     double2* phistage = nullptr;
     double2* dphistage = nullptr;
     const void* tables = nullptr;       // fastmath tables (device, shared per device)
+    // symmetric near field (near.cu): each unordered leaf pair evaluated once
+    bool sym = false;
+    int sym_tile = 0, sym_npass = 0, sym_rows = 0, slot_w = 0;
+    uint32_t* sym_mirror = nullptr;     // [strong leaf entries] position of t in row s
+    uint32_t* sym_selfpos = nullptr;    // [leaves] position of t in its own row = |lower(t)|
+    int64_t* sym_lower = nullptr;       // [leaves + 1] exclusive scan of sym_selfpos
+    double4* sym_slot = nullptr;        // [lower entries][slot_w] partial sums (Phi, Phi')
+    double4* sym_t = nullptr;           // [n] own-CTA sums + L2P, leaf order
     fmm2d::Stats stats;
     std::vector<void*> allocs;          // everything to free
 };
@@ -83,6 +91,7 @@ int run_m2l(fmm2d_plan* P);
 int run_downward(fmm2d_plan* P);
 int run_near(fmm2d_plan* P, double2* phi, double2* dphi);
 int prepare_near(fmm2d_plan* P);
+int prepare_near_sym(fmm2d_plan* P);
 int gather_strengths(fmm2d_plan* P, const double2* m);
 int upload_binomials(int p);
 // count of this library's own kernel launches (reported by bench.py as gpu_launches)

@@ -18,6 +18,8 @@
 // result is stored at the input position perm[i].
 // Leaves larger than NEAR_CHUNK (only when nlevels forces a shallow tree) take
 // k_near_wide, which reads sources straight from global memory.
+#include <cub/cub.cuh>
+
 #include "fastmath.cuh"
 #include "fmm2d_internal.cuh"
 
@@ -278,6 +280,257 @@ __global__ void __launch_bounds__(NEAR_T) k_near_wide(int p, const uint32_t* __r
     }
 }
 
+// ---------------------------------------------------------------------------------
+// Symmetric near field.  The strong relation is symmetric, so every
+// unordered pair of distinct leaves (t, s), s > t, is evaluated ONCE by the CTA of t:
+// the shared part of the pair (|dz|^2, log|dz|^2, Arg dz and Arg of the reversed
+// componentwise difference, 1/|dz|^2) feeds both Phi_i (t side, registers) and Phi_j
+// (s side).  The s-side partial sums of a chunk are reduced over the CTA's target
+// threads in shared memory in fixed order and written to the slot of (s, t): slot row
+// lower[s] + (position of t in s's list).  k_near_gather then adds, per point, its own
+// CTA's sum and its slots in ascending order -- deterministic, no atomics.
+// Own-leaf pairs (t, t) are evaluated one-sided (ordered, self pair neutralised).
+template <bool REAL>
+__device__ __forceinline__ void pair_sym(PairAcc& at, PairAcc& as, double dx, double dy, double mt_r, double mt_i,
+                                         double ms_r, double ms_i, const fm::Tables& T)
+{
+    // at: target i gets m_s Log(dz) and m_s/dz;  as: source j gets m_t Log(-dz) and -m_t/dz
+    const double r2 = fma(dx, dx, dy * dy);
+    const double l2 = fm::log_pos(r2, T.lg);
+    double th, thn;
+    fm::arg_pair(dx, dy, T.at, th, thn);
+    const double ir2 = fm::rcp(r2);
+    const double a2 = ms_r * ir2, b2 = mt_r * ir2;
+    at.ar = fma(ms_r, l2, at.ar);
+    at.br = fma(ms_r, th, at.br);
+    at.dr = fma(a2, dx, at.dr);
+    at.di = fma(-a2, dy, at.di);
+    as.ar = fma(mt_r, l2, as.ar);
+    as.br = fma(mt_r, thn, as.br);
+    as.dr = fma(-b2, dx, as.dr);                  // m conj(-dz) / |dz|^2
+    as.di = fma(b2, dy, as.di);
+    if (!REAL) {
+        const double ai2 = ms_i * ir2, bi2 = mt_i * ir2;
+        at.ai = fma(ms_i, l2, at.ai);
+        at.bi = fma(ms_i, th, at.bi);
+        at.dr = fma(ai2, dy, at.dr);
+        at.di = fma(ai2, dx, at.di);
+        as.ai = fma(mt_i, l2, as.ai);
+        as.bi = fma(mt_i, thn, as.bi);
+        as.dr = fma(-bi2, dy, as.dr);
+        as.di = fma(-bi2, dx, as.di);
+    }
+}
+
+struct SymArgs {
+    const uint32_t* off;       // leaf offsets
+    const int64_t* soff;       // strong CSR offsets (leaf level)
+    const uint32_t* sidx;
+    const uint32_t* mirror;    // per CSR entry: position of the row's leaf in the column leaf's row
+    const uint32_t* selfpos;   // per leaf: position of the leaf in its own row
+    const int64_t* lower;      // per leaf: first slot row
+    const double4* src;
+    const double* cx;
+    const double* cy;
+    const double2* loc;
+    const fm::Tables* tab;
+    double4* slot;
+    double4* tsum;
+    int p, G, tile, npass, rows, slot_w;
+};
+
+// dynamic shared memory: S[rows] | part[max(rows * tile, 2 * NEAR_T)] | Tables
+template <bool REAL>
+#ifndef FMM2D_SYM_MINB
+#define FMM2D_SYM_MINB 5
+#endif
+__global__ void __launch_bounds__(NEAR_T, FMM2D_SYM_MINB) k_near_sym(SymArgs A)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    double4* S = reinterpret_cast<double4*>(smem);
+    const int G = A.G, tile = A.tile, rows = A.rows;
+    const int npart = max(rows * tile, 2 * NEAR_T);
+    double4* part = S + rows;
+    fm::Tables& T = *reinterpret_cast<fm::Tables*>(part + npart);
+    __shared__ int cstart[33];
+    __shared__ int cleaf[32];
+    __shared__ int cinfo[1];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    load_tables(T, A.tab);
+    const int64_t t = blockIdx.x;
+    const uint32_t ts = A.off[t], te = A.off[t + 1];
+    const int nt = (int)(te - ts);
+    const int64_t q0 = A.soff[t], q1 = A.soff[t + 1];
+    const int64_t qself = q0 + A.selfpos[t];
+    const int per = (nt + A.npass - 1) / A.npass;            // targets per pass (<= 2 tile)
+    const int tp = tid % tile, g = tid / tile;
+    for (int pass = 0, i0 = 0; i0 < nt; ++pass, i0 += per) {
+        const int ni = min(per, nt - i0);
+        const int npair = (ni + 1) / 2;
+        const bool active = (g < G) && (tp < npair);
+        const int la = min(2 * tp, ni - 1), lb = min(2 * tp + 1, ni - 1);
+        const double4 PA = A.src[ts + i0 + la];
+        const double4 PB = A.src[ts + i0 + lb];
+        const double mbr = (2 * tp + 1 < ni) ? PB.z : 0.0;   // odd count: B duplicates A on the s side
+        const double mbi = (2 * tp + 1 < ni) ? PB.w : 0.0;
+        PairAcc aa, ab;
+        // ---- own leaf (one-sided, ordered pairs, j != i)
+        __syncthreads();
+        for (int e = tid; e < nt; e += NEAR_T) S[e] = A.src[ts + e];
+        __syncthreads();
+        if (active) {
+            const int sa = i0 + la, sb = i0 + lb;
+            for (int k = g; k < nt; k += G) {
+                const double4 s = S[k];
+                const bool xa = (k == sa), xb = (k == sb);
+                pair<REAL>(aa, xa ? 1.0 : PA.x - s.x, xa ? 0.0 : PA.y - s.y, xa ? 0.0 : s.z, xa ? 0.0 : s.w, T);
+                pair<REAL>(ab, xb ? 1.0 : PB.x - s.x, xb ? 0.0 : PB.y - s.y, xb ? 0.0 : s.z, xb ? 0.0 : s.w, T);
+            }
+        }
+        // ---- upper leaves s > t: symmetric
+        for (int64_t q = qself + 1; q < q1;) {
+            __syncthreads();
+            if (warp == 0) {
+                const int64_t qq = q + lane;
+                int sz = 0;
+                if (qq < q1) {
+                    const uint32_t lf = A.sidx[qq];
+                    sz = (int)(A.off[lf + 1] - A.off[lf]);
+                    cleaf[lane] = (int)lf;
+                }
+                int incl = sz;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const unsigned fit = __ballot_sync(0xffffffffu, qq < q1 && incl <= rows);
+                const int nl = __popc(fit);
+                if (lane < nl) cstart[lane + 1] = incl;
+                if (lane == 0) {
+                    cstart[0] = 0;
+                    cinfo[0] = nl;
+                }
+            }
+            __syncthreads();
+            const int nl = cinfo[0];
+            for (int l = warp; l < nl; l += NEAR_T / 32) {
+                const uint32_t s0 = A.off[cleaf[l]];
+                const int c0 = cstart[l], sz = cstart[l + 1] - c0;
+                for (int e = lane; e < sz; e += 32) S[c0 + e] = A.src[s0 + e];
+            }
+            __syncthreads();
+            const int total = cstart[nl];
+            if (active) {
+                for (int k = g; k < total; k += G) {
+                    const double4 s = S[k];
+                    PairAcc ss;
+                    pair_sym<REAL>(aa, ss, PA.x - s.x, PA.y - s.y, PA.z, PA.w, s.z, s.w, T);
+                    pair_sym<REAL>(ab, ss, PB.x - s.x, PB.y - s.y, mbr, mbi, s.z, s.w, T);
+                    part[k * tile + tp] = pack(ss);
+                }
+            }
+            __syncthreads();
+            // reduce the s-side partials of each row over the active target threads
+            if (tid < total) {
+                int l = 0;
+                while (cstart[l + 1] <= tid) ++l;
+                double4 v = part[tid * tile];
+                for (int u = 1; u < npair; ++u) {
+                    const double4 w = part[tid * tile + u];
+                    v.x += w.x;
+                    v.y += w.y;
+                    v.z += w.z;
+                    v.w += w.w;
+                }
+                const uint32_t sl = (uint32_t)cleaf[l];
+                double4* dst = A.slot + (A.lower[sl] + A.mirror[q + l]) * A.slot_w + (tid - cstart[l]);
+                if (pass > 0) {
+                    const double4 o = *dst;
+                    v.x += o.x;
+                    v.y += o.y;
+                    v.z += o.z;
+                    v.w += o.w;
+                }
+                *dst = v;
+            }
+            q += nl;
+        }
+        // ---- t side: reduce over groups, add L2P, store in leaf order
+        __syncthreads();
+        double4(*red)[NEAR_T] = reinterpret_cast<double4(*)[NEAR_T]>(part);
+        red[0][tid] = pack(aa);
+        red[1][tid] = pack(ab);
+        __syncthreads();
+        for (int kk = tid; kk < ni; kk += NEAR_T) {
+            const int ptp = kk >> 1, s = kk & 1;
+            double4 acc = red[s][ptp];
+            for (int gg = 1; gg < G; ++gg) {
+                const double4 v = red[s][gg * tile + ptp];
+                acc.x += v.x;
+                acc.y += v.y;
+                acc.z += v.z;
+                acc.w += v.w;
+            }
+            const uint32_t i = ts + i0 + kk;
+            const double4 me = A.src[i];
+            double fr, fi, gr, gi;
+            l2p(A.loc + t * (A.p + 1), A.p, me.x - A.cx[t], me.y - A.cy[t], fr, fi, gr, gi);
+            A.tsum[i] = make_double4(acc.x + fr, acc.y + fi, acc.z + gr, acc.w + gi);
+        }
+    }
+}
+
+// per point: own-CTA sum + its slots (ascending), written at the input position
+__global__ void __launch_bounds__(NEAR_T) k_near_gather(const uint32_t* __restrict__ off,
+                                                        const uint32_t* __restrict__ selfpos,
+                                                        const int64_t* __restrict__ lower, int slot_w,
+                                                        const double4* __restrict__ tsum,
+                                                        const double4* __restrict__ slot,
+                                                        const uint32_t* __restrict__ perm, double2* __restrict__ phi,
+                                                        double2* __restrict__ dphi)
+{
+    const int64_t s = blockIdx.x;
+    const uint32_t s0 = off[s], s1 = off[s + 1];
+    const int nlow = (int)selfpos[s];
+    const int64_t base = lower[s];
+    for (uint32_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+        double4 v = tsum[i];
+        for (int k = 0; k < nlow; ++k) {
+            const double4 w = slot[(base + k) * slot_w + (i - s0)];
+            v.x += w.x;
+            v.y += w.y;
+            v.z += w.z;
+            v.w += w.w;
+        }
+        const uint32_t o = perm[i];
+        if (phi) phi[o] = make_double2(v.x, v.y);
+        if (dphi) dphi[o] = make_double2(v.z, v.w);
+    }
+}
+
+// per leaf t: position of t in its own (sorted) row; per upper entry (t, s): position of t in row s
+__global__ void k_sym_index(int64_t nl, const int64_t* __restrict__ soff, const uint32_t* __restrict__ sidx,
+                            uint32_t* __restrict__ selfpos, uint32_t* __restrict__ mirror)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nl) return;
+    const int64_t q0 = soff[t], q1 = soff[t + 1];
+    for (int64_t q = q0; q < q1; ++q) {
+        const uint32_t s = sidx[q];
+        if (s == (uint32_t)t) selfpos[t] = (uint32_t)(q - q0);
+        if (s > (uint32_t)t) {
+            int64_t lo = soff[s], hi = soff[s + 1];             // lower_bound(t) in row s
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (sidx[mid] < (uint32_t)t) lo = mid + 1;
+                else hi = mid;
+            }
+            mirror[q] = (uint32_t)(lo - soff[s]);
+        }
+    }
+}
+
 inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
 // per-device table copy (built once on the host, long double evaluation)
@@ -321,6 +574,70 @@ int prepare_near(fmm2d_plan* P)
     return rc;
 }
 
+__global__ void k_to_i64(const uint32_t* __restrict__ a, int64_t n, int64_t* __restrict__ b)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i];
+    if (i == n) b[n] = 0;
+}
+
+constexpr int SYM_MAXLEAF = 64;
+
+static size_t sym_smem(const fmm2d_plan* P)
+{
+    const int npart = std::max(P->sym_rows * P->sym_tile, 2 * NEAR_T);
+    return sizeof(double4) * (P->sym_rows + npart) + sizeof(fm::Tables);
+}
+
+// Build-time set-up of the symmetric near field: leaves of at
+// most SYM_MAXLEAF points; otherwise (or if the slot buffer does not fit) the one-sided
+// kernel is used.
+int prepare_near_sym(fmm2d_plan* P)
+{
+    P->sym = false;
+    const int L = P->L, ml = P->stats.max_leaf;
+    if (L < 1 || ml > SYM_MAXLEAF || ml < 1 || !(P->flags & FMM2D_SYMMETRIC_P2P)) return 0;
+    cudaStream_t st = P->stream;
+    const int64_t nl = nboxes(L);
+    const Csr& S = P->strong[L];
+    P->sym_npass = (ml + 31) / 32;
+    const int per = (ml + P->sym_npass - 1) / P->sym_npass;
+    P->sym_tile = (per + 1) / 2;
+    P->sym_rows = std::max(ml, std::min(64, 2 * ml));
+    P->slot_w = ml;
+    FMM2D_TRY(dev_alloc(P, (void**)&P->sym_mirror, sizeof(uint32_t) * std::max<int64_t>(S.total, 1)));
+    FMM2D_TRY(dev_alloc(P, (void**)&P->sym_selfpos, sizeof(uint32_t) * nl));
+    FMM2D_TRY(dev_alloc(P, (void**)&P->sym_lower, sizeof(int64_t) * (nl + 1)));
+    k_sym_index<<<grid_for(nl, 256), 256, 0, st>>>(nl, S.off, S.idx, P->sym_selfpos, P->sym_mirror);
+    fmm2d::note_launch();
+    int64_t* cnt = nullptr;
+    void* scratch = nullptr;
+    size_t sb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, sb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(nl + 1), st);
+    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt, sizeof(int64_t) * (nl + 1), st));
+    FMM2D_CUDA_TRY(cudaMallocAsync(&scratch, sb, st));
+    k_to_i64<<<grid_for(nl + 1, 256), 256, 0, st>>>(P->sym_selfpos, nl, cnt);
+    fmm2d::note_launch();
+    FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, cnt, P->sym_lower, (int)(nl + 1), st));
+    int64_t total = 0;
+    FMM2D_CUDA_TRY(cudaMemcpyAsync(&total, P->sym_lower + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+    cudaFreeAsync(cnt, st);
+    cudaFreeAsync(scratch, st);
+    if (dev_alloc(P, (void**)&P->sym_slot, sizeof(double4) * std::max<int64_t>(total, 1) * P->slot_w) ||
+        dev_alloc(P, (void**)&P->sym_t, sizeof(double4) * P->n)) {
+        cudaGetLastError();                       // out of memory: keep the one-sided kernel
+        return 0;
+    }
+    const size_t smem = sym_smem(P);
+    if (smem > 48 * 1024) {
+        FMM2D_CUDA_TRY(cudaFuncSetAttribute(k_near_sym<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FMM2D_CUDA_TRY(cudaFuncSetAttribute(k_near_sym<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
+    P->sym = true;
+    return 0;
+}
+
 int run_near(fmm2d_plan* P, double2* phi, double2* dphi)
 {
     const int L = P->L;
@@ -331,6 +648,38 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi)
     const uint32_t* off = P->boff + P->obase[L];
     const bool real = (P->flags & FMM2D_REAL_STRENGTHS) != 0;
     const fm::Tables* tab = (const fm::Tables*)P->tables;
+    if (P->sym) {
+        SymArgs A;
+        A.off = off;
+        A.soff = P->strong[L].off;
+        A.sidx = P->strong[L].idx;
+        A.mirror = P->sym_mirror;
+        A.selfpos = P->sym_selfpos;
+        A.lower = P->sym_lower;
+        A.src = P->src;
+        A.cx = cx;
+        A.cy = cy;
+        A.loc = loc;
+        A.tab = tab;
+        A.slot = P->sym_slot;
+        A.tsum = P->sym_t;
+        A.p = P->p;
+        A.tile = P->sym_tile;
+        A.G = NEAR_T / P->sym_tile;
+        A.npass = P->sym_npass;
+        A.rows = P->sym_rows;
+        A.slot_w = P->slot_w;
+        const size_t smem = sym_smem(P);
+        if (real) k_near_sym<true><<<(unsigned)nl, NEAR_T, smem, P->stream>>>(A);
+        else      k_near_sym<false><<<(unsigned)nl, NEAR_T, smem, P->stream>>>(A);
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+        k_near_gather<<<(unsigned)nl, NEAR_T, 0, P->stream>>>(off, P->sym_selfpos, P->sym_lower, P->slot_w,
+                                                               P->sym_t, P->sym_slot, P->perm, phi, dphi);
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+        return 0;
+    }
     if (P->stats.max_leaf <= NEAR_CHUNK) {
         // target pairs per leaf, groups so that pairs * G <= 128
         const int pairs = (std::max(1, P->stats.max_leaf) + 1) / 2;

@@ -25,6 +25,7 @@ LIB_PATH = os.environ.get("FMM2D_LIB") or os.path.join(_HERE, "libfmm2d.so")
 PMAX = 32
 HOST_PTRS = 0x1
 REAL_STRENGTHS = 0x2
+SYMMETRIC_P2P = 0x4
 
 EXPORT_PERM, EXPORT_OFFSETS, EXPORT_DISCS, EXPORT_STRONG, EXPORT_WEAK, EXPORT_MPOLE, EXPORT_LOCAL, \
     EXPORT_STATS = range(1, 9)
@@ -117,7 +118,8 @@ class Fmm2d:
     plan then uses FMM2D_HOST_PTRS and host inputs/outputs)."""
 
     def __init__(self, z, theta: float = 0.5, p: int = 17, leaf_target: int = 40, nlevels: int = -1,
-                 real_strengths: bool = False, device: int | None = None, stream=None):
+                 real_strengths: bool = False, device: int | None = None, stream=None,
+                 symmetric_p2p: bool = False):
         L = lib()
         import torch
         host = not (isinstance(z, torch.Tensor) and z.is_cuda)
@@ -134,7 +136,8 @@ class Fmm2d:
         opt.p = int(p)
         opt.leaf_target = int(leaf_target)
         opt.nlevels = int(nlevels)
-        opt.flags = (HOST_PTRS if host else 0) | (REAL_STRENGTHS if real_strengths else 0)
+        opt.flags = ((HOST_PTRS if host else 0) | (REAL_STRENGTHS if real_strengths else 0)
+                     | (SYMMETRIC_P2P if symmetric_p2p else 0))
         opt.device = int(device)
         opt.stream = ctypes.c_void_p(stream.cuda_stream)
         self._opt = opt

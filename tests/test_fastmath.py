@@ -18,4 +18,5 @@ def test_fastmath_ulps(tmp_path):
     assert r["log_max_ulp"] <= 2.0
     assert r["log_max_abs"] <= 1e-14          # |log|dz|| up to ~42 here: < 1 ulp
     assert r["arg_max_ulp"] <= 2.0
+    assert r["argneg_max_ulp"] <= 2.0 and r["pair_mismatch"] == 0   # Arg(-dz) of arg_pair (symmetric P2P)
     assert r["log0_is_neg_inf"] == 1 and r["arg_pi"] == 1 and r["arg_zero"] == 1

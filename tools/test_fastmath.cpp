@@ -22,7 +22,8 @@ int main()
     std::mt19937_64 g(12345);
     std::uniform_real_distribution<double> U(-1.0, 1.0);
     std::uniform_real_distribution<double> E(-60.0, 60.0);
-    double mlog = 0, marg = 0, mabs_log = 0;
+    double mlog = 0, marg = 0, mabs_log = 0, margn = 0;
+    long pair_mismatch = 0;
     long n = 0;
     for (long k = 0; k < 4000000; ++k) {
         double s = std::ldexp(1.0, (int)E(g));
@@ -41,12 +42,19 @@ int main()
         if (fabsl(rl) > 1e-3L) mlog = std::fmax(mlog, el);
         mabs_log = std::fmax(mabs_log, (double)fabsl((long double)lg - rl));
         marg = std::fmax(marg, ulp_err(a, ra));
+        // Arg of the componentwise reverse difference (zeros stay +0) from arg_pair
+        double th, thn;
+        arg_pair(dx, dy, T.at, th, thn);
+        double dxn = (dx == 0.0) ? 0.0 : -dx, dyn = (dy == 0.0) ? 0.0 : -dy;
+        long double rn = atan2l((long double)dyn, (long double)dxn);
+        if (th != a) pair_mismatch++;
+        margn = std::fmax(margn, ulp_err(thn, rn));
         ++n;
     }
     double zero = log_pos(0.0, T.lg);
-    printf("{\"n\": %ld, \"log_max_ulp\": %.3f, \"log_max_abs\": %.3e, \"arg_max_ulp\": %.3f, \"log0_is_neg_inf\": %d, "
-           "\"arg_pi\": %d, \"arg_zero\": %d}\n",
-           n, mlog, mabs_log, marg, (int)(std::isinf(zero) && zero < 0),
+    printf("{\"n\": %ld, \"log_max_ulp\": %.3f, \"log_max_abs\": %.3e, \"arg_max_ulp\": %.3f, \"argneg_max_ulp\": %.3f, "
+           "\"pair_mismatch\": %ld, \"log0_is_neg_inf\": %d, \"arg_pi\": %d, \"arg_zero\": %d}\n",
+           n, mlog, mabs_log, marg, margn, pair_mismatch, (int)(std::isinf(zero) && zero < 0),
            (int)(arg(-1.0, 0.0, T.at) == M_PI), (int)(arg(2.0, 0.0, T.at) == 0.0));
     return 0;
 }
