@@ -60,6 +60,9 @@ extern "C" {
                                       rounding; needs a slot buffer; leaves <= 64 points).
                                       Default: every ordered pair separately (measured
                                       faster on B200)            */
+#define FMM2D_TREE_KEY64      0x8  /* diagnostic: presort both axes with full 64-bit keys
+                                      instead of 32-bit keys + run fix-up (same tree,
+                                      DESIGN.md section 6.1)                            */
 
 typedef struct fmm2d_plan fmm2d_plan;   /* opaque; owns all device memory */
 
@@ -71,7 +74,7 @@ typedef struct {
     int    leaf_target;  /* used when nlevels < 0: L = min L >= 0 with
                             n <= 2*leaf_target*4^L (DESIGN R4).          */
     int    nlevels;      /* >= 0 forces L (requires n >= 4^L); < 0 = automatic.     */
-    int    flags;        /* FMM2D_HOST_PTRS | FMM2D_REAL_STRENGTHS                   */
+    int    flags;        /* FMM2D_HOST_PTRS | FMM2D_REAL_STRENGTHS | ...             */
     int    device;       /* CUDA device ordinal                                      */
     void*  stream;       /* cudaStream_t for every kernel and copy (NULL = legacy
                             default stream)                                          */

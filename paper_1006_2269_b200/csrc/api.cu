@@ -126,6 +126,8 @@ int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan
     P->base.resize(L + 2);
     for (int l = 0; l <= L + 1; ++l) P->base[l] = level_base(l);
     P->nbox_total = P->base[L + 1];
+    P->pos0 = 0;
+    P->pos1 = (uint32_t)n;
 
     auto body = [&]() -> int {
         cudaEvent_t e0, e1, e2;
@@ -286,7 +288,8 @@ static int copy_out(const void* dsrc, void* dst, size_t bytes, size_t* cap, size
 /* STATS layout (double[16]): 0 n, 1 L, 2 p, 3 theta, 4 weak pairs (all levels),
  * 5 strong leaf pairs, 6 min leaf size, 7 max leaf size, 8 t_build_ms, 9 t_tree_ms,
  * 10 t_lists_ms, 11 number of boxes (all levels), 12 kernel launches of this library
- * since it was loaded (all plans), 13 ordered P2P pairs (j != i) of one eval, 14..15 reserved. */
+ * since it was loaded (all plans), 13 ordered P2P pairs (j != i) of one eval, 14 axes presorted
+ * with 64-bit keys (bit 0 x, bit 1 y), 15 reserved. */
 int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* bytes)
 {
     if (!P || !bytes) return FMM2D_EINVAL;
@@ -357,6 +360,7 @@ int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* by
             s[11] = (double)P->nbox_total;
             s[12] = (double)launch_count();
             s[13] = (double)P->stats.p2p_pairs;
+            s[14] = (double)P->stats.tree_key64;
             off = need;
             break;
         }

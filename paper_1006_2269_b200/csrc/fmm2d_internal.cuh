@@ -27,25 +27,35 @@ struct Csr {
     int64_t total = 0;
 };
 
-// tree record: position, input index, current box id (24 B)
-struct Rec {
-    double x, y;
-    uint32_t idx, box;
-};
-
 struct Stats {
     double t_build_ms = 0, t_tree_ms = 0, t_lists_ms = 0;
     int64_t weak_pairs = 0, strong_leaf_pairs = 0, p2p_pairs = 0;
     int max_leaf = 0, min_leaf = 0;
+    int tree_key64 = 0;                // axes presorted with 64-bit keys (bit 0 x, bit 1 y)
 };
 
 }  // namespace fmm2d
+
+namespace fmm2d {
+struct Shard;   // shard.cu: exchange tables and buffers of a sharded plan
+}
 
 struct fmm2d_plan {
     int64_t n = 0;
     int L = 0, p = 0, flags = 0, device = 0;
     double theta = 0.5;
     cudaStream_t stream = nullptr;
+    // partition: levels <= kpart are replicated on every rank,
+    // levels > kpart hold the rank's own subtrees [rank 4^l / P, (rank+1) 4^l / P).
+    // One GPU: nranks = 1, kpart = 0 (every box is "own").
+    int nranks = 1, rank = 0, kpart = 0;
+    uint32_t pos0 = 0, pos1 = 0;        // own source positions (leaf order)
+    int64_t own_lo(int l) const { return (nboxes_(l) / nranks) * rank; }          // l >= kpart
+    int64_t own_hi(int l) const { return (nboxes_(l) / nranks) * (rank + 1); }
+    int64_t box_lo(int l) const { return (l <= kpart) ? 0 : own_lo(l); }           // boxes computed
+    int64_t box_hi(int l) const { return (l <= kpart) ? nboxes_(l) : own_hi(l); }
+    static int64_t nboxes_(int l) { return (int64_t)1 << (2 * l); }
+    fmm2d::Shard* shard = nullptr;      // nranks > 1
     int64_t nbox_total = 0;
     std::vector<int64_t> base;          // base[l], l = 0..L+1
     // offsets of every level (uint32, n < 2^31), concatenated: level l at obase[l]
@@ -84,6 +94,7 @@ int dev_alloc(fmm2d_plan* P, void** ptr, size_t bytes);
 
 // build steps (tree.cu, lists.cu)
 int build_tree(fmm2d_plan* P, const double2* z_dev);
+int finish_radii(fmm2d_plan* P);
 int build_lists(fmm2d_plan* P);
 // eval steps (expansions.cu, near.cu)
 int run_upward(fmm2d_plan* P);

@@ -5,18 +5,29 @@
 // direction"; the points live in "a 2^d-tree cut at a certain maximum
 // level".  Readings R5-R8, R13.
 //
-// GPU formulation (bit-exact by construction): two record
-// lists are kept, one sorted by (x, idx) and one by (y, idx) inside every box.
-// A split along x takes the first ceil(n/2) of the x-list (trivially partitioned)
-// and stably partitions the y-list by "(x, idx) < the first x-high record": one
-// flag pass, one device-wide scan, one scatter.  Stability keeps both lists sorted,
-// so the y-split is the same step with the axes swapped.  The list that is only
-// trivially split is never rewritten: its records keep the id of the previous
-// (half-)level and every reader refines it from the record's position and the
-// offsets ("stale id + refine").  Box sizes are a pure function of N, so all
-// offsets come from a tiny per-level kernel.  The presort is two stable radix sorts
-// of orderable 64-bit keys (ties leave in index order); the sorted key itself gives
-// the sort coordinate back, only the other coordinate is gathered.
+// GPU formulation (bit-exact by construction):
+//  1. Ranks.  The total orders (x, idx) and (y, idx) (R6) are computed once, by
+//     stable radix sorts, as dense ranks rx[i], ry[i] in [0, n).  After that every
+//     comparison of the method is an integer comparison of ranks, and a point is an
+//     8-byte record {rx, ry}.  The sort key is a 32-bit monotone image of the
+//     coordinate, key = floor((c - cmin) * (2^32 - 1) / (cmax - cmin)); a stable sort
+//     by it yields (key, idx) order, and the runs of equal keys (distinct coordinates
+//     that share a bucket) are re-sorted by (c, idx) in place.  Runs longer than
+//     RUN_MAX (heavy ties or duplicates) switch that axis to a full 64-bit sort of the
+//     orderable coordinate bits -- same result, more passes.
+//  2. Two record lists are kept, one grouped by box and sorted by rx inside each box
+//     (the x-list), one sorted by ry inside each box (the y-list).  An x-split takes
+//     the first ceil(n/2) of the x-list segment (trivially partitioned; that list is
+//     not rewritten) and stably partitions the y-list segment by rx < the first high
+//     record's rx: one pass with a block scan and a decoupled look-back.  Stability
+//     keeps both lists sorted, so the y-split is the same step with the axes swapped.
+//     The segment of a record is found from its position (box sizes are a pure
+//     function of n, so all offsets come from a tiny per-level kernel).
+//  3. Bounding boxes are the coordinates of segment endpoints; after the last level
+//     the y-list IS the leaf order (leaves ascending, (y, idx) inside: R13).  One pass
+//     writes the permutation, the source rows and every level's exact radius.
+// Every kernel works on a position range [k0, k1) of whole boxes, so a rank of a
+// sharded build continues below the top levels with its own subtrees only.
 #include <cub/cub.cuh>
 
 #include "fmm2d_internal.cuh"
@@ -25,48 +36,159 @@ namespace fmm2d {
 
 namespace {
 
+constexpr int RUN_MAX = 32;            // longest equal-key run fixed in place
+
 __device__ __forceinline__ uint64_t orderable(double v)
 {
     uint64_t u = (uint64_t)__double_as_longlong(v);
     return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
+
+// orderable bits of min / max (atomicMin / atomicMax on uint64 keep the order)
+struct Bounds {
+    unsigned long long xmin, xmax, ymin, ymax;
+    int bad;
+};
+
+// A0 (pass 1): validate, map -0 -> +0 (x + 0.0), keep the canonical coordinates,
+// reduce the coordinate ranges.
+constexpr int CT = 256;
+__global__ void __launch_bounds__(CT) k_canon(const double2* __restrict__ z, int64_t n, double* __restrict__ xs,
+                                              double* __restrict__ ys, Bounds* __restrict__ B)
+{
+    int64_t i = (int64_t)blockIdx.x * CT + threadIdx.x;
+    uint64_t xmn = ~0ull, xmx = 0, ymn = ~0ull, ymx = 0;
+    int bad = 0;
+    for (; i < n; i += (int64_t)gridDim.x * CT) {
+        const double2 v = z[i];
+        const double x = __dadd_rn(v.x, 0.0), y = __dadd_rn(v.y, 0.0);
+        if (!isfinite(x) || !isfinite(y)) bad = 1;
+        xs[i] = x;
+        ys[i] = y;
+        const uint64_t kx = orderable(x), ky = orderable(y);
+        xmn = min(xmn, kx);
+        xmx = max(xmx, kx);
+        ymn = min(ymn, ky);
+        ymx = max(ymx, ky);
+    }
+    typedef cub::BlockReduce<unsigned long long, CT> R;
+    __shared__ typename R::TempStorage t0, t1, t2, t3;
+    const unsigned long long a = R(t0).Reduce((unsigned long long)xmn, cub::Min());
+    const unsigned long long b = R(t1).Reduce((unsigned long long)xmx, cub::Max());
+    const unsigned long long c = R(t2).Reduce((unsigned long long)ymn, cub::Min());
+    const unsigned long long d = R(t3).Reduce((unsigned long long)ymx, cub::Max());
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+        atomicMin(&B->xmin, a);
+        atomicMax(&B->xmax, b);
+        atomicMin(&B->ymin, c);
+        atomicMax(&B->ymax, d);
+        if (bad) atomicOr(&B->bad, 1);
+    }
+}
+
 __device__ __forceinline__ double from_orderable(uint64_t k)
 {
     uint64_t u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
     return __longlong_as_double((long long)u);
 }
 
-// A0: validate, map -0 -> +0 (x + 0.0), order keys, identity indices.
-__global__ void k_canon(const double2* __restrict__ z, int64_t n, double* __restrict__ xs,
-                        double* __restrict__ ys, uint64_t* __restrict__ kx, uint64_t* __restrict__ ky,
-                        uint32_t* __restrict__ iota, int* __restrict__ bad)
+// monotone (non-decreasing) 32-bit image of a coordinate: every step rounds
+// monotonically, so c <= c' implies key(c) <= key(c')
+__device__ __forceinline__ uint32_t key32(double c, double cmin, double scale)
 {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const double t = __dmul_rn(__dsub_rn(c, cmin), scale);
+    return (uint32_t)fmin(fmax(t, 0.0), 4294967295.0);
+}
+
+// A0 (pass 2): 32-bit keys of both axes and the identity payload
+__global__ void k_keys32(const double* __restrict__ xs, const double* __restrict__ ys, int64_t n,
+                         const Bounds* __restrict__ B, uint32_t* __restrict__ kx, uint32_t* __restrict__ ky,
+                         uint32_t* __restrict__ iota)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double2 v = z[i];
-    double x = __dadd_rn(v.x, 0.0), y = __dadd_rn(v.y, 0.0);
-    if (!isfinite(x) || !isfinite(y)) atomicOr(bad, 1);
-    xs[i] = x;
-    ys[i] = y;
-    kx[i] = orderable(x);
-    ky[i] = orderable(y);
+    const double xmn = from_orderable(B->xmin), xmx = from_orderable(B->xmax);
+    const double ymn = from_orderable(B->ymin), ymx = from_orderable(B->ymax);
+    const double wx = __dsub_rn(xmx, xmn), wy = __dsub_rn(ymx, ymn);
+    // width 0 or overflowing: scale 0, one run (the 64-bit path takes over)
+    double sx = (wx > 0.0 && isfinite(wx)) ? 4294967295.0 / wx : 0.0;
+    double sy = (wy > 0.0 && isfinite(wy)) ? 4294967295.0 / wy : 0.0;
+    if (!isfinite(sx)) sx = 0.0;
+    if (!isfinite(sy)) sy = 0.0;
+    kx[i] = key32(xs[i], xmn, sx);
+    ky[i] = key32(ys[i], ymn, sy);
     iota[i] = (uint32_t)i;
 }
 
-// records of one presorted list: the sort coordinate from the key, the other gathered
-__global__ void k_make_recs(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ order,
-                            const double* __restrict__ other, int axis, int64_t n, Rec* __restrict__ out)
+// 64-bit fallback keys of one axis
+__global__ void k_keys64(const double* __restrict__ c, int64_t n, uint64_t* __restrict__ k,
+                         uint32_t* __restrict__ iota)
 {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    k[i] = orderable(c[i]);
+    iota[i] = (uint32_t)i;
+}
+
+// Runs of equal 32-bit keys (already in idx order: the sort is stable) are re-sorted
+// by (c, idx) with a stable insertion sort by c.  A run longer than RUN_MAX raises
+// *overflow and is left alone (the caller redoes the axis with 64-bit keys).
+__global__ void k_fix_runs(const uint32_t* __restrict__ key, int64_t n, const double* __restrict__ c,
+                           uint32_t* __restrict__ ord, int* __restrict__ overflow)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    uint32_t i = order[k];
-    double c = from_orderable(keys[k]), o = other[i];
-    Rec r;
-    r.x = axis ? o : c;
-    r.y = axis ? c : o;
-    r.idx = i;
-    r.box = 0;
-    out[k] = r;
+    const uint32_t v = key[k];
+    if (k > 0 && key[k - 1] == v) return;            // not a run start
+    if (k + 1 >= n || key[k + 1] != v) return;       // run of one
+    int len = 2;
+    while (k + len < n && key[k + len] == v && len <= RUN_MAX) ++len;
+    if (len > RUN_MAX) {
+        atomicOr(overflow, 1);
+        return;
+    }
+    double cv[RUN_MAX];
+    uint32_t iv[RUN_MAX];
+    for (int a = 0; a < len; ++a) {
+        const uint32_t i = ord[k + a];
+        const double ci = c[i];
+        int b = a;
+        while (b > 0 && cv[b - 1] > ci) {           // strict: equal c keep idx order
+            cv[b] = cv[b - 1];
+            iv[b] = iv[b - 1];
+            --b;
+        }
+        cv[b] = ci;
+        iv[b] = i;
+    }
+    for (int a = 0; a < len; ++a) ord[k + a] = iv[a];
+}
+
+// ranks: rx[ord_x[k]] = k, ry[ord_y[k]] = k
+__global__ void k_ranks(const uint32_t* __restrict__ ox, const uint32_t* __restrict__ oy, int64_t n,
+                        uint32_t* __restrict__ rx, uint32_t* __restrict__ ry)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    rx[ox[k]] = (uint32_t)k;
+    ry[oy[k]] = (uint32_t)k;
+}
+
+// initial lists and the coordinates in rank order
+__global__ void k_make_lists(const uint32_t* __restrict__ ox, const uint32_t* __restrict__ oy,
+                             const uint32_t* __restrict__ rx, const uint32_t* __restrict__ ry,
+                             const double* __restrict__ xs, const double* __restrict__ ys, int64_t n,
+                             uint2* __restrict__ xl, uint2* __restrict__ yl, double* __restrict__ xcs,
+                             double* __restrict__ ycs)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t i = ox[k], j = oy[k];
+    xl[k] = make_uint2((uint32_t)k, ry[i]);
+    yl[k] = make_uint2(rx[j], (uint32_t)k);
+    xcs[k] = xs[i];
+    ycs[k] = ys[j];
 }
 
 // offsets of level 0
@@ -97,81 +219,128 @@ __global__ void k_child_off(const uint32_t* __restrict__ O, int64_t nb, uint32_t
     }
 }
 
-// (coord, idx) < (coord', idx') on axis 0 = x, 1 = y  (DESIGN R6)
-__device__ __forceinline__ bool rec_less(const Rec& a, const Rec& b, int axis)
+// largest p in [lo, hi) with O[p] <= k  (O ascending, O[lo] <= k)
+__device__ __forceinline__ uint32_t seg_search(const uint32_t* __restrict__ O, uint32_t lo, uint32_t hi, uint32_t k)
 {
-    double ca = axis ? a.y : a.x, cb = axis ? b.y : b.x;
-    return (ca < cb) || (ca == cb && a.idx < b.idx);
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (O[mid] <= k) lo = mid;
+        else hi = mid;
+    }
+    return lo;
 }
 
-// parent segment of position k: the record's (stale) id, refined by one split if needed
-__device__ __forceinline__ uint32_t parent_of(uint32_t box, int64_t k, const uint32_t* __restrict__ refine)
-{
-    return refine ? 2 * box + ((uint32_t)k >= refine[2 * box + 1] ? 1u : 0u) : box;
-}
-
-// Per parent segment p: number of high-side records (the split rule fixes it).
+// Per parent segment p in [p0, p1): number of high-side records (the split rule fixes it).
 __global__ void k_high_sizes(const uint32_t* __restrict__ par_off, const uint32_t* __restrict__ sub_off,
-                             int64_t np, uint32_t* __restrict__ hs)
+                             int64_t p0, int64_t np, uint32_t* __restrict__ hs)
 {
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < np) hs[p] = par_off[p + 1] - sub_off[2 * p + 1];
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < np) hs[q] = par_off[p0 + q + 1] - sub_off[2 * (p0 + q) + 1];
 }
 
-// One split step in a single pass (replaces flag -> device scan -> scatter):
-//   flag  = record is on the high side of its parent segment p, i.e.
-//           (coord, idx) >= the first high record split_list[sub_off[2p+1]];
-//   G(k)  = number of high records before position k over the whole list, from a
-//           block scan + decoupled look-back across tiles (tile ids taken in launch
-//           order from a counter, so predecessors always make progress);
+// One split step over the positions of the parent segments [p0, p1), in one pass:
+//   flag  = record is on the high side of its parent segment p, i.e. its rank on the
+//           split axis >= the rank of the first high record split_list[sub_off[2p+1]];
+//   G(k)  = high records before position k in the range, from a block scan plus a
+//           decoupled look-back across tiles (tile ids taken in launch order from a
+//           counter, so predecessors always make progress);
 //   dst   = stable position inside p: high -> sub_off[2p+1] + (G(k) - Gp[p]),
-//           low -> k - (G(k) - Gp[p]), where Gp[p] = high records before segment p
-//           (exclusive scan of k_high_sizes, a function of the offsets only).
+//           low -> k - (G(k) - Gp[p]), Gp[p] = highs before segment p (a scan of
+//           k_high_sizes, a function of the offsets only).
+// The segment table of the tile (start, first high position, Gp, split rank) is staged
+// in shared memory; each record finds its segment by binary search there.
 constexpr int PT = 256, PI = 4, PTILE = PT * PI;
+constexpr int SEGMAX = PTILE + 2;                   // segments one tile can touch
 constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_MASK = 3ull << 62;
 
-__global__ void __launch_bounds__(PT) k_partition(const Rec* __restrict__ list, const Rec* __restrict__ split_list,
-                                                  const uint32_t* __restrict__ refine,
-                                                  const uint32_t* __restrict__ par_off,
-                                                  const uint32_t* __restrict__ sub_off,
-                                                  const uint32_t* __restrict__ Gp, int axis, int64_t n,
-                                                  Rec* __restrict__ out, unsigned long long* __restrict__ tstate,
-                                                  unsigned int* __restrict__ ticket)
+struct SplitArgs {
+    const uint2* list;          // partitioned list (read)
+    const uint2* split_list;    // list sorted by the split axis inside each parent segment
+    const uint32_t* par_off;    // parent segment offsets
+    const uint32_t* sub_off;    // child offsets: children of p are 2p, 2p+1
+    const uint32_t* Gp;         // [p - p0] highs before segment p
+    uint2* out;
+    unsigned long long* tstate;
+    unsigned int* ticket;
+    uint32_t p0, p1;            // parent segments of the range
+    uint32_t k0, k1;            // positions of the range (= par_off[p0], par_off[p1])
+    int axis;                   // 0: compare rx, 1: compare ry
+};
+
+__global__ void __launch_bounds__(PT) k_partition(SplitArgs A)
 {
     typedef cub::BlockScan<uint32_t, PT> Scan;
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ uint32_t s_tile, s_prefix;
-    __shared__ __align__(16) Rec stage[PTILE];
+    __shared__ uint32_t s_tile, s_prefix, s_plo, s_nseg;
+    __shared__ __align__(16) uint2 stage[PTILE];
+    __shared__ uint32_t s_off[SEGMAX + 1], s_hi[SEGMAX], s_gp[SEGMAX], s_split[SEGMAX];
     const int tid = threadIdx.x;
-    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+    if (tid == 0) s_tile = atomicAdd(A.ticket, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
-    const int64_t k0 = (int64_t)tile * PTILE + (int64_t)tid * PI;
-    // stage the tile through shared memory with coalesced 16-byte loads (all independent)
-    const int64_t kt = (int64_t)tile * PTILE;
-    const int nrec = (int)((n - kt) < PTILE ? (n - kt) : PTILE);
-    {
-        const uint4* g = reinterpret_cast<const uint4*>(list + kt);
+    const uint32_t kt = A.k0 + tile * (uint32_t)PTILE;
+    const int nrec = (int)min((uint32_t)PTILE, A.k1 - kt);
+    // segment range of the tile
+    if (tid == 0) {
+        const uint32_t plo = seg_search(A.par_off, A.p0, A.p1, kt);
+        const uint32_t phi = seg_search(A.par_off, plo, A.p1, kt + nrec - 1);
+        s_plo = plo;
+        s_nseg = phi - plo + 1;
+    }
+    {   // stage the tile with coalesced 16-byte loads
+        const uint4* g = reinterpret_cast<const uint4*>(A.list + kt);
         uint4* s = reinterpret_cast<uint4*>(stage);
-        const int nvec = (nrec * (int)sizeof(Rec)) / 16;            // whole vectors
-        for (int v = tid; v < nvec; v += PT) s[v] = g[v];
-        if (tid == 0 && (nrec * (int)sizeof(Rec)) % 16) stage[nrec - 1] = list[kt + nrec - 1];
+        const int nvec = nrec / 2;
+        const bool aligned = ((kt & 1u) == 0);
+        if (aligned) {
+            for (int v = tid; v < nvec; v += PT) s[v] = g[v];
+            if (tid == 0 && (nrec & 1)) stage[nrec - 1] = A.list[kt + nrec - 1];
+        } else {
+            for (int v = tid; v < nrec; v += PT) stage[v] = A.list[kt + v];
+        }
     }
     __syncthreads();
-    Rec r[PI];
-    uint32_t par[PI], f[PI];
+    const uint32_t plo = s_plo;
+    const int nseg = (int)s_nseg;
+    for (int j = tid; j < nseg; j += PT) {
+        const uint32_t p = plo + j;
+        const uint32_t sp = A.sub_off[2 * p + 1];
+        const uint32_t pe = A.par_off[p + 1];
+        s_off[j] = A.par_off[p];
+        s_hi[j] = sp;
+        s_gp[j] = A.Gp[p - A.p0];
+        const uint2 r = (sp < pe) ? A.split_list[sp] : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+        s_split[j] = A.axis ? r.y : r.x;
+        if (j == nseg - 1) s_off[nseg] = pe;
+    }
+    __syncthreads();
+    uint2 r[PI];
+    uint32_t seg[PI], f[PI];
     uint32_t cnt = 0;
+    const int i0 = tid * PI;
+    uint32_t sj = 0;
+    if (i0 < nrec) {
+        // binary search in the staged offsets for the first item, then walk forward
+        uint32_t lo = 0, hi = (uint32_t)nseg;
+        const uint32_t k = kt + i0;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (s_off[mid] <= k) lo = mid;
+            else hi = mid;
+        }
+        sj = lo;
+    }
 #pragma unroll
     for (int u = 0; u < PI; ++u) {
-        const int64_t k = k0 + u;
         f[u] = 0;
-        par[u] = 0;
-        if (k < n) {
-            r[u] = stage[tid * PI + u];
-            const uint32_t p = parent_of(r[u].box, k, refine);
-            par[u] = p;
-            const uint32_t sp = sub_off[2 * p + 1];
-            if (sp < par_off[p + 1]) f[u] = rec_less(r[u], split_list[sp], axis) ? 0u : 1u;
+        seg[u] = 0;
+        if (i0 + u < nrec) {
+            const uint32_t k = kt + i0 + u;
+            while (k >= s_off[sj + 1]) ++sj;
+            r[u] = stage[i0 + u];
+            seg[u] = sj;
+            const uint32_t rank = A.axis ? r[u].y : r[u].x;
+            f[u] = (rank >= s_split[sj]) ? 1u : 0u;
         }
         cnt += f[u];
     }
@@ -181,15 +350,15 @@ __global__ void __launch_bounds__(PT) k_partition(const Rec* __restrict__ list, 
     if (tid < 32) {
         uint32_t prefix = 0;
         if (tile == 0) {
-            if (tid == 0) atomicExch(&tstate[0], ST_PRE | agg);
+            if (tid == 0) atomicExch(&A.tstate[0], ST_PRE | agg);
         } else {
-            if (tid == 0) atomicExch(&tstate[tile], ST_AGG | agg);
+            if (tid == 0) atomicExch(&A.tstate[tile], ST_AGG | agg);
             int64_t j = (int64_t)tile - 1 - tid;
             for (;;) {
                 unsigned long long s = 0;
                 if (j >= 0) {
                     do {
-                        s = *((volatile unsigned long long*)&tstate[j]);
+                        s = *((volatile unsigned long long*)&A.tstate[j]);
                     } while ((s & ST_MASK) == 0);
                 } else {
                     s = ST_PRE;                     // before tile 0: inclusive prefix 0
@@ -202,7 +371,7 @@ __global__ void __launch_bounds__(PT) k_partition(const Rec* __restrict__ list, 
                 if (pre) break;
                 j -= 32;
             }
-            if (tid == 0) atomicExch(&tstate[tile], ST_PRE | (prefix + agg));
+            if (tid == 0) atomicExch(&A.tstate[tile], ST_PRE | (prefix + agg));
         }
         if (tid == 0) s_prefix = prefix;
     }
@@ -210,14 +379,12 @@ __global__ void __launch_bounds__(PT) k_partition(const Rec* __restrict__ list, 
     uint32_t g = s_prefix + excl;             // G(k) for the first item of this thread
 #pragma unroll
     for (int u = 0; u < PI; ++u) {
-        const int64_t k = k0 + u;
-        if (k < n) {
-            const uint32_t p = par[u];
-            const uint32_t hb = g - Gp[p];    // highs before k inside p
-            const uint32_t dst = f[u] ? sub_off[2 * p + 1] + hb : (uint32_t)k - hb;
-            Rec o = r[u];
-            o.box = 2 * p + f[u];
-            out[dst] = o;
+        if (i0 + u < nrec) {
+            const uint32_t k = kt + i0 + u;
+            const uint32_t j = seg[u];
+            const uint32_t hb = g - s_gp[j];  // highs before k inside its segment
+            const uint32_t dst = f[u] ? s_hi[j] + hb : k - hb;
+            A.out[dst] = r[u];
         }
         g += f[u];
     }
@@ -225,14 +392,15 @@ __global__ void __launch_bounds__(PT) k_partition(const Rec* __restrict__ list, 
 
 // A2 (part 1): tight bounding box from the segment endpoints of both sorted lists;
 // centre = 0.5 (min + max) (DESIGN R8).  Radius reset for part 2.
-__global__ void k_bbox(const Rec* __restrict__ xl, const Rec* __restrict__ yl,
-                       const uint32_t* __restrict__ off, int64_t nb, double* __restrict__ cx,
-                       double* __restrict__ cy, double* __restrict__ r)
+__global__ void k_bbox(const uint2* __restrict__ xl, const uint2* __restrict__ yl, const double* __restrict__ xcs,
+                       const double* __restrict__ ycs, const uint32_t* __restrict__ off, int64_t b0, int64_t b1,
+                       double* __restrict__ cx, double* __restrict__ cy, double* __restrict__ r)
 {
-    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nb) return;
-    uint32_t s = off[b], e = off[b + 1];
-    double xmin = xl[s].x, xmax = xl[e - 1].x, ymin = yl[s].y, ymax = yl[e - 1].y;
+    const int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= b1) return;
+    const uint32_t s = off[b], e = off[b + 1];
+    const double xmin = xcs[xl[s].x], xmax = xcs[xl[e - 1].x];
+    const double ymin = ycs[yl[s].y], ymax = ycs[yl[e - 1].y];
     cx[b] = __dmul_rn(0.5, __dadd_rn(xmin, xmax));
     cy[b] = __dmul_rn(0.5, __dadd_rn(ymin, ymax));
     r[b] = 0.0;
@@ -250,43 +418,52 @@ struct RadArgs {
     const double* cy[FMM2D_MAXL + 1];
     double* r[FMM2D_MAXL + 1];
 };
-__global__ void __launch_bounds__(FIN_T) k_finish(const Rec* __restrict__ yl, int64_t n, int L,
-                                                  const uint32_t* __restrict__ offL, uint32_t* __restrict__ perm,
+__global__ void __launch_bounds__(FIN_T) k_finish(const uint2* __restrict__ yl, const uint32_t* __restrict__ oy,
+                                                  const double* __restrict__ xcs, const double* __restrict__ ycs,
+                                                  uint32_t k0, uint32_t k1, int L, const uint32_t* __restrict__ offL,
+                                                  uint32_t lf0, uint32_t lf1, uint32_t* __restrict__ perm,
                                                   double4* __restrict__ src, RadArgs A)
 {
     __shared__ uint32_t sleaf[FIN_T];
+    __shared__ uint32_t s_lo, s_hi;
     __shared__ double wmax[FIN_T / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t k0 = (int64_t)blockIdx.x * FIN_T;
-    const int64_t k = k0 + tid;
-    const int nvalid = (int)((n - k0) < FIN_T ? (n - k0) : FIN_T);
-    const bool valid = k < n;
+    const uint32_t kb = k0 + blockIdx.x * FIN_T;
+    const uint32_t k = kb + tid;
+    const int nvalid = (int)min((uint32_t)FIN_T, k1 - kb);
+    const bool valid = k < k1;
+    if (tid == 0) {
+        const uint32_t lo = seg_search(offL, lf0, lf1, kb);
+        s_lo = lo;
+        s_hi = seg_search(offL, lo, lf1, kb + nvalid - 1) + 1;
+    }
+    __syncthreads();
     double x = 0.0, y = 0.0;
     uint32_t leaf = 0;
     if (valid) {
-        Rec r = yl[k];
-        leaf = (L > 0) ? parent_of(r.box, k, offL) : 0u;
-        x = r.x;
-        y = r.y;
-        perm[k] = r.idx;
+        const uint2 r = yl[k];
+        leaf = seg_search(offL, s_lo, s_hi, k);
+        x = xcs[r.x];
+        y = ycs[r.y];
+        perm[k] = oy[r.y];
         src[k] = make_double4(x, y, 0.0, 0.0);
     }
     sleaf[tid] = leaf;
     __syncthreads();
-    const uint32_t lf0 = sleaf[0], lf1 = sleaf[nvalid - 1];
+    const uint32_t l0 = sleaf[0], l1 = sleaf[nvalid - 1];
     for (int l = L; l >= 0; --l) {
         const int sh = 2 * (L - l);
         const uint32_t box = leaf >> sh;
         double d = 0.0;
         if (valid) d = rn_dist2(x, y, A.cx[l][box], A.cy[l][box]);     // squared; sqrt below
-        if ((lf0 >> sh) == (lf1 >> sh)) {                 // block-uniform (warp-uniform too)
+        if ((l0 >> sh) == (l1 >> sh)) {                   // block-uniform (warp-uniform too)
             for (int o = 16; o; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
             if (lane == 0) wmax[warp] = d;
             __syncthreads();
             if (tid == 0) {
                 double m = wmax[0];
                 for (int w = 1; w < FIN_T / 32; ++w) m = fmax(m, wmax[w]);
-                atomicMax((unsigned long long*)(A.r[l] + (lf0 >> sh)), (unsigned long long)__double_as_longlong(m));
+                atomicMax((unsigned long long*)(A.r[l] + (l0 >> sh)), (unsigned long long)__double_as_longlong(m));
             }
             __syncthreads();
         } else {
@@ -304,7 +481,7 @@ __global__ void __launch_bounds__(FIN_T) k_finish(const Rec* __restrict__ yl, in
     }
 }
 
-// r = sqrt_rn(max squared distance), every box of every level
+// r = sqrt_rn(max squared distance)
 __global__ void k_sqrt(double* __restrict__ r, int64_t nb)
 {
     int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -314,6 +491,16 @@ __global__ void k_sqrt(double* __restrict__ r, int64_t nb)
 inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
 }  // namespace
+
+// r = sqrt_rn(max squared distance) for every box of the plan (after the cross-rank
+// max of the replicated top levels in a sharded build)
+int finish_radii(fmm2d_plan* P)
+{
+    k_sqrt<<<grid_for(P->nbox_total, 256), 256, 0, P->stream>>>(P->r, P->nbox_total);
+    fmm2d::note_launch();
+    FMM2D_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
 
 int build_tree(fmm2d_plan* P, const double2* z)
 {
@@ -341,24 +528,27 @@ int build_tree(fmm2d_plan* P, const double2* z)
     P->stats.max_leaf = (int)((n + nboxes(L) - 1) / nboxes(L));
 
     // ---- scratch
-    double *xs, *ys;
-    uint64_t *kx, *ky, *ksort;
-    uint32_t *iota, *ord, *hs, *Gp;
-    Rec *xl, *yl, *tmp;
-    int* bad;
+    double *xs, *ys, *xcs, *ycs;
+    uint32_t *kx, *ky, *ksort, *iota, *ox, *oy, *rx, *ry, *hs, *Gp;
+    uint64_t *k64, *k64s;
+    uint2 *xl, *yl, *tmp;
+    Bounds* bnd;
+    int* ovf;
     unsigned long long* tstate;
     unsigned int* ticket;
     void* scratch = nullptr;
-    size_t sort_bytes = 0, scan_bytes = 0;
+    size_t sort32 = 0, sort64 = 0, scan_bytes = 0;
     const int64_t npmax = (L > 0) ? 2 * nboxes(L - 1) : 1;        // parents of the widest step
     const int64_t ntiles = (n + PTILE - 1) / PTILE;
-    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr,
-                                    (uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 64, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, sort32, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int)n, 0, 32, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, sort64, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int)n, 0, 64, st);
     cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)npmax, st);
-    size_t cub_bytes = std::max(sort_bytes, scan_bytes);
+    const size_t cub_bytes = std::max(std::max(sort32, sort64), scan_bytes);
     std::vector<void*> tmp_ptrs;
     auto talloc = [&](void** p, size_t b) -> int {
-        cudaError_t e = cudaMallocAsync(p, b, st);
+        cudaError_t e = cudaMallocAsync(p, b ? b : 16, st);
         if (e != cudaSuccess) return FMM2D_ENOMEM;
         tmp_ptrs.push_back(*p);
         return 0;
@@ -371,91 +561,159 @@ int build_tree(fmm2d_plan* P, const double2* z)
     do {
         if ((rc = talloc((void**)&xs, 8 * n))) break;
         if ((rc = talloc((void**)&ys, 8 * n))) break;
-        if ((rc = talloc((void**)&kx, 8 * n))) break;
-        if ((rc = talloc((void**)&ky, 8 * n))) break;
-        if ((rc = talloc((void**)&ksort, 8 * n))) break;
+        if ((rc = talloc((void**)&xcs, 8 * n))) break;
+        if ((rc = talloc((void**)&ycs, 8 * n))) break;
+        if ((rc = talloc((void**)&kx, 4 * n))) break;
+        if ((rc = talloc((void**)&ky, 4 * n))) break;
+        if ((rc = talloc((void**)&ksort, 4 * n))) break;
         if ((rc = talloc((void**)&iota, 4 * n))) break;
-        if ((rc = talloc((void**)&ord, 4 * n))) break;
+        if ((rc = talloc((void**)&ox, 4 * n))) break;
+        if ((rc = talloc((void**)&oy, 4 * n))) break;
         if ((rc = talloc((void**)&hs, 4 * npmax))) break;
         if ((rc = talloc((void**)&Gp, 4 * npmax))) break;
         if ((rc = talloc((void**)&tstate, 8 * ntiles))) break;
         if ((rc = talloc((void**)&ticket, 4))) break;
-        if ((rc = talloc((void**)&xl, sizeof(Rec) * n))) break;
-        if ((rc = talloc((void**)&yl, sizeof(Rec) * n))) break;
-        if ((rc = talloc((void**)&tmp, sizeof(Rec) * n))) break;
-        if ((rc = talloc((void**)&bad, sizeof(int)))) break;
+        if ((rc = talloc((void**)&xl, sizeof(uint2) * n))) break;
+        if ((rc = talloc((void**)&yl, sizeof(uint2) * n))) break;
+        if ((rc = talloc((void**)&tmp, sizeof(uint2) * n))) break;
+        if ((rc = talloc((void**)&bnd, sizeof(Bounds)))) break;
+        if ((rc = talloc((void**)&ovf, 2 * sizeof(int)))) break;
         if ((rc = talloc(&scratch, cub_bytes))) break;
     } while (0);
     if (rc) { tfree(); return rc; }
+    rx = kx;          // reused once the sorts are done
+    ry = ky;
 
     auto body = [&]() -> int {
-        FMM2D_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
-        k_canon<<<grid_for(n, BS), BS, 0, st>>>(z, n, xs, ys, kx, ky, iota, bad);
+        // ---- A0: validate, canonical coordinates, ranges
+        {
+            Bounds h;
+            h.xmin = h.ymin = ~0ull;
+            h.xmax = h.ymax = 0;
+            h.bad = 0;
+            FMM2D_CUDA_TRY(cudaMemcpyAsync(bnd, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+            const unsigned g = (unsigned)std::min<int64_t>(grid_for(n, CT), 148 * 8);
+            k_canon<<<g, CT, 0, st>>>(z, n, xs, ys, bnd);
+            fmm2d::note_launch();
+            FMM2D_CUDA_TRY(cudaGetLastError());
+            FMM2D_CUDA_TRY(cudaMemcpyAsync(&h, bnd, sizeof(h), cudaMemcpyDeviceToHost, st));
+            FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+            if (h.bad) return FMM2D_ENONFINITE;
+        }
+        // ---- presort: 32-bit monotone keys, stable (ties in idx order), equal-key runs fixed
+        k_keys32<<<grid_for(n, BS), BS, 0, st>>>(xs, ys, n, bnd, kx, ky, iota);
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), st));
+        const bool force64 = (P->flags & FMM2D_TREE_KEY64) != 0;
+        int h_ovf[2] = {force64 ? 1 : 0, force64 ? 1 : 0};
+        if (!force64) {
+            size_t sb = cub_bytes;
+            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, kx, ksort, iota, ox, (int)n, 0, 32, st));
+            k_fix_runs<<<grid_for(n, BS), BS, 0, st>>>(ksort, n, xs, ox, ovf);
+            fmm2d::note_launch();
+            sb = cub_bytes;
+            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, ky, ksort, iota, oy, (int)n, 0, 32, st));
+            k_fix_runs<<<grid_for(n, BS), BS, 0, st>>>(ksort, n, ys, oy, ovf + 1);
+            fmm2d::note_launch();
+            FMM2D_CUDA_TRY(cudaGetLastError());
+            FMM2D_CUDA_TRY(cudaMemcpyAsync(h_ovf, ovf, sizeof(h_ovf), cudaMemcpyDeviceToHost, st));
+            FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+        }
+        for (int ax = 0; ax < 2; ++ax) {
+            if (!h_ovf[ax]) continue;
+            // heavy ties: full 64-bit sort of the orderable coordinate bits for this axis
+            void* p64 = nullptr;
+            FMM2D_CUDA_TRY(cudaMallocAsync(&p64, 16 * n, st));
+            k64 = (uint64_t*)p64;
+            k64s = k64 + n;
+            k_keys64<<<grid_for(n, BS), BS, 0, st>>>(ax ? ys : xs, n, k64, iota);
+            fmm2d::note_launch();
+            size_t sb = cub_bytes;
+            cudaError_t e = cub::DeviceRadixSort::SortPairs(scratch, sb, k64, k64s, iota, ax ? oy : ox, (int)n, 0, 64,
+                                                            st);
+            cudaFreeAsync(p64, st);
+            FMM2D_CUDA_TRY(e);
+        }
+        P->stats.tree_key64 = h_ovf[0] + 2 * h_ovf[1];
+        k_ranks<<<grid_for(n, BS), BS, 0, st>>>(ox, oy, n, rx, ry);
+        fmm2d::note_launch();
+        k_make_lists<<<grid_for(n, BS), BS, 0, st>>>(ox, oy, rx, ry, xs, ys, n, xl, yl, xcs, ycs);
         fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
-        int h_bad = 0;
-        FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-        FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
-        if (h_bad) return FMM2D_ENONFINITE;
-        // presort (stable LSD radix: ties stay in index order)
-        size_t sb = cub_bytes;
-        FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, kx, ksort, iota, ord, (int)n, 0, 64, st));
-        k_make_recs<<<grid_for(n, BS), BS, 0, st>>>(ksort, ord, ys, 0, n, xl);
+        k_bbox<<<1, 32, 0, st>>>(xl, yl, xcs, ycs, P->boff + P->obase[0], 0, 1, P->cx + P->base[0],
+                                 P->cy + P->base[0], P->r + P->base[0]);
         fmm2d::note_launch();
-        sb = cub_bytes;
-        FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, ky, ksort, iota, ord, (int)n, 0, 64, st));
-        k_make_recs<<<grid_for(n, BS), BS, 0, st>>>(ksort, ord, xs, 1, n, yl);
-        fmm2d::note_launch();
-        FMM2D_CUDA_TRY(cudaGetLastError());
-        k_bbox<<<1, 32, 0, st>>>(xl, yl, P->boff + P->obase[0], 1, P->cx + P->base[0], P->cy + P->base[0],
-                                 P->r + P->base[0]);
-        fmm2d::note_launch();
-        // one split step: partition `list` inside the parent segments (par_off) into the
-        // sub-segments sub_off, comparing against `split` on `axis`
-        auto split_step = [&](const Rec* list, const Rec* split, const uint32_t* refine, const uint32_t* par_off,
-                              const uint32_t* sub_off, int64_t np, int axis, Rec* out) -> int {
-            k_high_sizes<<<grid_for(np, BS), BS, 0, st>>>(par_off, sub_off, np, hs);
+        // one split step: partition `list` inside the parent segments (par_off) [p0, p1),
+        // positions [k0, k1), into the sub-segments sub_off, comparing ranks on `axis`
+        // against `split`
+        auto split_step = [&](const uint2* list, const uint2* split, const uint32_t* par_off, const uint32_t* sub_off,
+                              int64_t p0, int64_t p1, uint32_t k0, uint32_t k1, int axis, uint2* out) -> int {
+            const int64_t np = p1 - p0;
+            k_high_sizes<<<grid_for(np, BS), BS, 0, st>>>(par_off, sub_off, p0, np, hs);
             fmm2d::note_launch();
             size_t b2 = cub_bytes;
             FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, b2, hs, Gp, (int)np, st));
-            FMM2D_CUDA_TRY(cudaMemsetAsync(tstate, 0, 8 * ntiles, st));
+            // positions of the range: par_off[p0] .. par_off[p1] (read back once per level below)
+            SplitArgs A;
+            A.list = list;
+            A.split_list = split;
+            A.par_off = par_off;
+            A.sub_off = sub_off;
+            A.Gp = Gp;
+            A.out = out;
+            A.tstate = tstate;
+            A.ticket = ticket;
+            A.p0 = (uint32_t)p0;
+            A.p1 = (uint32_t)p1;
+            A.k0 = k0;
+            A.k1 = k1;
+            A.axis = axis;
+            const int64_t nt = ((int64_t)A.k1 - A.k0 + PTILE - 1) / PTILE;
+            FMM2D_CUDA_TRY(cudaMemsetAsync(tstate, 0, 8 * nt, st));
             FMM2D_CUDA_TRY(cudaMemsetAsync(ticket, 0, 4, st));
-            k_partition<<<(unsigned)ntiles, PT, 0, st>>>(list, split, refine, par_off, sub_off, Gp, axis, n, out,
-                                                        tstate, ticket);
+            k_partition<<<(unsigned)nt, PT, 0, st>>>(A);
             fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
             return 0;
         };
+        // levels 0..kpart-1: every box (replicated on every rank); levels >= kpart: the
+        // rank's own subtrees only (the whole tree on one GPU, kpart = 0)
         for (int l = 0; l < L; ++l) {
             const uint32_t* O = P->boff + P->obase[l];
             const uint32_t* H = P->boff + hbase[l];
             const uint32_t* C = P->boff + P->obase[l + 1];
-            // x-split: the y-list (ids: half-level l-1/2, refined by O) is partitioned by
-            // (x, idx) against the x-list's first high record
-            const uint32_t* yref = (l == 0) ? nullptr : O;
-            FMM2D_TRY(split_step(yl, xl, yref, O, H, nboxes(l), 0, tmp));
+            const int64_t b0 = (l < P->kpart) ? 0 : P->own_lo(l), b1 = (l < P->kpart) ? nboxes(l) : P->own_hi(l);
+            const uint32_t k0 = (l < P->kpart) ? 0u : P->pos0, k1 = (l < P->kpart) ? (uint32_t)n : P->pos1;
+            // x-split: the y-list (grouped by level-l boxes) is partitioned by rx against
+            // the x-list's first high record of each box
+            FMM2D_TRY(split_step(yl, xl, O, H, b0, b1, k0, k1, 0, tmp));
             std::swap(yl, tmp);
-            // y-split of each half: the x-list (ids: level l, refined by H) is partitioned
-            // by (y, idx) against the y-list's first high record
-            FMM2D_TRY(split_step(xl, yl, H, H, C, 2 * nboxes(l), 1, tmp));
+            // y-split of each half: the x-list (grouped by half-level boxes) is partitioned
+            // by ry against the y-list's first high record of each half
+            FMM2D_TRY(split_step(xl, yl, H, C, 2 * b0, 2 * b1, k0, k1, 1, tmp));
             std::swap(xl, tmp);
-            int64_t nb = nboxes(l + 1);
-            k_bbox<<<grid_for(nb, BS), BS, 0, st>>>(xl, yl, C, nb, P->cx + P->base[l + 1], P->cy + P->base[l + 1],
-                                                    P->r + P->base[l + 1]);
+            const int64_t c0 = P->box_lo(l + 1), c1 = P->box_hi(l + 1);
+            k_bbox<<<grid_for(c1 - c0, BS), BS, 0, st>>>(xl, yl, xcs, ycs, C, c0, c1, P->cx + P->base[l + 1],
+                                                         P->cy + P->base[l + 1], P->r + P->base[l + 1]);
             fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
         }
+        // radii of every level from the own positions (squared; a sharded build
+        // max-reduces the replicated top levels across ranks before the square root)
+        FMM2D_CUDA_TRY(cudaMemsetAsync(P->r, 0, sizeof(double) * P->base[P->kpart + 1], st));
         RadArgs A;
         for (int l = 0; l <= L; ++l) {
             A.cx[l] = P->cx + P->base[l];
             A.cy[l] = P->cy + P->base[l];
             A.r[l] = P->r + P->base[l];
         }
-        k_finish<<<grid_for(n, FIN_T), FIN_T, 0, st>>>(yl, n, L, P->boff + P->obase[L], P->perm, P->src, A);
-        fmm2d::note_launch();
-        k_sqrt<<<grid_for(P->nbox_total, BS), BS, 0, st>>>(P->r, P->nbox_total);
+        const uint32_t nown = P->pos1 - P->pos0;
+        k_finish<<<grid_for(nown, FIN_T), FIN_T, 0, st>>>(yl, oy, xcs, ycs, P->pos0, P->pos1, L,
+                                                          P->boff + P->obase[L], (uint32_t)P->box_lo(L),
+                                                          (uint32_t)P->box_hi(L), P->perm, P->src, A);
         fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
+        if (P->nranks == 1) FMM2D_TRY(finish_radii(P));
         return 0;
     };
     rc = body();

@@ -26,6 +26,7 @@ PMAX = 32
 HOST_PTRS = 0x1
 REAL_STRENGTHS = 0x2
 SYMMETRIC_P2P = 0x4
+TREE_KEY64 = 0x8
 
 EXPORT_PERM, EXPORT_OFFSETS, EXPORT_DISCS, EXPORT_STRONG, EXPORT_WEAK, EXPORT_MPOLE, EXPORT_LOCAL, \
     EXPORT_STATS = range(1, 9)
@@ -119,7 +120,7 @@ class Fmm2d:
 
     def __init__(self, z, theta: float = 0.5, p: int = 17, leaf_target: int = 40, nlevels: int = -1,
                  real_strengths: bool = False, device: int | None = None, stream=None,
-                 symmetric_p2p: bool = False):
+                 symmetric_p2p: bool = False, tree_key64: bool = False):
         L = lib()
         import torch
         host = not (isinstance(z, torch.Tensor) and z.is_cuda)
@@ -137,7 +138,7 @@ class Fmm2d:
         opt.leaf_target = int(leaf_target)
         opt.nlevels = int(nlevels)
         opt.flags = ((HOST_PTRS if host else 0) | (REAL_STRENGTHS if real_strengths else 0)
-                     | (SYMMETRIC_P2P if symmetric_p2p else 0))
+                     | (SYMMETRIC_P2P if symmetric_p2p else 0) | (TREE_KEY64 if tree_key64 else 0))
         opt.device = int(device)
         opt.stream = ctypes.c_void_p(stream.cuda_stream)
         self._opt = opt
@@ -228,7 +229,7 @@ class Fmm2d:
     def stats(self) -> dict:
         s = np.frombuffer(self._export(EXPORT_STATS), np.float64)
         keys = ["n", "L", "p", "theta", "weak_pairs", "strong_leaf_pairs", "min_leaf", "max_leaf",
-                "t_build_ms", "t_tree_ms", "t_lists_ms", "nboxes", "launches", "p2p_pairs"]
+                "t_build_ms", "t_tree_ms", "t_lists_ms", "nboxes", "launches", "p2p_pairs", "tree_key64"]
         return {k: float(v) for k, v in zip(keys, s)}
 
     def close(self):

@@ -99,6 +99,29 @@ def test_tree_tiny_and_forced_levels(orc):
         _check_structure(gp, op, L)
 
 
+def test_tree_presort_paths(orc):
+    """The 32-bit-key presort with equal-key runs fixed in place (DESIGN 6.1) and the
+    64-bit-key fallback build the same tree as the oracle.  Near-ties: distinct x that
+    share a 32-bit key bucket (runs of 2..32, fixed in place); heavy ties: runs longer
+    than 32 (the axis falls back to 64-bit keys)."""
+    from paper_1006_2269_b200 import Fmm2d
+    rng = np.random.default_rng(17)
+    n = 10_000
+    x = np.round(rng.random(n) * 1000) / 1000 + rng.random(n) * 1e-13     # ~10 per bucket
+    y = rng.random(n)
+    near = x + 1j * y
+    heavy = np.round(rng.random(n) * 100) / 100 + 1j * y                     # ~100 per value
+    for z, key64_expected in ((near, 0), (heavy, 1)):
+        L = 4
+        op = orc.plan(z, 0.5, L)
+        gp = _gpu_plan(z, 0.5, 8, L)
+        assert int(gp.stats()["tree_key64"]) == key64_expected
+        _check_structure(gp, op, L)
+        g64 = Fmm2d(torch.from_numpy(z).cuda(), theta=0.5, p=8, nlevels=L, tree_key64=True)
+        assert int(g64.stats()["tree_key64"]) == 3
+        _check_structure(g64, op, L)
+
+
 EVAL_CASES = [
     ("C1", "C1", None, 0.5, 17),
     ("C2-t.5-p17", "C2", None, 0.5, 17),
