@@ -115,6 +115,46 @@ FMM2D_API int fmm2d_eval_timed(fmm2d_plan* plan, const double* m, double* phi, d
  * threads; CUB's internal launches are not counted). */
 FMM2D_API int64_t fmm2d_launch_count(void);
 
+/* ---- several GPUs ------------------------------------------
+ * The pass is partitioned by the balanced tree's level-k subtrees: with
+ * P ranks (a power of two), k is the smallest level with P | 4^k and rank r owns the
+ * level-k subtrees [r 4^k/P, (r+1) 4^k/P) -- equal point counts up to 1 per box.
+ * Multi-process (one process per GPU, NCCL): every rank calls fmm2d_build with the
+ * SAME full z, n and options except opt.rank, with opt.nranks = P and opt.nccl_id =
+ * the 128-byte ncclUniqueId made by fmm2d_nccl_unique_id on one rank and broadcast
+ * (e.g. torch.distributed).  fmm2d_build is then collective (all ranks must call it),
+ * and so is every fmm2d_eval: each rank passes the same full m and receives Phi, Phi'
+ * at the input positions of the sources it owns (other entries are not written).
+ * The union over ranks equals the one-GPU result.  Errors: ENOTSUP (P not a power of
+ * two, or the tree has no level below k), ENCCL (libnccl.so.2 missing or a NCCL
+ * failure). */
+
+/* Create a NCCL unique id (128 bytes at out) for a multi-process build. */
+FMM2D_API int fmm2d_nccl_unique_id(void* out);
+
+/* Partition facts without a GPU (host arithmetic only; offsets are a function of n):
+ * info[0] L, [1] partition level k, [2..3] own leaves [lo, hi), [4..5] own source
+ * positions in leaf order [lo, hi), [6..7] own level-k subtrees [lo, hi).
+ * opt supplies theta, p, leaf_target and nlevels (validated as in fmm2d_build). */
+FMM2D_API int fmm2d_partition_info(int64_t n, const fmm2d_options* opt, int nranks, int rank, int64_t* info);
+
+/* Loopback partition on ONE device (tests of the partitioned path): builds nshards
+ * plans, plans[i] being rank i of nshards, in one process on opt->device and
+ * opt->stream; every transfer between ranks is a device copy.  Device pointers only
+ * (FMM2D_HOST_PTRS: ENOTSUP).  out: array of nshards plan pointers (each freed with
+ * fmm2d_free). */
+FMM2D_API int fmm2d_build_shards(const double* z, int64_t n, const fmm2d_options* opt, int nshards,
+                                 fmm2d_plan** out);
+/* Evaluate all shards of a loopback build; every rank writes its own entries of phi
+ * and dphi, so on return (stream-ordered) they hold the complete result. */
+FMM2D_API int fmm2d_eval_shards(fmm2d_plan* const* plans, int nshards, const double* m, double* phi,
+                                double* dphi);
+
+/* Halo facts of a plan: info[0] imported leaves, [1] imported multipoles (per eval),
+ * [2] exported leaves, [3] exported multipoles, [4] nranks, [5] rank, [6] k,
+ * [7..8] own positions [lo, hi). */
+FMM2D_API int fmm2d_halo_info(const fmm2d_plan* plan, int64_t* info);
+
 /* Free the plan and all its device memory.  NULL-safe. */
 FMM2D_API void fmm2d_free(fmm2d_plan* plan);
 

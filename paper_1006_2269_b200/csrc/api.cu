@@ -18,6 +18,11 @@ void fmm2d_set_last_cuda_error(cudaError_t e, const char* what, const char* file
     snprintf(g_last_err, sizeof(g_last_err), "%s: %s (%s:%d)", cudaGetErrorString(e), what, file, line);
 }
 
+void fmm2d_set_last_error_text(const char* msg, const char* what, const char* file, int line)
+{
+    snprintf(g_last_err, sizeof(g_last_err), "%s: %s (%s:%d)", msg ? msg : "", what, file, line);
+}
+
 namespace fmm2d {
 
 static std::atomic<int64_t> g_launches{0};
@@ -83,6 +88,7 @@ void fmm2d_free(fmm2d_plan* P)
     cudaSetDevice(P->device);
     for (void* p : P->allocs) cudaFreeAsync(p, P->stream);
     cudaStreamSynchronize(P->stream);
+    shard_free(P);
     delete P;
 }
 
@@ -95,15 +101,12 @@ static int depth_rule(int64_t n, int leaf_target)
     return L;
 }
 
-int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan** out)
+// validated depth of the tree for n points (or a negative error code)
+static int plan_depth(int64_t n, const fmm2d_options* opt)
 {
-    if (!out) return FMM2D_EINVAL;
-    *out = nullptr;
-    if (!z || !opt) return FMM2D_EINVAL;
     if (!(opt->theta > 0.0 && opt->theta < 1.0)) return FMM2D_EINVAL;        // P:119, not clamped
     if (opt->p < 1 || opt->p > FMM2D_PMAX) return FMM2D_EINVAL;
     if (n < 1 || n >= ((int64_t)1 << 31)) return FMM2D_EINVAL;
-    if (opt->nranks != 1 || opt->rank != 0) return FMM2D_ENOTSUP;
     int L;
     if (opt->nlevels >= 0) {
         L = opt->nlevels;
@@ -112,6 +115,22 @@ int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan
         if (opt->leaf_target < 1) return FMM2D_EINVAL;
         L = depth_rule(n, opt->leaf_target);
         while (L > 0 && n < nboxes(L)) --L;
+    }
+    return L;
+}
+
+// Stage 1 of a build: plan fields, partition, allocations, the tree (A0-A2).  For one
+// GPU it also runs the lists (A3).  Sharded plans continue in shard_build_rest.
+static int build_stage_tree(const double* z, int64_t n, const fmm2d_options* opt, int nranks, int rank,
+                            const void* nccl_id, fmm2d_plan** out)
+{
+    *out = nullptr;
+    const int L = plan_depth(n, opt);
+    if (L < 0) return L;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return FMM2D_EINVAL;
+    if (nranks > 1) {                                   // partitionable? (before any device work)
+        const int k = partition_level(nranks);
+        if (k < 0 || L <= k) return FMM2D_ENOTSUP;
     }
     if (cudaSetDevice(opt->device) != cudaSuccess) return FMM2D_ECUDA;
     fmm2d_plan* P = new (std::nothrow) fmm2d_plan();
@@ -130,6 +149,7 @@ int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan
     P->pos1 = (uint32_t)n;
 
     auto body = [&]() -> int {
+        FMM2D_TRY(shard_setup(P, nranks, rank, nccl_id));
         cudaEvent_t e0, e1, e2;
         FMM2D_CUDA_TRY(cudaEventCreate(&e0));
         FMM2D_CUDA_TRY(cudaEventCreate(&e1));
@@ -165,8 +185,10 @@ int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan
         if (zstage) cudaFreeAsync(zstage, P->stream);
         if (rc) return rc;
         FMM2D_CUDA_TRY(cudaEventRecord(e1, P->stream));
-        FMM2D_TRY(build_lists(P));
-        FMM2D_TRY(prepare_near_sym(P));
+        if (P->nranks == 1) {
+            FMM2D_TRY(build_lists(P));
+            FMM2D_TRY(prepare_near_sym(P));
+        }
         FMM2D_CUDA_TRY(cudaEventRecord(e2, P->stream));
         FMM2D_CUDA_TRY(cudaEventSynchronize(e2));
         float a = 0, b = 0;
@@ -175,7 +197,6 @@ int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan
         P->stats.t_tree_ms = a;
         P->stats.t_lists_ms = b;
         P->stats.t_build_ms = a + b;
-        // P2P pair count (ordered, including i == j exclusions already removed)
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         cudaEventDestroy(e2);
@@ -190,57 +211,125 @@ int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan
     return 0;
 }
 
-static int eval_impl(fmm2d_plan* P, const double* m, double* phi, double* dphi, cudaEvent_t* ev)
+int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan** out)
 {
-    if (!P || !m) return FMM2D_EINVAL;
-    FMM2D_CUDA_TRY(cudaSetDevice(P->device));
-    const int64_t n = P->n;
-    const bool host = (P->flags & FMM2D_HOST_PTRS) != 0;
+    if (!out) return FMM2D_EINVAL;
+    *out = nullptr;
+    if (!z || !opt) return FMM2D_EINVAL;
+    const int R = opt->nranks, r = opt->rank;
+    if (R < 1 || r < 0 || r >= R) return FMM2D_EINVAL;
+    if (R > 1 && !opt->nccl_id) return FMM2D_EINVAL;
+    fmm2d_plan* P = nullptr;
+    FMM2D_TRY(build_stage_tree(z, n, opt, R, r, opt->nccl_id, &P));
+    if (R > 1) {
+        const int rc = shard_build_rest(&P, 1);
+        if (rc) {
+            fmm2d_free(P);
+            return rc;
+        }
+    }
+    *out = P;
+    return 0;
+}
+
+int fmm2d_build_shards(const double* z, int64_t n, const fmm2d_options* opt, int nshards, fmm2d_plan** out)
+{
+    if (!out || !z || !opt || nshards < 1 || nshards > 64) return FMM2D_EINVAL;
+    if (opt->flags & FMM2D_HOST_PTRS) return FMM2D_ENOTSUP;
+    for (int i = 0; i < nshards; ++i) out[i] = nullptr;
+    int rc = 0;
+    for (int i = 0; i < nshards && !rc; ++i) rc = build_stage_tree(z, n, opt, nshards, i, nullptr, &out[i]);
+    if (!rc && nshards > 1) rc = shard_build_rest(out, nshards);
+    if (rc) {
+        for (int i = 0; i < nshards; ++i) {
+            fmm2d_free(out[i]);
+            out[i] = nullptr;
+        }
+    }
+    return rc;
+}
+
+// One evaluation pass over the plans of this process: one plan (one GPU, or one
+// rank of an NCCL-sharded build) or every rank of a loopback build, stage by stage.
+static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi, double* dphi, cudaEvent_t* ev)
+{
+    if (!Ps || np < 1 || !m) return FMM2D_EINVAL;
+    for (int i = 0; i < np; ++i)
+        if (!Ps[i]) return FMM2D_EINVAL;
+    fmm2d_plan* P0 = Ps[0];
+    FMM2D_CUDA_TRY(cudaSetDevice(P0->device));
+    const int64_t n = P0->n;
+    const bool host = (P0->flags & FMM2D_HOST_PTRS) != 0;
+    const bool sharded = P0->nranks > 1;
     const double2* md = (const double2*)m;
     double2* phid = (double2*)phi;
     double2* dphid = (double2*)dphi;
     if (host) {
-        if (!P->mstage) {
-            FMM2D_TRY(dev_alloc(P, (void**)&P->mstage, sizeof(double2) * n));
-            FMM2D_TRY(dev_alloc(P, (void**)&P->phistage, sizeof(double2) * n));
-            FMM2D_TRY(dev_alloc(P, (void**)&P->dphistage, sizeof(double2) * n));
+        if (np != 1) return FMM2D_ENOTSUP;
+        if (!P0->mstage) {
+            FMM2D_TRY(dev_alloc(P0, (void**)&P0->mstage, sizeof(double2) * n));
+            FMM2D_TRY(dev_alloc(P0, (void**)&P0->phistage, sizeof(double2) * n));
+            FMM2D_TRY(dev_alloc(P0, (void**)&P0->dphistage, sizeof(double2) * n));
         }
-        FMM2D_CUDA_TRY(cudaMemcpyAsync(P->mstage, m, sizeof(double2) * n, cudaMemcpyHostToDevice, P->stream));
-        md = P->mstage;
-        phid = phi ? P->phistage : nullptr;
-        dphid = dphi ? P->dphistage : nullptr;
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(P0->mstage, m, sizeof(double2) * n, cudaMemcpyHostToDevice, P0->stream));
+        md = P0->mstage;
+        phid = phi ? P0->phistage : nullptr;
+        dphid = dphi ? P0->dphistage : nullptr;
     }
-    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[0], P->stream));
-    FMM2D_TRY(gather_strengths(P, md));
-    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[1], P->stream));
-    FMM2D_TRY(run_upward(P));
-    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[2], P->stream));
-    FMM2D_TRY(run_m2l(P));
-    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[3], P->stream));
-    FMM2D_TRY(run_downward(P));
-    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[4], P->stream));
-    FMM2D_TRY(run_near(P, phid, dphid));
-    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[5], P->stream));
+    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[0], P0->stream));
+    for (int i = 0; i < np; ++i) {
+        FMM2D_TRY(gather_strengths(Ps[i], md));
+        if (sharded) FMM2D_TRY(shard_gather_halo(Ps[i], md));
+    }
+    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[1], P0->stream));
+    for (int i = 0; i < np; ++i) FMM2D_TRY(run_upward(Ps[i]));
+    if (sharded) {
+        FMM2D_TRY(shard_comm_top(Ps, np));
+        for (int i = 0; i < np; ++i) {
+            FMM2D_TRY(run_upward_top(Ps[i]));
+            FMM2D_TRY(shard_pack_mp(Ps[i]));
+        }
+        FMM2D_TRY(shard_comm_mp(Ps, np));
+        for (int i = 0; i < np; ++i) FMM2D_TRY(shard_unpack_mp(Ps[i]));
+    }
+    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[2], P0->stream));
+    for (int i = 0; i < np; ++i) FMM2D_TRY(run_m2l(Ps[i]));
+    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[3], P0->stream));
+    for (int i = 0; i < np; ++i) FMM2D_TRY(run_downward(Ps[i]));
+    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[4], P0->stream));
+    for (int i = 0; i < np; ++i) FMM2D_TRY(run_near(Ps[i], phid, dphid));
+    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[5], P0->stream));
     if (host) {
-        if (phi) FMM2D_CUDA_TRY(cudaMemcpyAsync(phi, phid, sizeof(double2) * n, cudaMemcpyDeviceToHost, P->stream));
-        if (dphi) FMM2D_CUDA_TRY(cudaMemcpyAsync(dphi, dphid, sizeof(double2) * n, cudaMemcpyDeviceToHost, P->stream));
-        FMM2D_CUDA_TRY(cudaStreamSynchronize(P->stream));
+        if (phi) FMM2D_CUDA_TRY(cudaMemcpyAsync(phi, phid, sizeof(double2) * n, cudaMemcpyDeviceToHost, P0->stream));
+        if (dphi) FMM2D_CUDA_TRY(cudaMemcpyAsync(dphi, dphid, sizeof(double2) * n, cudaMemcpyDeviceToHost, P0->stream));
+        FMM2D_CUDA_TRY(cudaStreamSynchronize(P0->stream));
     }
     return 0;
 }
 
 int fmm2d_eval(fmm2d_plan* P, const double* m, double* phi, double* dphi)
 {
-    return eval_impl(P, m, phi, dphi, nullptr);
+    if (P && P->nranks > 1 && !shard_has_comm(P)) return FMM2D_EINVAL;   // loopback: eval_shards
+    return eval_impl(&P, 1, m, phi, dphi, nullptr);
+}
+
+int fmm2d_eval_shards(fmm2d_plan* const* plans, int nshards, const double* m, double* phi, double* dphi)
+{
+    if (!plans || nshards < 1) return FMM2D_EINVAL;
+    for (int i = 0; i < nshards; ++i)
+        if (!plans[i] || plans[i]->nranks != nshards || plans[i]->rank != i || shard_has_comm(plans[i]))
+            return FMM2D_EINVAL;
+    return eval_impl(plans, nshards, m, phi, dphi, nullptr);
 }
 
 int fmm2d_eval_timed(fmm2d_plan* P, const double* m, double* phi, double* dphi, double* ms_out)
 {
     if (!P || !m || !ms_out) return FMM2D_EINVAL;
+    if (P->nranks > 1 && !shard_has_comm(P)) return FMM2D_EINVAL;
     FMM2D_CUDA_TRY(cudaSetDevice(P->device));
     cudaEvent_t ev[6];
     for (int i = 0; i < 6; ++i) FMM2D_CUDA_TRY(cudaEventCreate(&ev[i]));
-    int rc = eval_impl(P, m, phi, dphi, ev);
+    int rc = eval_impl(&P, 1, m, phi, dphi, ev);
     if (rc == 0) {
         cudaError_t e = cudaEventSynchronize(ev[5]);
         if (e != cudaSuccess) {
@@ -263,7 +352,47 @@ int fmm2d_eval_timed(fmm2d_plan* P, const double* m, double* phi, double* dphi, 
     return rc;
 }
 
+int fmm2d_nccl_unique_id(void* out)
+{
+    if (!out) return FMM2D_EINVAL;
+    return nccl_unique_id(out);
+}
+
+int fmm2d_partition_info(int64_t n, const fmm2d_options* opt, int nranks, int rank, int64_t* info)
+{
+    if (!opt || !info || nranks < 1 || rank < 0 || rank >= nranks) return FMM2D_EINVAL;
+    const int L = plan_depth(n, opt);
+    if (L < 0) return L;
+    int k = 0;
+    if (nranks > 1) {
+        k = partition_level(nranks);
+        if (k < 0 || L <= k) return FMM2D_ENOTSUP;
+    }
+    const int64_t nk = nboxes(k), nl = nboxes(L);
+    info[0] = L;
+    info[1] = k;
+    info[2] = nl / nranks * rank;                       // own leaves [info2, info3)
+    info[3] = nl / nranks * (rank + 1);
+    info[4] = (nranks == 1) ? 0 : box_start_host(n, k, nk / nranks * rank);    // own positions
+    info[5] = (nranks == 1 || rank + 1 == nranks) ? n : box_start_host(n, k, nk / nranks * (rank + 1));
+    info[6] = nk / nranks * rank;                       // own level-k subtrees
+    info[7] = nk / nranks * (rank + 1);
+    return 0;
+}
+
 int64_t fmm2d_launch_count(void) { return launch_count(); }
+
+int fmm2d_halo_info(const fmm2d_plan* P, int64_t* info)
+{
+    if (!P || !info) return FMM2D_EINVAL;
+    shard_halo_sizes(P, &info[0], &info[1], &info[2], &info[3]);
+    info[4] = P->nranks;
+    info[5] = P->rank;
+    info[6] = P->kpart;
+    info[7] = P->pos0;
+    info[8] = P->pos1;
+    return 0;
+}
 
 int fmm2d_plan_info(const fmm2d_plan* P, int64_t* n, int* nlevels, int* p, int64_t* weak_pairs,
                     int64_t* strong_leaf_pairs)

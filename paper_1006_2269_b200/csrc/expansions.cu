@@ -66,12 +66,12 @@ __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_dou
 
 // ---------------------------------------------------------------- P2M (A4)
 template <int P>
-__global__ void __launch_bounds__(128) k_p2m(int64_t nleaf, const uint32_t* __restrict__ off,
+__global__ void __launch_bounds__(128) k_p2m(int64_t b0, int64_t b1, const uint32_t* __restrict__ off,
                                              const double4* __restrict__ src, const double* __restrict__ cx,
                                              const double* __restrict__ cy, double2* __restrict__ mp)
 {
-    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nleaf) return;
+    int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= b1) return;
     double2 a[P + 1];
 #pragma unroll
     for (int k = 0; k <= P; ++k) a[k] = make_double2(0.0, 0.0);
@@ -95,13 +95,13 @@ __global__ void __launch_bounds__(128) k_p2m(int64_t nleaf, const uint32_t* __re
 
 // ---------------------------------------------------------------- M2M (A5)
 template <int P>
-__global__ void __launch_bounds__(128) k_m2m(int64_t nb, const double* __restrict__ cxp,
+__global__ void __launch_bounds__(128) k_m2m(int64_t b0, int64_t b1, const double* __restrict__ cxp,
                                              const double* __restrict__ cyp, const double* __restrict__ cxc,
                                              const double* __restrict__ cyc, const double2* __restrict__ mc,
                                              double2* __restrict__ mpar)
 {
-    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nb) return;
+    int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= b1) return;
     double2 acc[P + 1];
 #pragma unroll
     for (int k = 0; k <= P; ++k) acc[k] = make_double2(0.0, 0.0);
@@ -136,6 +136,8 @@ struct M2LArgs {
     const int64_t* woff[FMM2D_MAXL + 1];
     const uint32_t* widx[FMM2D_MAXL + 1];
     int64_t base[FMM2D_MAXL + 2];
+    int64_t lo[FMM2D_MAXL + 1];       // target boxes of level l: [lo[l], lo[l] + (pre[l+1] - pre[l]))
+    int64_t pre[FMM2D_MAXL + 2];      // work prefix over levels 1..L
     int L;
     const double* cx;
     const double* cy;
@@ -213,16 +215,17 @@ constexpr int M2L_T = 128;
 // (Tried and measured slower at p = 17 on B200: accumulators in shared memory, and a
 // k-outer contraction with beta in registers.)
 template <int P, int NS>
-__global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l(M2LArgs A, int64_t g0, int64_t g1)
+__global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l(M2LArgs A)
 {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int lane = threadIdx.x & 31;
     int64_t warp = t >> 5;
     int part = (int)(warp % NS);
-    int64_t g = g0 + (warp / NS) * 32 + lane;
-    if (g >= g1) return;
+    int64_t w = (warp / NS) * 32 + lane;         // work item: one target box
+    if (w >= A.pre[A.L + 1]) return;
     int lev = 1;
-    while (lev < A.L && g >= A.base[lev + 1]) ++lev;
+    while (lev < A.L && w >= A.pre[lev + 1]) ++lev;
+    const int64_t g = A.base[lev] + A.lo[lev] + (w - A.pre[lev]);
     // part q computes coefficients [q H, min((q+1) H, P+1)), H = ceil((P+1)/NS)
     constexpr int H = (P + NS) / NS;
     constexpr int E1 = (2 * H < P + 1) ? 2 * H : P + 1;
@@ -242,13 +245,13 @@ __global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l(M2LArgs A, int64_
 
 // ---------------------------------------------------------------- L2L (A8)
 template <int P>
-__global__ void __launch_bounds__(128) k_l2l(int64_t nb, const double* __restrict__ cxp,
+__global__ void __launch_bounds__(128) k_l2l(int64_t c0, int64_t c1, const double* __restrict__ cxp,
                                              const double* __restrict__ cyp, const double* __restrict__ cxc,
                                              const double* __restrict__ cyc, const double2* __restrict__ lpar,
                                              double2* __restrict__ lch)
 {
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nb) return;
+    int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= c1) return;
     int64_t b = c >> 2;
     const double2* B = lpar + b * (P + 1);
     double2 d[P + 1];
@@ -268,19 +271,38 @@ __global__ void __launch_bounds__(128) k_l2l(int64_t nb, const double* __restric
 
 inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
+// P2M of the own leaves, then M2M for parent levels L-1 .. lstop (own parents; the
+// replicated levels above the partition level are done by upward_top_p)
 template <int P>
 int upward_p(fmm2d_plan* Pl)
 {
     cudaStream_t st = Pl->stream;
     const int L = Pl->L;
-    int64_t nl = nboxes(L);
-    k_p2m<P><<<grid_for(nl, 128), 128, 0, st>>>(nl, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
-                                               Pl->cy + Pl->base[L], Pl->mpole + Pl->base[L] * (P + 1)); fmm2d::note_launch();
+    const int64_t l0 = Pl->box_lo(L), l1 = Pl->box_hi(L);
+    k_p2m<P><<<grid_for(l1 - l0, 128), 128, 0, st>>>(l0, l1, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
+                                                    Pl->cy + Pl->base[L], Pl->mpole + Pl->base[L] * (P + 1));
+    fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
-    for (int l = L - 1; l >= 0; --l) {
-        int64_t nb = nboxes(l);
+    for (int l = L - 1; l >= Pl->kpart; --l) {
+        const int64_t b0 = Pl->own_lo(l), b1 = Pl->own_hi(l);
+        k_m2m<P><<<grid_for(b1 - b0, 128), 128, 0, st>>>(
+            b0, b1, Pl->cx + Pl->base[l], Pl->cy + Pl->base[l], Pl->cx + Pl->base[l + 1], Pl->cy + Pl->base[l + 1],
+            Pl->mpole + Pl->base[l + 1] * (P + 1), Pl->mpole + Pl->base[l] * (P + 1)); fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    }
+    return 0;
+}
+
+// M2M of the replicated levels kpart-1 .. 0 (every box; after the level-kpart
+// multipoles have been all-gathered)
+template <int P>
+int upward_top_p(fmm2d_plan* Pl)
+{
+    cudaStream_t st = Pl->stream;
+    for (int l = Pl->kpart - 1; l >= 0; --l) {
+        const int64_t nb = nboxes(l);
         k_m2m<P><<<grid_for(nb, 128), 128, 0, st>>>(
-            nb, Pl->cx + Pl->base[l], Pl->cy + Pl->base[l], Pl->cx + Pl->base[l + 1], Pl->cy + Pl->base[l + 1],
+            0, nb, Pl->cx + Pl->base[l], Pl->cy + Pl->base[l], Pl->cx + Pl->base[l + 1], Pl->cy + Pl->base[l + 1],
             Pl->mpole + Pl->base[l + 1] * (P + 1), Pl->mpole + Pl->base[l] * (P + 1)); fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
     }
@@ -305,6 +327,12 @@ int m2l_p(fmm2d_plan* Pl)
         A.widx[l] = Pl->weak[l].idx;
     }
     for (int l = 0; l <= L + 1; ++l) A.base[l] = Pl->base[l];
+    A.pre[0] = A.pre[1] = 0;
+    A.lo[0] = 0;
+    for (int l = 1; l <= L; ++l) {
+        A.lo[l] = Pl->box_lo(l);
+        A.pre[l + 1] = A.pre[l] + (Pl->box_hi(l) - Pl->box_lo(l));
+    }
     A.L = L;
     A.cx = Pl->cx;
     A.cy = Pl->cy;
@@ -313,9 +341,9 @@ int m2l_p(fmm2d_plan* Pl)
     // level-0 local is zero (no M2L at the root)
     FMM2D_CUDA_TRY(cudaMemsetAsync(Pl->local, 0, sizeof(double2) * (P + 1), st));
     constexpr int NS = m2l_split<P>();
-    int64_t g0 = Pl->base[1], g1 = Pl->base[L + 1];
-    int64_t nthreads = ((g1 - g0 + 31) / 32) * 32 * NS;
-    k_m2l<P, NS><<<grid_for(nthreads, M2L_T), M2L_T, 0, st>>>(A, g0, g1); fmm2d::note_launch();
+    const int64_t work = A.pre[L + 1];
+    int64_t nthreads = ((work + 31) / 32) * 32 * NS;
+    k_m2l<P, NS><<<grid_for(nthreads, M2L_T), M2L_T, 0, st>>>(A); fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     return 0;
 }
@@ -325,9 +353,9 @@ int downward_p(fmm2d_plan* Pl)
 {
     cudaStream_t st = Pl->stream;
     for (int l = 2; l <= Pl->L; ++l) {
-        int64_t nb = nboxes(l);
-        k_l2l<P><<<grid_for(nb, 128), 128, 0, st>>>(
-            nb, Pl->cx + Pl->base[l - 1], Pl->cy + Pl->base[l - 1], Pl->cx + Pl->base[l], Pl->cy + Pl->base[l],
+        const int64_t c0 = Pl->box_lo(l), c1 = Pl->box_hi(l);
+        k_l2l<P><<<grid_for(c1 - c0, 128), 128, 0, st>>>(
+            c0, c1, Pl->cx + Pl->base[l - 1], Pl->cy + Pl->base[l - 1], Pl->cx + Pl->base[l], Pl->cy + Pl->base[l],
             Pl->local + Pl->base[l - 1] * (P + 1), Pl->local + Pl->base[l] * (P + 1)); fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
     }
@@ -352,6 +380,11 @@ int downward_p(fmm2d_plan* Pl)
 int run_upward(fmm2d_plan* P)
 {
     switch (P->p) { FMM2D_P_CASES(upward_p) default: return FMM2D_EINVAL; }
+}
+
+int run_upward_top(fmm2d_plan* P)
+{
+    switch (P->p) { FMM2D_P_CASES(upward_top_p) default: return FMM2D_EINVAL; }
 }
 
 int run_m2l(fmm2d_plan* P)

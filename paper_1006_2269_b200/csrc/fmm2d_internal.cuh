@@ -104,6 +104,21 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi);
 int prepare_near(fmm2d_plan* P);
 int prepare_near_sym(fmm2d_plan* P);
 int gather_strengths(fmm2d_plan* P, const double2* m);
+int run_upward_top(fmm2d_plan* P);
+// sharding (shard.cu)
+int64_t box_start_host(int64_t n, int l, int64_t b);
+int partition_level(int nranks);
+int shard_setup(fmm2d_plan* P, int nranks, int rank, const void* nccl_id);
+void shard_free(fmm2d_plan* P);
+int shard_build_rest(fmm2d_plan* const* Ps, int np);
+int shard_gather_halo(fmm2d_plan* P, const double2* m);
+int shard_comm_top(fmm2d_plan* const* Ps, int np);
+int shard_pack_mp(fmm2d_plan* P);
+int shard_comm_mp(fmm2d_plan* const* Ps, int np);
+int shard_unpack_mp(fmm2d_plan* P);
+bool shard_has_comm(const fmm2d_plan* P);
+void shard_halo_sizes(const fmm2d_plan* P, int64_t* leaves, int64_t* mpoles, int64_t* exp_leaves, int64_t* exp_mp);
+int nccl_unique_id(void* out);
 int upload_binomials(int p);
 // count of this library's own kernel launches (reported by bench.py as gpu_launches)
 void note_launch();
@@ -127,6 +142,7 @@ int64_t launch_count();
     } while (0)
 
 void fmm2d_set_last_cuda_error(cudaError_t e, const char* what, const char* file, int line);
+void fmm2d_set_last_error_text(const char* msg, const char* what, const char* file, int line);
 
 // IEEE round-to-nearest helpers with no FMA contraction (DESIGN R11).  The squared
 // distance is what the radius pass maximises: sqrt_rn is monotone, so

@@ -34,16 +34,16 @@ __device__ __forceinline__ bool well_separated(double cbx, double cby, double rb
 }
 
 template <bool FILL>
-__global__ void k_lists(int64_t nb, const double* __restrict__ cx, const double* __restrict__ cy,
+__global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, const double* __restrict__ cy,
                         const double* __restrict__ r, double theta, const int64_t* __restrict__ poff,
                         const uint32_t* __restrict__ pidx, int64_t* __restrict__ wcnt,
                         int64_t* __restrict__ scnt, const int64_t* __restrict__ woff,
                         const int64_t* __restrict__ soff, uint32_t* __restrict__ widx,
                         uint32_t* __restrict__ sidx)
 {
-    int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t b = b0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     int lane = threadIdx.x & 31;
-    if (b >= nb) return;
+    if (b >= b1) return;
     int64_t par = b >> 2;
     int64_t o0 = poff[par];
     int64_t ncand = 4 * (poff[par + 1] - o0);
@@ -76,12 +76,13 @@ __global__ void k_lists(int64_t nb, const double* __restrict__ cx, const double*
 }
 
 // ordered P2P pairs (j != i) of one evaluation: sum_t n_t * sum_{s in S(t)} n_s - N
-__global__ void k_pair_count(int64_t nb, const uint32_t* __restrict__ off, const int64_t* __restrict__ soff,
-                             const uint32_t* __restrict__ sidx, unsigned long long* __restrict__ total)
+__global__ void k_pair_count(int64_t t0, int64_t t1, const uint32_t* __restrict__ off,
+                             const int64_t* __restrict__ soff, const uint32_t* __restrict__ sidx,
+                             unsigned long long* __restrict__ total)
 {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t t = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long v = 0;
-    if (t < nb) {
+    if (t < t1) {
         unsigned long long ns = 0;
         for (int64_t q = soff[t]; q < soff[t + 1]; ++q) {
             uint32_t s = sidx[q];
@@ -142,10 +143,17 @@ int build_lists(fmm2d_plan* P)
             const double* r = P->r + P->base[l];
             FMM2D_TRY(dev_alloc(P, (void**)&W.off, sizeof(int64_t) * (nb + 1)));
             FMM2D_TRY(dev_alloc(P, (void**)&S.off, sizeof(int64_t) * (nb + 1)));
-            FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_w + nb, 0, sizeof(int64_t), st));
-            FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_s + nb, 0, sizeof(int64_t), st));
-            unsigned grid = grid_for(nb * 32, 256);
-            k_lists<false><<<grid, 256, 0, st>>>(nb, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w, cnt_s,
+            // boxes of this rank: all of a replicated level, the own subtrees below it
+            const int64_t b0 = P->box_lo(l), b1 = P->box_hi(l);
+            if (b1 - b0 < nb) {
+                FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_w, 0, sizeof(int64_t) * (nb + 1), st));
+                FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_s, 0, sizeof(int64_t) * (nb + 1), st));
+            } else {
+                FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_w + nb, 0, sizeof(int64_t), st));
+                FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_s + nb, 0, sizeof(int64_t), st));
+            }
+            unsigned grid = grid_for((b1 - b0) * 32, 256);
+            k_lists<false><<<grid, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w, cnt_s,
                                                  nullptr, nullptr, nullptr, nullptr); fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
             size_t sb = scan_bytes;
@@ -160,7 +168,7 @@ int build_lists(fmm2d_plan* P)
             S.total = tot[1];
             FMM2D_TRY(dev_alloc(P, (void**)&W.idx, sizeof(uint32_t) * std::max<int64_t>(W.total, 1)));
             FMM2D_TRY(dev_alloc(P, (void**)&S.idx, sizeof(uint32_t) * std::max<int64_t>(S.total, 1)));
-            k_lists<true><<<grid, 256, 0, st>>>(nb, cx, cy, r, P->theta, PS.off, PS.idx, nullptr, nullptr,
+            k_lists<true><<<grid, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, nullptr, nullptr,
                                                 W.off, S.off, W.idx, S.idx); fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
             P->stats.weak_pairs += W.total;
@@ -168,8 +176,9 @@ int build_lists(fmm2d_plan* P)
         P->stats.strong_leaf_pairs = P->strong[L].total;
         unsigned long long* d_tot = (unsigned long long*)cnt_w;   // reuse scratch
         FMM2D_CUDA_TRY(cudaMemsetAsync(d_tot, 0, sizeof(unsigned long long), st));
-        k_pair_count<<<grid_for(nbmax, 256), 256, 0, st>>>(nbmax, P->boff + P->obase[L], P->strong[L].off,
-                                                           P->strong[L].idx, d_tot); fmm2d::note_launch();
+        const int64_t t0 = P->box_lo(L), t1 = P->box_hi(L);
+        k_pair_count<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, P->boff + P->obase[L], P->strong[L].off,
+                                                             P->strong[L].idx, d_tot); fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
         unsigned long long h_tot = 0;
         FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_tot, d_tot, sizeof(h_tot), cudaMemcpyDeviceToHost, st));

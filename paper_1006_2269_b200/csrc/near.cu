@@ -37,11 +37,11 @@ constexpr int NEAR_T = 128;
 constexpr int NEAR_CHUNK = FMM2D_NEAR_CHUNK;    // >= 256: the chunk buffer doubles as reduction space
 static_assert(NEAR_CHUNK >= 2 * NEAR_T, "chunk buffer too small for the reduction");
 
-__global__ void k_gather_m(const double2* __restrict__ m, const uint32_t* __restrict__ perm, int64_t n,
+__global__ void k_gather_m(const double2* __restrict__ m, const uint32_t* __restrict__ perm, int64_t k0, int64_t k1,
                            double4* __restrict__ src)
 {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
+    int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= k1) return;
     double2 v = m[perm[k]];
     double4 s = src[k];
     s.z = v.x;
@@ -124,7 +124,7 @@ __device__ __forceinline__ int first_in_class(int b, int g, int G)
 }
 
 template <bool REAL>
-__global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, const uint32_t* __restrict__ off,
+__global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, int64_t t0, const uint32_t* __restrict__ off,
                                                  const int64_t* __restrict__ soff, const uint32_t* __restrict__ sidx,
                                                  const double4* __restrict__ src, const double* __restrict__ cx,
                                                  const double* __restrict__ cy, const double2* __restrict__ loc,
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
     __shared__ int cinfo[2];                 // [0] leaves in chunk, [1] chunk row of leaf t (-1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     load_tables(T, gtab);
-    const int64_t t = blockIdx.x;
+    const int64_t t = t0 + blockIdx.x;
     const uint32_t ts = off[t], te = off[t + 1];
     const int nt = (int)(te - ts);
     const int64_t q0 = soff[t], q1 = soff[t + 1];
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
 
 // Wide leaves (> NEAR_CHUNK points): sources straight from global memory.
 template <bool REAL>
-__global__ void __launch_bounds__(NEAR_T) k_near_wide(int p, const uint32_t* __restrict__ off,
+__global__ void __launch_bounds__(NEAR_T) k_near_wide(int p, int64_t t0, const uint32_t* __restrict__ off,
                                                       const int64_t* __restrict__ soff,
                                                       const uint32_t* __restrict__ sidx,
                                                       const double4* __restrict__ src, const double* __restrict__ cx,
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(NEAR_T) k_near_wide(int p, const uint32_t* __r
     __shared__ fm::Tables T;
     load_tables(T, gtab);
     __syncthreads();
-    const int64_t t = blockIdx.x;
+    const int64_t t = t0 + blockIdx.x;
     const uint32_t ts = off[t], te = off[t + 1];
     for (uint32_t i = ts + threadIdx.x; i < te; i += NEAR_T) {
         const double4 me = src[i];
@@ -561,7 +561,8 @@ const fm::Tables* device_tables(int dev, int* rc)
 
 int gather_strengths(fmm2d_plan* P, const double2* m)
 {
-    k_gather_m<<<grid_for(P->n, 256), 256, 0, P->stream>>>(m, P->perm, P->n, P->src);
+    const int64_t k0 = P->pos0, k1 = P->pos1;
+    k_gather_m<<<grid_for(k1 - k0, 256), 256, 0, P->stream>>>(m, P->perm, k0, k1, P->src);
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     return 0;
@@ -596,7 +597,7 @@ int prepare_near_sym(fmm2d_plan* P)
 {
     P->sym = false;
     const int L = P->L, ml = P->stats.max_leaf;
-    if (L < 1 || ml > SYM_MAXLEAF || ml < 1 || !(P->flags & FMM2D_SYMMETRIC_P2P)) return 0;
+    if (L < 1 || ml > SYM_MAXLEAF || ml < 1 || !(P->flags & FMM2D_SYMMETRIC_P2P) || P->nranks > 1) return 0;
     cudaStream_t st = P->stream;
     const int64_t nl = nboxes(L);
     const Csr& S = P->strong[L];
@@ -641,7 +642,7 @@ int prepare_near_sym(fmm2d_plan* P)
 int run_near(fmm2d_plan* P, double2* phi, double2* dphi)
 {
     const int L = P->L;
-    const int64_t nl = nboxes(L);
+    const int64_t t0 = P->box_lo(L), nl = P->box_hi(L) - t0;    // own target leaves
     const double* cx = P->cx + P->base[L];
     const double* cy = P->cy + P->base[L];
     const double2* loc = P->local + P->base[L] * (P->p + 1);
@@ -686,17 +687,17 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi)
         int G = NEAR_T / std::min(pairs, NEAR_T);
         if (G < 1) G = 1;
         if (real)
-            k_near<true><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(G, P->p, off, P->strong[L].off, P->strong[L].idx,
+            k_near<true><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(G, P->p, t0, off, P->strong[L].off, P->strong[L].idx,
                                                                 P->src, cx, cy, loc, P->perm, tab, phi, dphi);
         else
-            k_near<false><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(G, P->p, off, P->strong[L].off, P->strong[L].idx,
+            k_near<false><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(G, P->p, t0, off, P->strong[L].off, P->strong[L].idx,
                                                                  P->src, cx, cy, loc, P->perm, tab, phi, dphi);
     } else {
         if (real)
-            k_near_wide<true><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, off, P->strong[L].off, P->strong[L].idx,
+            k_near_wide<true><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, t0, off, P->strong[L].off, P->strong[L].idx,
                                                                      P->src, cx, cy, loc, P->perm, tab, phi, dphi);
         else
-            k_near_wide<false><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, off, P->strong[L].off,
+            k_near_wide<false><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, t0, off, P->strong[L].off,
                                                                       P->strong[L].idx, P->src, cx, cy, loc,
                                                                       P->perm, tab, phi, dphi);
     }

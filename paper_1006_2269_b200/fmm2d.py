@@ -33,7 +33,9 @@ EXPORT_PERM, EXPORT_OFFSETS, EXPORT_DISCS, EXPORT_STRONG, EXPORT_WEAK, EXPORT_MP
 
 # every symbol include/fmm2d.h declares
 SYMBOLS = ["fmm2d_default_options", "fmm2d_build", "fmm2d_eval", "fmm2d_eval_timed", "fmm2d_launch_count",
-           "fmm2d_free", "fmm2d_strerror", "fmm2d_last_error_detail", "fmm2d_plan_info", "fmm2d_export"]
+           "fmm2d_free", "fmm2d_strerror", "fmm2d_last_error_detail", "fmm2d_plan_info", "fmm2d_export",
+           "fmm2d_nccl_unique_id", "fmm2d_partition_info", "fmm2d_build_shards", "fmm2d_eval_shards",
+           "fmm2d_halo_info"]
 
 
 class Options(ctypes.Structure):
@@ -79,6 +81,13 @@ def lib():
                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64),
                                       ctypes.POINTER(ctypes.c_int64)]
         L.fmm2d_export.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_size_t)]
+        L.fmm2d_nccl_unique_id.argtypes = [vp]
+        L.fmm2d_partition_info.argtypes = [ctypes.c_int64, ctypes.POINTER(Options), ctypes.c_int, ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_int64)]
+        L.fmm2d_build_shards.argtypes = [vp, ctypes.c_int64, ctypes.POINTER(Options), ctypes.c_int,
+                                         ctypes.POINTER(vp)]
+        L.fmm2d_eval_shards.argtypes = [ctypes.POINTER(vp), ctypes.c_int, vp, vp, vp]
+        L.fmm2d_halo_info.argtypes = [vp, ctypes.POINTER(ctypes.c_int64)]
         _lib = L
     return _lib
 
@@ -91,6 +100,40 @@ def launch_count() -> int:
 def _check(rc: int, what: str):
     if rc != 0:
         raise FmmError(rc, what)
+
+
+def _options(theta=0.5, p=17, leaf_target=40, nlevels=-1, flags=0, device=0, stream=None, nranks=1, rank=0):
+    opt = Options()
+    lib().fmm2d_default_options(ctypes.byref(opt))
+    opt.theta = float(theta)
+    opt.p = int(p)
+    opt.leaf_target = int(leaf_target)
+    opt.nlevels = int(nlevels)
+    opt.flags = int(flags)
+    opt.device = int(device)
+    opt.stream = ctypes.c_void_p(stream)
+    opt.nranks = int(nranks)
+    opt.rank = int(rank)
+    return opt
+
+
+def partition_info(n: int, nranks: int, rank: int, theta: float = 0.5, p: int = 17, leaf_target: int = 40,
+                   nlevels: int = -1) -> dict:
+    """Partition of the tree across ranks (host arithmetic only, no GPU needed):
+    depth L, partition level k, own leaves, own leaf-order positions, own level-k subtrees."""
+    info = (ctypes.c_int64 * 8)()
+    opt = _options(theta, p, leaf_target, nlevels)
+    _check(lib().fmm2d_partition_info(int(n), ctypes.byref(opt), int(nranks), int(rank), info),
+           "fmm2d_partition_info")
+    return {"L": info[0], "k": info[1], "leaves": (info[2], info[3]), "positions": (info[4], info[5]),
+            "subtrees": (info[6], info[7])}
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (make it on one rank, broadcast it to the others)."""
+    buf = (ctypes.c_char * 128)()
+    _check(lib().fmm2d_nccl_unique_id(buf), "fmm2d_nccl_unique_id")
+    return bytes(buf)
 
 
 def _ptr_of(a, host: bool):
@@ -120,7 +163,8 @@ class Fmm2d:
 
     def __init__(self, z, theta: float = 0.5, p: int = 17, leaf_target: int = 40, nlevels: int = -1,
                  real_strengths: bool = False, device: int | None = None, stream=None,
-                 symmetric_p2p: bool = False, tree_key64: bool = False):
+                 symmetric_p2p: bool = False, tree_key64: bool = False, nranks: int = 1, rank: int = 0,
+                 nccl_id: bytes | None = None):
         L = lib()
         import torch
         host = not (isinstance(z, torch.Tensor) and z.is_cuda)
@@ -141,6 +185,15 @@ class Fmm2d:
                      | (SYMMETRIC_P2P if symmetric_p2p else 0) | (TREE_KEY64 if tree_key64 else 0))
         opt.device = int(device)
         opt.stream = ctypes.c_void_p(stream.cuda_stream)
+        opt.nranks = int(nranks)
+        opt.rank = int(rank)
+        self._nccl_id = None
+        if nranks > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("nranks > 1 needs the 128-byte nccl_id shared by all ranks")
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            opt.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
+        self.nranks, self.rank = int(nranks), int(rank)
         self._opt = opt
         zp, keep = _ptr_of(z, host)
         self.n = int(keep.shape[0])
@@ -226,6 +279,13 @@ class Fmm2d:
         raw = self._export(EXPORT_LOCAL if kind == "local" else EXPORT_MPOLE, level)
         return np.frombuffer(raw, np.complex128).reshape(4 ** level, self.p + 1).copy()
 
+    def halo_info(self) -> dict:
+        info = (ctypes.c_int64 * 9)()
+        _check(lib().fmm2d_halo_info(self._h, info), "fmm2d_halo_info")
+        return {"import_leaves": info[0], "import_mpoles": info[1], "export_leaves": info[2],
+                "export_mpoles": info[3], "nranks": info[4], "rank": info[5], "k": info[6],
+                "positions": (info[7], info[8])}
+
     def stats(self) -> dict:
         s = np.frombuffer(self._export(EXPORT_STATS), np.float64)
         keys = ["n", "L", "p", "theta", "weak_pairs", "strong_leaf_pairs", "min_leaf", "max_leaf",
@@ -248,3 +308,64 @@ class Fmm2d:
 
     def __exit__(self, *exc):
         self.close()
+
+
+class _ShardHandle(Fmm2d):
+    """One rank of a loopback build (exports only; evaluate through LoopbackShards)."""
+
+    def __init__(self, h, n, p, theta, device, stream):      # noqa: D401 - no build here
+        self._h = h
+        self.n = n
+        self.theta = theta
+        self.device = device
+        self.stream = stream
+        self.host = False
+        nl = ctypes.c_int()
+        pp = ctypes.c_int()
+        _check(lib().fmm2d_plan_info(h, None, ctypes.byref(nl), ctypes.byref(pp), None, None), "fmm2d_plan_info")
+        self.L = nl.value
+        self.p = pp.value
+
+
+class LoopbackShards:
+    """The partitioned (multi-GPU) pass with all ranks as plans on ONE device, every
+    transfer between ranks a device copy.  ``eval`` returns the
+    complete Phi, Phi' (each rank writes the entries of the sources it owns)."""
+
+    def __init__(self, z, nshards: int, theta: float = 0.5, p: int = 17, leaf_target: int = 40,
+                 nlevels: int = -1, real_strengths: bool = False, stream=None):
+        import torch
+        if not (isinstance(z, torch.Tensor) and z.is_cuda):
+            raise TypeError("loopback shards take a complex128 CUDA tensor")
+        device = z.device.index if z.device.index is not None else torch.cuda.current_device()
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.n = int(z.shape[0])
+        self.device = device
+        self.stream = stream
+        flags = REAL_STRENGTHS if real_strengths else 0
+        opt = _options(theta, p, leaf_target, nlevels, flags, device, stream.cuda_stream, nshards, 0)
+        hs = (ctypes.c_void_p * nshards)()
+        zp, _ = _ptr_of(z, False)
+        _check(lib().fmm2d_build_shards(ctypes.c_void_p(zp), self.n, ctypes.byref(opt), int(nshards), hs),
+               "fmm2d_build_shards")
+        self._hs = hs
+        self.shards = [_ShardHandle(ctypes.c_void_p(hs[i]), self.n, p, theta, device, stream) for i in range(nshards)]
+
+    def eval(self, m, phi=None, dphi=None):
+        import torch
+        dev = torch.device("cuda", self.device)
+        if phi is None:
+            phi = torch.zeros(self.n, dtype=torch.complex128, device=dev)
+        if dphi is None:
+            dphi = torch.zeros(self.n, dtype=torch.complex128, device=dev)
+        mp = _ptr_of(m, False)[0]
+        _check(lib().fmm2d_eval_shards(self._hs, len(self.shards), ctypes.c_void_p(mp),
+                                       ctypes.c_void_p(phi.data_ptr()), ctypes.c_void_p(dphi.data_ptr())),
+               "fmm2d_eval_shards")
+        return phi, dphi
+
+    def close(self):
+        for s in self.shards:
+            s.close()
+        self.shards = []

@@ -71,5 +71,12 @@ def test_build_rejects_bad_sizes_and_nulls():
     assert L.fmm2d_build(ctypes.c_void_p(z.ctypes.data), 4, None, ctypes.byref(h)) == -1
     assert L.fmm2d_eval(None, None, None, None) == -1
     L.fmm2d_free(None)                     # NULL-safe
-    o.nranks = 2                           # multi-rank builds are not in this ABI version
+    o.nranks = 2                           # a multi-rank build needs the shared NCCL id
+    assert L.fmm2d_build(ctypes.c_void_p(z.ctypes.data), 4, ctypes.byref(o), ctypes.byref(h)) == -1
+    nid = ctypes.create_string_buffer(128)
+    o.nccl_id = ctypes.cast(nid, ctypes.c_void_p)
+    o.nranks = 3                           # not a power of two: no level with 3 | 4^k
     assert L.fmm2d_build(ctypes.c_void_p(z.ctypes.data), 4, ctypes.byref(o), ctypes.byref(h)) == -6
+    o.nranks = 2                           # n = 4: a one-level tree has nothing below k = 1
+    assert L.fmm2d_build(ctypes.c_void_p(z.ctypes.data), 4, ctypes.byref(o), ctypes.byref(h)) == -6
+    assert not h.value
