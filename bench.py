@@ -18,8 +18,11 @@ cpu_baseline = the oracle (oracle/, plain C++, OpenMP) on a bounded sample of th
              workload: the C5 recipe at N = 390,625 (same leaf occupancy, L = 7)
 
 --impl reference runs the oracle itself (the reference arm for this tier) on rank 0.
-Multi-GPU (torchrun, N > 1): each rank evaluates its own independent seeded instance of
-the config ("replicas", weak scaling, no data-path collective) -- see DESIGN.md section 8.
+Multi-GPU (torchrun, N > 1): ONE instance of the config partitioned across the ranks by
+the balanced tree's level-k subtrees (strong scaling): every rank
+holds the full z and m, builds its share (replicated top levels, own subtrees below,
+NCCL halo exchange) and evaluates its own sources.  value = N * steps / max-over-ranks
+device time.
 """
 from __future__ import annotations
 
@@ -185,7 +188,7 @@ def run_reference(args, cfg, rank, world):
     cores = _env_int("OMP_NUM_THREADS", os.cpu_count() or 1)
     line = {"metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{cfg.name} recipe at N={n} (bounded CPU sample)", "n": n, "theta": cfg.theta,
                        "p": cfg.p, "leaf_target": cfg.leaf_target, "levels": L + 1},
@@ -220,6 +223,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1006_2269_b200 import Fmm2d
+    from paper_1006_2269_b200.dist import shared_nccl_id
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -231,8 +235,10 @@ def main():
         if world > 1:
             dist.barrier()
 
-    # inputs resident in HBM (each rank: its own independent seeded instance)
-    z_np, m_np = W.make(cfg.dist, cfg.n, cfg.strengths, seed=W.SEED_BASE + 4 + 1000 * rank)
+    # inputs resident in HBM (one instance; every rank holds all of it)
+    z_np, m_np = W.make(cfg.dist, cfg.n, cfg.strengths, seed=W.SEED_BASE + 4)
+    nccl_id = shared_nccl_id() if world > 1 else None
+    shard_kw = dict(nranks=world, rank=rank, nccl_id=nccl_id) if world > 1 else {}
     z = torch.from_numpy(z_np).to(dev)
     m = torch.from_numpy(m_np).to(dev)
     real = cfg.strengths == "real"
@@ -242,7 +248,7 @@ def main():
 
     def step():
         plan = Fmm2d(z, theta=cfg.theta, p=cfg.p, leaf_target=cfg.leaf_target, real_strengths=real,
-                     stream=stream)
+                     stream=stream, **shard_kw)
         plan.eval(m, phi, dphi)
         return plan
 
@@ -282,10 +288,10 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    value = cfg.n * world * args.steps / (ms_max / 1e3)
+    value = cfg.n * args.steps / (ms_max / 1e3)          # one instance of N points per step
 
     # per-phase breakdown + roofline of the dominant kernel (k_near) on one extra pass
-    phase = phase_times(z, m, phi, dphi, cfg, real, stream)
+    phase = phase_times(z, m, phi, dphi, cfg, real, stream, shard_kw)
     peak, peak_src = fp64_peak()
     pairs = st.get("p2p_pairs", 0.0)
     near_ms = phase["near_ms"]
@@ -301,25 +307,26 @@ def main():
     # end to end through the C ABI with host (pinned) buffers
     e2e = None
     if not args.no_e2e:
-        e2e = end_to_end(z_np, m_np, cfg, real, stream, args)
+        e2e = end_to_end(z_np, m_np, cfg, real, stream, args, shard_kw)
         if world > 1:
             t = torch.tensor([e2e["ms"]], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e["ms"] = float(t.item())
-        e2e = {"value": cfg.n * world / (e2e["ms"] / 1e3), "unit": "points/s",
-               "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]}
+        e2e = {"value": cfg.n / (e2e["ms"] / 1e3), "unit": "points/s",
+               "h2d_bytes_per_step": e2e["h2d"] * world, "d2h_bytes_per_step": e2e["d2h"] * world}
 
     launches_per_step = phase["launches"]
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"{cfg.name}: {cfg.dist} N={cfg.n} ({'replicas' if world > 1 else 'single'})",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{cfg.name}: {cfg.dist} N={cfg.n}"
+                                       + (f" partitioned over {world} GPUs" if world > 1 else " (single GPU)"),
                            "n": cfg.n, "theta": cfg.theta, "p": cfg.p, "leaf_target": cfg.leaf_target,
                            "levels": L + 1, "strengths": cfg.strengths,
                            "step": "fmm2d_build + fmm2d_eval (rows A0-A11)",
                            "l2": "inputs larger than L2 (no flush needed)",
-                           "parallelism": f"replicas{world}" if world > 1 else "single"},
+                           "parallelism": f"subtrees{world}" if world > 1 else "single"},
                 "phases_ms": phase, "host_ms_per_step": host_ms / args.steps, "eval_only_points_per_s": cfg.n / (phase["eval_ms"] / 1e3),
                 "m2l_tflops": m2l_tf,
                 "roofline": roof, "gpu_launches": launches_per_step * args.steps,
@@ -333,7 +340,7 @@ def main():
         dist.destroy_process_group()
 
 
-def phase_times(z, m, phi, dphi, cfg, real, stream):
+def phase_times(z, m, phi, dphi, cfg, real, stream, shard_kw):
     """Device time of each phase of one extra pass (CUDA events on the launching stream)
     and the number of this library's kernel launches in one pass."""
     import torch
@@ -343,7 +350,8 @@ def phase_times(z, m, phi, dphi, cfg, real, stream):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     n0 = launch_count()
     ev[0].record(stream)
-    plan = Fmm2d(z, theta=cfg.theta, p=cfg.p, leaf_target=cfg.leaf_target, real_strengths=real, stream=stream)
+    plan = Fmm2d(z, theta=cfg.theta, p=cfg.p, leaf_target=cfg.leaf_target, real_strengths=real, stream=stream,
+                 **shard_kw)
     ev[1].record(stream)
     pt = plan.eval_timed(m, phi, dphi)
     launches = launch_count() - n0
@@ -352,7 +360,7 @@ def phase_times(z, m, phi, dphi, cfg, real, stream):
     return {"build_ms": build_ms, "launches": launches, **pt}
 
 
-def end_to_end(z_np, m_np, cfg, real, stream, args):
+def end_to_end(z_np, m_np, cfg, real, stream, args, shard_kw):
     """Build + eval through the C ABI with host pinned buffers; copies inside the timing."""
     import torch
     from paper_1006_2269_b200 import Fmm2d
@@ -362,7 +370,7 @@ def end_to_end(z_np, m_np, cfg, real, stream, args):
     dh = torch.empty(cfg.n, dtype=torch.complex128).pin_memory()
     for _ in range(1):
         Fmm2d(zh, theta=cfg.theta, p=cfg.p, leaf_target=cfg.leaf_target, real_strengths=real,
-              stream=stream).eval(mh, ph, dh)
+              stream=stream, **shard_kw).eval(mh, ph, dh)
     torch.cuda.synchronize()
     steps = max(1, min(args.steps, 3))
     e0 = torch.cuda.Event(enable_timing=True)
@@ -370,7 +378,7 @@ def end_to_end(z_np, m_np, cfg, real, stream, args):
     e0.record(stream)
     for _ in range(steps):
         plan = Fmm2d(zh, theta=cfg.theta, p=cfg.p, leaf_target=cfg.leaf_target, real_strengths=real,
-                     stream=stream)
+                     stream=stream, **shard_kw)
         plan.eval(mh, ph, dh)
         plan.close()
     e1.record(stream)

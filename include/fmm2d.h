@@ -125,6 +125,8 @@ FMM2D_API int64_t fmm2d_launch_count(void);
  * (e.g. torch.distributed).  fmm2d_build is then collective (all ranks must call it),
  * and so is every fmm2d_eval: each rank passes the same full m and receives Phi, Phi'
  * at the input positions of the sources it owns (other entries are not written).
+ * The library creates one NCCL communicator per distinct id and keeps it for the
+ * life of the process; later builds with the same id (same nranks, same rank) reuse it.
  * The union over ranks equals the one-GPU result.  Errors: ENOTSUP (P not a power of
  * two, or the tree has no level below k), ENCCL (libnccl.so.2 missing or a NCCL
  * failure). */

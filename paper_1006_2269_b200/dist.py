@@ -29,10 +29,14 @@ def my_partition(n: int, group=None, **kw) -> dict:
     return partition_info(n, dist.get_world_size(group), dist.get_rank(group), **kw)
 
 
-def sharded_plan(z, group=None, **kw) -> Fmm2d:
-    """Collective build of this rank's part of the partitioned plan (one GPU per rank)."""
+def sharded_plan(z, group=None, nccl_id: bytes | None = None, **kw) -> Fmm2d:
+    """Collective build of this rank's part of the partitioned plan (one GPU per rank).
+    The library keeps one NCCL communicator per id: pass the same `nccl_id` (from
+    shared_nccl_id) to every build of a job to reuse it; None makes a new one."""
     import torch.distributed as dist
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     if world == 1:
         return Fmm2d(z, **kw)
-    return Fmm2d(z, nranks=world, rank=rank, nccl_id=shared_nccl_id(group), **kw)
+    if nccl_id is None:
+        nccl_id = shared_nccl_id(group)
+    return Fmm2d(z, nranks=world, rank=rank, nccl_id=nccl_id, **kw)
