@@ -53,8 +53,8 @@ struct Bounds {
 // A0 (pass 1): validate, map -0 -> +0 (x + 0.0), keep the canonical coordinates,
 // reduce the coordinate ranges.
 constexpr int CT = 256;
-__global__ void __launch_bounds__(CT) k_canon(const double2* __restrict__ z, int64_t n, double* __restrict__ xs,
-                                              double* __restrict__ ys, Bounds* __restrict__ B)
+__global__ void __launch_bounds__(CT) k_canon(const double2* __restrict__ z, int64_t n, double2* __restrict__ zc,
+                                              Bounds* __restrict__ B)
 {
     int64_t i = (int64_t)blockIdx.x * CT + threadIdx.x;
     uint64_t xmn = ~0ull, xmx = 0, ymn = ~0ull, ymx = 0;
@@ -63,8 +63,7 @@ __global__ void __launch_bounds__(CT) k_canon(const double2* __restrict__ z, int
         const double2 v = z[i];
         const double x = __dadd_rn(v.x, 0.0), y = __dadd_rn(v.y, 0.0);
         if (!isfinite(x) || !isfinite(y)) bad = 1;
-        xs[i] = x;
-        ys[i] = y;
+        zc[i] = make_double2(x, y);
         const uint64_t kx = orderable(x), ky = orderable(y);
         xmn = min(xmn, kx);
         xmx = max(xmx, kx);
@@ -101,41 +100,68 @@ __device__ __forceinline__ uint32_t key32(double c, double cmin, double scale)
     return (uint32_t)fmin(fmax(t, 0.0), 4294967295.0);
 }
 
-// A0 (pass 2): 32-bit keys of both axes and the identity payload
-__global__ void k_keys32(const double* __restrict__ xs, const double* __restrict__ ys, int64_t n,
-                         const Bounds* __restrict__ B, uint32_t* __restrict__ kx, uint32_t* __restrict__ ky,
-                         uint32_t* __restrict__ iota)
+__device__ __forceinline__ double key_scale(unsigned long long omin, unsigned long long omax, double* cmin)
 {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double xmn = from_orderable(B->xmin), xmx = from_orderable(B->xmax);
-    const double ymn = from_orderable(B->ymin), ymx = from_orderable(B->ymax);
-    const double wx = __dsub_rn(xmx, xmn), wy = __dsub_rn(ymx, ymn);
+    const double mn = from_orderable(omin), mx = from_orderable(omax);
+    const double w = __dsub_rn(mx, mn);
     // width 0 or overflowing: scale 0, one run (the 64-bit path takes over)
-    double sx = (wx > 0.0 && isfinite(wx)) ? 4294967295.0 / wx : 0.0;
-    double sy = (wy > 0.0 && isfinite(wy)) ? 4294967295.0 / wy : 0.0;
-    if (!isfinite(sx)) sx = 0.0;
-    if (!isfinite(sy)) sy = 0.0;
-    kx[i] = key32(xs[i], xmn, sx);
-    ky[i] = key32(ys[i], ymn, sy);
-    iota[i] = (uint32_t)i;
+    double sc = (w > 0.0 && isfinite(w)) ? 4294967295.0 / w : 0.0;
+    if (!isfinite(sc)) sc = 0.0;
+    *cmin = mn;
+    return sc;
 }
 
-// 64-bit fallback keys of one axis
-__global__ void k_keys64(const double* __restrict__ c, int64_t n, uint64_t* __restrict__ k,
-                         uint32_t* __restrict__ iota)
+// A0 (pass 2): the x-sort's keys (32-bit image of x, or the full orderable 64 bits)
+// and its payload {idx, 32-bit image of y} -- the y key rides along, so the y-sort's
+// input comes out of the x-sort in x order without a gather.
+template <bool K64>
+__global__ void k_keys_x(const double2* __restrict__ zc, int64_t n, const Bounds* __restrict__ B,
+                         uint32_t* __restrict__ k32, uint64_t* __restrict__ k64, uint64_t* __restrict__ val)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    k[i] = orderable(c[i]);
-    iota[i] = (uint32_t)i;
+    double xmn, ymn;
+    const double sx = key_scale(B->xmin, B->xmax, &xmn);
+    const double sy = key_scale(B->ymin, B->ymax, &ymn);
+    const double2 v = zc[i];
+    if (K64) k64[i] = orderable(v.x);
+    else k32[i] = key32(v.x, xmn, sx);
+    val[i] = (uint64_t)(uint32_t)i | ((uint64_t)key32(v.y, ymn, sy) << 32);
 }
 
-// Runs of equal 32-bit keys (already in idx order: the sort is stable) are re-sorted
-// by (c, idx) with a stable insertion sort by c.  A run longer than RUN_MAX raises
-// *overflow and is left alone (the caller redoes the axis with 64-bit keys).
-__global__ void k_fix_runs(const uint32_t* __restrict__ key, int64_t n, const double* __restrict__ c,
-                           uint32_t* __restrict__ ord, int* __restrict__ overflow)
+// y-sort input in x order: key = 32-bit image of y, payload {x rank, idx}
+__global__ void k_prep_y(const uint64_t* __restrict__ vx, int64_t n, uint32_t* __restrict__ key,
+                         uint64_t* __restrict__ val)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint64_t v = vx[k];
+    key[k] = (uint32_t)(v >> 32);
+    val[k] = (uint64_t)(uint32_t)k | (v << 32);          // {rx = k, idx}
+}
+
+// 64-bit fallback of the y-sort: input in idx order (so ties leave in idx order),
+// payload {x rank, idx}; the x ranks are scattered once (rare path)
+__global__ void k_scatter_rx(const uint64_t* __restrict__ vx, int64_t n, uint32_t* __restrict__ rx)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) rx[(uint32_t)vx[k]] = (uint32_t)k;
+}
+__global__ void k_keys_y64(const double2* __restrict__ zc, const uint32_t* __restrict__ rx, int64_t n,
+                           uint64_t* __restrict__ k64, uint64_t* __restrict__ val)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    k64[i] = orderable(zc[i].y);
+    val[i] = (uint64_t)rx[i] | ((uint64_t)(uint32_t)i << 32);
+}
+
+// Runs of equal 32-bit keys are re-sorted by (c, idx) (insertion sort, exact
+// coordinates from zc; idx sits at bit `ishift` of the 64-bit payload).  A run
+// longer than RUN_MAX raises *overflow and is left alone (the caller redoes the axis
+// with 64-bit keys).
+__global__ void k_fix_runs(const uint32_t* __restrict__ key, int64_t n, const double2* __restrict__ zc, int axis,
+                           int ishift, uint64_t* __restrict__ val, int* __restrict__ overflow)
 {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -150,45 +176,43 @@ __global__ void k_fix_runs(const uint32_t* __restrict__ key, int64_t n, const do
     }
     double cv[RUN_MAX];
     uint32_t iv[RUN_MAX];
+    uint64_t pv[RUN_MAX];
     for (int a = 0; a < len; ++a) {
-        const uint32_t i = ord[k + a];
-        const double ci = c[i];
+        const uint64_t pl = val[k + a];
+        const uint32_t i = (uint32_t)(pl >> ishift);
+        const double2 zz = zc[i];
+        const double ci = axis ? zz.y : zz.x;
         int b = a;
-        while (b > 0 && cv[b - 1] > ci) {           // strict: equal c keep idx order
+        while (b > 0 && (cv[b - 1] > ci || (cv[b - 1] == ci && iv[b - 1] > i))) {
             cv[b] = cv[b - 1];
             iv[b] = iv[b - 1];
+            pv[b] = pv[b - 1];
             --b;
         }
         cv[b] = ci;
         iv[b] = i;
+        pv[b] = pl;
     }
-    for (int a = 0; a < len; ++a) ord[k + a] = iv[a];
+    for (int a = 0; a < len; ++a) val[k + a] = pv[a];
 }
 
-// ranks: rx[ord_x[k]] = k, ry[ord_y[k]] = k
-__global__ void k_ranks(const uint32_t* __restrict__ ox, const uint32_t* __restrict__ oy, int64_t n,
-                        uint32_t* __restrict__ rx, uint32_t* __restrict__ ry)
+// y-list and the x-ranks in y order (the key of the sort that inverts them)
+__global__ void k_make_ylist(const uint64_t* __restrict__ vy, int64_t n, uint2* __restrict__ yl,
+                             uint32_t* __restrict__ keyd, uint32_t* __restrict__ iota)
 {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    rx[ox[k]] = (uint32_t)k;
-    ry[oy[k]] = (uint32_t)k;
+    const uint32_t rx = (uint32_t)vy[k];
+    yl[k] = make_uint2(rx, (uint32_t)k);
+    keyd[k] = rx;
+    iota[k] = (uint32_t)k;
 }
 
-// initial lists and the coordinates in rank order
-__global__ void k_make_lists(const uint32_t* __restrict__ ox, const uint32_t* __restrict__ oy,
-                             const uint32_t* __restrict__ rx, const uint32_t* __restrict__ ry,
-                             const double* __restrict__ xs, const double* __restrict__ ys, int64_t n,
-                             uint2* __restrict__ xl, uint2* __restrict__ yl, double* __restrict__ xcs,
-                             double* __restrict__ ycs)
+// x-list from the y ranks in x order
+__global__ void k_make_xlist(const uint32_t* __restrict__ ryx, int64_t n, uint2* __restrict__ xl)
 {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const uint32_t i = ox[k], j = oy[k];
-    xl[k] = make_uint2((uint32_t)k, ry[i]);
-    yl[k] = make_uint2(rx[j], (uint32_t)k);
-    xcs[k] = xs[i];
-    ycs[k] = ys[j];
+    if (k < n) xl[k] = make_uint2((uint32_t)k, ryx[k]);
 }
 
 // offsets of level 0
@@ -392,15 +416,17 @@ __global__ void __launch_bounds__(PT) k_partition(SplitArgs A)
 
 // A2 (part 1): tight bounding box from the segment endpoints of both sorted lists;
 // centre = 0.5 (min + max) (DESIGN R8).  Radius reset for part 2.
-__global__ void k_bbox(const uint2* __restrict__ xl, const uint2* __restrict__ yl, const double* __restrict__ xcs,
-                       const double* __restrict__ ycs, const uint32_t* __restrict__ off, int64_t b0, int64_t b1,
-                       double* __restrict__ cx, double* __restrict__ cy, double* __restrict__ r)
+// (x rank -> idx: low half of vx; y rank -> idx: high half of vy)
+__global__ void k_bbox(const uint2* __restrict__ xl, const uint2* __restrict__ yl, const uint64_t* __restrict__ vx,
+                       const uint64_t* __restrict__ vy, const double2* __restrict__ zc,
+                       const uint32_t* __restrict__ off, int64_t b0, int64_t b1, double* __restrict__ cx,
+                       double* __restrict__ cy, double* __restrict__ r)
 {
     const int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= b1) return;
     const uint32_t s = off[b], e = off[b + 1];
-    const double xmin = xcs[xl[s].x], xmax = xcs[xl[e - 1].x];
-    const double ymin = ycs[yl[s].y], ymax = ycs[yl[e - 1].y];
+    const double xmin = zc[(uint32_t)vx[xl[s].x]].x, xmax = zc[(uint32_t)vx[xl[e - 1].x]].x;
+    const double ymin = zc[(uint32_t)(vy[yl[s].y] >> 32)].y, ymax = zc[(uint32_t)(vy[yl[e - 1].y] >> 32)].y;
     cx[b] = __dmul_rn(0.5, __dadd_rn(xmin, xmax));
     cy[b] = __dmul_rn(0.5, __dadd_rn(ymin, ymax));
     r[b] = 0.0;
@@ -418,8 +444,8 @@ struct RadArgs {
     const double* cy[FMM2D_MAXL + 1];
     double* r[FMM2D_MAXL + 1];
 };
-__global__ void __launch_bounds__(FIN_T) k_finish(const uint2* __restrict__ yl, const uint32_t* __restrict__ oy,
-                                                  const double* __restrict__ xcs, const double* __restrict__ ycs,
+__global__ void __launch_bounds__(FIN_T) k_finish(const uint2* __restrict__ yl, const uint64_t* __restrict__ vy,
+                                                  const double2* __restrict__ zc,
                                                   uint32_t k0, uint32_t k1, int L, const uint32_t* __restrict__ offL,
                                                   uint32_t lf0, uint32_t lf1, uint32_t* __restrict__ perm,
                                                   double4* __restrict__ src, RadArgs A)
@@ -441,11 +467,13 @@ __global__ void __launch_bounds__(FIN_T) k_finish(const uint2* __restrict__ yl, 
     double x = 0.0, y = 0.0;
     uint32_t leaf = 0;
     if (valid) {
-        const uint2 r = yl[k];
+        const uint32_t ry = yl[k].y;
         leaf = seg_search(offL, s_lo, s_hi, k);
-        x = xcs[r.x];
-        y = ycs[r.y];
-        perm[k] = oy[r.y];
+        const uint32_t idx = (uint32_t)(vy[ry] >> 32);
+        const double2 zz = zc[idx];
+        x = zz.x;
+        y = zz.y;
+        perm[k] = idx;
         src[k] = make_double4(x, y, 0.0, 0.0);
     }
     sleaf[tid] = leaf;
@@ -528,24 +556,28 @@ int build_tree(fmm2d_plan* P, const double2* z)
     P->stats.max_leaf = (int)((n + nboxes(L) - 1) / nboxes(L));
 
     // ---- scratch
-    double *xs, *ys, *xcs, *ycs;
-    uint32_t *kx, *ky, *ksort, *iota, *ox, *oy, *rx, *ry, *hs, *Gp;
-    uint64_t *k64, *k64s;
+    double2* zc;
+    uint32_t *k32a, *k32b, *u32a, *u32b, *hs, *Gp;
+    uint64_t *vx, *vy, *v64a, *k64a, *k64b;
     uint2 *xl, *yl, *tmp;
     Bounds* bnd;
     int* ovf;
     unsigned long long* tstate;
     unsigned int* ticket;
     void* scratch = nullptr;
-    size_t sort32 = 0, sort64 = 0, scan_bytes = 0;
+    size_t s32 = 0, s64 = 0, sd = 0, scan_bytes = 0;
     const int64_t npmax = (L > 0) ? 2 * nboxes(L - 1) : 1;        // parents of the widest step
     const int64_t ntiles = (n + PTILE - 1) / PTILE;
-    cub::DeviceRadixSort::SortPairs(nullptr, sort32, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                    (uint32_t*)nullptr, (int)n, 0, 32, st);
-    cub::DeviceRadixSort::SortPairs(nullptr, sort64, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
-                                    (uint32_t*)nullptr, (int)n, 0, 64, st);
+    int nbits = 1;
+    while (((int64_t)1 << nbits) < n) ++nbits;
+    cub::DeviceRadixSort::SortPairs(nullptr, s32, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint64_t*)nullptr,
+                                    (uint64_t*)nullptr, (int)n, 0, 32, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, s64, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint64_t*)nullptr,
+                                    (uint64_t*)nullptr, (int)n, 0, 64, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, sd, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int)n, 0, nbits, st);
     cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)npmax, st);
-    const size_t cub_bytes = std::max(std::max(sort32, sort64), scan_bytes);
+    const size_t cub_bytes = std::max(std::max(s32, s64), std::max(sd, scan_bytes));
     std::vector<void*> tmp_ptrs;
     auto talloc = [&](void** p, size_t b) -> int {
         cudaError_t e = cudaMallocAsync(p, b ? b : 16, st);
@@ -559,16 +591,14 @@ int build_tree(fmm2d_plan* P, const double2* z)
     };
     int rc = 0;
     do {
-        if ((rc = talloc((void**)&xs, 8 * n))) break;
-        if ((rc = talloc((void**)&ys, 8 * n))) break;
-        if ((rc = talloc((void**)&xcs, 8 * n))) break;
-        if ((rc = talloc((void**)&ycs, 8 * n))) break;
-        if ((rc = talloc((void**)&kx, 4 * n))) break;
-        if ((rc = talloc((void**)&ky, 4 * n))) break;
-        if ((rc = talloc((void**)&ksort, 4 * n))) break;
-        if ((rc = talloc((void**)&iota, 4 * n))) break;
-        if ((rc = talloc((void**)&ox, 4 * n))) break;
-        if ((rc = talloc((void**)&oy, 4 * n))) break;
+        if ((rc = talloc((void**)&zc, 16 * n))) break;
+        if ((rc = talloc((void**)&k32a, 4 * n))) break;
+        if ((rc = talloc((void**)&k32b, 4 * n))) break;
+        if ((rc = talloc((void**)&u32a, 4 * n))) break;
+        if ((rc = talloc((void**)&u32b, 4 * n))) break;
+        if ((rc = talloc((void**)&v64a, 8 * n))) break;
+        if ((rc = talloc((void**)&vx, 8 * n))) break;
+        if ((rc = talloc((void**)&vy, 8 * n))) break;
         if ((rc = talloc((void**)&hs, 4 * npmax))) break;
         if ((rc = talloc((void**)&Gp, 4 * npmax))) break;
         if ((rc = talloc((void**)&tstate, 8 * ntiles))) break;
@@ -581,8 +611,9 @@ int build_tree(fmm2d_plan* P, const double2* z)
         if ((rc = talloc(&scratch, cub_bytes))) break;
     } while (0);
     if (rc) { tfree(); return rc; }
-    rx = kx;          // reused once the sorts are done
-    ry = ky;
+    // 64-bit keys of the fallback live in the (then unused) list buffers
+    k64a = reinterpret_cast<uint64_t*>(xl);
+    k64b = reinterpret_cast<uint64_t*>(yl);
 
     auto body = [&]() -> int {
         // ---- A0: validate, canonical coordinates, ranges
@@ -593,54 +624,66 @@ int build_tree(fmm2d_plan* P, const double2* z)
             h.bad = 0;
             FMM2D_CUDA_TRY(cudaMemcpyAsync(bnd, &h, sizeof(h), cudaMemcpyHostToDevice, st));
             const unsigned g = (unsigned)std::min<int64_t>(grid_for(n, CT), 148 * 8);
-            k_canon<<<g, CT, 0, st>>>(z, n, xs, ys, bnd);
+            k_canon<<<g, CT, 0, st>>>(z, n, zc, bnd);
             fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
             FMM2D_CUDA_TRY(cudaMemcpyAsync(&h, bnd, sizeof(h), cudaMemcpyDeviceToHost, st));
             FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
             if (h.bad) return FMM2D_ENONFINITE;
         }
-        // ---- presort: 32-bit monotone keys, stable (ties in idx order), equal-key runs fixed
-        k_keys32<<<grid_for(n, BS), BS, 0, st>>>(xs, ys, n, bnd, kx, ky, iota);
-        fmm2d::note_launch();
-        FMM2D_CUDA_TRY(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), st));
+        // ---- presort: the (x, idx) order, then the (y, idx) order, as ranks (DESIGN 6.1)
         const bool force64 = (P->flags & FMM2D_TREE_KEY64) != 0;
-        int h_ovf[2] = {force64 ? 1 : 0, force64 ? 1 : 0};
+        int h_ovf[2] = {0, 0};
+        FMM2D_CUDA_TRY(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), st));
+        size_t sb = cub_bytes;
         if (!force64) {
-            size_t sb = cub_bytes;
-            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, kx, ksort, iota, ox, (int)n, 0, 32, st));
-            k_fix_runs<<<grid_for(n, BS), BS, 0, st>>>(ksort, n, xs, ox, ovf);
+            // x: stable sort of 32-bit keys, payload {idx, y key}; equal-key runs fixed
+            k_keys_x<false><<<grid_for(n, BS), BS, 0, st>>>(zc, n, bnd, k32a, nullptr, v64a);
             fmm2d::note_launch();
-            sb = cub_bytes;
-            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, ky, ksort, iota, oy, (int)n, 0, 32, st));
-            k_fix_runs<<<grid_for(n, BS), BS, 0, st>>>(ksort, n, ys, oy, ovf + 1);
+            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, v64a, vx, (int)n, 0, 32, st));
+            k_fix_runs<<<grid_for(n, BS), BS, 0, st>>>(k32b, n, zc, 0, 0, vx, ovf);
             fmm2d::note_launch();
-            FMM2D_CUDA_TRY(cudaGetLastError());
-            FMM2D_CUDA_TRY(cudaMemcpyAsync(h_ovf, ovf, sizeof(h_ovf), cudaMemcpyDeviceToHost, st));
+            FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_ovf[0], ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
             FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
         }
-        for (int ax = 0; ax < 2; ++ax) {
-            if (!h_ovf[ax]) continue;
-            // heavy ties: full 64-bit sort of the orderable coordinate bits for this axis
-            void* p64 = nullptr;
-            FMM2D_CUDA_TRY(cudaMallocAsync(&p64, 16 * n, st));
-            k64 = (uint64_t*)p64;
-            k64s = k64 + n;
-            k_keys64<<<grid_for(n, BS), BS, 0, st>>>(ax ? ys : xs, n, k64, iota);
+        if (force64 || h_ovf[0]) {
+            // heavy ties in x: full 64-bit orderable keys (ties leave in idx order)
+            k_keys_x<true><<<grid_for(n, BS), BS, 0, st>>>(zc, n, bnd, nullptr, k64a, v64a);
             fmm2d::note_launch();
-            size_t sb = cub_bytes;
-            cudaError_t e = cub::DeviceRadixSort::SortPairs(scratch, sb, k64, k64s, iota, ax ? oy : ox, (int)n, 0, 64,
-                                                            st);
-            cudaFreeAsync(p64, st);
-            FMM2D_CUDA_TRY(e);
+            sb = cub_bytes;
+            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k64a, k64b, v64a, vx, (int)n, 0, 64, st));
         }
-        P->stats.tree_key64 = h_ovf[0] + 2 * h_ovf[1];
-        k_ranks<<<grid_for(n, BS), BS, 0, st>>>(ox, oy, n, rx, ry);
+        if (!force64) {
+            // y: input in x order, key = y key, payload {x rank, idx}; runs fixed by (y, idx)
+            k_prep_y<<<grid_for(n, BS), BS, 0, st>>>(vx, n, k32a, v64a);
+            fmm2d::note_launch();
+            sb = cub_bytes;
+            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, v64a, vy, (int)n, 0, 32, st));
+            k_fix_runs<<<grid_for(n, BS), BS, 0, st>>>(k32b, n, zc, 1, 32, vy, ovf + 1);
+            fmm2d::note_launch();
+            FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_ovf[1], ovf + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+            FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+        }
+        if (force64 || h_ovf[1]) {
+            // heavy ties in y: 64-bit keys over the input in idx order
+            k_scatter_rx<<<grid_for(n, BS), BS, 0, st>>>(vx, n, u32a);
+            fmm2d::note_launch();
+            k_keys_y64<<<grid_for(n, BS), BS, 0, st>>>(zc, u32a, n, k64a, v64a);
+            fmm2d::note_launch();
+            sb = cub_bytes;
+            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k64a, k64b, v64a, vy, (int)n, 0, 64, st));
+        }
+        FMM2D_CUDA_TRY(cudaGetLastError());
+        P->stats.tree_key64 = (force64 || h_ovf[0] ? 1 : 0) + (force64 || h_ovf[1] ? 2 : 0);
+        // y-list {rx, k}; the y ranks in x order by one more sort (keys = x ranks)
+        k_make_ylist<<<grid_for(n, BS), BS, 0, st>>>(vy, n, yl, k32a, u32a);
         fmm2d::note_launch();
-        k_make_lists<<<grid_for(n, BS), BS, 0, st>>>(ox, oy, rx, ry, xs, ys, n, xl, yl, xcs, ycs);
+        sb = cub_bytes;
+        FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, u32a, u32b, (int)n, 0, nbits, st));
+        k_make_xlist<<<grid_for(n, BS), BS, 0, st>>>(u32b, n, xl);
         fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
-        k_bbox<<<1, 32, 0, st>>>(xl, yl, xcs, ycs, P->boff + P->obase[0], 0, 1, P->cx + P->base[0],
+        k_bbox<<<1, 32, 0, st>>>(xl, yl, vx, vy, zc, P->boff + P->obase[0], 0, 1, P->cx + P->base[0],
                                  P->cy + P->base[0], P->r + P->base[0]);
         fmm2d::note_launch();
         // one split step: partition `list` inside the parent segments (par_off) [p0, p1),
@@ -693,7 +736,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
             FMM2D_TRY(split_step(xl, yl, H, C, 2 * b0, 2 * b1, k0, k1, 1, tmp));
             std::swap(xl, tmp);
             const int64_t c0 = P->box_lo(l + 1), c1 = P->box_hi(l + 1);
-            k_bbox<<<grid_for(c1 - c0, BS), BS, 0, st>>>(xl, yl, xcs, ycs, C, c0, c1, P->cx + P->base[l + 1],
+            k_bbox<<<grid_for(c1 - c0, BS), BS, 0, st>>>(xl, yl, vx, vy, zc, C, c0, c1, P->cx + P->base[l + 1],
                                                          P->cy + P->base[l + 1], P->r + P->base[l + 1]);
             fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
@@ -708,7 +751,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
             A.r[l] = P->r + P->base[l];
         }
         const uint32_t nown = P->pos1 - P->pos0;
-        k_finish<<<grid_for(nown, FIN_T), FIN_T, 0, st>>>(yl, oy, xcs, ycs, P->pos0, P->pos1, L,
+        k_finish<<<grid_for(nown, FIN_T), FIN_T, 0, st>>>(yl, vy, zc, P->pos0, P->pos1, L,
                                                           P->boff + P->obase[L], (uint32_t)P->box_lo(L),
                                                           (uint32_t)P->box_hi(L), P->perm, P->src, A);
         fmm2d::note_launch();
