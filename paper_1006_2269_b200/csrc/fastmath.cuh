@@ -31,6 +31,9 @@
 struct double2 {
     double x, y;
 };
+struct double4 {
+    double x, y, z, w;
+};
 #endif
 
 #ifdef __CUDA_ARCH__
@@ -56,8 +59,9 @@ struct Tables {
 // [0..3] log1p series -1/6, 1/5, -1/4, 1/3, [4] -1/2, [5] unused, [6..7] atan series 1/5, -1/3,
 // [8] ln2 * 2^-32 (exact scaling of the double nearest ln 2), [9] unused, [10] pi/2, [11] unused,
 // [12] pi, [13] unused, [14] 2^52 + 1023 * 2^32 (exponent extraction), [15] 1.5 * 2^44
-// (rounding to a multiple of 1/256)
-FM_CONST double kC[16] = {
+// (rounding to a multiple of 1/256), [16..17] asin series 3/40, 1/6, [18] 1.5 * 2^52 (rounding
+// to an integer), [19] 3/8, [20] 1/2
+FM_CONST double kC[21] = {
     -1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -0.5, 0.0,
     1.0 / 5.0, -1.0 / 3.0,
     6.931471805599453094e-01 / 4294967296.0, 0.0,
@@ -112,6 +116,27 @@ FM_HD double rcp(double x)
     return fma_(r, fma_(e, e, e), r);      // cubic step: err^3
 }
 
+// log(r2) with a degree-5 series (|u| < 2^-9: truncation < 2^-54 / 6 absolute), used
+// by the near-field kernel where only the absolute error of each term matters.
+FM_HD double log_pos5(double r2, const double2* __restrict__ tab)
+{
+    const int64_t b = as_bits(r2);
+    const int hi = (int)(b >> 32);
+    const int j = (hi >> (20 - LOG_BITS)) & (LOG_N - 1);
+    const int eb = (hi >> 20) + (j >> (LOG_BITS - 1));
+    const double e32 = from_bits((int64_t)(0x43300000 | eb) << 32) - kC[14];
+    const double f = from_bits((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
+    const double2 T = tab[j];
+    const double u = fma_(f, T.x, -1.0);
+    // log1p(u) = u - u^2/2 + u^3/3 - u^4/4 + u^5/5
+    double p = fma_(kC[1], u, kC[2]);
+    p = fma_(p, u, kC[3]);
+    p = fma_(p, u, kC[4]);
+    const double lp = fma_(p, u * u, u);
+    const double r = fma_(e32, kC[8], T.y + lp);
+    return (r2 == 0.0) ? -HUGE_VAL : r;
+}
+
 // log(r2) for r2 > 0 normal; -inf for r2 == 0.
 FM_HD double log_pos(double r2, const double2* __restrict__ tab)
 {
@@ -148,7 +173,7 @@ FM_HD double octant_fix(double a, bool swap, bool neg, int64_t signbit)
 // principal Arg(dx + i dy) = atan2(dy, dx) in (-pi, pi]; dy = +0 gives 0 or pi.
 FM_HD double arg(double dx, double dy, const double2* __restrict__ tab)
 {
-    const int64_t bx = as_bits(dx), by = as_bits(dy);
+    const int hx = (int)(as_bits(dx) >> 32), hy = (int)(as_bits(dy) >> 32);   // sign tests on the high words
     const bool swap = fabs(dy) > fabs(dx);    // one DSETP with |.| operand modifiers
     // select the signed values; |.| is applied as an operand modifier by the consumers
     const double mns = swap ? dx : dy;
@@ -169,7 +194,7 @@ FM_HD double arg(double dx, double dy, const double2* __restrict__ tab)
     const double at = fma_(p * t2, t, t);
     const double2 T = tab[j];
     const double a = T.x + (at + T.y);                    // atan(mn/mx) in [0, pi/4]
-    return octant_fix(a, swap, bx < 0, by & (int64_t)0x8000000000000000ull);
+    return octant_fix(a, swap, hx < 0, (int64_t)(uint32_t)(hy & (int)0x80000000u) << 32);
 }
 
 // Arg(dz) and Arg(-dz), the latter of the componentwise difference z_j - z_i (zeros stay

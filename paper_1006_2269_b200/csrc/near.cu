@@ -34,6 +34,9 @@ constexpr int NEAR_T = 128;
 #ifndef FMM2D_NEAR_MINB
 #define FMM2D_NEAR_MINB 8
 #endif
+#ifndef FMM2D_NEAR_LOG5
+#define FMM2D_NEAR_LOG5 1         // degree-5 log1p (absolute error < 2^-52: tests/test_fastmath.py)
+#endif
 constexpr int NEAR_CHUNK = FMM2D_NEAR_CHUNK;    // >= 256: the chunk buffer doubles as reduction space
 static_assert(NEAR_CHUNK >= 2 * NEAR_T, "chunk buffer too small for the reduction");
 
@@ -63,7 +66,11 @@ __device__ __forceinline__ void pair(PairAcc& a, double dx, double dy, double mr
                                      const fm::Tables& T)
 {
     const double r2 = fma(dx, dx, dy * dy);
-    const double l2 = fm::log_pos(r2, T.lg);                          // log |dz|^2
+#if FMM2D_NEAR_LOG5
+    const double l2 = fm::log_pos5(r2, T.lg);                         // log |dz|^2
+#else
+    const double l2 = fm::log_pos(r2, T.lg);
+#endif
     const double th = fm::arg(dx, dy, T.at);                          // Arg dz
     const double ir2 = fm::rcp(r2);
     const double mr2 = mr * ir2;

@@ -23,6 +23,7 @@ int main()
     std::uniform_real_distribution<double> U(-1.0, 1.0);
     std::uniform_real_distribution<double> E(-60.0, 60.0);
     double mlog = 0, marg = 0, mabs_log = 0, margn = 0;
+    double mlog5_abs = 0;
     long pair_mismatch = 0;
     long n = 0;
     for (long k = 0; k < 4000000; ++k) {
@@ -49,10 +50,15 @@ int main()
         long double rn = atan2l((long double)dyn, (long double)dxn);
         if (th != a) pair_mismatch++;
         margn = std::fmax(margn, ulp_err(thn, rn));
+        // near-field log: degree-5 series, absolute error in units of 2^-52 max(1, |log|)
+        double lg5 = 0.5 * log_pos5(r2, T.lg);
+        double sc = std::fmax(1.0, (double)fabsl(rl)) * 2.220446049250313e-16;
+        mlog5_abs = std::fmax(mlog5_abs, (double)(fabsl((long double)lg5 - rl) / sc));
         ++n;
     }
     double zero = log_pos(0.0, T.lg);
-    printf("{\"n\": %ld, \"log_max_ulp\": %.3f, \"log_max_abs\": %.3e, \"arg_max_ulp\": %.3f, \"argneg_max_ulp\": %.3f, "
+    printf("{\"log5_max_abs_eps\": %.3f, ", mlog5_abs);
+    printf("\"n\": %ld, \"log_max_ulp\": %.3f, \"log_max_abs\": %.3e, \"arg_max_ulp\": %.3f, \"argneg_max_ulp\": %.3f, "
            "\"pair_mismatch\": %ld, \"log0_is_neg_inf\": %d, \"arg_pi\": %d, \"arg_zero\": %d}\n",
            n, mlog, mabs_log, marg, margn, pair_mismatch, (int)(std::isinf(zero) && zero < 0),
            (int)(arg(-1.0, 0.0, T.at) == M_PI), (int)(arg(2.0, 0.0, T.at) == 0.0));
