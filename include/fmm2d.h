@@ -63,6 +63,8 @@ extern "C" {
 #define FMM2D_TREE_KEY64      0x8  /* diagnostic: presort both axes with full 64-bit keys
                                       instead of 32-bit keys + run fix-up (same tree,
                                       DESIGN.md section 6.1)                            */
+#define FMM2D_TREE_GLOBAL_ONLY 0x10 /* diagnostic: every split step in global memory (no
+                                      on-chip finish of the deepest levels; same tree)  */
 
 typedef struct fmm2d_plan fmm2d_plan;   /* opaque; owns all device memory */
 

@@ -254,40 +254,67 @@ __device__ __forceinline__ uint32_t seg_search(const uint32_t* __restrict__ O, u
     return lo;
 }
 
-// Per parent segment p in [p0, p1): number of high-side records (the split rule fixes it).
-__global__ void k_high_sizes(const uint32_t* __restrict__ par_off, const uint32_t* __restrict__ sub_off,
-                             int64_t p0, int64_t np, uint32_t* __restrict__ hs)
+// Per parent segment p in [p0, p1) (threads q < np): the number of its high-side
+// records (a function of the offsets) and the rank of its first high record on the
+// split axis (the split value; ~0 if the high side is empty).  Per partition tile
+// (threads q < ntiles): the segment of its first position (binary search).
+__global__ void k_seg_prep(const uint32_t* __restrict__ par_off, const uint32_t* __restrict__ sub_off,
+                           const uint2* __restrict__ split_list, int axis, int64_t p0, int64_t np, uint32_t k0,
+                           int64_t ntiles, int tile_shift, uint32_t* __restrict__ hs, uint32_t* __restrict__ split,
+                           uint32_t* __restrict__ tile_seg)
 {
-    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q < np) hs[q] = par_off[p0 + q + 1] - sub_off[2 * (p0 + q) + 1];
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < np) {
+        const int64_t p = p0 + q;
+        const uint32_t pe = par_off[p + 1], sp = sub_off[2 * p + 1];
+        hs[q] = pe - sp;
+        uint32_t v = 0xFFFFFFFFu;
+        if (sp < pe) {
+            const uint2 r = split_list[sp];
+            v = axis ? r.y : r.x;
+        }
+        split[q] = v;
+    }
+    if (q < ntiles) {
+        const uint32_t k = k0 + ((uint32_t)q << tile_shift);
+        int64_t lo = p0, hi = p0 + np;                 // largest p with par_off[p] <= k
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (par_off[mid] <= k) lo = mid;
+            else hi = mid;
+        }
+        tile_seg[q] = (uint32_t)(lo - p0);
+    }
 }
 
 // One split step over the positions of the parent segments [p0, p1), in one pass:
 //   flag  = record is on the high side of its parent segment p, i.e. its rank on the
-//           split axis >= the rank of the first high record split_list[sub_off[2p+1]];
+//           split axis >= split[p];
 //   G(k)  = high records before position k in the range, from a block scan plus a
-//           decoupled look-back across tiles (tile ids taken in launch order from a
-//           counter, so predecessors always make progress);
+//           decoupled look-back across tiles (tiles in launch order);
 //   dst   = stable position inside p: high -> sub_off[2p+1] + (G(k) - Gp[p]),
-//           low -> k - (G(k) - Gp[p]), Gp[p] = highs before segment p (a scan of
-//           k_high_sizes, a function of the offsets only).
-// The segment table of the tile (start, first high position, Gp, split rank) is staged
-// in shared memory; each record finds its segment by binary search there.
-constexpr int PT = 256, PI = 4, PTILE = PT * PI;
-constexpr int SEGMAX = PTILE + 2;                   // segments one tile can touch
+//           low -> k - (G(k) - Gp[p]), Gp[p] = highs before segment p (a scan of the
+//           high sizes, a function of the offsets only).
+// The tile's segments (from tile_seg, no search in global memory) and their table
+// (start, first high position, Gp, split rank) are staged in shared memory; each record
+// finds its segment by binary search there.
+constexpr int PT = 256, PI = 8, PTILE = PT * PI, PTILE_SHIFT = 11;
+static_assert(PTILE == (1 << PTILE_SHIFT), "tile size");
+constexpr int SEGMAX = 512;                          // larger tile spans: segment search in global memory
 constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_MASK = 3ull << 62;
 
 struct SplitArgs {
     const uint2* list;          // partitioned list (read)
-    const uint2* split_list;    // list sorted by the split axis inside each parent segment
     const uint32_t* par_off;    // parent segment offsets
     const uint32_t* sub_off;    // child offsets: children of p are 2p, 2p+1
     const uint32_t* Gp;         // [p - p0] highs before segment p
+    const uint32_t* split;      // [p - p0] split rank
+    const uint32_t* tile_seg;   // [tile] segment (relative to p0) of the tile's first position
     uint2* out;
     unsigned long long* tstate;
-    unsigned int* ticket;
     uint32_t p0, p1;            // parent segments of the range
     uint32_t k0, k1;            // positions of the range (= par_off[p0], par_off[p1])
+    uint32_t ntiles;
     int axis;                   // 0: compare rx, 1: compare ry
 };
 
@@ -295,47 +322,37 @@ __global__ void __launch_bounds__(PT) k_partition(SplitArgs A)
 {
     typedef cub::BlockScan<uint32_t, PT> Scan;
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ uint32_t s_tile, s_prefix, s_plo, s_nseg;
+    __shared__ uint32_t s_prefix;
     __shared__ __align__(16) uint2 stage[PTILE];
     __shared__ uint32_t s_off[SEGMAX + 1], s_hi[SEGMAX], s_gp[SEGMAX], s_split[SEGMAX];
     const int tid = threadIdx.x;
-    if (tid == 0) s_tile = atomicAdd(A.ticket, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
+    const uint32_t tile = blockIdx.x;
     const uint32_t kt = A.k0 + tile * (uint32_t)PTILE;
     const int nrec = (int)min((uint32_t)PTILE, A.k1 - kt);
-    // segment range of the tile
-    if (tid == 0) {
-        const uint32_t plo = seg_search(A.par_off, A.p0, A.p1, kt);
-        const uint32_t phi = seg_search(A.par_off, plo, A.p1, kt + nrec - 1);
-        s_plo = plo;
-        s_nseg = phi - plo + 1;
-    }
+    const uint32_t qlo = A.tile_seg[tile];                                   // relative to p0
+    const uint32_t qhi = (tile + 1 < A.ntiles) ? A.tile_seg[tile + 1] : (A.p1 - A.p0 - 1);
+    const int nseg = (int)(qhi - qlo + 1);
+    const bool small = nseg <= SEGMAX;
     {   // stage the tile with coalesced 16-byte loads
         const uint4* g = reinterpret_cast<const uint4*>(A.list + kt);
-        uint4* s = reinterpret_cast<uint4*>(stage);
+        uint4* sv = reinterpret_cast<uint4*>(stage);
         const int nvec = nrec / 2;
-        const bool aligned = ((kt & 1u) == 0);
-        if (aligned) {
-            for (int v = tid; v < nvec; v += PT) s[v] = g[v];
+        if ((kt & 1u) == 0) {
+            for (int v = tid; v < nvec; v += PT) sv[v] = g[v];
             if (tid == 0 && (nrec & 1)) stage[nrec - 1] = A.list[kt + nrec - 1];
         } else {
             for (int v = tid; v < nrec; v += PT) stage[v] = A.list[kt + v];
         }
     }
-    __syncthreads();
-    const uint32_t plo = s_plo;
-    const int nseg = (int)s_nseg;
-    for (int j = tid; j < nseg; j += PT) {
-        const uint32_t p = plo + j;
-        const uint32_t sp = A.sub_off[2 * p + 1];
-        const uint32_t pe = A.par_off[p + 1];
-        s_off[j] = A.par_off[p];
-        s_hi[j] = sp;
-        s_gp[j] = A.Gp[p - A.p0];
-        const uint2 r = (sp < pe) ? A.split_list[sp] : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
-        s_split[j] = A.axis ? r.y : r.x;
-        if (j == nseg - 1) s_off[nseg] = pe;
+    if (small) {
+        for (int j = tid; j < nseg; j += PT) {
+            const uint32_t q = qlo + j, p = A.p0 + q;
+            s_off[j] = A.par_off[p];
+            s_hi[j] = A.sub_off[2 * p + 1];
+            s_gp[j] = A.Gp[q];
+            s_split[j] = A.split[q];
+            if (j == nseg - 1) s_off[nseg] = A.par_off[p + 1];
+        }
     }
     __syncthreads();
     uint2 r[PI];
@@ -344,15 +361,25 @@ __global__ void __launch_bounds__(PT) k_partition(SplitArgs A)
     const int i0 = tid * PI;
     uint32_t sj = 0;
     if (i0 < nrec) {
-        // binary search in the staged offsets for the first item, then walk forward
-        uint32_t lo = 0, hi = (uint32_t)nseg;
+        // first item: binary search in the tile's segment table, then walk forward
         const uint32_t k = kt + i0;
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (s_off[mid] <= k) lo = mid;
-            else hi = mid;
+        if (small) {
+            uint32_t lo = 0, hi = (uint32_t)nseg;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (s_off[mid] <= k) lo = mid;
+                else hi = mid;
+            }
+            sj = lo;
+        } else {
+            uint32_t lo = A.p0 + qlo, hi = A.p0 + qhi + 1;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (A.par_off[mid] <= k) lo = mid;
+                else hi = mid;
+            }
+            sj = lo - A.p0;                                                  // relative to p0
         }
-        sj = lo;
     }
 #pragma unroll
     for (int u = 0; u < PI; ++u) {
@@ -360,11 +387,18 @@ __global__ void __launch_bounds__(PT) k_partition(SplitArgs A)
         seg[u] = 0;
         if (i0 + u < nrec) {
             const uint32_t k = kt + i0 + u;
-            while (k >= s_off[sj + 1]) ++sj;
+            uint32_t sv;
+            if (small) {
+                while (k >= s_off[sj + 1]) ++sj;
+                sv = s_split[sj];
+            } else {
+                while (k >= A.par_off[A.p0 + sj + 1]) ++sj;
+                sv = A.split[sj];
+            }
             r[u] = stage[i0 + u];
             seg[u] = sj;
             const uint32_t rank = A.axis ? r[u].y : r[u].x;
-            f[u] = (rank >= s_split[sj]) ? 1u : 0u;
+            f[u] = (rank >= sv) ? 1u : 0u;
         }
         cnt += f[u];
     }
@@ -406,12 +440,172 @@ __global__ void __launch_bounds__(PT) k_partition(SplitArgs A)
         if (i0 + u < nrec) {
             const uint32_t k = kt + i0 + u;
             const uint32_t j = seg[u];
-            const uint32_t hb = g - s_gp[j];  // highs before k inside its segment
-            const uint32_t dst = f[u] ? s_hi[j] + hb : k - hb;
+            uint32_t gp, hstart;
+            if (small) {
+                gp = s_gp[j];
+                hstart = s_hi[j];
+            } else {
+                gp = A.Gp[j];
+                hstart = A.sub_off[2 * (A.p0 + j) + 1];
+            }
+            const uint32_t hb = g - gp;       // highs before k inside its segment
+            const uint32_t dst = f[u] ? hstart + hb : k - hb;
             A.out[dst] = r[u];
         }
         g += f[u];
     }
+}
+
+// The deepest levels in shared memory: once a box holds at most LMAX points, one CTA
+// takes it (both of its sorted lists) and performs every remaining split step and the
+// bounding boxes of every level below it on chip, then writes its final y-list (the
+// leaf order) back in place.  The step is the same stable segmented partition as
+// k_partition: one block-wide scan of the high flags, "highs before k inside its
+// segment" = scan - Gp[segment] (Gp from the offsets), segments found by binary search
+// in the box's local offsets.
+constexpr int LT = 512, LI = 4, LMAX = LT * LI;      // 2048 points per box
+constexpr int LLEV = 4;                              // at most 4 levels on chip
+constexpr int LSEG = 1 << (2 * LLEV - 1);            // half-level segments of the last step (128)
+
+struct LocalArgs {
+    uint2* yl;                                       // y-list (in: level l0 grouping, out: leaf order)
+    const uint2* xl;                                 // x-list (level l0 grouping)
+    const uint32_t* boff;
+    int64_t obase[FMM2D_MAXL + 1];
+    int64_t hbase[FMM2D_MAXL + 1];
+    int l0, L;
+    int64_t b0;                                      // first box (level l0) of the launch
+    const uint64_t* vx;
+    const uint64_t* vy;
+    const double2* zc;
+    double* cx[FMM2D_MAXL + 1];
+    double* cy[FMM2D_MAXL + 1];
+    double* r[FMM2D_MAXL + 1];
+};
+
+struct LocalSmem {
+    uint2 buf[3][LMAX];
+    uint32_t segs[2 * LSEG + 1];                     // segment starts (local positions)
+    uint32_t subs[4 * LSEG + 1];                     // sub-segment starts
+    uint32_t split[2 * LSEG], gp[2 * LSEG];
+};
+
+__device__ __forceinline__ uint32_t local_seg(const uint32_t* __restrict__ O, int nseg, uint32_t k)
+{
+    int lo = 0, hi = nseg;                           // largest j < nseg with O[j] <= k
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (O[mid] <= k) lo = mid;
+        else hi = mid;
+    }
+    return (uint32_t)lo;
+}
+
+#ifndef FMM2D_LOCAL_MINB
+#define FMM2D_LOCAL_MINB 3
+#endif
+__global__ void __launch_bounds__(LT, FMM2D_LOCAL_MINB) k_tree_local(LocalArgs A)
+{
+    extern __shared__ __align__(16) unsigned char lsm[];
+    LocalSmem& S = *reinterpret_cast<LocalSmem*>(lsm);
+    typedef cub::BlockScan<uint32_t, LT> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    const int tid = threadIdx.x;
+    const int64_t b = A.b0 + blockIdx.x;
+    const uint32_t* O0 = A.boff + A.obase[A.l0];
+    const uint32_t s0 = O0[b];
+    const int n = (int)(O0[b + 1] - s0);
+    uint2* X = S.buf[0];
+    uint2* Y = S.buf[1];
+    uint2* T = S.buf[2];
+    for (int k = tid; k < n; k += LT) {
+        X[k] = A.xl[s0 + k];
+        Y[k] = A.yl[s0 + k];
+    }
+    for (int l = A.l0; l < A.L; ++l) {
+        const int64_t nb = (int64_t)1 << (2 * (l - A.l0));         // level-l boxes of this CTA
+        const int64_t gb = b * nb;                                  // first one, level-local id
+        const uint32_t* O = A.boff + A.obase[l] + gb;
+        const uint32_t* H = A.boff + A.hbase[l] + 2 * gb;
+        const uint32_t* C = A.boff + A.obase[l + 1] + 4 * gb;
+        // two steps: x-split of Y (segments: boxes, subs: halves, split on rx from X),
+        // then y-split of X (segments: halves, subs: children, split on ry from Y)
+        for (int step = 0; step < 2; ++step) {
+            const int nseg = (int)(step == 0 ? nb : 2 * nb);
+            const uint32_t* SO = step == 0 ? O : H;
+            const uint32_t* SU = step == 0 ? H : C;
+            uint2* L_ = step == 0 ? Y : X;                         // list partitioned
+            const uint2* SL = step == 0 ? X : Y;                   // list giving the split ranks
+            __syncthreads();
+            for (int j = tid; j <= nseg; j += LT) S.segs[j] = SO[j] - s0;
+            for (int j = tid; j <= 2 * nseg; j += LT) S.subs[j] = SU[j] - s0;
+            __syncthreads();
+            if (tid < 32) {                                        // split ranks and Gp (warp 0)
+                uint32_t run = 0;
+                for (int j0 = 0; j0 < nseg; j0 += 32) {
+                    const int j = j0 + tid;
+                    uint32_t hsz = 0;
+                    if (j < nseg) {
+                        const uint32_t sp = S.subs[2 * j + 1], pe = S.segs[j + 1];
+                        hsz = pe - sp;
+                        const uint2 rr = (sp < pe) ? SL[sp] : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+                        S.split[j] = step == 0 ? rr.x : rr.y;
+                    }
+                    uint32_t incl = hsz;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (tid >= o) incl += v;
+                    }
+                    if (j < nseg) S.gp[j] = run + incl - hsz;
+                    run += __shfl_sync(0xffffffffu, incl, 31);
+                }
+            }
+            __syncthreads();
+            uint2 rec[LI];
+            uint32_t f[LI], sg[LI], cnt = 0;
+#pragma unroll
+            for (int u = 0; u < LI; ++u) {
+                const int k = tid * LI + u;
+                f[u] = 0;
+                sg[u] = 0;
+                if (k < n) {
+                    rec[u] = L_[k];
+                    sg[u] = local_seg(S.segs, nseg, (uint32_t)k);
+                    const uint32_t rank = step == 0 ? rec[u].x : rec[u].y;
+                    f[u] = rank >= S.split[sg[u]] ? 1u : 0u;
+                }
+                cnt += f[u];
+            }
+            uint32_t excl;
+            Scan(scan_tmp).ExclusiveSum(cnt, excl);
+#pragma unroll
+            for (int u = 0; u < LI; ++u) {
+                const int k = tid * LI + u;
+                if (k < n) {
+                    const uint32_t hb = excl - S.gp[sg[u]];
+                    const uint32_t dst = f[u] ? S.subs[2 * sg[u] + 1] + hb : (uint32_t)k - hb;
+                    T[dst] = rec[u];
+                }
+                excl += f[u];
+            }
+            __syncthreads();
+            if (step == 0) { uint2* t = Y; Y = T; T = t; }
+            else           { uint2* t = X; X = T; T = t; }
+        }
+        // bounding boxes of the level-(l+1) boxes (S.subs holds their local starts)
+        for (int c = tid; c < 4 * nb; c += LT) {
+            const uint32_t s = S.subs[c], e = S.subs[c + 1];
+            const double xmin = A.zc[(uint32_t)A.vx[X[s].x]].x, xmax = A.zc[(uint32_t)A.vx[X[e - 1].x]].x;
+            const double ymin = A.zc[(uint32_t)(A.vy[Y[s].y] >> 32)].y;
+            const double ymax = A.zc[(uint32_t)(A.vy[Y[e - 1].y] >> 32)].y;
+            const int64_t gbx = 4 * gb + c;
+            A.cx[l + 1][gbx] = __dmul_rn(0.5, __dadd_rn(xmin, xmax));
+            A.cy[l + 1][gbx] = __dmul_rn(0.5, __dadd_rn(ymin, ymax));
+            A.r[l + 1][gbx] = 0.0;
+        }
+    }
+    __syncthreads();
+    for (int k = tid; k < n; k += LT) A.yl[s0 + k] = Y[k];
 }
 
 // A2 (part 1): tight bounding box from the segment endpoints of both sorted lists;
@@ -557,13 +751,12 @@ int build_tree(fmm2d_plan* P, const double2* z)
 
     // ---- scratch
     double2* zc;
-    uint32_t *k32a, *k32b, *u32a, *u32b, *hs, *Gp;
+    uint32_t *k32a, *k32b, *u32a, *u32b, *hs, *Gp, *spl, *tseg;
     uint64_t *vx, *vy, *v64a, *k64a, *k64b;
     uint2 *xl, *yl, *tmp;
     Bounds* bnd;
     int* ovf;
     unsigned long long* tstate;
-    unsigned int* ticket;
     void* scratch = nullptr;
     size_t s32 = 0, s64 = 0, sd = 0, scan_bytes = 0;
     const int64_t npmax = (L > 0) ? 2 * nboxes(L - 1) : 1;        // parents of the widest step
@@ -601,8 +794,9 @@ int build_tree(fmm2d_plan* P, const double2* z)
         if ((rc = talloc((void**)&vy, 8 * n))) break;
         if ((rc = talloc((void**)&hs, 4 * npmax))) break;
         if ((rc = talloc((void**)&Gp, 4 * npmax))) break;
+        if ((rc = talloc((void**)&spl, 4 * npmax))) break;
+        if ((rc = talloc((void**)&tseg, 4 * (ntiles + 1)))) break;
         if ((rc = talloc((void**)&tstate, 8 * ntiles))) break;
-        if ((rc = talloc((void**)&ticket, 4))) break;
         if ((rc = talloc((void**)&xl, sizeof(uint2) * n))) break;
         if ((rc = talloc((void**)&yl, sizeof(uint2) * n))) break;
         if ((rc = talloc((void**)&tmp, sizeof(uint2) * n))) break;
@@ -692,28 +886,28 @@ int build_tree(fmm2d_plan* P, const double2* z)
         auto split_step = [&](const uint2* list, const uint2* split, const uint32_t* par_off, const uint32_t* sub_off,
                               int64_t p0, int64_t p1, uint32_t k0, uint32_t k1, int axis, uint2* out) -> int {
             const int64_t np = p1 - p0;
-            k_high_sizes<<<grid_for(np, BS), BS, 0, st>>>(par_off, sub_off, p0, np, hs);
+            const int64_t nt = ((int64_t)k1 - k0 + PTILE - 1) / PTILE;
+            k_seg_prep<<<grid_for(std::max(np, nt), BS), BS, 0, st>>>(par_off, sub_off, split, axis, p0, np, k0, nt,
+                                                                      PTILE_SHIFT, hs, spl, tseg);
             fmm2d::note_launch();
             size_t b2 = cub_bytes;
             FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, b2, hs, Gp, (int)np, st));
-            // positions of the range: par_off[p0] .. par_off[p1] (read back once per level below)
             SplitArgs A;
             A.list = list;
-            A.split_list = split;
             A.par_off = par_off;
             A.sub_off = sub_off;
             A.Gp = Gp;
+            A.split = spl;
+            A.tile_seg = tseg;
             A.out = out;
             A.tstate = tstate;
-            A.ticket = ticket;
             A.p0 = (uint32_t)p0;
             A.p1 = (uint32_t)p1;
             A.k0 = k0;
             A.k1 = k1;
             A.axis = axis;
-            const int64_t nt = ((int64_t)A.k1 - A.k0 + PTILE - 1) / PTILE;
+            A.ntiles = (uint32_t)nt;
             FMM2D_CUDA_TRY(cudaMemsetAsync(tstate, 0, 8 * nt, st));
-            FMM2D_CUDA_TRY(cudaMemsetAsync(ticket, 0, 4, st));
             k_partition<<<(unsigned)nt, PT, 0, st>>>(A);
             fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
@@ -721,7 +915,13 @@ int build_tree(fmm2d_plan* P, const double2* z)
         };
         // levels 0..kpart-1: every box (replicated on every rank); levels >= kpart: the
         // rank's own subtrees only (the whole tree on one GPU, kpart = 0)
-        for (int l = 0; l < L; ++l) {
+        // levels l0 .. L-1 on chip (k_tree_local): boxes of at most LMAX points, at most
+        // LLEV levels below them; never above the partition level
+        int l0 = L;
+        for (int l = std::max(P->kpart, L - LLEV); l < L; ++l)
+            if ((n + nboxes(l) - 1) / nboxes(l) <= LMAX) { l0 = l; break; }
+        if (P->flags & FMM2D_TREE_GLOBAL_ONLY) l0 = L;
+        for (int l = 0; l < l0; ++l) {
             const uint32_t* O = P->boff + P->obase[l];
             const uint32_t* H = P->boff + hbase[l];
             const uint32_t* C = P->boff + P->obase[l + 1];
@@ -738,6 +938,31 @@ int build_tree(fmm2d_plan* P, const double2* z)
             const int64_t c0 = P->box_lo(l + 1), c1 = P->box_hi(l + 1);
             k_bbox<<<grid_for(c1 - c0, BS), BS, 0, st>>>(xl, yl, vx, vy, zc, C, c0, c1, P->cx + P->base[l + 1],
                                                          P->cy + P->base[l + 1], P->r + P->base[l + 1]);
+            fmm2d::note_launch();
+            FMM2D_CUDA_TRY(cudaGetLastError());
+        }
+        if (l0 < L) {
+            LocalArgs A;
+            A.yl = yl;
+            A.xl = xl;
+            A.boff = P->boff;
+            for (int l = 0; l <= L; ++l) A.obase[l] = P->obase[l];
+            for (int l = 0; l < L; ++l) A.hbase[l] = hbase[l];
+            A.l0 = l0;
+            A.L = L;
+            const int64_t b0 = (l0 < P->kpart) ? 0 : P->own_lo(l0), b1 = (l0 < P->kpart) ? nboxes(l0) : P->own_hi(l0);
+            A.b0 = b0;
+            A.vx = vx;
+            A.vy = vy;
+            A.zc = zc;
+            for (int l = 0; l <= L; ++l) {
+                A.cx[l] = P->cx + P->base[l];
+                A.cy[l] = P->cy + P->base[l];
+                A.r[l] = P->r + P->base[l];
+            }
+            const int smem = (int)sizeof(LocalSmem);
+            FMM2D_CUDA_TRY(cudaFuncSetAttribute(k_tree_local, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            k_tree_local<<<(unsigned)(b1 - b0), LT, smem, st>>>(A);
             fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
         }

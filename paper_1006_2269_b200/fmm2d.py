@@ -27,6 +27,7 @@ HOST_PTRS = 0x1
 REAL_STRENGTHS = 0x2
 SYMMETRIC_P2P = 0x4
 TREE_KEY64 = 0x8
+TREE_GLOBAL_ONLY = 0x10
 
 EXPORT_PERM, EXPORT_OFFSETS, EXPORT_DISCS, EXPORT_STRONG, EXPORT_WEAK, EXPORT_MPOLE, EXPORT_LOCAL, \
     EXPORT_STATS = range(1, 9)
@@ -163,7 +164,8 @@ class Fmm2d:
 
     def __init__(self, z, theta: float = 0.5, p: int = 17, leaf_target: int = 40, nlevels: int = -1,
                  real_strengths: bool = False, device: int | None = None, stream=None,
-                 symmetric_p2p: bool = False, tree_key64: bool = False, nranks: int = 1, rank: int = 0,
+                 symmetric_p2p: bool = False, tree_key64: bool = False, tree_global_only: bool = False,
+                 nranks: int = 1, rank: int = 0,
                  nccl_id: bytes | None = None):
         L = lib()
         import torch
@@ -182,7 +184,8 @@ class Fmm2d:
         opt.leaf_target = int(leaf_target)
         opt.nlevels = int(nlevels)
         opt.flags = ((HOST_PTRS if host else 0) | (REAL_STRENGTHS if real_strengths else 0)
-                     | (SYMMETRIC_P2P if symmetric_p2p else 0) | (TREE_KEY64 if tree_key64 else 0))
+                     | (SYMMETRIC_P2P if symmetric_p2p else 0) | (TREE_KEY64 if tree_key64 else 0)
+                     | (TREE_GLOBAL_ONLY if tree_global_only else 0))
         opt.device = int(device)
         opt.stream = ctypes.c_void_p(stream.cuda_stream)
         opt.nranks = int(nranks)

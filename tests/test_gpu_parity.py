@@ -122,6 +122,18 @@ def test_tree_presort_paths(orc):
         _check_structure(g64, op, L)
 
 
+@pytest.mark.parametrize("cfg,n", [("C1", None), ("C2", None), ("C3", 200_000)])
+def test_tree_global_only_equals_on_chip_finish(orc, cfg, n):
+    """The deepest levels split on chip (k_tree_local) and every step in global memory
+    (k_partition only) give the same tree as the oracle (DESIGN 6.1)."""
+    from paper_1006_2269_b200 import Fmm2d
+    z, _ = W.make_config(cfg, n=n)
+    L = orc.nlevels(len(z), 35)
+    op = orc.plan(z, 0.5, L)
+    g = Fmm2d(torch.from_numpy(z).cuda(), theta=0.5, p=8, nlevels=L, tree_global_only=True)
+    _check_structure(g, op, L)
+
+
 EVAL_CASES = [
     ("C1", "C1", None, 0.5, 17),
     ("C2-t.5-p17", "C2", None, 0.5, 17),
