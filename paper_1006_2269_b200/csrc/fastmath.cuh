@@ -117,7 +117,9 @@ FM_HD double rcp(double x)
 }
 
 // log(r2) with a degree-5 series (|u| < 2^-9: truncation < 2^-54 / 6 absolute), used
-// by the near-field kernel where only the absolute error of each term matters.
+// by the near-field kernel where only the absolute error of each term matters.  No
+// special case for r2 == 0 (coincident distinct points): there arg_t gives NaN, so
+// the pair's Phi and Phi' are non-finite anyway.
 FM_HD double log_pos5(double r2, const double2* __restrict__ tab)
 {
     const int64_t b = as_bits(r2);
@@ -134,7 +136,7 @@ FM_HD double log_pos5(double r2, const double2* __restrict__ tab)
     p = fma_(p, u, kC[4]);
     const double lp = fma_(p, u * u, u);
     const double r = fma_(e32, kC[8], T.y + lp);
-    return (r2 == 0.0) ? -HUGE_VAL : r;
+    return r;                    // r2 == 0 gives a finite value; Arg(0) is NaN (see k_near)
 }
 
 // log(r2) for r2 > 0 normal; -inf for r2 == 0.
@@ -197,6 +199,36 @@ FM_HD double arg(double dx, double dy, const double2* __restrict__ tab)
     return octant_fix(a, swap, hx < 0, (int64_t)(uint32_t)(hy & (int)0x80000000u) << 32);
 }
 
+// arg with the octant base read from the table (rows OCT_ROW, OCT_ROW+1 = {0, pi},
+// {pi/2, pi/2} indexed by 2 swap + neg) instead of selects; same result bit for bit.
+constexpr int OCT_ROW = ATAN_N + 4;
+FM_HD double arg_t(double dx, double dy, const double2* __restrict__ tab)
+{
+    const int hx = (int)(as_bits(dx) >> 32), hy = (int)(as_bits(dy) >> 32);
+    const bool swap = fabs(dy) > fabs(dx);
+    const double mns = swap ? dx : dy;
+    const double mxs = swap ? dy : dx;
+    const double mn = fabs(mns), mx = fabs(mxs);
+    const double q0 = fabs(mns * rcp_approx(mxs));
+    const double y = q0 + kC[15];
+    const int jr = (int)as_bits(y) & (2 * ATAN_N - 1);
+    const int j = jr < ATAN_N ? jr : ATAN_N;
+    const double c = y - kC[15];
+    const double num = fma_(-c, mx, mn);
+    const double den = fma_(c, mn, mx);
+    const double t = num * rcp(den);
+    const double t2 = t * t;
+    const double p = fma_(kC[6], t2, kC[7]);
+    const double at = fma_(p * t2, t, t);
+    const double2 T = tab[j];
+    const double a = T.x + (at + T.y);
+    const bool neg = hx < 0;
+    const double base = reinterpret_cast<const double*>(tab + OCT_ROW)[2 * (int)swap + (int)neg];
+    const double sa = from_bits(as_bits(a) ^ ((int64_t)(swap != neg) << 63));
+    const double res = base + sa;
+    return from_bits(as_bits(res) | ((int64_t)(uint32_t)(hy & (int)0x80000000u) << 32));
+}
+
 // Arg(dz) and Arg(-dz), the latter of the componentwise difference z_j - z_i (zeros stay
 // +0, DESIGN R2): the same reduced angle, mirrored octant (-dx < 0 iff dx > 0) and sign
 // (-dy < 0 iff dy > 0).  Used by the symmetric near-field kernel.
@@ -240,6 +272,11 @@ static inline void make_tables(Tables* T)
         T->at[j].x = hi;
         T->at[j].y = (double)(th - (long double)hi);
     }
+    // octant bases for arg_t (rows never reached by the clamped index j <= ATAN_N)
+    T->at[OCT_ROW].x = 0.0;
+    T->at[OCT_ROW].y = kC[12];
+    T->at[OCT_ROW + 1].x = kC[10];
+    T->at[OCT_ROW + 1].y = kC[10];
 }
 
 }  // namespace fm

@@ -71,7 +71,7 @@ __device__ __forceinline__ void pair(PairAcc& a, double dx, double dy, double mr
 #else
     const double l2 = fm::log_pos(r2, T.lg);
 #endif
-    const double th = fm::arg(dx, dy, T.at);                          // Arg dz
+    const double th = fm::arg_t(dx, dy, T.at);                        // Arg dz
     const double ir2 = fm::rcp(r2);
     const double mr2 = mr * ir2;
     a.ar = fma(mr, l2, a.ar);

@@ -228,6 +228,18 @@ def test_eval_deterministic_and_reusable():
     assert not np.array_equal(c[0], a[0])
 
 
+def test_coincident_distinct_points_are_nonfinite():
+    """Coincident DISTINCT points are not an error (DESIGN R21): their pair has dz = 0,
+    so Phi and Phi' of both points are non-finite; every other point stays finite."""
+    z, m = W.make("uniform", 3000, seed=5)
+    z[1234] = z[77]
+    phi, dphi = _gpu_eval(_gpu_plan(z, 0.5, 17, 3), m)
+    bad = np.zeros(len(z), bool)
+    bad[[77, 1234]] = True
+    assert not np.isfinite(phi[bad]).all() and not np.isfinite(dphi[bad]).all()
+    assert np.isfinite(phi[~bad]).all() and np.isfinite(dphi[~bad]).all()
+
+
 def test_nonfinite_rejected():
     from paper_1006_2269_b200 import Fmm2d, FmmError
     z = np.zeros(100, np.complex128) + np.arange(100)

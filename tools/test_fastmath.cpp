@@ -49,6 +49,7 @@ int main()
         double dxn = (dx == 0.0) ? 0.0 : -dx, dyn = (dy == 0.0) ? 0.0 : -dy;
         long double rn = atan2l((long double)dyn, (long double)dxn);
         if (th != a) pair_mismatch++;
+        if (arg_t(dx, dy, T.at) != a) pair_mismatch++;       // table-based octant: bit-identical
         margn = std::fmax(margn, ulp_err(thn, rn));
         // near-field log: degree-5 series, absolute error in units of 2^-52 max(1, |log|)
         double lg5 = 0.5 * log_pos5(r2, T.lg);
