@@ -34,6 +34,9 @@ constexpr int NEAR_T = 128;
 #ifndef FMM2D_NEAR_MINB
 #define FMM2D_NEAR_MINB 8
 #endif
+#ifndef FMM2D_NEAR_SKIPBAR
+#define FMM2D_NEAR_SKIPBAR 1      // no barrier before the first chunk of a pass
+#endif
 #ifndef FMM2D_NEAR_LOG5
 #define FMM2D_NEAR_LOG5 1         // degree-5 log1p (absolute error < 2^-52: tests/test_fastmath.py)
 #endif
@@ -144,7 +147,7 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
     __shared__ int cstart[33];
     __shared__ int cinfo[2];                 // [0] leaves in chunk, [1] chunk row of leaf t (-1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    load_tables(T, gtab);
+    load_tables(T, gtab);                    // (the first chunk's barriers cover it)
     const int64_t t = t0 + blockIdx.x;
     const uint32_t ts = off[t], te = off[t + 1];
     const int nt = (int)(te - ts);
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
         const double4 B = src[ts + i0 + lb];
         PairAcc aa, ab;
         for (int64_t q = q0; q < q1;) {
-            __syncthreads();                      // previous chunk consumed
+            if (q != q0 || !FMM2D_NEAR_SKIPBAR) __syncthreads();   // previous chunk consumed
             if (warp == 0) {
                 const int64_t qq = q + lane;
                 int sz = 0;
@@ -238,13 +241,14 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                 acc.z += v.z;
                 acc.w += v.w;
             }
-            const uint32_t i = ts + i0 + kk;
-            const double4 me = src[i];
-            double fr, fi, gr, gi;
-            l2p(loc + t * (p + 1), p, me.x - cx[t], me.y - cy[t], fr, fi, gr, gi);
-            const uint32_t o = perm[i];
-            if (phi) phi[o] = make_double2(acc.x + fr, acc.y + fi);
-            if (dphi) dphi[o] = make_double2(acc.z + gr, acc.w + gi);
+            double4 f;                            // L2P (Horner) of the target
+            {
+                const double4 me = src[ts + i0 + kk];
+                l2p(loc + t * (p + 1), p, me.x - cx[t], me.y - cy[t], f.x, f.y, f.z, f.w);
+            }
+            const uint32_t o = perm[ts + i0 + kk];
+            if (phi) phi[o] = make_double2(acc.x + f.x, acc.y + f.y);
+            if (dphi) dphi[o] = make_double2(acc.z + f.z, acc.w + f.w);
         }
         __syncthreads();
     }
