@@ -138,6 +138,7 @@ struct M2LArgs {
     int64_t base[FMM2D_MAXL + 2];
     int64_t lo[FMM2D_MAXL + 1];       // target boxes of level l: [lo[l], lo[l] + (pre[l+1] - pre[l]))
     int64_t pre[FMM2D_MAXL + 2];      // work prefix over levels 1..L
+    const uint32_t* order;            // [pre[L+1]] target box of each work item (level-local id)
     int L;
     const double* cx;
     const double* cy;
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l(M2LArgs A)
     if (w >= A.pre[A.L + 1]) return;
     int lev = 1;
     while (lev < A.L && w >= A.pre[lev + 1]) ++lev;
-    const int64_t g = A.base[lev] + A.lo[lev] + (w - A.pre[lev]);
+    const int64_t g = A.base[lev] + A.order[w];
     // part q computes coefficients [q H, min((q+1) H, P+1)), H = ceil((P+1)/NS)
     constexpr int H = (P + NS) / NS;
     constexpr int E1 = (2 * H < P + 1) ? 2 * H : P + 1;
@@ -333,6 +334,7 @@ int m2l_p(fmm2d_plan* Pl)
         A.lo[l] = Pl->box_lo(l);
         A.pre[l + 1] = A.pre[l] + (Pl->box_hi(l) - Pl->box_lo(l));
     }
+    A.order = Pl->m2l_order;
     A.L = L;
     A.cx = Pl->cx;
     A.cy = Pl->cy;

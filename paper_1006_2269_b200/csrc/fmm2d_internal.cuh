@@ -67,6 +67,7 @@ struct fmm2d_plan {
     double *cx = nullptr, *cy = nullptr, *r = nullptr;   // [nbox_total]
     // connectivity
     std::vector<fmm2d::Csr> strong, weak;   // per level
+    uint32_t* m2l_order = nullptr;      // M2L targets per level (levels 1..L concatenated), by list length
     // expansions
     double2* mpole = nullptr;           // [nbox_total][p+1]
     double2* local = nullptr;           // [nbox_total][p+1]

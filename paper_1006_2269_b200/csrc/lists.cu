@@ -75,6 +75,24 @@ __global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, c
     }
 }
 
+// M2L work order of one level: inside each window of M2L_WIN consecutive boxes (tree
+// order: neighbouring targets share source multipoles in cache), targets by descending
+// weak-list length (clamped to 255), so the 32 targets of a warp walk lists of nearly
+// equal length.  key = window << 8 | (255 - len), value = box.
+#ifndef FMM2D_M2L_WIN
+#define FMM2D_M2L_WIN 16384
+#endif
+__global__ void k_m2l_keys(int64_t b0, int64_t b1, const int64_t* __restrict__ woff, uint32_t* __restrict__ key,
+                           uint32_t* __restrict__ box)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t b = b0 + i;
+    if (b >= b1) return;
+    const int64_t len = woff[b + 1] - woff[b];
+    key[i] = ((uint32_t)(i / FMM2D_M2L_WIN) << 8) | (uint32_t)(255 - (len < 255 ? len : 255));
+    box[i] = (uint32_t)b;
+}
+
 // ordered P2P pairs (j != i) of one evaluation: sum_t n_t * sum_{s in S(t)} n_s - N
 __global__ void k_pair_count(int64_t t0, int64_t t1, const uint32_t* __restrict__ off,
                              const int64_t* __restrict__ soff, const uint32_t* __restrict__ sidx,
@@ -172,6 +190,38 @@ int build_lists(fmm2d_plan* P)
                                                 W.off, S.off, W.idx, S.idx); fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
             P->stats.weak_pairs += W.total;
+        }
+        // M2L work order (k_m2l_keys)
+        {
+            int64_t tot = 0;
+            for (int l = 1; l <= L; ++l) tot += P->box_hi(l) - P->box_lo(l);
+            FMM2D_TRY(dev_alloc(P, (void**)&P->m2l_order, sizeof(uint32_t) * std::max<int64_t>(tot, 1)));
+            uint32_t *k0 = nullptr, *k1 = nullptr;
+            uint32_t* v0 = nullptr;
+            void* sc = nullptr;
+            size_t sb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, sb, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                            (uint32_t*)nullptr, (int)nbmax, 0, 32, st);
+            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&k0, sizeof(uint32_t) * nbmax, st));
+            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&k1, sizeof(uint32_t) * nbmax, st));
+            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&v0, sizeof(uint32_t) * nbmax, st));
+            FMM2D_CUDA_TRY(cudaMallocAsync(&sc, std::max<size_t>(sb, 16), st));
+            int64_t o = 0;
+            for (int l = 1; l <= L; ++l) {
+                const int64_t b0 = P->box_lo(l), b1 = P->box_hi(l), nb = b1 - b0;
+                k_m2l_keys<<<grid_for(nb, 256), 256, 0, st>>>(b0, b1, P->weak[l].off, k0, v0);
+                fmm2d::note_launch();
+                int bits = 8;
+                while (((int64_t)1 << (bits - 8)) * FMM2D_M2L_WIN < nb) ++bits;
+                size_t s2 = sb;
+                FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(sc, s2, k0, k1, v0, P->m2l_order + o, (int)nb, 0, bits,
+                                                               st));
+                o += nb;
+            }
+            cudaFreeAsync(k0, st);
+            cudaFreeAsync(k1, st);
+            cudaFreeAsync(v0, st);
+            cudaFreeAsync(sc, st);
         }
         P->stats.strong_leaf_pairs = P->strong[L].total;
         unsigned long long* d_tot = (unsigned long long*)cnt_w;   // reuse scratch
