@@ -22,6 +22,11 @@ Parity status of each oracle function (what pins it, see tests/test_oracle_*.py)
                 unit charge about 4, [1,1]->[2,1]), translation identities
   eval          pinned: error vs direct sum within the paper's a-priori law
                 (P:281-285), decay slope ~ log10(theta), ordering in theta
+  rr exchange   pinned (O7): predicate worked examples + the exchanged
+                geometric meaning, P2L closed form and P2L = M2L o P2M identity, M2P of a
+                single charge, conversion-list audit (exchanged holds, original fails,
+                symmetric bookkeeping), exactly-once pair coverage, the whole pass vs
+                the direct sum within the gate
 No function is "parity unpinned".
 """
 from __future__ import annotations
@@ -64,6 +69,10 @@ def lib():
         L.oracle_well_separated.argtypes = [ctypes.c_double] * 7
         L.oracle_nlevels.argtypes = [ctypes.c_int64, ctypes.c_int]
         L.oracle_build.argtypes = [dp, ctypes.c_int64, ctypes.c_double, ctypes.c_int, ctypes.POINTER(vp)]
+        L.oracle_build_ex.argtypes = [dp, ctypes.c_int64, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                      ctypes.POINTER(vp)]
+        L.oracle_rr_exchange.argtypes = [ctypes.c_double] * 7
+        L.oracle_p2l.argtypes = [dp, dp, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int, dp]
         L.oracle_free.argtypes = [vp]
         L.oracle_free.restype = None
         L.oracle_levels.argtypes = [vp]
@@ -141,13 +150,15 @@ class Plan:
     """Oracle tree + discs + lists for fixed (z, theta, L); ``eval(m, p)`` runs the
     evaluation pass.  Arrays are returned as numpy copies."""
 
-    def __init__(self, z, theta: float, L: int):
+    def __init__(self, z, theta: float, L: int, rr_exchange: bool = False):
         z = _c128(z)
         self.n = int(z.shape[0])
         self.theta = float(theta)
         self.L = int(L)
+        self.rr_exchange = bool(rr_exchange)
         h = ctypes.c_void_p()
-        rc = lib().oracle_build(_dp(_as_f64(z)), self.n, self.theta, self.L, ctypes.byref(h))
+        rc = lib().oracle_build_ex(_dp(_as_f64(z)), self.n, self.theta, self.L, 1 if rr_exchange else 0,
+                                   ctypes.byref(h))
         if rc:
             raise ValueError(f"oracle_build: {rc}")
         self._h = h
@@ -175,8 +186,9 @@ class Plan:
         return cx, cy, r
 
     def list(self, level: int, kind: str):
-        """kind 'strong' or 'weak' -> CSR (off int64[4^l+1], idx uint32[])."""
-        k = 1 if kind == "weak" else 0
+        """kind 'strong' or 'weak' (any level), 'near' / 'p2l' / 'm2p' (leaf level, the
+        r/R exchange split of the strong list, O7) -> CSR (off int64[4^l+1], idx uint32[])."""
+        k = {"strong": 0, "weak": 1, "near": 2, "p2l": 3, "m2p": 4}[kind]
         tot = lib().oracle_list_total(self._h, level, k)
         off = np.empty(4 ** level + 1, np.int64)
         idx = np.empty(max(tot, 1), np.uint32)
@@ -203,8 +215,25 @@ class Plan:
         return out
 
 
-def plan(z, theta: float, L: int) -> Plan:
-    return Plan(z, theta, L)
+def plan(z, theta: float, L: int, rr_exchange: bool = False) -> Plan:
+    return Plan(z, theta, L, rr_exchange)
+
+
+def rr_exchange(cb, rb, cc, rc, theta) -> bool:
+    """O7: Criterion 1 with the roles of r and R exchanged, r + theta R <= theta d,
+    for r < R strictly."""
+    cb = complex(cb)
+    cc = complex(cc)
+    return bool(lib().oracle_rr_exchange(cb.real, cb.imag, rb, cc.real, cc.imag, rc, theta))
+
+
+def p2l(z, m, c, p):
+    """O7 P2L: local expansion about c of the sources (z, m)."""
+    z, m = _c128(z), _c128(m)
+    b = np.zeros(p + 1, np.complex128)
+    c = complex(c)
+    lib().oracle_p2l(_dp(_as_f64(z)), _dp(_as_f64(m)), z.shape[0], c.real, c.imag, p, _dp(_as_f64(b)))
+    return b
 
 
 # --- single operators (pins) -------------------------------------------------

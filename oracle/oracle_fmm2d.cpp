@@ -17,6 +17,7 @@
  *   O4 connectivity
  *   O5 expansions / shifts   P:355-362, classical complex forms P:436-440
  *   O6 branch conventions    DESIGN R2
+ *   O7 r/R exchange          P:370-377 (optional; leaf level: P2L + M2P instead of P2P)
  * Floating point: compiled with -O2 -ffp-contract=off (no FMA contraction), no
  * fast-math; sqrt is IEEE correctly rounded.  OpenMP is used only across
  * independent boxes / targets, each of which is summed in a fixed order, so
@@ -87,6 +88,23 @@ int oracle_well_separated(double cbx, double cby, double rb,
 }
 
 /* O1: depth rule (DESIGN R4): smallest L >= 0 with n <= 2 * leaf_target * 4^L. */
+/* ------------------------------------------------------------------------- */
+/* O7 predicate: Criterion 1 "when the roles of r and R are exchanged"          */
+/* (P:370-377): for boxes of radii r < R (strictly; equal radii make the two   */
+/* criteria identical), r + theta R <= theta d.  Same operation order as the   */
+/* criterion (DESIGN R11); d > 0 as R9.  Returns 1 when the exchanged criterion */
+/* holds (the caller asks only about pairs that failed Criterion 1).           */
+/* ------------------------------------------------------------------------- */
+int oracle_rr_exchange(double cbx, double cby, double rb, double ccx, double ccy, double rc, double theta)
+{
+    double dx = cbx - ccx;
+    double dy = cby - ccy;
+    double d = std::sqrt(dx * dx + dy * dy);
+    double R = std::max(rb, rc);
+    double r = std::min(rb, rc);
+    return (r < R) && (d > 0.0) && (r + theta * R <= theta * d);
+}
+
 int oracle_nlevels(int64_t n, int leaf_target)
 {
     if (n < 1 || leaf_target < 1) return -1;
@@ -108,6 +126,11 @@ struct oracle_plan {
     std::vector<std::vector<int64_t>> off;           /* per level: 4^l + 1 offsets    */
     std::vector<std::vector<double>> cx, cy, rad;    /* per level: 4^l discs          */
     std::vector<std::vector<std::vector<uint32_t>>> strong, weak; /* per level, box */
+    /* O7 (rr exchange on): the leaf strong list split into P2P (near), P2L into
+     * this smaller box from a larger one (p2l_in), M2P of a smaller box at this
+     * larger box's points (m2p_in).  Off: near = strong[L], the others empty. */
+    int rr;
+    std::vector<std::vector<uint32_t>> near, p2l_in, m2p_in;
     /* expansions from the last oracle_eval (diagnostics) */
     int p;
     std::vector<std::vector<cplx>> mpole, local;     /* per level: 4^l * (p+1)        */
@@ -241,7 +264,46 @@ static void build_lists(oracle_plan* P)
     }
 }
 
+/* O7: the optional finest-level optimisation of P:370-377.  "A related idea at
+ * the finest level is to investigate strongly coupled boxes of very different
+ * radii, r << R, say.  If the theta-criterion is true when the roles of r and R
+ * are exchanged, then the sources in the larger box can be directly converted
+ * into a near field expansion in the smaller box, and the outgoing expansion
+ * from the smaller can simply be evaluated at each point in the larger box."
+ * For leaf t and each s in its strong list, s != t: if r_t < r_s and the
+ * exchanged criterion holds, s's sources go into t's local (p2l_in[t]); if
+ * r_s < r_t and it holds, s's multipole is evaluated at t's points (m2p_in[t]);
+ * otherwise the pair stays direct (near[t]).  Lists keep the strong order. */
+static void build_rr(oracle_plan* P)
+{
+    const int L = P->L;
+    const int64_t nb = nboxes(L);
+    P->near.assign(nb, {});
+    P->p2l_in.assign(nb, {});
+    P->m2p_in.assign(nb, {});
+    const std::vector<double>& cx = P->cx[L];
+    const std::vector<double>& cy = P->cy[L];
+    const std::vector<double>& rr = P->rad[L];
+    for (int64_t t = 0; t < nb; ++t) {
+        for (uint32_t s : P->strong[L][t]) {
+            bool conv = P->rr && (int64_t)s != t &&
+                        oracle_rr_exchange(cx[t], cy[t], rr[t], cx[s], cy[s], rr[s], P->theta);
+            if (!conv) P->near[t].push_back(s);
+            else if (rr[t] < rr[s]) P->p2l_in[t].push_back(s);
+            else P->m2p_in[t].push_back(s);
+        }
+    }
+}
+
+int oracle_build_ex(const double* z, int64_t n, double theta, int L, int flags, oracle_plan** out);
+
 int oracle_build(const double* z, int64_t n, double theta, int L, oracle_plan** out)
+{
+    return oracle_build_ex(z, n, theta, L, 0, out);
+}
+
+/* flags bit 0: r/R exchange (O7) */
+int oracle_build_ex(const double* z, int64_t n, double theta, int L, int flags, oracle_plan** out)
 {
     if (!out) return -1;
     *out = nullptr;
@@ -258,9 +320,11 @@ int oracle_build(const double* z, int64_t n, double theta, int L, oracle_plan** 
         P->x[i] = z[2 * i] + 0.0;
         P->y[i] = z[2 * i + 1] + 0.0;
     }
+    P->rr = (flags & 1) ? 1 : 0;
     build_tree(P);
     build_discs(P);
     build_lists(P);
+    build_rr(P);
     *out = P;
     return 0;
 }
@@ -292,11 +356,23 @@ int oracle_get_discs(const oracle_plan* P, int l, double* cx, double* cy, double
     return 0;
 }
 
-/* kind 0 = strong, 1 = weak.  count-only when off == NULL (returns total). */
+/* kind 0 = strong, 1 = weak; leaf level only: 2 = near (P2P), 3 = p2l_in,
+ * 4 = m2p_in (O7). */
+static const std::vector<std::vector<uint32_t>>& list_of(const oracle_plan* P, int l, int kind)
+{
+    switch (kind) {
+        case 1: return P->weak[l];
+        case 2: return P->near;
+        case 3: return P->p2l_in;
+        case 4: return P->m2p_in;
+        default: return P->strong[l];
+    }
+}
+
 int64_t oracle_list_total(const oracle_plan* P, int l, int kind)
 {
-    if (l < 0 || l > P->L) return -1;
-    const auto& LL = kind ? P->weak[l] : P->strong[l];
+    if (l < 0 || l > P->L || kind < 0 || kind > 4 || (kind >= 2 && l != P->L)) return -1;
+    const auto& LL = list_of(P, l, kind);
     int64_t t = 0;
     for (const auto& v : LL) t += (int64_t)v.size();
     return t;
@@ -304,8 +380,8 @@ int64_t oracle_list_total(const oracle_plan* P, int l, int kind)
 
 int oracle_get_list(const oracle_plan* P, int l, int kind, int64_t* off, uint32_t* idx)
 {
-    if (l < 0 || l > P->L) return -1;
-    const auto& LL = kind ? P->weak[l] : P->strong[l];
+    if (l < 0 || l > P->L || kind < 0 || kind > 4 || (kind >= 2 && l != P->L)) return -1;
+    const auto& LL = list_of(P, l, kind);
     int64_t t = 0;
     for (size_t b = 0; b < LL.size(); ++b) {
         off[b] = t;
@@ -403,6 +479,53 @@ static void l2l(const cplx* b, cplx h, int p, const std::vector<std::vector<doub
     }
 }
 
+/* O7 P2L: the local (near-field) expansion about c of sources z_j, m_j outside
+ * the target disc ("the sources in the larger box can be directly
+ * converted into a near field expansion in the smaller box"):
+ *   log(z - z_j) = Log(c - z_j) + sum_{l>=1} -(z - c)^l / (l (z_j - c)^l),
+ * so b_0 += sum_j m_j Log(c - z_j) (componentwise difference, DESIGN R2) and
+ * b_l += -sum_j m_j / (l (z_j - c)^l), l = 1..p. */
+static void p2l(const cplx* zs, const cplx* ms, int64_t ns, cplx c, int p, cplx* b)
+{
+    for (int64_t j = 0; j < ns; ++j) {
+        cplx u(c.real() - zs[j].real(), c.imag() - zs[j].imag());     /* c - z_j */
+        cplx v(zs[j].real() - c.real(), zs[j].imag() - c.imag());     /* z_j - c */
+        b[0] += ms[j] * std::log(u);
+        cplx iv = 1.0 / v, ivl = 1.0;
+        for (int l = 1; l <= p; ++l) {
+            ivl *= iv;
+            b[l] -= ms[j] * ivl / (double)l;
+        }
+    }
+}
+
+/* O7 M2P: the outgoing expansion of a (smaller) box at c evaluated at z (P:375-376,
+ * "the outgoing expansion from the smaller can simply be evaluated at each point
+ * in the larger box"): Phi += a_0 Log(z - c) + sum_k a_k (z - c)^-k,
+ * dPhi += a_0/(z - c) - sum_k k a_k (z - c)^-(k+1); z - c componentwise. */
+static void m2p_eval(const cplx* a, cplx c, int p, cplx z, cplx* phi, cplx* dphi)
+{
+    cplx w(z.real() - c.real(), z.imag() - c.imag());
+    cplx iw = 1.0 / w, iwk = 1.0;
+    cplx f = a[0] * std::log(w), df = a[0] * iw;
+    for (int k = 1; k <= p; ++k) {
+        iwk *= iw;
+        f += a[k] * iwk;
+        df -= (double)k * a[k] * iwk * iw;
+    }
+    *phi += f;
+    *dphi += df;
+}
+
+int oracle_p2l(const double* z, const double* m, int64_t n, double cx, double cy, int p, double* b)
+{
+    std::vector<cplx> zs(n), ms(n), B(p + 1, 0.0);
+    for (int64_t j = 0; j < n; ++j) { zs[j] = cplx(z[2*j], z[2*j+1]); ms[j] = cplx(m[2*j], m[2*j+1]); }
+    p2l(zs.data(), ms.data(), n, cplx(cx, cy), p, B.data());
+    for (int k = 0; k <= p; ++k) { b[2*k] = B[k].real(); b[2*k+1] = B[k].imag(); }
+    return 0;
+}
+
 /* exported single-operator entry points (pins; same code as the pipeline) */
 int oracle_p2m(const double* z, const double* m, int64_t n, double cx, double cy, int p, double* a)
 {
@@ -471,22 +594,15 @@ int oracle_l2p(const double* b, double cx, double cy, int p, const double* z, in
     return 0;
 }
 
-/* Multipole far-field evaluation (used by pins only):
- * a_0 log(z-c) + sum_k a_k (z-c)^-k and its derivative. */
+/* Multipole far-field evaluation (O7 M2P; also a pin of P2M) */
 int oracle_m2p(const double* a, double cx, double cy, int p, const double* z, int64_t n,
                double* phi, double* dphi)
 {
+    std::vector<cplx> A(p + 1);
+    for (int k = 0; k <= p; ++k) A[k] = cplx(a[2*k], a[2*k+1]);
     for (int64_t i = 0; i < n; ++i) {
-        cplx w(z[2*i] - cx, z[2*i+1] - cy);
-        cplx iw = 1.0 / w, iwk = 1.0;
-        cplx a0(a[0], a[1]);
-        cplx f = a0 * std::log(w), df = a0 * iw;
-        for (int k = 1; k <= p; ++k) {
-            cplx ak(a[2*k], a[2*k+1]);
-            iwk *= iw;
-            f += ak * iwk;
-            df -= (double)k * ak * iwk * iw;
-        }
+        cplx f = 0.0, df = 0.0;
+        m2p_eval(A.data(), cplx(cx, cy), p, cplx(z[2*i], z[2*i+1]), &f, &df);
         phi[2*i] = f.real(); phi[2*i+1] = f.imag();
         dphi[2*i] = df.real(); dphi[2*i+1] = df.imag();
     }
@@ -553,7 +669,18 @@ int oracle_eval(oracle_plan* P, const double* m, int p, double* phi, double* dph
             l2l(P->local[l - 1].data() + b * P1, h, p, C, P->local[l].data() + c * P1);
         }
     }
-    /* leaves: L2P + P2P over the strong leaf connections */
+    /* O7 (rr exchange): sources of larger strongly coupled leaves into the local
+     * of the smaller one (after M2L + L2L) */
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t t = 0; t < nboxes(L); ++t) {
+        for (uint32_t s : P->p2l_in[t]) {
+            int64_t ss = P->off[L][s], se = P->off[L][s + 1];
+            p2l(zl.data() + ss, ml.data() + ss, se - ss, cplx(P->cx[L][t], P->cy[L][t]), p,
+                P->local[L].data() + t * P1);
+        }
+    }
+    /* leaves: L2P + P2P over the strong leaf connections -- the near
+     * list, i.e. the strong list less the O7 conversions -- + O7 M2P */
     std::vector<cplx> f(P->n), df(P->n);
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t t = 0; t < nboxes(L); ++t) {
@@ -561,7 +688,7 @@ int oracle_eval(oracle_plan* P, const double* m, int p, double* phi, double* dph
         for (int64_t i = ts; i < te; ++i) {
             cplx fi = 0.0, dfi = 0.0;
             l2p(P->local[L].data() + t * P1, cplx(P->cx[L][t], P->cy[L][t]), p, zl[i], &fi, &dfi);
-            for (uint32_t s : P->strong[L][t]) {
+            for (uint32_t s : P->near[t]) {
                 int64_t ss = P->off[L][s], se = P->off[L][s + 1];
                 for (int64_t j = ss; j < se; ++j) {
                     if (j == i) continue;                              /* j != i */
@@ -570,6 +697,9 @@ int oracle_eval(oracle_plan* P, const double* m, int p, double* phi, double* dph
                     dfi += ml[j] / dz;
                 }
             }
+            for (uint32_t s : P->m2p_in[t])                            /* O7 */
+                m2p_eval(P->mpole[L].data() + (int64_t)s * P1, cplx(P->cx[L][s], P->cy[L][s]), p, zl[i],
+                         &fi, &dfi);
             f[i] = fi; df[i] = dfi;
         }
     }
