@@ -63,6 +63,12 @@ extern "C" {
 #define FMM2D_TREE_KEY64      0x8  /* diagnostic: presort both axes with full 64-bit keys
                                       instead of 32-bit keys + run fix-up (same tree,
                                       DESIGN.md section 6.1)                            */
+#define FMM2D_RR_EXCHANGE     0x20  /* the finest-level r/R exchange of P:370-377: strongly
+                                      coupled leaves of radii r < R with r + theta R <= theta d
+                                      interact by P2L (larger leaf's sources into the
+                                      smaller leaf's local) and M2P (smaller leaf's multipole
+                                      at the larger leaf's points) instead of the direct
+                                      sum (R23).  One GPU only (nranks > 1: ENOTSUP) */
 #define FMM2D_TREE_GLOBAL_ONLY 0x10 /* diagnostic: every split step in global memory (no
                                       on-chip finish of the deepest levels; same tree)  */
 
@@ -183,6 +189,9 @@ FMM2D_API int fmm2d_plan_info(const fmm2d_plan* plan, int64_t* n, int* nlevels, 
 #define FMM2D_EXPORT_MPOLE       6  /* l      complex128[4^l][p+1] (after an eval)    */
 #define FMM2D_EXPORT_LOCAL       7  /* l      complex128[4^l][p+1] (after an eval)    */
 #define FMM2D_EXPORT_STATS       8  /* -      double[16]: see fmm2d_api.cu            */
+#define FMM2D_EXPORT_NEAR        9  /* L      int64[4^L+1] offsets then uint32[]: direct pairs */
+#define FMM2D_EXPORT_RR_P2L     10  /* L      same layout: P2L sources of each leaf (r/R exch.) */
+#define FMM2D_EXPORT_RR_M2P     11  /* L      same layout: M2P sources of each leaf (r/R exch.) */
 /* If dst is NULL, *bytes receives the required size.  Otherwise *bytes must hold
  * the capacity of dst; on success it receives the bytes written.  Synchronises the
  * plan's stream.  Errors: EINVAL (bad what/level/capacity), ECUDA. */

@@ -128,6 +128,7 @@ static int build_stage_tree(const double* z, int64_t n, const fmm2d_options* opt
     const int L = plan_depth(n, opt);
     if (L < 0) return L;
     if (nranks < 1 || rank < 0 || rank >= nranks) return FMM2D_EINVAL;
+    if (nranks > 1 && (opt->flags & FMM2D_RR_EXCHANGE)) return FMM2D_ENOTSUP;
     if (nranks > 1) {                                   // partitionable? (before any device work)
         const int k = partition_level(nranks);
         if (k < 0 || L <= k) return FMM2D_ENOTSUP;
@@ -296,7 +297,9 @@ static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi
     for (int i = 0; i < np; ++i) FMM2D_TRY(run_m2l(Ps[i]));
     if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[3], P0->stream));
     for (int i = 0; i < np; ++i) FMM2D_TRY(run_downward(Ps[i]));
+    for (int i = 0; i < np; ++i) FMM2D_TRY(run_rr_p2l(Ps[i]));      // r/R exchange: into the locals
     if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[4], P0->stream));
+    for (int i = 0; i < np; ++i) FMM2D_TRY(run_rr_m2p(Ps[i]));      // r/R exchange: M2P sums
     for (int i = 0; i < np; ++i) FMM2D_TRY(run_near(Ps[i], phid, dphid));
     if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[5], P0->stream));
     if (host) {
@@ -423,11 +426,21 @@ int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* by
 {
     if (!P || !bytes) return FMM2D_EINVAL;
     if (cudaSetDevice(P->device) != cudaSuccess) return FMM2D_ECUDA;
+    const bool leaf_list = (what == FMM2D_EXPORT_NEAR || what == FMM2D_EXPORT_RR_P2L ||
+                            what == FMM2D_EXPORT_RR_M2P);
     const bool per_level = (what == FMM2D_EXPORT_OFFSETS || what == FMM2D_EXPORT_DISCS ||
                             what == FMM2D_EXPORT_STRONG || what == FMM2D_EXPORT_WEAK ||
-                            what == FMM2D_EXPORT_MPOLE || what == FMM2D_EXPORT_LOCAL);
+                            what == FMM2D_EXPORT_MPOLE || what == FMM2D_EXPORT_LOCAL || leaf_list);
     if (per_level && (level < 0 || level > P->L)) return FMM2D_EINVAL;
+    if (leaf_list && level != P->L) return FMM2D_EINVAL;
     const int64_t nb = per_level ? nboxes(level) : 0;
+    // leaf lists: without r/R exchange the conversion lists are empty
+    Csr empty_csr;
+    const Csr* LC = nullptr;
+    if (leaf_list) {
+        LC = (what == FMM2D_EXPORT_NEAR) ? &P->near : (what == FMM2D_EXPORT_RR_P2L ? &P->rr_p2l : &P->rr_m2p);
+        if (!LC->off) LC = &empty_csr;
+    }
     size_t need = 0;
     switch (what) {
         case FMM2D_EXPORT_PERM: need = sizeof(uint32_t) * P->n; break;
@@ -440,6 +453,9 @@ int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* by
         case FMM2D_EXPORT_MPOLE:
         case FMM2D_EXPORT_LOCAL: need = sizeof(double2) * nb * (P->p + 1); break;
         case FMM2D_EXPORT_STATS: need = sizeof(double) * 16; break;
+        case FMM2D_EXPORT_NEAR:
+        case FMM2D_EXPORT_RR_P2L:
+        case FMM2D_EXPORT_RR_M2P: need = sizeof(int64_t) * (nb + 1) + sizeof(uint32_t) * LC->total; break;
         default: return FMM2D_EINVAL;
     }
     if (!dst) {
@@ -473,6 +489,17 @@ int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* by
             FMM2D_TRY(copy_out(C.idx, dst, sizeof(uint32_t) * C.total, &cap, &off, st));
             break;
         }
+        case FMM2D_EXPORT_NEAR:
+        case FMM2D_EXPORT_RR_P2L:
+        case FMM2D_EXPORT_RR_M2P:
+            if (LC->off) {
+                FMM2D_TRY(copy_out(LC->off, dst, sizeof(int64_t) * (nb + 1), &cap, &off, st));
+                FMM2D_TRY(copy_out(LC->idx, dst, sizeof(uint32_t) * LC->total, &cap, &off, st));
+            } else {
+                memset(dst, 0, sizeof(int64_t) * (nb + 1));
+                off = sizeof(int64_t) * (nb + 1);
+            }
+            break;
         case FMM2D_EXPORT_MPOLE:
         case FMM2D_EXPORT_LOCAL: {
             const double2* E = (what == FMM2D_EXPORT_MPOLE) ? P->mpole : P->local;

@@ -272,6 +272,120 @@ __global__ void __launch_bounds__(128) k_l2l(int64_t c0, int64_t c1, const doubl
 
 inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
+// ---------------------------------------------------------------- r/R exchange (DESIGN R23)
+// P2L: the sources of the larger leaves in a leaf's P2L list go straight into
+// its local expansion: b_0 += m Log(c - z_j), b_l += -m / (l (z_j - c)^l) (c - z_j and
+// z_j - c each formed componentwise, R2).  One warp per leaf with P2L work: lanes over
+// the sources, coefficients in registers, fixed-order warp reduction, added to the local.
+template <int P>
+__global__ void __launch_bounds__(128) k_rr_p2l(const uint32_t* __restrict__ leaves, int64_t nleaves,
+                                                const int64_t* __restrict__ off, const uint32_t* __restrict__ idx,
+                                                const uint32_t* __restrict__ boff, const double4* __restrict__ src,
+                                                const double* __restrict__ cx, const double* __restrict__ cy,
+                                                double2* __restrict__ loc)
+{
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nleaves) return;
+    const uint32_t t = leaves[w];
+    const double ctx = cx[t], cty = cy[t];
+    double2 b[P + 1];
+#pragma unroll
+    for (int l = 0; l <= P; ++l) b[l] = make_double2(0.0, 0.0);
+    for (int64_t q = off[t]; q < off[t + 1]; ++q) {
+        const uint32_t s = idx[q];
+        for (uint32_t j = boff[s] + lane; j < boff[s + 1]; j += 32) {
+            const double4 z = src[j];
+            const double2 m = make_double2(z.z, z.w);
+            const double ux = ctx - z.x, uy = cty - z.y;              // c - z_j
+            const double2 lg = make_double2(0.5 * log(ux * ux + uy * uy), atan2(uy, ux));
+            b[0] = cadd(b[0], cmul(m, lg));
+            const double vx = z.x - ctx, vy = z.y - cty;              // z_j - c
+            const double iv2 = 1.0 / (vx * vx + vy * vy);
+            const double2 iv = make_double2(vx * iv2, -vy * iv2);
+            double2 ivl = iv;
+#pragma unroll
+            for (int l = 1; l <= P; ++l) {
+                b[l] = csub(b[l], cscale(cmul(m, ivl), 1.0 / l));
+                if (l < P) ivl = cmul(ivl, iv);
+            }
+        }
+    }
+#pragma unroll
+    for (int l = 0; l <= P; ++l) {
+        for (int o = 16; o; o >>= 1) {
+            b[l].x += __shfl_xor_sync(0xffffffffu, b[l].x, o);
+            b[l].y += __shfl_xor_sync(0xffffffffu, b[l].y, o);
+        }
+    }
+    if (lane == 0) {
+        double2* Lc = loc + (int64_t)t * (P + 1);
+#pragma unroll
+        for (int l = 0; l <= P; ++l) Lc[l] = cadd(Lc[l], b[l]);
+    }
+}
+
+// M2P: the multipoles of the smaller leaves in a leaf's M2P list evaluated at
+// each of its points: a_0 Log(w) + sum_k a_k w^-k and a_0 / w - sum_k k a_k w^-(k+1),
+// w = z_i - c_s (componentwise), Horner in 1/w.  One block per leaf with M2P work; the
+// sums go to acc[i] (leaf order) and k_near adds them.
+template <int P>
+__global__ void __launch_bounds__(128) k_rr_m2p(const uint32_t* __restrict__ leaves, const int64_t* __restrict__ off,
+                                                const uint32_t* __restrict__ idx, const uint32_t* __restrict__ boff,
+                                                const double4* __restrict__ src, const double* __restrict__ cx,
+                                                const double* __restrict__ cy, const double2* __restrict__ mp,
+                                                double4* __restrict__ acc)
+{
+    const uint32_t t = leaves[blockIdx.x];
+    for (uint32_t i = boff[t] + threadIdx.x; i < boff[t + 1]; i += blockDim.x) {
+        const double4 z = src[i];
+        double2 f = make_double2(0.0, 0.0), df = make_double2(0.0, 0.0);
+        for (int64_t q = off[t]; q < off[t + 1]; ++q) {
+            const uint32_t s = idx[q];
+            const double2* A = mp + (int64_t)s * (P + 1);
+            const double wx = z.x - cx[s], wy = z.y - cy[s];
+            const double iw2 = 1.0 / (wx * wx + wy * wy);
+            const double2 iw = make_double2(wx * iw2, -wy * iw2);
+            double2 h = A[P], dh = cscale(A[P], (double)P);
+#pragma unroll
+            for (int k = P - 1; k >= 1; --k) {
+                h = cadd(cmul(h, iw), A[k]);
+                dh = cadd(cmul(dh, iw), cscale(A[k], (double)k));
+            }
+            const double2 lg = make_double2(0.5 * log(wx * wx + wy * wy), atan2(wy, wx));
+            f = cadd(f, cadd(cmul(A[0], lg), cmul(h, iw)));
+            df = cadd(df, csub(cmul(A[0], iw), cmul(dh, cmul(iw, iw))));
+        }
+        acc[i] = make_double4(f.x, f.y, df.x, df.y);
+    }
+}
+
+template <int P>
+int rr_p2l_p(fmm2d_plan* Pl)
+{
+    if (Pl->rr_np2l == 0) return 0;
+    const int L = Pl->L;
+    k_rr_p2l<P><<<grid_for(Pl->rr_np2l * 32, 128), 128, 0, Pl->stream>>>(
+        Pl->rr_p2l_leaves, Pl->rr_np2l, Pl->rr_p2l.off, Pl->rr_p2l.idx, Pl->boff + Pl->obase[L], Pl->src,
+        Pl->cx + Pl->base[L], Pl->cy + Pl->base[L], Pl->local + Pl->base[L] * (P + 1));
+    fmm2d::note_launch();
+    FMM2D_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+template <int P>
+int rr_m2p_p(fmm2d_plan* Pl)
+{
+    if (Pl->rr_nm2p == 0) return 0;
+    const int L = Pl->L;
+    k_rr_m2p<P><<<(unsigned)Pl->rr_nm2p, 128, 0, Pl->stream>>>(
+        Pl->rr_m2p_leaves, Pl->rr_m2p.off, Pl->rr_m2p.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
+        Pl->cy + Pl->base[L], Pl->mpole + Pl->base[L] * (P + 1), Pl->rr_acc);
+    fmm2d::note_launch();
+    FMM2D_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
 // P2M of the own leaves, then M2M for parent levels L-1 .. lstop (own parents; the
 // replicated levels above the partition level are done by upward_top_p)
 template <int P>
@@ -387,6 +501,18 @@ int run_upward(fmm2d_plan* P)
 int run_upward_top(fmm2d_plan* P)
 {
     switch (P->p) { FMM2D_P_CASES(upward_top_p) default: return FMM2D_EINVAL; }
+}
+
+int run_rr_p2l(fmm2d_plan* P)
+{
+    if (!(P->flags & FMM2D_RR_EXCHANGE)) return 0;
+    switch (P->p) { FMM2D_P_CASES(rr_p2l_p) default: return FMM2D_EINVAL; }
+}
+
+int run_rr_m2p(fmm2d_plan* P)
+{
+    if (!(P->flags & FMM2D_RR_EXCHANGE)) return 0;
+    switch (P->p) { FMM2D_P_CASES(rr_m2p_p) default: return FMM2D_EINVAL; }
 }
 
 int run_m2l(fmm2d_plan* P)

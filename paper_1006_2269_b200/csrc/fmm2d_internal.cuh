@@ -68,6 +68,13 @@ struct fmm2d_plan {
     // connectivity
     std::vector<fmm2d::Csr> strong, weak;   // per level
     uint32_t* m2l_order = nullptr;      // M2L targets per level (levels 1..L concatenated), by list length
+    // leaf-level direct pairs: the strong lists, or with FMM2D_RR_EXCHANGE the strong lists less
+    // the conversions: P2L into the smaller leaf, M2P of the smaller leaf
+    fmm2d::Csr near, rr_p2l, rr_m2p;
+    uint32_t* rr_p2l_leaves = nullptr;  // leaves with a non-empty P2L / M2P list
+    uint32_t* rr_m2p_leaves = nullptr;
+    int64_t rr_np2l = 0, rr_nm2p = 0;
+    double4* rr_acc = nullptr;          // [n] M2P sums (leaf order; valid on leaves with M2P work)
     // expansions
     double2* mpole = nullptr;           // [nbox_total][p+1]
     double2* local = nullptr;           // [nbox_total][p+1]
@@ -106,6 +113,8 @@ int prepare_near(fmm2d_plan* P);
 int prepare_near_sym(fmm2d_plan* P);
 int gather_strengths(fmm2d_plan* P, const double2* m);
 int run_upward_top(fmm2d_plan* P);
+int run_rr_p2l(fmm2d_plan* P);
+int run_rr_m2p(fmm2d_plan* P);
 // sharding (shard.cu)
 int64_t box_start_host(int64_t n, int l, int64_t b);
 int partition_level(int nranks);

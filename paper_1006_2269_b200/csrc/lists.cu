@@ -93,6 +93,71 @@ __global__ void k_m2l_keys(int64_t b0, int64_t b1, const int64_t* __restrict__ w
     box[i] = (uint32_t)b;
 }
 
+// r/R exchange (DESIGN R23): Criterion 1 with the roles of r and R exchanged,
+// r + theta R <= theta d for r < R strictly, evaluated in the same operation order.
+__device__ __forceinline__ bool rr_exchange(double cbx, double cby, double rb, double ccx, double ccy, double rc,
+                                            double theta)
+{
+    double dx = __dsub_rn(cbx, ccx);
+    double dy = __dsub_rn(cby, ccy);
+    double d = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+    double R = fmax(rb, rc);
+    double r = fmin(rb, rc);
+    return (r < R) && (d > 0.0) && (__dadd_rn(r, __dmul_rn(theta, R)) <= __dmul_rn(theta, d));
+}
+
+// Split of the leaf strong lists (one warp per leaf, ballot compaction keeps the order):
+// class 0 near (direct), 1 P2L into this smaller leaf, 2 M2P of a smaller leaf here.
+template <bool FILL>
+__global__ void k_rr_lists(int64_t t0, int64_t t1, const double* __restrict__ cx, const double* __restrict__ cy,
+                           const double* __restrict__ r, double theta, const int64_t* __restrict__ soff,
+                           const uint32_t* __restrict__ sidx, int64_t* __restrict__ cnt,   // [3][nl + 1]
+                           const int64_t* __restrict__ o0, const int64_t* __restrict__ o1,
+                           const int64_t* __restrict__ o2, uint32_t* __restrict__ i0, uint32_t* __restrict__ i1,
+                           uint32_t* __restrict__ i2, int64_t nl)
+{
+    const int64_t t = t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= t1) return;
+    const double tx = cx[t], ty = cy[t], tr = r[t];
+    const unsigned lt = (1u << lane) - 1u;
+    int64_t n0 = 0, n1 = 0, n2 = 0;
+    for (int64_t q0 = soff[t]; q0 < soff[t + 1]; q0 += 32) {
+        const int64_t q = q0 + lane;
+        const bool valid = q < soff[t + 1];
+        uint32_t s = 0;
+        int cls = 0;
+        if (valid) {
+            s = sidx[q];
+            if (s != (uint32_t)t && rr_exchange(tx, ty, tr, cx[s], cy[s], r[s], theta)) cls = (tr < r[s]) ? 1 : 2;
+        }
+        const unsigned m0 = __ballot_sync(0xffffffffu, valid && cls == 0);
+        const unsigned m1 = __ballot_sync(0xffffffffu, valid && cls == 1);
+        const unsigned m2 = __ballot_sync(0xffffffffu, valid && cls == 2);
+        if (FILL && valid) {
+            if (cls == 0) i0[o0[t] + n0 + __popc(m0 & lt)] = s;
+            else if (cls == 1) i1[o1[t] + n1 + __popc(m1 & lt)] = s;
+            else i2[o2[t] + n2 + __popc(m2 & lt)] = s;
+        }
+        n0 += __popc(m0);
+        n1 += __popc(m1);
+        n2 += __popc(m2);
+    }
+    if (!FILL && lane == 0) {
+        cnt[t] = n0;
+        cnt[(nl + 1) + t] = n1;
+        cnt[2 * (nl + 1) + t] = n2;
+    }
+}
+
+// leaves with a non-empty list (compacted ids)
+__global__ void k_nonempty(int64_t t0, int64_t t1, const int64_t* __restrict__ off, uint32_t* __restrict__ out,
+                           unsigned int* __restrict__ n)
+{
+    const int64_t t = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < t1 && off[t + 1] > off[t]) out[atomicAdd(n, 1u)] = (uint32_t)t;
+}
+
 // ordered P2P pairs (j != i) of one evaluation: sum_t n_t * sum_{s in S(t)} n_s - N
 __global__ void k_pair_count(int64_t t0, int64_t t1, const uint32_t* __restrict__ off,
                              const int64_t* __restrict__ soff, const uint32_t* __restrict__ sidx,
@@ -117,6 +182,70 @@ inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / b
 
 }  // namespace
 
+// r/R exchange (DESIGN R23): split the leaf strong lists into near / P2L / M2P CSR
+// lists and collect the leaves that have P2L or M2P work.
+static int build_rr_lists(fmm2d_plan* P)
+{
+    cudaStream_t st = P->stream;
+    const int L = P->L;
+    const int64_t nl = nboxes(L), t0 = P->box_lo(L), t1 = P->box_hi(L);
+    const double* cx = P->cx + P->base[L];
+    const double* cy = P->cy + P->base[L];
+    const double* r = P->r + P->base[L];
+    const Csr& S = P->strong[L];
+    int64_t* cnt = nullptr;
+    void* scratch = nullptr;
+    size_t sb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, sb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(nl + 1), st);
+    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt, sizeof(int64_t) * 3 * (nl + 1), st));
+    FMM2D_CUDA_TRY(cudaMallocAsync(&scratch, sb, st));
+    auto body = [&]() -> int {
+        FMM2D_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * 3 * (nl + 1), st));
+        const unsigned grid = grid_for((t1 - t0) * 32, 256);
+        k_rr_lists<false><<<grid, 256, 0, st>>>(t0, t1, cx, cy, r, P->theta, S.off, S.idx, cnt, nullptr, nullptr,
+                                                nullptr, nullptr, nullptr, nullptr, nl);
+        note_launch();
+        Csr* C[3] = {&P->near, &P->rr_p2l, &P->rr_m2p};
+        int64_t tot[3];
+        for (int c = 0; c < 3; ++c) {
+            *C[c] = Csr();
+            FMM2D_TRY(dev_alloc(P, (void**)&C[c]->off, sizeof(int64_t) * (nl + 1)));
+            size_t s2 = sb;
+            FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, s2, cnt + c * (nl + 1), C[c]->off, (int)(nl + 1), st));
+            FMM2D_CUDA_TRY(cudaMemcpyAsync(&tot[c], C[c]->off + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        }
+        FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+        for (int c = 0; c < 3; ++c) {
+            C[c]->total = tot[c];
+            FMM2D_TRY(dev_alloc(P, (void**)&C[c]->idx, sizeof(uint32_t) * std::max<int64_t>(tot[c], 1)));
+        }
+        k_rr_lists<true><<<grid, 256, 0, st>>>(t0, t1, cx, cy, r, P->theta, S.off, S.idx, nullptr, P->near.off,
+                                               P->rr_p2l.off, P->rr_m2p.off, P->near.idx, P->rr_p2l.idx,
+                                               P->rr_m2p.idx, nl);
+        note_launch();
+        // leaves with P2L / M2P work (the order is irrelevant: each leaf is independent)
+        unsigned int* d_n = (unsigned int*)cnt;
+        FMM2D_CUDA_TRY(cudaMemsetAsync(d_n, 0, 2 * sizeof(unsigned int), st));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->rr_p2l_leaves, sizeof(uint32_t) * std::max<int64_t>(t1 - t0, 1)));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->rr_m2p_leaves, sizeof(uint32_t) * std::max<int64_t>(t1 - t0, 1)));
+        k_nonempty<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, P->rr_p2l.off, P->rr_p2l_leaves, d_n);
+        note_launch();
+        k_nonempty<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, P->rr_m2p.off, P->rr_m2p_leaves, d_n + 1);
+        note_launch();
+        unsigned int h_n[2];
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(h_n, d_n, sizeof(h_n), cudaMemcpyDeviceToHost, st));
+        FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+        P->rr_np2l = h_n[0];
+        P->rr_nm2p = h_n[1];
+        FMM2D_TRY(dev_alloc(P, (void**)&P->rr_acc, sizeof(double4) * P->n));
+        return 0;
+    };
+    const int rc = body();
+    cudaFreeAsync(cnt, st);
+    cudaFreeAsync(scratch, st);
+    return rc;
+}
+
 int build_lists(fmm2d_plan* P)
 {
     const int L = P->L;
@@ -140,6 +269,7 @@ int build_lists(fmm2d_plan* P)
     if (L == 0) {
         P->stats.strong_leaf_pairs = 1;
         P->stats.p2p_pairs = P->n * (P->n - 1);
+        P->near = P->strong[0];
         return 0;
     }
     int64_t nbmax = nboxes(L);
@@ -224,11 +354,13 @@ int build_lists(fmm2d_plan* P)
             cudaFreeAsync(sc, st);
         }
         P->stats.strong_leaf_pairs = P->strong[L].total;
+        const int64_t t0 = P->box_lo(L), t1 = P->box_hi(L);
+        P->near = P->strong[L];                     // the direct pairs (all strong pairs unless r/R exchange)
+        if (P->flags & FMM2D_RR_EXCHANGE) FMM2D_TRY(build_rr_lists(P));
         unsigned long long* d_tot = (unsigned long long*)cnt_w;   // reuse scratch
         FMM2D_CUDA_TRY(cudaMemsetAsync(d_tot, 0, sizeof(unsigned long long), st));
-        const int64_t t0 = P->box_lo(L), t1 = P->box_hi(L);
-        k_pair_count<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, P->boff + P->obase[L], P->strong[L].off,
-                                                             P->strong[L].idx, d_tot); fmm2d::note_launch();
+        k_pair_count<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, P->boff + P->obase[L], P->near.off,
+                                                             P->near.idx, d_tot); fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
         unsigned long long h_tot = 0;
         FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_tot, d_tot, sizeof(h_tot), cudaMemcpyDeviceToHost, st));

@@ -139,7 +139,8 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                                                  const double4* __restrict__ src, const double* __restrict__ cx,
                                                  const double* __restrict__ cy, const double2* __restrict__ loc,
                                                  const uint32_t* __restrict__ perm, const fm::Tables* __restrict__ gtab,
-                                                 double2* __restrict__ phi, double2* __restrict__ dphi)
+                                                 double2* __restrict__ phi, double2* __restrict__ dphi,
+                                                 const int64_t* __restrict__ m2p_off, const double4* __restrict__ m2p_acc)
 {
     __shared__ double4 S[NEAR_CHUNK];
     __shared__ fm::Tables T;
@@ -246,6 +247,13 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                 const double4 me = src[ts + i0 + kk];
                 l2p(loc + t * (p + 1), p, me.x - cx[t], me.y - cy[t], f.x, f.y, f.z, f.w);
             }
+            if (m2p_off && m2p_off[t + 1] > m2p_off[t]) {      // r/R exchange: M2P sums
+                const double4 g = m2p_acc[ts + i0 + kk];
+                f.x += g.x;
+                f.y += g.y;
+                f.z += g.z;
+                f.w += g.w;
+            }
             const uint32_t o = perm[ts + i0 + kk];
             if (phi) phi[o] = make_double2(acc.x + f.x, acc.y + f.y);
             if (dphi) dphi[o] = make_double2(acc.z + f.z, acc.w + f.w);
@@ -263,7 +271,8 @@ __global__ void __launch_bounds__(NEAR_T) k_near_wide(int p, int64_t t0, const u
                                                       const double* __restrict__ cy, const double2* __restrict__ loc,
                                                       const uint32_t* __restrict__ perm,
                                                       const fm::Tables* __restrict__ gtab, double2* __restrict__ phi,
-                                                      double2* __restrict__ dphi)
+                                                      double2* __restrict__ dphi, const int64_t* __restrict__ m2p_off,
+                                                      const double4* __restrict__ m2p_acc)
 {
     __shared__ fm::Tables T;
     load_tables(T, gtab);
@@ -284,6 +293,13 @@ __global__ void __launch_bounds__(NEAR_T) k_near_wide(int p, int64_t t0, const u
         }
         double fr, fi, gr, gi;
         l2p(loc + t * (p + 1), p, me.x - cx[t], me.y - cy[t], fr, fi, gr, gi);
+        if (m2p_off && m2p_off[t + 1] > m2p_off[t]) {          // r/R exchange: M2P sums
+            const double4 g = m2p_acc[i];
+            fr += g.x;
+            fi += g.y;
+            gr += g.z;
+            gi += g.w;
+        }
         const uint32_t o = perm[i];
         const double2 f = acc.phi(), d = acc.dphi();
         if (phi) phi[o] = make_double2(f.x + fr, f.y + fi);
@@ -608,7 +624,9 @@ int prepare_near_sym(fmm2d_plan* P)
 {
     P->sym = false;
     const int L = P->L, ml = P->stats.max_leaf;
-    if (L < 1 || ml > SYM_MAXLEAF || ml < 1 || !(P->flags & FMM2D_SYMMETRIC_P2P) || P->nranks > 1) return 0;
+    if (L < 1 || ml > SYM_MAXLEAF || ml < 1 || !(P->flags & FMM2D_SYMMETRIC_P2P) || P->nranks > 1 ||
+        (P->flags & FMM2D_RR_EXCHANGE))
+        return 0;
     cudaStream_t st = P->stream;
     const int64_t nl = nboxes(L);
     const Csr& S = P->strong[L];
@@ -660,6 +678,7 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi)
     const uint32_t* off = P->boff + P->obase[L];
     const bool real = (P->flags & FMM2D_REAL_STRENGTHS) != 0;
     const fm::Tables* tab = (const fm::Tables*)P->tables;
+    const int64_t* m2p_off = (P->rr_nm2p > 0) ? P->rr_m2p.off : nullptr;     // r/R exchange
     if (P->sym) {
         SymArgs A;
         A.off = off;
@@ -698,19 +717,22 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi)
         int G = NEAR_T / std::min(pairs, NEAR_T);
         if (G < 1) G = 1;
         if (real)
-            k_near<true><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(G, P->p, t0, off, P->strong[L].off, P->strong[L].idx,
-                                                                P->src, cx, cy, loc, P->perm, tab, phi, dphi);
+            k_near<true><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(G, P->p, t0, off, P->near.off, P->near.idx, P->src,
+                                                                cx, cy, loc, P->perm, tab, phi, dphi, m2p_off,
+                                                                P->rr_acc);
         else
-            k_near<false><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(G, P->p, t0, off, P->strong[L].off, P->strong[L].idx,
-                                                                 P->src, cx, cy, loc, P->perm, tab, phi, dphi);
+            k_near<false><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(G, P->p, t0, off, P->near.off, P->near.idx, P->src,
+                                                                 cx, cy, loc, P->perm, tab, phi, dphi, m2p_off,
+                                                                 P->rr_acc);
     } else {
         if (real)
-            k_near_wide<true><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, t0, off, P->strong[L].off, P->strong[L].idx,
-                                                                     P->src, cx, cy, loc, P->perm, tab, phi, dphi);
+            k_near_wide<true><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, t0, off, P->near.off, P->near.idx,
+                                                                     P->src, cx, cy, loc, P->perm, tab, phi, dphi,
+                                                                     m2p_off, P->rr_acc);
         else
-            k_near_wide<false><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, t0, off, P->strong[L].off,
-                                                                      P->strong[L].idx, P->src, cx, cy, loc,
-                                                                      P->perm, tab, phi, dphi);
+            k_near_wide<false><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, t0, off, P->near.off, P->near.idx,
+                                                                      P->src, cx, cy, loc, P->perm, tab, phi, dphi,
+                                                                      m2p_off, P->rr_acc);
     }
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());

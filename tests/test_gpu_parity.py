@@ -268,3 +268,30 @@ def test_symmetric_near_field_equals_one_sided(orc, cfg, n):
     assert _nerr(out[False][0], out[True][0]) <= 1e-13 and _nerr(out[False][1], out[True][1]) <= 1e-13
     phi_o, dphi_o = orc.plan(z, 0.5, L).eval(m, 17)
     assert _nerr(out[False][0], phi_o) <= TOL and _nerr(out[False][1], dphi_o) <= TOL
+
+
+RR_CASES = [("C3-100k", "C3", 100_000), ("C4-100k", "C4", 100_000), ("C3-30k-p8", "C3", 30_000)]
+
+
+@pytest.mark.parametrize("name,cfg,n", RR_CASES, ids=[c[0] for c in RR_CASES])
+def test_rr_exchange_lists_and_eval_match_oracle(orc, name, cfg, n):
+    """FMM2D_RR_EXCHANGE (DESIGN R23): the near / P2L / M2P split of the leaf
+    strong lists bit-exact, Phi and Phi' within 1e-12 of the oracle pass with the same
+    conversions, and the conversions actually remove direct pairs."""
+    from paper_1006_2269_b200 import Fmm2d
+    z, m = W.make_config(cfg, n=n)
+    L = orc.nlevels(len(z), 35)
+    p = 8 if name.endswith("p8") else 17
+    op = orc.plan(z, 0.5, L, rr_exchange=True)
+    gp = Fmm2d(torch.from_numpy(z).cuda(), theta=0.5, p=p, nlevels=L, rr_exchange=True)
+    for kind in ("strong", "near", "p2l", "m2p"):
+        go, gi = gp.list(L, kind)
+        oo, oi = op.list(L, kind)
+        np.testing.assert_array_equal(go, oo, err_msg=kind)
+        np.testing.assert_array_equal(gi, oi, err_msg=kind)
+    assert op.list(L, "p2l")[1].size > 0
+    phi_o, dphi_o = op.eval(m, p)
+    phi_g, dphi_g = _gpu_eval(gp, m)
+    assert _nerr(phi_g, phi_o) <= TOL and _nerr(dphi_g, dphi_o) <= TOL
+    off = Fmm2d(torch.from_numpy(z).cuda(), theta=0.5, p=p, nlevels=L)
+    assert gp.stats()["p2p_pairs"] < off.stats()["p2p_pairs"]
