@@ -151,6 +151,18 @@ class ClockSampler:
                 "source": self.source}
 
 
+def k_near_traffic(cfg, default_cfg):
+    """DRAM bytes per k_near launch from the committed ncu --set full capture
+    (profiles/traffic.json) -- only for the configuration it was captured on."""
+    if not default_cfg:
+        return None, None
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["k_near"]
+        return float(d["dram_bytes_per_launch"]), d["source"]
+    except Exception:
+        return None, None
+
+
 def cpu_baseline(cfg, seconds_hint=True):
     """Oracle (plain C++ + OpenMP) on a bounded sample of the same workload."""
     import oracle
@@ -208,6 +220,7 @@ def main():
     ap.add_argument("--impl", default="fmm2d", choices=["fmm2d", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--rr-exchange", action="store_true", help="FMM2D_RR_EXCHANGE (P:370-377; one GPU)")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.config]
     if args.n:
@@ -239,6 +252,8 @@ def main():
     z_np, m_np = W.make(cfg.dist, cfg.n, cfg.strengths, seed=W.SEED_BASE + 4)
     nccl_id = shared_nccl_id() if world > 1 else None
     shard_kw = dict(nranks=world, rank=rank, nccl_id=nccl_id) if world > 1 else {}
+    if args.rr_exchange:
+        shard_kw["rr_exchange"] = True
     z = torch.from_numpy(z_np).to(dev)
     m = torch.from_numpy(m_np).to(dev)
     real = cfg.strengths == "real"
@@ -296,8 +311,13 @@ def main():
     pairs = st.get("p2p_pairs", 0.0)
     near_ms = phase["near_ms"]
     achieved = pairs * P2P_FLOPS_PER_PAIR / (near_ms / 1e3) / 1e12
+    traffic, traffic_src = k_near_traffic(cfg, args.config == "C5" and not args.n and world == 1
+                                          and not args.rr_exchange)
+    nleaf = 4 ** L if L else 1
+    algo_bytes = 32.0 * cfg.n * 2 + 4.0 * cfg.n + 288.0 * nleaf        # rows in, Phi/Phi' out, perm, locals
     roof = {"bound": "alu", "kernel": "k_near (P2P+L2P)", "achieved": achieved, "peak": peak,
-            "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+            "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+            "algorithmic_bytes_per_launch": algo_bytes,
             "flops_per_launch": pairs * P2P_FLOPS_PER_PAIR, "pairs_per_launch": pairs,
             "peak_source": peak_src,
             "flop_convention": f"{P2P_FLOPS_PER_PAIR:.0f} FP64 flop per ordered P2P pair (SURVEY 8(d))"}

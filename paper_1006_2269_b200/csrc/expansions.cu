@@ -146,19 +146,15 @@ struct M2LArgs {
     double2* local;
 };
 
-// One thread computes output coefficients l in [L0, L1) of one target box.
+// Output coefficients l in [L0, L1) of target box g, summed over the weak pairs
+// q = qa, qa + qs, ... < qb into acc.
 template <int P, int L0, int L1>
-__device__ __forceinline__ void m2l_target(const M2LArgs& A, int64_t g, int lev)
+__device__ __forceinline__ void m2l_accum(const M2LArgs& A, int64_t g, int lev, int64_t qa, int64_t qb, int64_t qs,
+                                          double2 (&acc)[L1 - L0])
 {
-    int64_t b = g - A.base[lev];
-    const int64_t* off = A.woff[lev];
     const uint32_t* idx = A.widx[lev];
     const double ctx = A.cx[g], cty = A.cy[g];
-    double2 acc[L1 - L0];
-#pragma unroll
-    for (int l = 0; l < L1 - L0; ++l) acc[l] = make_double2(0.0, 0.0);
-    const int64_t q0 = off[b], q1 = off[b + 1];
-    for (int64_t q = q0; q < q1; ++q) {
+    for (int64_t q = qa; q < qb; q += qs) {
         const int64_t s = A.base[lev] + idx[q];
         const double csx = A.cx[s], csy = A.cy[s];
         const double2* M = A.mpole + s * (P + 1);
@@ -202,9 +198,44 @@ __device__ __forceinline__ void m2l_target(const M2LArgs& A, int64_t g, int lev)
             acc[l - L0] = cadd(acc[l - L0], v);
         }
     }
+}
+
+// One thread computes output coefficients l in [L0, L1) of one target box.
+template <int P, int L0, int L1>
+__device__ __forceinline__ void m2l_target(const M2LArgs& A, int64_t g, int lev)
+{
+    const int64_t b = g - A.base[lev];
+    double2 acc[L1 - L0];
+#pragma unroll
+    for (int l = 0; l < L1 - L0; ++l) acc[l] = make_double2(0.0, 0.0);
+    m2l_accum<P, L0, L1>(A, g, lev, A.woff[lev][b], A.woff[lev][b + 1], 1, acc);
     double2* out = A.local + g * (P + 1);
 #pragma unroll
     for (int l = L0; l < L1; ++l) out[l] = acc[l - L0];
+}
+
+// Long weak lists (non-uniform inputs): one warp per target, lanes over the pairs, a
+// fixed-order shuffle reduction -- so one box's list no longer serialises on one thread.
+template <int P, int L0, int L1>
+__device__ __forceinline__ void m2l_target_warp(const M2LArgs& A, int64_t g, int lev, int lane)
+{
+    const int64_t b = g - A.base[lev];
+    double2 acc[L1 - L0];
+#pragma unroll
+    for (int l = 0; l < L1 - L0; ++l) acc[l] = make_double2(0.0, 0.0);
+    m2l_accum<P, L0, L1>(A, g, lev, A.woff[lev][b] + lane, A.woff[lev][b + 1], 32, acc);
+#pragma unroll
+    for (int l = 0; l < L1 - L0; ++l) {
+        for (int o = 16; o; o >>= 1) {
+            acc[l].x += __shfl_xor_sync(0xffffffffu, acc[l].x, o);
+            acc[l].y += __shfl_xor_sync(0xffffffffu, acc[l].y, o);
+        }
+    }
+    if (lane == 0) {
+        double2* out = A.local + g * (P + 1);
+#pragma unroll
+        for (int l = L0; l < L1; ++l) out[l] = acc[l - L0];
+    }
 }
 
 #ifndef FMM2D_M2L_MINB
@@ -227,6 +258,10 @@ __global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l(M2LArgs A)
     int lev = 1;
     while (lev < A.L && w >= A.pre[lev + 1]) ++lev;
     const int64_t g = A.base[lev] + A.order[w];
+    {   // long lists are done by k_m2l_long
+        const int64_t b = g - A.base[lev];
+        if (A.woff[lev][b + 1] - A.woff[lev][b] > FMM2D_M2L_LONG) return;
+    }
     // part q computes coefficients [q H, min((q+1) H, P+1)), H = ceil((P+1)/NS)
     constexpr int H = (P + NS) / NS;
     constexpr int E1 = (2 * H < P + 1) ? 2 * H : P + 1;
@@ -241,6 +276,34 @@ __global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l(M2LArgs A)
         if (part == 0)      m2l_target<P, 0, H>(A, g, lev);
         else if (part == 1) m2l_target<P, H, E1>(A, g, lev);
         else                m2l_target<P, E1, E2>(A, g, lev);
+    }
+}
+
+// one warp (per coefficient part) per long-list target; long[] holds global box ids
+template <int P, int NS>
+__global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l_long(M2LArgs A, const uint32_t* __restrict__ longs,
+                                                                   int64_t nlong)
+{
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int part = (int)(warp % NS);
+    const int64_t w = warp / NS;
+    if (w >= nlong) return;
+    const int64_t g = longs[w];
+    int lev = 1;
+    while (lev < A.L && g >= A.base[lev + 1]) ++lev;
+    constexpr int H = (P + NS) / NS;
+    constexpr int E1 = (2 * H < P + 1) ? 2 * H : P + 1;
+    constexpr int E2 = (3 * H < P + 1) ? 3 * H : P + 1;
+    if constexpr (NS == 1) {
+        m2l_target_warp<P, 0, P + 1>(A, g, lev, lane);
+    } else if constexpr (NS == 2) {
+        if (part == 0) m2l_target_warp<P, 0, H>(A, g, lev, lane);
+        else           m2l_target_warp<P, H, P + 1>(A, g, lev, lane);
+    } else {
+        if (part == 0)      m2l_target_warp<P, 0, H>(A, g, lev, lane);
+        else if (part == 1) m2l_target_warp<P, H, E1>(A, g, lev, lane);
+        else                m2l_target_warp<P, E1, E2>(A, g, lev, lane);
     }
 }
 
@@ -461,6 +524,12 @@ int m2l_p(fmm2d_plan* Pl)
     int64_t nthreads = ((work + 31) / 32) * 32 * NS;
     k_m2l<P, NS><<<grid_for(nthreads, M2L_T), M2L_T, 0, st>>>(A); fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
+    if (Pl->m2l_nlong > 0) {
+        k_m2l_long<P, NS><<<grid_for(Pl->m2l_nlong * NS * 32, M2L_T), M2L_T, 0, st>>>(A, Pl->m2l_long,
+                                                                                  Pl->m2l_nlong);
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    }
     return 0;
 }
 

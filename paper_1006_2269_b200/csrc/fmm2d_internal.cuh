@@ -15,6 +15,12 @@
 #include "../../include/fmm2d.h"
 
 #define FMM2D_MAXL 15
+#ifndef FMM2D_NEAR_SPLIT
+#define FMM2D_NEAR_SPLIT 4096       // near lists with more source rows: split over several CTAs
+#endif
+#ifndef FMM2D_M2L_LONG
+#define FMM2D_M2L_LONG 96           // weak lists longer than this: one warp per target (k_m2l_long)
+#endif
 
 namespace fmm2d {
 
@@ -25,6 +31,12 @@ struct Csr {
     int64_t* off = nullptr;   // device, 4^l + 1
     uint32_t* idx = nullptr;  // device, off[4^l] entries (level-local box ids)
     int64_t total = 0;
+};
+
+// a part of a long leaf strong list, evaluated by its own k_near CTA (partial sums)
+struct NearSeg {
+    int64_t qa, qb;      // list entries [qa, qb)
+    uint32_t t, pad;     // target leaf
 };
 
 struct Stats {
@@ -68,6 +80,8 @@ struct fmm2d_plan {
     // connectivity
     std::vector<fmm2d::Csr> strong, weak;   // per level
     uint32_t* m2l_order = nullptr;      // M2L targets per level (levels 1..L concatenated), by list length
+    uint32_t* m2l_long = nullptr;       // global ids of targets with more than FMM2D_M2L_LONG weak pairs
+    int64_t m2l_nlong = 0;
     // leaf-level direct pairs: the strong lists, or with FMM2D_RR_EXCHANGE the strong lists less
     // the conversions: P2L into the smaller leaf, M2P of the smaller leaf
     fmm2d::Csr near, rr_p2l, rr_m2p;
@@ -75,6 +89,12 @@ struct fmm2d_plan {
     uint32_t* rr_m2p_leaves = nullptr;
     int64_t rr_np2l = 0, rr_nm2p = 0;
     double4* rr_acc = nullptr;          // [n] M2P sums (leaf order; valid on leaves with M2P work)
+    // long near lists split into segments of at most FMM2D_NEAR_SPLIT source rows
+    int64_t* near_seg_off = nullptr;    // [leaves + 1] segments of each leaf (empty: not split)
+    fmm2d::NearSeg* near_segs = nullptr;
+    uint32_t* near_split = nullptr;     // split leaves
+    double4* near_part = nullptr;       // [segments][max_leaf] partial sums
+    int64_t near_nseg = 0, near_nsplit = 0;
     // expansions
     double2* mpole = nullptr;           // [nbox_total][p+1]
     double2* local = nullptr;           // [nbox_total][p+1]

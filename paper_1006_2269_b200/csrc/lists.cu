@@ -150,12 +150,70 @@ __global__ void k_rr_lists(int64_t t0, int64_t t1, const double* __restrict__ cx
     }
 }
 
+// targets of one level with a long weak list (global ids; order irrelevant)
+__global__ void k_long_lists(int64_t b0, int64_t b1, int64_t gbase, const int64_t* __restrict__ woff,
+                             uint32_t* __restrict__ out, unsigned int* __restrict__ n)
+{
+    const int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < b1 && woff[b + 1] - woff[b] > FMM2D_M2L_LONG) out[atomicAdd(n, 1u)] = (uint32_t)(gbase + b);
+}
+
 // leaves with a non-empty list (compacted ids)
 __global__ void k_nonempty(int64_t t0, int64_t t1, const int64_t* __restrict__ off, uint32_t* __restrict__ out,
                            unsigned int* __restrict__ n)
 {
     const int64_t t = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < t1 && off[t + 1] > off[t]) out[atomicAdd(n, 1u)] = (uint32_t)t;
+}
+
+// Long near lists (non-uniform inputs: a leaf can be strongly coupled to thousands of
+// leaves): cut at leaf boundaries into segments of about FMM2D_NEAR_SPLIT source rows,
+// each evaluated by its own k_near CTA.  Entry q lies in bucket floor(rows before q /
+// FMM2D_NEAR_SPLIT); a segment starts at every entry whose bucket differs from the
+// previous entry's.  One warp per leaf (scans + ballots); lists of at most
+// FMM2D_NEAR_SPLIT rows are not split (count 0).  Pass 1 counts, pass 2 writes.
+template <bool FILL>
+__global__ void k_near_segs(int64_t t0, int64_t t1, const int64_t* __restrict__ noff, const uint32_t* __restrict__ nidx,
+                            const uint32_t* __restrict__ boff, int64_t* __restrict__ cnt,
+                            const int64_t* __restrict__ seg_off, NearSeg* __restrict__ segs)
+{
+    const int64_t t = t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= t1) return;
+    if (FILL && seg_off[t + 1] == seg_off[t]) return;
+    const int64_t q0 = noff[t], q1 = noff[t + 1];
+    const int64_t base = FILL ? seg_off[t] : 0;
+    int64_t run = 0, prev_bucket = -1, nstart = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t qc = q0; qc < q1; qc += 32) {
+        const int64_t q = qc + lane;
+        const bool valid = q < q1;
+        const int64_t sz = valid ? (int64_t)(boff[nidx[q] + 1] - boff[nidx[q]]) : 0;
+        int64_t incl = sz;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int64_t bucket = (run + incl - sz) / FMM2D_NEAR_SPLIT;
+        int64_t pb = __shfl_up_sync(0xffffffffu, bucket, 1);
+        if (lane == 0) pb = prev_bucket;
+        const bool start = valid && bucket != pb;
+        const unsigned sm = __ballot_sync(0xffffffffu, start);
+        if (FILL && start) {
+            const int64_t k = nstart + __popc(sm & lt);     // segment number
+            segs[base + k].qa = q;
+            segs[base + k].t = (uint32_t)t;
+            if (k > 0) segs[base + k - 1].qb = q;
+        }
+        nstart += __popc(sm);
+        const int last = (int)min((int64_t)31, q1 - 1 - qc);
+        prev_bucket = __shfl_sync(0xffffffffu, bucket, last);
+        run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+        if (FILL) segs[base + nstart - 1].qb = q1;
+        else cnt[t] = (run > FMM2D_NEAR_SPLIT) ? nstart : 0;
+    }
 }
 
 // ordered P2P pairs (j != i) of one evaluation: sum_t n_t * sum_{s in S(t)} n_s - N
@@ -238,6 +296,55 @@ static int build_rr_lists(fmm2d_plan* P)
         P->rr_np2l = h_n[0];
         P->rr_nm2p = h_n[1];
         FMM2D_TRY(dev_alloc(P, (void**)&P->rr_acc, sizeof(double4) * P->n));
+        return 0;
+    };
+    const int rc = body();
+    cudaFreeAsync(cnt, st);
+    cudaFreeAsync(scratch, st);
+    return rc;
+}
+
+static int build_near_segments(fmm2d_plan* P)
+{
+    cudaStream_t st = P->stream;
+    const int L = P->L;
+    const int64_t nl = nboxes(L), t0 = P->box_lo(L), t1 = P->box_hi(L);
+    const uint32_t* boff = P->boff + P->obase[L];
+    int64_t* cnt = nullptr;
+    void* scratch = nullptr;
+    size_t sb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, sb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(nl + 1), st);
+    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt, sizeof(int64_t) * (nl + 1), st));
+    FMM2D_CUDA_TRY(cudaMallocAsync(&scratch, sb, st));
+    auto body = [&]() -> int {
+        FMM2D_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (nl + 1), st));
+        k_near_segs<false><<<grid_for((t1 - t0) * 32, 256), 256, 0, st>>>(t0, t1, P->near.off, P->near.idx, boff,
+                                                                           cnt, nullptr, nullptr);
+        note_launch();
+        int64_t* soff = nullptr;
+        FMM2D_TRY(dev_alloc(P, (void**)&soff, sizeof(int64_t) * (nl + 1)));
+        size_t s2 = sb;
+        FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, s2, cnt, soff, (int)(nl + 1), st));
+        int64_t tot = 0;
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(&tot, soff + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+        P->near_nseg = tot;
+        if (tot == 0) return 0;                         // nothing split: k_near skips the lookups
+        P->near_seg_off = soff;
+        FMM2D_TRY(dev_alloc(P, (void**)&P->near_segs, sizeof(NearSeg) * tot));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->near_part, sizeof(double4) * tot * std::max(1, P->stats.max_leaf)));
+        k_near_segs<true><<<grid_for((t1 - t0) * 32, 256), 256, 0, st>>>(t0, t1, P->near.off, P->near.idx, boff,
+                                                                          nullptr, soff, P->near_segs);
+        note_launch();
+        FMM2D_TRY(dev_alloc(P, (void**)&P->near_split, sizeof(uint32_t) * std::max<int64_t>(t1 - t0, 1)));
+        unsigned int* d_n = (unsigned int*)cnt;
+        FMM2D_CUDA_TRY(cudaMemsetAsync(d_n, 0, sizeof(unsigned int), st));
+        k_nonempty<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, soff, P->near_split, d_n);
+        note_launch();
+        unsigned int h_n = 0;
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_n, d_n, sizeof(h_n), cudaMemcpyDeviceToHost, st));
+        FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+        P->near_nsplit = h_n;
         return 0;
     };
     const int rc = body();
@@ -334,7 +441,7 @@ int build_lists(fmm2d_plan* P)
                                             (uint32_t*)nullptr, (int)nbmax, 0, 32, st);
             FMM2D_CUDA_TRY(cudaMallocAsync((void**)&k0, sizeof(uint32_t) * nbmax, st));
             FMM2D_CUDA_TRY(cudaMallocAsync((void**)&k1, sizeof(uint32_t) * nbmax, st));
-            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&v0, sizeof(uint32_t) * nbmax, st));
+            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&v0, sizeof(uint32_t) * std::max<int64_t>(tot, nbmax), st));
             FMM2D_CUDA_TRY(cudaMallocAsync(&sc, std::max<size_t>(sb, 16), st));
             int64_t o = 0;
             for (int l = 1; l <= L; ++l) {
@@ -348,6 +455,21 @@ int build_lists(fmm2d_plan* P)
                                                                st));
                 o += nb;
             }
+            // targets with long weak lists (k_m2l_long)
+            unsigned int* d_n = (unsigned int*)k1;
+            FMM2D_CUDA_TRY(cudaMemsetAsync(d_n, 0, sizeof(unsigned int), st));
+            for (int l = 1; l <= L; ++l) {
+                const int64_t b0 = P->box_lo(l), b1 = P->box_hi(l);
+                k_long_lists<<<grid_for(b1 - b0, 256), 256, 0, st>>>(b0, b1, P->base[l], P->weak[l].off, v0, d_n);
+                fmm2d::note_launch();
+            }
+            unsigned int h_n = 0;
+            FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_n, d_n, sizeof(h_n), cudaMemcpyDeviceToHost, st));
+            FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+            P->m2l_nlong = h_n;
+            FMM2D_TRY(dev_alloc(P, (void**)&P->m2l_long, sizeof(uint32_t) * std::max<int64_t>(h_n, 1)));
+            if (h_n)
+                FMM2D_CUDA_TRY(cudaMemcpyAsync(P->m2l_long, v0, sizeof(uint32_t) * h_n, cudaMemcpyDeviceToDevice, st));
             cudaFreeAsync(k0, st);
             cudaFreeAsync(k1, st);
             cudaFreeAsync(v0, st);
@@ -357,6 +479,7 @@ int build_lists(fmm2d_plan* P)
         const int64_t t0 = P->box_lo(L), t1 = P->box_hi(L);
         P->near = P->strong[L];                     // the direct pairs (all strong pairs unless r/R exchange)
         if (P->flags & FMM2D_RR_EXCHANGE) FMM2D_TRY(build_rr_lists(P));
+        if (P->stats.max_leaf <= 256) FMM2D_TRY(build_near_segments(P));     // k_near's chunk size
         unsigned long long* d_tot = (unsigned long long*)cnt_w;   // reuse scratch
         FMM2D_CUDA_TRY(cudaMemsetAsync(d_tot, 0, sizeof(unsigned long long), st));
         k_pair_count<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, P->boff + P->obase[L], P->near.off,

@@ -133,8 +133,15 @@ __device__ __forceinline__ int first_in_class(int b, int g, int G)
     return b + (r < 0 ? r + G : r);
 }
 
+// Work items: blockIdx.x < nmain is target leaf t0 + blockIdx.x over its whole list
+// (skipped if the leaf is split: seg_off[t+1] > seg_off[t]); the items after it are the
+// segments of split leaves (long strong lists of non-uniform inputs), each over a part of
+// the list, writing partial sums to part[] (k_near_combine finishes those leaves).
 template <bool REAL>
-__global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, int64_t t0, const uint32_t* __restrict__ off,
+__global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, int64_t t0, int64_t nmain,
+                                                 const int64_t* __restrict__ seg_off, const NearSeg* __restrict__ segs,
+                                                 double4* __restrict__ part, int part_w,
+                                                 const uint32_t* __restrict__ off,
                                                  const int64_t* __restrict__ soff, const uint32_t* __restrict__ sidx,
                                                  const double4* __restrict__ src, const double* __restrict__ cx,
                                                  const double* __restrict__ cy, const double2* __restrict__ loc,
@@ -148,11 +155,22 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
     __shared__ int cstart[33];
     __shared__ int cinfo[2];                 // [0] leaves in chunk, [1] chunk row of leaf t (-1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int64_t t, q0, q1, segi = -1;
+    if ((int64_t)blockIdx.x < nmain) {
+        t = t0 + blockIdx.x;
+        if (seg_off && seg_off[t + 1] > seg_off[t]) return;      // split leaf: segments + combine
+        q0 = soff[t];
+        q1 = soff[t + 1];
+    } else {
+        segi = (int64_t)blockIdx.x - nmain;
+        const NearSeg sg = segs[segi];
+        t = sg.t;
+        q0 = sg.qa;
+        q1 = sg.qb;
+    }
     load_tables(T, gtab);                    // (the first chunk's barriers cover it)
-    const int64_t t = t0 + blockIdx.x;
     const uint32_t ts = off[t], te = off[t + 1];
     const int nt = (int)(te - ts);
-    const int64_t q0 = soff[t], q1 = soff[t + 1];
     const int tile = NEAR_T / G;                 // target pairs per pass
     for (int i0 = 0; i0 < nt; i0 += 2 * tile) {
         const int tp = tid % tile;
@@ -242,6 +260,10 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                 acc.z += v.z;
                 acc.w += v.w;
             }
+            if (segi >= 0) {                      // a segment of a split leaf: partial sums only
+                part[segi * part_w + i0 + kk] = acc;
+                continue;
+            }
             double4 f;                            // L2P (Horner) of the target
             {
                 const double4 me = src[ts + i0 + kk];
@@ -259,6 +281,43 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
             if (dphi) dphi[o] = make_double2(acc.z + f.z, acc.w + f.w);
         }
         __syncthreads();
+    }
+}
+
+// Split leaves: the partial sums of their segments (in segment order) + L2P + M2P.
+__global__ void __launch_bounds__(NEAR_T) k_near_combine(const uint32_t* __restrict__ leaves,
+                                                         const int64_t* __restrict__ seg_off, const double4* __restrict__ part,
+                                                         int part_w, int p, const uint32_t* __restrict__ off,
+                                                         const double4* __restrict__ src, const double* __restrict__ cx,
+                                                         const double* __restrict__ cy, const double2* __restrict__ loc,
+                                                         const uint32_t* __restrict__ perm, double2* __restrict__ phi,
+                                                         double2* __restrict__ dphi, const int64_t* __restrict__ m2p_off,
+                                                         const double4* __restrict__ m2p_acc)
+{
+    const uint32_t t = leaves[blockIdx.x];
+    const uint32_t ts = off[t], te = off[t + 1];
+    for (uint32_t i = ts + threadIdx.x; i < te; i += NEAR_T) {
+        double4 acc = part[seg_off[t] * part_w + (i - ts)];
+        for (int64_t sg = seg_off[t] + 1; sg < seg_off[t + 1]; ++sg) {
+            const double4 v = part[sg * part_w + (i - ts)];
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+        }
+        const double4 me = src[i];
+        double4 f;
+        l2p(loc + (int64_t)t * (p + 1), p, me.x - cx[t], me.y - cy[t], f.x, f.y, f.z, f.w);
+        if (m2p_off && m2p_off[t + 1] > m2p_off[t]) {
+            const double4 g = m2p_acc[i];
+            f.x += g.x;
+            f.y += g.y;
+            f.z += g.z;
+            f.w += g.w;
+        }
+        const uint32_t o = perm[i];
+        if (phi) phi[o] = make_double2(acc.x + f.x, acc.y + f.y);
+        if (dphi) dphi[o] = make_double2(acc.z + f.z, acc.w + f.w);
     }
 }
 
@@ -716,14 +775,24 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi)
         const int pairs = (std::max(1, P->stats.max_leaf) + 1) / 2;
         int G = NEAR_T / std::min(pairs, NEAR_T);
         if (G < 1) G = 1;
+        const unsigned grid = (unsigned)(nl + P->near_nseg);
         if (real)
-            k_near<true><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(G, P->p, t0, off, P->near.off, P->near.idx, P->src,
-                                                                cx, cy, loc, P->perm, tab, phi, dphi, m2p_off,
-                                                                P->rr_acc);
+            k_near<true><<<grid, NEAR_T, 0, P->stream>>>(G, P->p, t0, nl, P->near_seg_off, P->near_segs,
+                                                        P->near_part, P->stats.max_leaf, off, P->near.off,
+                                                        P->near.idx, P->src, cx, cy, loc, P->perm, tab, phi, dphi,
+                                                        m2p_off, P->rr_acc);
         else
-            k_near<false><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(G, P->p, t0, off, P->near.off, P->near.idx, P->src,
-                                                                 cx, cy, loc, P->perm, tab, phi, dphi, m2p_off,
-                                                                 P->rr_acc);
+            k_near<false><<<grid, NEAR_T, 0, P->stream>>>(G, P->p, t0, nl, P->near_seg_off, P->near_segs,
+                                                         P->near_part, P->stats.max_leaf, off, P->near.off,
+                                                         P->near.idx, P->src, cx, cy, loc, P->perm, tab, phi, dphi,
+                                                         m2p_off, P->rr_acc);
+        if (P->near_nsplit > 0) {
+            fmm2d::note_launch();
+            FMM2D_CUDA_TRY(cudaGetLastError());
+            k_near_combine<<<(unsigned)P->near_nsplit, NEAR_T, 0, P->stream>>>(
+                P->near_split, P->near_seg_off, P->near_part, P->stats.max_leaf, P->p, off, P->src, cx, cy, loc,
+                P->perm, phi, dphi, m2p_off, P->rr_acc);
+        }
     } else {
         if (real)
             k_near_wide<true><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, t0, off, P->near.off, P->near.idx,

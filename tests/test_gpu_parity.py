@@ -295,3 +295,20 @@ def test_rr_exchange_lists_and_eval_match_oracle(orc, name, cfg, n):
     assert _nerr(phi_g, phi_o) <= TOL and _nerr(dphi_g, dphi_o) <= TOL
     off = Fmm2d(torch.from_numpy(z).cuda(), theta=0.5, p=p, nlevels=L)
     assert gp.stats()["p2p_pairs"] < off.stats()["p2p_pairs"]
+
+
+def test_near_split_long_lists(orc):
+    """Leaves whose near lists exceed FMM2D_NEAR_SPLIT source rows are evaluated in
+    segments by several CTAs and combined in segment order: same results as the oracle
+    (clustered input: leaves strongly coupled to thousands of leaves)."""
+    z, m = W.make_config("C3", n=200_000)
+    L = orc.nlevels(len(z), 35)
+    op = orc.plan(z, 0.5, L)
+    so, si = op.list(L, "strong")
+    offL = op.offsets(L)
+    sizes = np.diff(offL)
+    rows = np.array([sizes[si[so[t]:so[t + 1]]].sum() for t in range(4 ** L)])
+    assert (rows > 4096).sum() > 0
+    phi_o, dphi_o = op.eval(m, 17)
+    phi_g, dphi_g = _gpu_eval(_gpu_plan(z, 0.5, 17, L), m)
+    assert _nerr(phi_g, phi_o) <= TOL and _nerr(dphi_g, dphi_o) <= TOL
