@@ -67,6 +67,17 @@ def positions(dist: str, n: int, rng: np.random.Generator) -> np.ndarray:
         t = rng.random(n)
         e = 1e-4 * rng.standard_normal((n, 2))
         return (t + e[:, 0]) + 1j * (0.1 * np.sin(8.0 * np.pi * t) + e[:, 1])
+    if dist == "disc":
+        # Fig. 3 (i): uniform in the unit disc
+        r = np.sqrt(rng.random(n))
+        a = 2.0 * np.pi * rng.random(n)
+        return r * np.cos(a) + 1j * (r * np.sin(a))
+    if dist == "disc_r":
+        # Fig. 3 (ii): "radial density proportional to 1/r" in the unit disc;
+        # reading R24: the areal density is ~1/r, so the radius is uniform on [0, 1)
+        r = rng.random(n)
+        a = 2.0 * np.pi * rng.random(n)
+        return r * np.cos(a) + 1j * (r * np.sin(a))
     raise ValueError(dist)
 
 
@@ -75,6 +86,8 @@ def strengths(kind: str, n: int, rng: np.random.Generator) -> np.ndarray:
         return (2.0 * rng.random(n) - 1.0).astype(np.complex128)     # U[-1,1], Im m = 0
     if kind == "phase":
         return np.exp(1j * (2.0 * np.pi * rng.random(n)))               # e^{i phi}
+    if kind == "mass":
+        return np.full(n, 1.0 / n, np.complex128)                       # total mass 1 (Fig. 3)
     raise ValueError(kind)
 
 
