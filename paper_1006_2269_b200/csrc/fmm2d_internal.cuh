@@ -15,6 +15,9 @@
 #include "../../include/fmm2d.h"
 
 #define FMM2D_MAXL 15
+#ifndef FMM2D_NEAR_CHUNK
+#define FMM2D_NEAR_CHUNK 384        // k_near: source rows staged per chunk (C5: one chunk per leaf)
+#endif
 #ifndef FMM2D_NEAR_SPLIT
 #define FMM2D_NEAR_SPLIT 4096       // near lists with more source rows: split over several CTAs
 #endif

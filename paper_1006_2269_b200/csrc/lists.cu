@@ -219,10 +219,10 @@ __global__ void k_near_segs(int64_t t0, int64_t t1, const int64_t* __restrict__ 
 // ordered P2P pairs (j != i) of one evaluation: sum_t n_t * sum_{s in S(t)} n_s - N
 __global__ void k_pair_count(int64_t t0, int64_t t1, const uint32_t* __restrict__ off,
                              const int64_t* __restrict__ soff, const uint32_t* __restrict__ sidx,
-                             unsigned long long* __restrict__ total)
+                             unsigned long long* __restrict__ total, unsigned long long* __restrict__ max_rows)
 {
     int64_t t = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long v = 0;
+    unsigned long long v = 0, mx = 0;
     if (t < t1) {
         unsigned long long ns = 0;
         for (int64_t q = soff[t]; q < soff[t + 1]; ++q) {
@@ -231,9 +231,14 @@ __global__ void k_pair_count(int64_t t0, int64_t t1, const uint32_t* __restrict_
         }
         unsigned long long nt = off[t + 1] - off[t];
         v = nt * ns - nt;
+        mx = ns;
     }
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = 16; o; o >>= 1) {
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(total, v);
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(max_rows, mx);     // longest near list (source rows)
 }
 
 inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
@@ -479,16 +484,17 @@ int build_lists(fmm2d_plan* P)
         const int64_t t0 = P->box_lo(L), t1 = P->box_hi(L);
         P->near = P->strong[L];                     // the direct pairs (all strong pairs unless r/R exchange)
         if (P->flags & FMM2D_RR_EXCHANGE) FMM2D_TRY(build_rr_lists(P));
-        if (P->stats.max_leaf <= 256) FMM2D_TRY(build_near_segments(P));     // k_near's chunk size
         unsigned long long* d_tot = (unsigned long long*)cnt_w;   // reuse scratch
-        FMM2D_CUDA_TRY(cudaMemsetAsync(d_tot, 0, sizeof(unsigned long long), st));
+        FMM2D_CUDA_TRY(cudaMemsetAsync(d_tot, 0, 2 * sizeof(unsigned long long), st));
         k_pair_count<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, P->boff + P->obase[L], P->near.off,
-                                                             P->near.idx, d_tot); fmm2d::note_launch();
+                                                             P->near.idx, d_tot, d_tot + 1); fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
-        unsigned long long h_tot = 0;
-        FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_tot, d_tot, sizeof(h_tot), cudaMemcpyDeviceToHost, st));
+        unsigned long long h_tot[2] = {0, 0};
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(h_tot, d_tot, sizeof(h_tot), cudaMemcpyDeviceToHost, st));
         FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
-        P->stats.p2p_pairs = (int64_t)h_tot;
+        P->stats.p2p_pairs = (int64_t)h_tot[0];
+        // long near lists: segments for k_near (only if some list exceeds the split size)
+        if (P->stats.max_leaf <= FMM2D_NEAR_CHUNK && h_tot[1] > FMM2D_NEAR_SPLIT) FMM2D_TRY(build_near_segments(P));
         return 0;
     };
     int rc = body();

@@ -28,9 +28,6 @@ namespace fmm2d {
 namespace {
 
 constexpr int NEAR_T = 128;
-#ifndef FMM2D_NEAR_CHUNK
-#define FMM2D_NEAR_CHUNK 256
-#endif
 #ifndef FMM2D_NEAR_MINB
 #define FMM2D_NEAR_MINB 8
 #endif
