@@ -69,6 +69,10 @@ extern "C" {
                                       smaller leaf's local) and M2P (smaller leaf's multipole
                                       at the larger leaf's points) instead of the direct
                                       sum (R23).  One GPU only (nranks > 1: ENOTSUP) */
+#define FMM2D_PARENT_MERGE    0x40  /* the parent merge of P:364-370: a box weakly coupled to
+                                      all four children of a box q interacts with q itself
+                                      (cross-level M2L from level l-1) when Criterion 1
+                                      holds for the pair (R25)                 */
 #define FMM2D_TREE_GLOBAL_ONLY 0x10 /* diagnostic: every split step in global memory (no
                                       on-chip finish of the deepest levels; same tree)  */
 
@@ -192,6 +196,8 @@ FMM2D_API int fmm2d_plan_info(const fmm2d_plan* plan, int64_t* n, int* nlevels, 
 #define FMM2D_EXPORT_NEAR        9  /* L      int64[4^L+1] offsets then uint32[]: direct pairs */
 #define FMM2D_EXPORT_RR_P2L     10  /* L      same layout: P2L sources of each leaf (r/R exch.) */
 #define FMM2D_EXPORT_RR_M2P     11  /* L      same layout: M2P sources of each leaf (r/R exch.) */
+#define FMM2D_EXPORT_XWEAK      12  /* l      same layout: cross-level weak entries (ids of level
+                                       l-1; parent merge; empty when off)               */
 /* If dst is NULL, *bytes receives the required size.  Otherwise *bytes must hold
  * the capacity of dst; on success it receives the bytes written.  Synchronises the
  * plan's stream.  Errors: EINVAL (bad what/level/capacity), ECUDA. */

@@ -22,6 +22,9 @@ Parity status of each oracle function (what pins it, see tests/test_oracle_*.py)
                 unit charge about 4, [1,1]->[2,1]), translation identities
   eval          pinned: error vs direct sum within the paper's a-priori law
                 (P:281-285), decay slope ~ log10(theta), ordering in theta
+  parent merge  pinned (O8): list audit (each cross pair replaces exactly four
+                weak children and is itself well separated), exactly-once pair coverage,
+                the pass against the direct sum within the gate, fewer M2L pairs
   rr exchange   pinned (O7): predicate worked examples + the exchanged
                 geometric meaning, P2L closed form and P2L = M2L o P2M identity, M2P of a
                 single charge, conversion-list audit (exchanged holds, original fails,
@@ -150,15 +153,16 @@ class Plan:
     """Oracle tree + discs + lists for fixed (z, theta, L); ``eval(m, p)`` runs the
     evaluation pass.  Arrays are returned as numpy copies."""
 
-    def __init__(self, z, theta: float, L: int, rr_exchange: bool = False):
+    def __init__(self, z, theta: float, L: int, rr_exchange: bool = False, parent_merge: bool = False):
         z = _c128(z)
         self.n = int(z.shape[0])
         self.theta = float(theta)
         self.L = int(L)
         self.rr_exchange = bool(rr_exchange)
+        self.parent_merge = bool(parent_merge)
         h = ctypes.c_void_p()
-        rc = lib().oracle_build_ex(_dp(_as_f64(z)), self.n, self.theta, self.L, 1 if rr_exchange else 0,
-                                   ctypes.byref(h))
+        rc = lib().oracle_build_ex(_dp(_as_f64(z)), self.n, self.theta, self.L,
+                                   (1 if rr_exchange else 0) | (2 if parent_merge else 0), ctypes.byref(h))
         if rc:
             raise ValueError(f"oracle_build: {rc}")
         self._h = h
@@ -188,7 +192,7 @@ class Plan:
     def list(self, level: int, kind: str):
         """kind 'strong' or 'weak' (any level), 'near' / 'p2l' / 'm2p' (leaf level, the
         r/R exchange split of the strong list, O7) -> CSR (off int64[4^l+1], idx uint32[])."""
-        k = {"strong": 0, "weak": 1, "near": 2, "p2l": 3, "m2p": 4}[kind]
+        k = {"strong": 0, "weak": 1, "near": 2, "p2l": 3, "m2p": 4, "xweak": 5}[kind]
         tot = lib().oracle_list_total(self._h, level, k)
         off = np.empty(4 ** level + 1, np.int64)
         idx = np.empty(max(tot, 1), np.uint32)
@@ -215,8 +219,8 @@ class Plan:
         return out
 
 
-def plan(z, theta: float, L: int, rr_exchange: bool = False) -> Plan:
-    return Plan(z, theta, L, rr_exchange)
+def plan(z, theta: float, L: int, rr_exchange: bool = False, parent_merge: bool = False) -> Plan:
+    return Plan(z, theta, L, rr_exchange, parent_merge)
 
 
 def rr_exchange(cb, rb, cc, rc, theta) -> bool:

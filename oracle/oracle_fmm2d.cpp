@@ -18,6 +18,7 @@
  *   O5 expansions / shifts   P:355-362, classical complex forms P:436-440
  *   O6 branch conventions    DESIGN R2
  *   O7 r/R exchange          P:370-377 (optional; leaf level: P2L + M2P instead of P2P)
+ *   O8 parent merge          P:364-370 (optional; cross-level M2L from a parent box)
  * Floating point: compiled with -O2 -ffp-contract=off (no FMA contraction), no
  * fast-math; sqrt is IEEE correctly rounded.  OpenMP is used only across
  * independent boxes / targets, each of which is summed in a fixed order, so
@@ -131,6 +132,11 @@ struct oracle_plan {
      * larger box's points (m2p_in).  Off: near = strong[L], the others empty. */
     int rr;
     std::vector<std::vector<uint32_t>> near, p2l_in, m2p_in;
+    /* O8 (parent merge on): per level l >= 2, box b's cross-level weak list: boxes q of
+     * level l-1 whose four children were all weak to b and that are themselves well
+     * separated from b; those children are then not in weak[l][b]. */
+    int pm;
+    std::vector<std::vector<std::vector<uint32_t>>> xweak;
     /* expansions from the last oracle_eval (diagnostics) */
     int p;
     std::vector<std::vector<cplx>> mpole, local;     /* per level: 4^l * (p+1)        */
@@ -240,6 +246,8 @@ static void build_lists(oracle_plan* P)
 {
     P->strong.assign(P->L + 1, {});
     P->weak.assign(P->L + 1, {});
+    P->xweak.assign(P->L + 1, {});
+    for (int l = 0; l <= P->L; ++l) P->xweak[l].assign(nboxes(l), {});
     P->strong[0].assign(1, std::vector<uint32_t>{0});
     P->weak[0].assign(1, std::vector<uint32_t>{});
     for (int l = 1; l <= P->L; ++l) {
@@ -253,11 +261,22 @@ static void build_lists(oracle_plan* P)
         for (int64_t b = 0; b < nb; ++b) {
             int64_t parent = b / 4;
             for (uint32_t q : P->strong[l - 1][parent]) {
+                bool ws[4];
+                for (int64_t c = 4 * (int64_t)q; c < 4 * (int64_t)q + 4; ++c)
+                    ws[c - 4 * q] = (c != b) && oracle_well_separated(cx[b], cy[b], rr[b],
+                                                                      cx[c], cy[c], rr[c], P->theta);
+                /* O8: "a box weakly coupled to all children of a parent box can
+                 * often interact via the latter instead (whenever the theta-criterion with
+                 * respect to that parent is true)".  The parent q is at level l-1. */
+                if (P->pm && l >= 2 && ws[0] && ws[1] && ws[2] && ws[3] &&
+                    oracle_well_separated(cx[b], cy[b], rr[b], P->cx[l - 1][q], P->cy[l - 1][q],
+                                          P->rad[l - 1][q], P->theta)) {
+                    P->xweak[l][b].push_back(q);
+                    continue;
+                }
                 for (int64_t c = 4 * (int64_t)q; c < 4 * (int64_t)q + 4; ++c) {
-                    bool ws = (c != b) && oracle_well_separated(cx[b], cy[b], rr[b],
-                                                                cx[c], cy[c], rr[c], P->theta);
-                    if (ws) P->weak[l][b].push_back((uint32_t)c);
-                    else    P->strong[l][b].push_back((uint32_t)c);
+                    if (ws[c - 4 * q]) P->weak[l][b].push_back((uint32_t)c);
+                    else               P->strong[l][b].push_back((uint32_t)c);
                 }
             }
         }
@@ -302,7 +321,7 @@ int oracle_build(const double* z, int64_t n, double theta, int L, oracle_plan** 
     return oracle_build_ex(z, n, theta, L, 0, out);
 }
 
-/* flags bit 0: r/R exchange (O7) */
+/* flags bit 0: r/R exchange (O7), bit 1: parent merge (O8) */
 int oracle_build_ex(const double* z, int64_t n, double theta, int L, int flags, oracle_plan** out)
 {
     if (!out) return -1;
@@ -321,6 +340,7 @@ int oracle_build_ex(const double* z, int64_t n, double theta, int L, int flags, 
         P->y[i] = z[2 * i + 1] + 0.0;
     }
     P->rr = (flags & 1) ? 1 : 0;
+    P->pm = (flags & 2) ? 1 : 0;
     build_tree(P);
     build_discs(P);
     build_lists(P);
@@ -356,12 +376,13 @@ int oracle_get_discs(const oracle_plan* P, int l, double* cx, double* cy, double
     return 0;
 }
 
-/* kind 0 = strong, 1 = weak; leaf level only: 2 = near (P2P), 3 = p2l_in,
- * 4 = m2p_in (O7). */
+/* kind 0 = strong, 1 = weak, 5 = cross-level weak (O8, ids of level l-1); leaf level
+ * only: 2 = near (P2P), 3 = p2l_in, 4 = m2p_in (O7). */
 static const std::vector<std::vector<uint32_t>>& list_of(const oracle_plan* P, int l, int kind)
 {
     switch (kind) {
         case 1: return P->weak[l];
+        case 5: return P->xweak[l];
         case 2: return P->near;
         case 3: return P->p2l_in;
         case 4: return P->m2p_in;
@@ -371,7 +392,7 @@ static const std::vector<std::vector<uint32_t>>& list_of(const oracle_plan* P, i
 
 int64_t oracle_list_total(const oracle_plan* P, int l, int kind)
 {
-    if (l < 0 || l > P->L || kind < 0 || kind > 4 || (kind >= 2 && l != P->L)) return -1;
+    if (l < 0 || l > P->L || kind < 0 || kind > 5 || (kind >= 2 && kind <= 4 && l != P->L)) return -1;
     const auto& LL = list_of(P, l, kind);
     int64_t t = 0;
     for (const auto& v : LL) t += (int64_t)v.size();
@@ -380,7 +401,7 @@ int64_t oracle_list_total(const oracle_plan* P, int l, int kind)
 
 int oracle_get_list(const oracle_plan* P, int l, int kind, int64_t* off, uint32_t* idx)
 {
-    if (l < 0 || l > P->L || kind < 0 || kind > 4 || (kind >= 2 && l != P->L)) return -1;
+    if (l < 0 || l > P->L || kind < 0 || kind > 5 || (kind >= 2 && kind <= 4 && l != P->L)) return -1;
     const auto& LL = list_of(P, l, kind);
     int64_t t = 0;
     for (size_t b = 0; b < LL.size(); ++b) {
@@ -651,12 +672,16 @@ int oracle_eval(oracle_plan* P, const double* m, int p, double* phi, double* dph
             }
         }
     }
-    /* M2L along the weak connectivity of every level */
+    /* M2L along the weak connectivity of every level, then O8's
+     * cross-level pairs (multipole of a level l-1 box into a level l local) */
     for (int l = 1; l <= L; ++l) {
 #pragma omp parallel for schedule(dynamic, 64)
         for (int64_t t = 0; t < nboxes(l); ++t) {
             for (uint32_t s : P->weak[l][t])
                 m2l(P->mpole[l].data() + (int64_t)s * P1, P->cx[l][s], P->cy[l][s],
+                    P->cx[l][t], P->cy[l][t], p, C, P->local[l].data() + t * P1);
+            for (uint32_t q : P->xweak[l][t])
+                m2l(P->mpole[l - 1].data() + (int64_t)q * P1, P->cx[l - 1][q], P->cy[l - 1][q],
                     P->cx[l][t], P->cy[l][t], p, C, P->local[l].data() + t * P1);
         }
     }

@@ -430,7 +430,8 @@ int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* by
                             what == FMM2D_EXPORT_RR_M2P);
     const bool per_level = (what == FMM2D_EXPORT_OFFSETS || what == FMM2D_EXPORT_DISCS ||
                             what == FMM2D_EXPORT_STRONG || what == FMM2D_EXPORT_WEAK ||
-                            what == FMM2D_EXPORT_MPOLE || what == FMM2D_EXPORT_LOCAL || leaf_list);
+                            what == FMM2D_EXPORT_MPOLE || what == FMM2D_EXPORT_LOCAL || leaf_list ||
+                            what == FMM2D_EXPORT_XWEAK);
     if (per_level && (level < 0 || level > P->L)) return FMM2D_EINVAL;
     if (leaf_list && level != P->L) return FMM2D_EINVAL;
     const int64_t nb = per_level ? nboxes(level) : 0;
@@ -439,6 +440,10 @@ int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* by
     const Csr* LC = nullptr;
     if (leaf_list) {
         LC = (what == FMM2D_EXPORT_NEAR) ? &P->near : (what == FMM2D_EXPORT_RR_P2L ? &P->rr_p2l : &P->rr_m2p);
+        if (!LC->off) LC = &empty_csr;
+    }
+    if (what == FMM2D_EXPORT_XWEAK) {
+        LC = (level < (int)P->xweak.size()) ? &P->xweak[level] : &empty_csr;
         if (!LC->off) LC = &empty_csr;
     }
     size_t need = 0;
@@ -455,7 +460,8 @@ int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* by
         case FMM2D_EXPORT_STATS: need = sizeof(double) * 16; break;
         case FMM2D_EXPORT_NEAR:
         case FMM2D_EXPORT_RR_P2L:
-        case FMM2D_EXPORT_RR_M2P: need = sizeof(int64_t) * (nb + 1) + sizeof(uint32_t) * LC->total; break;
+        case FMM2D_EXPORT_RR_M2P:
+        case FMM2D_EXPORT_XWEAK: need = sizeof(int64_t) * (nb + 1) + sizeof(uint32_t) * LC->total; break;
         default: return FMM2D_EINVAL;
     }
     if (!dst) {
@@ -492,6 +498,7 @@ int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* by
         case FMM2D_EXPORT_NEAR:
         case FMM2D_EXPORT_RR_P2L:
         case FMM2D_EXPORT_RR_M2P:
+        case FMM2D_EXPORT_XWEAK:
             if (LC->off) {
                 FMM2D_TRY(copy_out(LC->off, dst, sizeof(int64_t) * (nb + 1), &cap, &off, st));
                 FMM2D_TRY(copy_out(LC->idx, dst, sizeof(uint32_t) * LC->total, &cap, &off, st));

@@ -135,6 +135,8 @@ __global__ void __launch_bounds__(128) k_m2m(int64_t b0, int64_t b1, const doubl
 struct M2LArgs {
     const int64_t* woff[FMM2D_MAXL + 1];
     const uint32_t* widx[FMM2D_MAXL + 1];
+    const int64_t* xoff[FMM2D_MAXL + 1];     // cross-level entries (parent merge) or nullptr
+    const uint32_t* xidx[FMM2D_MAXL + 1];
     int64_t base[FMM2D_MAXL + 2];
     int64_t lo[FMM2D_MAXL + 1];       // target boxes of level l: [lo[l], lo[l] + (pre[l+1] - pre[l]))
     int64_t pre[FMM2D_MAXL + 2];      // work prefix over levels 1..L
@@ -146,57 +148,71 @@ struct M2LArgs {
     double2* local;
 };
 
-// Output coefficients l in [L0, L1) of target box g, summed over the weak pairs
-// q = qa, qa + qs, ... < qb into acc.
+// One weak pair: the multipole of source box s (global id) into coefficients l in
+// [L0, L1) of the local about (ctx, cty), accumulated into acc.
 template <int P, int L0, int L1>
-__device__ __forceinline__ void m2l_accum(const M2LArgs& A, int64_t g, int lev, int64_t qa, int64_t qb, int64_t qs,
-                                          double2 (&acc)[L1 - L0])
+__device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, double ctx, double cty, double2 (&acc)[L1 - L0])
 {
-    const uint32_t* idx = A.widx[lev];
-    const double ctx = A.cx[g], cty = A.cy[g];
-    for (int64_t q = qa; q < qb; q += qs) {
-        const int64_t s = A.base[lev] + idx[q];
-        const double csx = A.cx[s], csy = A.cy[s];
-        const double2* M = A.mpole + s * (P + 1);
-        // z0 = c_s - c_t and 1/z0
-        const double dx = csx - ctx, dy = csy - cty;
-        const double r2 = dx * dx + dy * dy;
-        const double ir2 = 1.0 / r2;
-        const double2 iz = make_double2(dx * ir2, -dy * ir2);
-        const double2 w = make_double2(-iz.x, -iz.y);
-        // pre-scale: alpha_k = a_k (-1/z0)^k
-        double2 al[P + 1];
-        double2 wk = w;
+    const double csx = A.cx[s], csy = A.cy[s];
+    const double2* M = A.mpole + s * (P + 1);
+    // z0 = c_s - c_t and 1/z0
+    const double dx = csx - ctx, dy = csy - cty;
+    const double r2 = dx * dx + dy * dy;
+    const double ir2 = 1.0 / r2;
+    const double2 iz = make_double2(dx * ir2, -dy * ir2);
+    const double2 w = make_double2(-iz.x, -iz.y);
+    // pre-scale: alpha_k = a_k (-1/z0)^k
+    double2 al[P + 1];
+    double2 wk = w;
+#pragma unroll
+    for (int k = 1; k <= P; ++k) {
+        al[k] = cmul(M[k], wk);
+        if (k < P) wk = cmul(wk, w);
+    }
+    const double2 a0 = M[0];
+    double2 izl = make_double2(1.0, 0.0);
+#pragma unroll
+    for (int l = 0; l < L1; ++l) {
+        if (l >= 1) izl = cmul(izl, iz);            // z0^-l
+        if (l < L0) continue;
+        double2 beta = make_double2(0.0, 0.0);
 #pragma unroll
         for (int k = 1; k <= P; ++k) {
-            al[k] = cmul(M[k], wk);
-            if (k < P) wk = cmul(wk, w);
+            const double c = c_m2l[l * S1 + k];
+            beta.x = fma(c, al[k].x, beta.x);
+            beta.y = fma(c, al[k].y, beta.y);
         }
-        const double2 a0 = M[0];
-        double2 izl = make_double2(1.0, 0.0);
-#pragma unroll
-        for (int l = 0; l < L1; ++l) {
-            if (l >= 1) izl = cmul(izl, iz);            // z0^-l
-            if (l < L0) continue;
-            double2 beta = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int k = 1; k <= P; ++k) {
-                const double c = c_m2l[l * S1 + k];
-                beta.x = fma(c, al[k].x, beta.x);
-                beta.y = fma(c, al[k].y, beta.y);
-            }
-            double2 v;
-            if (l == 0) {
-                // a_0 Log(c_t - c_s), componentwise difference (DESIGN R2)
-                const double tx = ctx - csx, ty = cty - csy;
-                const double2 lg = make_double2(0.5 * log(r2), atan2(ty, tx));
-                v = cadd(cmul(a0, lg), beta);
-            } else {
-                const double2 t = csub(beta, cscale(a0, 1.0 / l));
-                v = cmul(t, izl);
-            }
-            acc[l - L0] = cadd(acc[l - L0], v);
+        double2 v;
+        if (l == 0) {
+            // a_0 Log(c_t - c_s), componentwise difference (DESIGN R2)
+            const double tx = ctx - csx, ty = cty - csy;
+            const double2 lg = make_double2(0.5 * log(r2), atan2(ty, tx));
+            v = cadd(cmul(a0, lg), beta);
+        } else {
+            const double2 t = csub(beta, cscale(a0, 1.0 / l));
+            v = cmul(t, izl);
         }
+        acc[l - L0] = cadd(acc[l - L0], v);
+    }
+}
+
+// Output coefficients l in [L0, L1) of target box g (level lev, level-local b), summed
+// over the entries j = ja, ja + js, ... < jb of its weak list followed by its cross-level
+// (parent merge) list.
+template <int P, int L0, int L1>
+__device__ __forceinline__ void m2l_accum(const M2LArgs& A, int64_t g, int lev, int64_t b, int64_t ja, int64_t js,
+                                          double2 (&acc)[L1 - L0])
+{
+    const int64_t w0 = A.woff[lev][b], nw = A.woff[lev][b + 1] - w0;
+    const int64_t x0 = A.xoff[lev] ? A.xoff[lev][b] : 0;
+    const int64_t jb = nw + (A.xoff[lev] ? A.xoff[lev][b + 1] - x0 : 0);
+    const uint32_t* __restrict__ widx = A.widx[lev];
+    const uint32_t* __restrict__ xidx = A.xidx[lev];
+    const int64_t wbase = A.base[lev], xbase = lev > 0 ? A.base[lev - 1] : 0;
+    const double ctx = A.cx[g], cty = A.cy[g];
+    for (int64_t j = ja; j < jb; j += js) {
+        const int64_t s = (j < nw) ? wbase + widx[w0 + j] : xbase + xidx[x0 + (j - nw)];
+        m2l_pair<P, L0, L1>(A, s, ctx, cty, acc);
     }
 }
 
@@ -208,7 +224,7 @@ __device__ __forceinline__ void m2l_target(const M2LArgs& A, int64_t g, int lev)
     double2 acc[L1 - L0];
 #pragma unroll
     for (int l = 0; l < L1 - L0; ++l) acc[l] = make_double2(0.0, 0.0);
-    m2l_accum<P, L0, L1>(A, g, lev, A.woff[lev][b], A.woff[lev][b + 1], 1, acc);
+    m2l_accum<P, L0, L1>(A, g, lev, b, 0, 1, acc);
     double2* out = A.local + g * (P + 1);
 #pragma unroll
     for (int l = L0; l < L1; ++l) out[l] = acc[l - L0];
@@ -223,7 +239,7 @@ __device__ __forceinline__ void m2l_target_warp(const M2LArgs& A, int64_t g, int
     double2 acc[L1 - L0];
 #pragma unroll
     for (int l = 0; l < L1 - L0; ++l) acc[l] = make_double2(0.0, 0.0);
-    m2l_accum<P, L0, L1>(A, g, lev, A.woff[lev][b] + lane, A.woff[lev][b + 1], 32, acc);
+    m2l_accum<P, L0, L1>(A, g, lev, b, lane, 32, acc);
 #pragma unroll
     for (int l = 0; l < L1 - L0; ++l) {
         for (int o = 16; o; o >>= 1) {
@@ -260,7 +276,8 @@ __global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l(M2LArgs A)
     const int64_t g = A.base[lev] + A.order[w];
     {   // long lists are done by k_m2l_long
         const int64_t b = g - A.base[lev];
-        if (A.woff[lev][b + 1] - A.woff[lev][b] > FMM2D_M2L_LONG) return;
+        const int64_t len = A.woff[lev][b + 1] - A.woff[lev][b] + (A.xoff[lev] ? A.xoff[lev][b + 1] - A.xoff[lev][b] : 0);
+        if (len > FMM2D_M2L_LONG) return;
     }
     // part q computes coefficients [q H, min((q+1) H, P+1)), H = ceil((P+1)/NS)
     constexpr int H = (P + NS) / NS;
@@ -503,6 +520,8 @@ int m2l_p(fmm2d_plan* Pl)
     for (int l = 0; l <= L; ++l) {
         A.woff[l] = Pl->weak[l].off;
         A.widx[l] = Pl->weak[l].idx;
+        A.xoff[l] = Pl->xweak[l].off;
+        A.xidx[l] = Pl->xweak[l].idx;
     }
     for (int l = 0; l <= L + 1; ++l) A.base[l] = Pl->base[l];
     A.pre[0] = A.pre[1] = 0;

@@ -82,6 +82,7 @@ struct fmm2d_plan {
     double *cx = nullptr, *cy = nullptr, *r = nullptr;   // [nbox_total]
     // connectivity
     std::vector<fmm2d::Csr> strong, weak;   // per level
+    std::vector<fmm2d::Csr> xweak;          // per level: cross-level weak entries (parent merge; ids of level l-1)
     uint32_t* m2l_order = nullptr;      // M2L targets per level (levels 1..L concatenated), by list length
     uint32_t* m2l_long = nullptr;       // global ids of targets with more than FMM2D_M2L_LONG weak pairs
     int64_t m2l_nlong = 0;

@@ -33,13 +33,18 @@ __device__ __forceinline__ bool well_separated(double cbx, double cby, double rb
     return (d > 0.0) && (__dadd_rn(R, __dmul_rn(theta, r)) <= __dmul_rn(theta, d));
 }
 
+// Parent merge (DESIGN R25; `merge`): a candidate group of four children of q
+// (four consecutive lanes) that are ALL weak to b, with Criterion 1 also true for (b, q)
+// itself (q's disc at level l-1: pcx, pcy, pr), becomes one cross-level entry q.
 template <bool FILL>
 __global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, const double* __restrict__ cy,
                         const double* __restrict__ r, double theta, const int64_t* __restrict__ poff,
                         const uint32_t* __restrict__ pidx, int64_t* __restrict__ wcnt,
                         int64_t* __restrict__ scnt, const int64_t* __restrict__ woff,
                         const int64_t* __restrict__ soff, uint32_t* __restrict__ widx,
-                        uint32_t* __restrict__ sidx)
+                        uint32_t* __restrict__ sidx, bool merge, const double* __restrict__ pcx,
+                        const double* __restrict__ pcy, const double* __restrict__ pr, int64_t* __restrict__ xcnt,
+                        const int64_t* __restrict__ xoff, uint32_t* __restrict__ xidx)
 {
     int64_t b = b0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     int lane = threadIdx.x & 31;
@@ -48,30 +53,47 @@ __global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, c
     int64_t o0 = poff[par];
     int64_t ncand = 4 * (poff[par + 1] - o0);
     double bx = cx[b], by = cy[b], br = r[b];
-    int64_t nw = 0, ns = 0;
-    int64_t wbase = FILL ? woff[b] : 0, sbase = FILL ? soff[b] : 0;
+    int64_t nw = 0, ns = 0, nx = 0;
+    int64_t wbase = FILL ? woff[b] : 0, sbase = FILL ? soff[b] : 0, xbase = (FILL && merge) ? xoff[b] : 0;
     unsigned lt = (1u << lane) - 1u;
     for (int64_t t0 = 0; t0 < ncand; t0 += 32) {
         int64_t t = t0 + lane;
         bool valid = t < ncand;
-        uint32_t c = 0;
+        uint32_t c = 0, q = 0;
         bool ws = false;
         if (valid) {
-            c = 4u * pidx[o0 + (t >> 2)] + (uint32_t)(t & 3);
+            q = pidx[o0 + (t >> 2)];
+            c = 4u * q + (uint32_t)(t & 3);
             ws = (c != (uint32_t)b) && well_separated(bx, by, br, cx[c], cy[c], r[c], theta);
         }
         unsigned wm = __ballot_sync(0xffffffffu, valid && ws);
+        bool merged = false;                        // my group of four merges into its parent q
+        if (merge) {
+            const bool all4 = ((wm >> (lane & ~3)) & 0xFu) == 0xFu;
+            bool mq = false;
+            if (all4 && (lane & 3) == 0) mq = well_separated(bx, by, br, pcx[q], pcy[q], pr[q], theta);
+            merged = __shfl_sync(0xffffffffu, mq ? 1 : 0, lane & ~3) != 0;
+            wm = __ballot_sync(0xffffffffu, valid && ws && !merged);
+        }
         unsigned sm = __ballot_sync(0xffffffffu, valid && !ws);
+        unsigned xm = __ballot_sync(0xffffffffu, merged && (lane & 3) == 0);
         if (FILL && valid) {
-            if (ws) widx[wbase + nw + __popc(wm & lt)] = c;
-            else    sidx[sbase + ns + __popc(sm & lt)] = c;
+            if (merged) {
+                if ((lane & 3) == 0) xidx[xbase + nx + __popc(xm & lt)] = q;
+            } else if (ws) {
+                widx[wbase + nw + __popc(wm & lt)] = c;
+            } else {
+                sidx[sbase + ns + __popc(sm & lt)] = c;
+            }
         }
         nw += __popc(wm);
         ns += __popc(sm);
+        nx += __popc(xm);
     }
     if (!FILL && lane == 0) {
         wcnt[b] = nw;
         scnt[b] = ns;
+        if (merge) xcnt[b] = nx;
     }
 }
 
@@ -82,13 +104,13 @@ __global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, c
 #ifndef FMM2D_M2L_WIN
 #define FMM2D_M2L_WIN 16384
 #endif
-__global__ void k_m2l_keys(int64_t b0, int64_t b1, const int64_t* __restrict__ woff, uint32_t* __restrict__ key,
-                           uint32_t* __restrict__ box)
+__global__ void k_m2l_keys(int64_t b0, int64_t b1, const int64_t* __restrict__ woff, const int64_t* __restrict__ xoff,
+                           uint32_t* __restrict__ key, uint32_t* __restrict__ box)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t b = b0 + i;
     if (b >= b1) return;
-    const int64_t len = woff[b + 1] - woff[b];
+    const int64_t len = woff[b + 1] - woff[b] + (xoff ? xoff[b + 1] - xoff[b] : 0);
     key[i] = ((uint32_t)(i / FMM2D_M2L_WIN) << 8) | (uint32_t)(255 - (len < 255 ? len : 255));
     box[i] = (uint32_t)b;
 }
@@ -152,10 +174,11 @@ __global__ void k_rr_lists(int64_t t0, int64_t t1, const double* __restrict__ cx
 
 // targets of one level with a long weak list (global ids; order irrelevant)
 __global__ void k_long_lists(int64_t b0, int64_t b1, int64_t gbase, const int64_t* __restrict__ woff,
-                             uint32_t* __restrict__ out, unsigned int* __restrict__ n)
+                             const int64_t* __restrict__ xoff, uint32_t* __restrict__ out, unsigned int* __restrict__ n)
 {
     const int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < b1 && woff[b + 1] - woff[b] > FMM2D_M2L_LONG) out[atomicAdd(n, 1u)] = (uint32_t)(gbase + b);
+    if (b < b1 && woff[b + 1] - woff[b] + (xoff ? xoff[b + 1] - xoff[b] : 0) > FMM2D_M2L_LONG)
+        out[atomicAdd(n, 1u)] = (uint32_t)(gbase + b);
 }
 
 // leaves with a non-empty list (compacted ids)
@@ -364,6 +387,7 @@ int build_lists(fmm2d_plan* P)
     cudaStream_t st = P->stream;
     P->strong.assign(L + 1, Csr());
     P->weak.assign(L + 1, Csr());
+    P->xweak.assign(L + 1, Csr());
     // level 0: S(root) = {root}, no weak pairs
     {
         int64_t h_off[2] = {0, 1}, h_woff[2] = {0, 0};
@@ -385,53 +409,72 @@ int build_lists(fmm2d_plan* P)
         return 0;
     }
     int64_t nbmax = nboxes(L);
-    int64_t *cnt_w = nullptr, *cnt_s = nullptr;
+    int64_t *cnt_w = nullptr, *cnt_s = nullptr, *cnt_x = nullptr;
     void* scratch = nullptr;
     size_t scan_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)(nbmax + 1), st);
     FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt_w, sizeof(int64_t) * (nbmax + 1), st));
     FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt_s, sizeof(int64_t) * (nbmax + 1), st));
+    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt_x, sizeof(int64_t) * (nbmax + 1), st));
     FMM2D_CUDA_TRY(cudaMallocAsync(&scratch, scan_bytes, st));
     auto body = [&]() -> int {
+        const bool merge_on = (P->flags & FMM2D_PARENT_MERGE) != 0;
         for (int l = 1; l <= L; ++l) {
             int64_t nb = nboxes(l);
             Csr& W = P->weak[l];
             Csr& S = P->strong[l];
+            Csr& X = P->xweak[l];
             const Csr& PS = P->strong[l - 1];
             const double* cx = P->cx + P->base[l];
             const double* cy = P->cy + P->base[l];
             const double* r = P->r + P->base[l];
+            const bool merge = merge_on && l >= 2;
             FMM2D_TRY(dev_alloc(P, (void**)&W.off, sizeof(int64_t) * (nb + 1)));
             FMM2D_TRY(dev_alloc(P, (void**)&S.off, sizeof(int64_t) * (nb + 1)));
+            if (merge) FMM2D_TRY(dev_alloc(P, (void**)&X.off, sizeof(int64_t) * (nb + 1)));
             // boxes of this rank: all of a replicated level, the own subtrees below it
             const int64_t b0 = P->box_lo(l), b1 = P->box_hi(l);
-            if (b1 - b0 < nb) {
+            if (b1 - b0 < nb || merge) {
                 FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_w, 0, sizeof(int64_t) * (nb + 1), st));
                 FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_s, 0, sizeof(int64_t) * (nb + 1), st));
+                if (merge) FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_x, 0, sizeof(int64_t) * (nb + 1), st));
             } else {
                 FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_w + nb, 0, sizeof(int64_t), st));
                 FMM2D_CUDA_TRY(cudaMemsetAsync(cnt_s + nb, 0, sizeof(int64_t), st));
             }
+            const double* pcx = P->cx + P->base[l - 1];
+            const double* pcy = P->cy + P->base[l - 1];
+            const double* pr = P->r + P->base[l - 1];
             unsigned grid = grid_for((b1 - b0) * 32, 256);
             k_lists<false><<<grid, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w, cnt_s,
-                                                 nullptr, nullptr, nullptr, nullptr); fmm2d::note_launch();
+                                                 nullptr, nullptr, nullptr, nullptr, merge, pcx, pcy, pr, cnt_x,
+                                                 nullptr, nullptr); fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
             size_t sb = scan_bytes;
             FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, cnt_w, W.off, (int)(nb + 1), st));
             sb = scan_bytes;
             FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, cnt_s, S.off, (int)(nb + 1), st));
-            int64_t tot[2];
+            if (merge) {
+                sb = scan_bytes;
+                FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, cnt_x, X.off, (int)(nb + 1), st));
+            }
+            int64_t tot[3] = {0, 0, 0};
             FMM2D_CUDA_TRY(cudaMemcpyAsync(&tot[0], W.off + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             FMM2D_CUDA_TRY(cudaMemcpyAsync(&tot[1], S.off + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            if (merge)
+                FMM2D_CUDA_TRY(cudaMemcpyAsync(&tot[2], X.off + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
             W.total = tot[0];
             S.total = tot[1];
+            X.total = tot[2];
             FMM2D_TRY(dev_alloc(P, (void**)&W.idx, sizeof(uint32_t) * std::max<int64_t>(W.total, 1)));
             FMM2D_TRY(dev_alloc(P, (void**)&S.idx, sizeof(uint32_t) * std::max<int64_t>(S.total, 1)));
+            if (merge) FMM2D_TRY(dev_alloc(P, (void**)&X.idx, sizeof(uint32_t) * std::max<int64_t>(X.total, 1)));
             k_lists<true><<<grid, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, nullptr, nullptr,
-                                                W.off, S.off, W.idx, S.idx); fmm2d::note_launch();
+                                                W.off, S.off, W.idx, S.idx, merge, pcx, pcy, pr, nullptr, X.off,
+                                                X.idx); fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
-            P->stats.weak_pairs += W.total;
+            P->stats.weak_pairs += W.total + X.total;
         }
         // M2L work order (k_m2l_keys)
         {
@@ -451,7 +494,7 @@ int build_lists(fmm2d_plan* P)
             int64_t o = 0;
             for (int l = 1; l <= L; ++l) {
                 const int64_t b0 = P->box_lo(l), b1 = P->box_hi(l), nb = b1 - b0;
-                k_m2l_keys<<<grid_for(nb, 256), 256, 0, st>>>(b0, b1, P->weak[l].off, k0, v0);
+                k_m2l_keys<<<grid_for(nb, 256), 256, 0, st>>>(b0, b1, P->weak[l].off, P->xweak[l].off, k0, v0);
                 fmm2d::note_launch();
                 int bits = 8;
                 while (((int64_t)1 << (bits - 8)) * FMM2D_M2L_WIN < nb) ++bits;
@@ -465,7 +508,8 @@ int build_lists(fmm2d_plan* P)
             FMM2D_CUDA_TRY(cudaMemsetAsync(d_n, 0, sizeof(unsigned int), st));
             for (int l = 1; l <= L; ++l) {
                 const int64_t b0 = P->box_lo(l), b1 = P->box_hi(l);
-                k_long_lists<<<grid_for(b1 - b0, 256), 256, 0, st>>>(b0, b1, P->base[l], P->weak[l].off, v0, d_n);
+                k_long_lists<<<grid_for(b1 - b0, 256), 256, 0, st>>>(b0, b1, P->base[l], P->weak[l].off,
+                                                                     P->xweak[l].off, v0, d_n);
                 fmm2d::note_launch();
             }
             unsigned int h_n = 0;
@@ -500,6 +544,7 @@ int build_lists(fmm2d_plan* P)
     int rc = body();
     cudaFreeAsync(cnt_w, st);
     cudaFreeAsync(cnt_s, st);
+    cudaFreeAsync(cnt_x, st);
     cudaFreeAsync(scratch, st);
     return rc;
 }

@@ -430,6 +430,14 @@ static int halo_requests(fmm2d_plan* P)
                                                                         P->base[l], nboxes(l) / P->nranks, P->rank,
                                                                         need);
             note_launch();
+            // parent merge: cross-level sources at level l-1 (remote only below the
+            // replicated levels; level k's multipoles are all-gathered)
+            if (P->xweak[l].off && l - 1 > k) {
+                k_flag_remote<<<grid_for((b1 - b0) * 32, 256), 256, 0, st>>>(b0, b1, P->xweak[l].off,
+                                                                            P->xweak[l].idx, P->base[l - 1],
+                                                                            nboxes(l - 1) / P->nranks, P->rank, need);
+                note_launch();
+            }
             FMM2D_CUDA_TRY(cudaGetLastError());
         }
         FMM2D_TRY(compact_requests(P, need, P->nbox_total, S->mp));

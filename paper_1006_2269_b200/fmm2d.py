@@ -29,9 +29,10 @@ SYMMETRIC_P2P = 0x4
 TREE_KEY64 = 0x8
 TREE_GLOBAL_ONLY = 0x10
 RR_EXCHANGE = 0x20
+PARENT_MERGE = 0x40
 
 EXPORT_PERM, EXPORT_OFFSETS, EXPORT_DISCS, EXPORT_STRONG, EXPORT_WEAK, EXPORT_MPOLE, EXPORT_LOCAL, \
-    EXPORT_STATS, EXPORT_NEAR, EXPORT_RR_P2L, EXPORT_RR_M2P = range(1, 12)
+    EXPORT_STATS, EXPORT_NEAR, EXPORT_RR_P2L, EXPORT_RR_M2P, EXPORT_XWEAK = range(1, 13)
 
 # every symbol include/fmm2d.h declares
 SYMBOLS = ["fmm2d_default_options", "fmm2d_build", "fmm2d_eval", "fmm2d_eval_timed", "fmm2d_launch_count",
@@ -166,7 +167,7 @@ class Fmm2d:
     def __init__(self, z, theta: float = 0.5, p: int = 17, leaf_target: int = 40, nlevels: int = -1,
                  real_strengths: bool = False, device: int | None = None, stream=None,
                  symmetric_p2p: bool = False, tree_key64: bool = False, tree_global_only: bool = False,
-                 rr_exchange: bool = False,
+                 rr_exchange: bool = False, parent_merge: bool = False,
                  nranks: int = 1, rank: int = 0,
                  nccl_id: bytes | None = None):
         L = lib()
@@ -187,7 +188,8 @@ class Fmm2d:
         opt.nlevels = int(nlevels)
         opt.flags = ((HOST_PTRS if host else 0) | (REAL_STRENGTHS if real_strengths else 0)
                      | (SYMMETRIC_P2P if symmetric_p2p else 0) | (TREE_KEY64 if tree_key64 else 0)
-                     | (TREE_GLOBAL_ONLY if tree_global_only else 0) | (RR_EXCHANGE if rr_exchange else 0))
+                     | (TREE_GLOBAL_ONLY if tree_global_only else 0) | (RR_EXCHANGE if rr_exchange else 0)
+                     | (PARENT_MERGE if parent_merge else 0))
         opt.device = int(device)
         opt.stream = ctypes.c_void_p(stream.cuda_stream)
         opt.nranks = int(nranks)
@@ -277,7 +279,7 @@ class Fmm2d:
         """kind 'strong' / 'weak' (any level); 'near' / 'p2l' / 'm2p' (leaf level: the direct
         pairs and the r/R exchange conversions) -> CSR (off int64[4^l+1], idx uint32[])."""
         what = {"strong": EXPORT_STRONG, "weak": EXPORT_WEAK, "near": EXPORT_NEAR, "p2l": EXPORT_RR_P2L,
-                "m2p": EXPORT_RR_M2P}[kind]
+                "m2p": EXPORT_RR_M2P, "xweak": EXPORT_XWEAK}[kind]
         raw = self._export(what, level)
         nb = 4 ** level
         off = np.frombuffer(raw[: 8 * (nb + 1)], np.int64).copy()
@@ -342,7 +344,7 @@ class LoopbackShards:
     complete Phi, Phi' (each rank writes the entries of the sources it owns)."""
 
     def __init__(self, z, nshards: int, theta: float = 0.5, p: int = 17, leaf_target: int = 40,
-                 nlevels: int = -1, real_strengths: bool = False, stream=None):
+                 nlevels: int = -1, real_strengths: bool = False, stream=None, parent_merge: bool = False):
         import torch
         if not (isinstance(z, torch.Tensor) and z.is_cuda):
             raise TypeError("loopback shards take a complex128 CUDA tensor")
@@ -352,7 +354,7 @@ class LoopbackShards:
         self.n = int(z.shape[0])
         self.device = device
         self.stream = stream
-        flags = REAL_STRENGTHS if real_strengths else 0
+        flags = (REAL_STRENGTHS if real_strengths else 0) | (PARENT_MERGE if parent_merge else 0)
         opt = _options(theta, p, leaf_target, nlevels, flags, device, stream.cuda_stream, nshards, 0)
         hs = (ctypes.c_void_p * nshards)()
         zp, _ = _ptr_of(z, False)

@@ -312,3 +312,30 @@ def test_near_split_long_lists(orc):
     phi_o, dphi_o = op.eval(m, 17)
     phi_g, dphi_g = _gpu_eval(_gpu_plan(z, 0.5, 17, L), m)
     assert _nerr(phi_g, phi_o) <= TOL and _nerr(dphi_g, dphi_o) <= TOL
+
+
+PM_CASES = [("C2", None, 0.5, 17), ("C3-100k", 100_000, 0.5, 17), ("C2-t.3-p8", None, 0.3, 8)]
+
+
+@pytest.mark.parametrize("name,n,theta,p", PM_CASES, ids=[c[0] for c in PM_CASES])
+def test_parent_merge_lists_and_eval_match_oracle(orc, name, n, theta, p):
+    """FMM2D_PARENT_MERGE (DESIGN R25): weak, strong and cross-level lists of
+    every level bit-exact, Phi and Phi' within 1e-12 of the oracle pass with the merge."""
+    from paper_1006_2269_b200 import Fmm2d
+    cfg = name.split("-")[0]
+    z, m = W.make_config(cfg, n=n)
+    L = orc.nlevels(len(z), 35)
+    op = orc.plan(z, theta, L, parent_merge=True)
+    gp = Fmm2d(torch.from_numpy(z).cuda(), theta=theta, p=p, nlevels=L, parent_merge=True)
+    nx = 0
+    for l in range(L + 1):
+        for kind in ("strong", "weak", "xweak"):
+            go, gi = gp.list(l, kind)
+            oo, oi = op.list(l, kind)
+            np.testing.assert_array_equal(go, oo, err_msg=f"{kind} {l}")
+            np.testing.assert_array_equal(gi, oi, err_msg=f"{kind} {l}")
+        nx += op.list(l, "xweak")[1].size
+    assert nx > 0
+    phi_o, dphi_o = op.eval(m, p)
+    phi_g, dphi_g = _gpu_eval(gp, m)
+    assert _nerr(phi_g, phi_o) <= TOL and _nerr(dphi_g, dphi_o) <= TOL

@@ -97,3 +97,19 @@ def test_shards_reject_unpartitionable():
         LoopbackShards(z, 3, nlevels=3)             # P = 3: no level with 3 | 4^k
     with pytest.raises(FmmError):
         LoopbackShards(z, 8, nlevels=2)             # k = 2 needs L > 2
+
+
+def test_loopback_shards_with_parent_merge(orc):
+    """Cross-level halo multipoles (parent merge) through the partition: bit-identical."""
+    from paper_1006_2269_b200 import Fmm2d, LoopbackShards
+    z_np, m_np = W.make_config("C2", n=60_000)
+    L = orc.nlevels(len(z_np), 35)
+    z, m = torch.from_numpy(z_np).cuda(), torch.from_numpy(m_np).cuda()
+    ref = Fmm2d(z, theta=0.5, p=17, nlevels=L, parent_merge=True)
+    a = ref.eval(m)
+    for P in (2, 8):
+        sh = LoopbackShards(z, P, theta=0.5, p=17, nlevels=L, parent_merge=True)
+        b = sh.eval(m)
+        torch.cuda.synchronize()
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+        sh.close()
