@@ -222,6 +222,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--rr-exchange", action="store_true", help="FMM2D_RR_EXCHANGE (P:370-377; one GPU)")
     ap.add_argument("--parent-merge", action="store_true", help="FMM2D_PARENT_MERGE (P:364-370)")
+    ap.add_argument("--symmetric-p2p", action="store_true", help="FMM2D_SYMMETRIC_P2P (one GPU)")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.config]
     if args.n:
@@ -257,6 +258,8 @@ def main():
         shard_kw["rr_exchange"] = True
     if args.parent_merge:
         shard_kw["parent_merge"] = True
+    if args.symmetric_p2p:
+        shard_kw["symmetric_p2p"] = True
     z = torch.from_numpy(z_np).to(dev)
     m = torch.from_numpy(m_np).to(dev)
     real = cfg.strengths == "real"
@@ -315,7 +318,8 @@ def main():
     near_ms = phase["near_ms"]
     achieved = pairs * P2P_FLOPS_PER_PAIR / (near_ms / 1e3) / 1e12
     traffic, traffic_src = k_near_traffic(cfg, args.config == "C5" and not args.n and world == 1
-                                          and not args.rr_exchange and not args.parent_merge)
+                                          and not args.rr_exchange and not args.parent_merge
+                                          and not args.symmetric_p2p)
     nleaf = 4 ** L if L else 1
     algo_bytes = 32.0 * cfg.n * 2 + 4.0 * cfg.n + 288.0 * nleaf        # rows in, Phi/Phi' out, perm, locals
     roof = {"bound": "alu", "kernel": "k_near (P2P+L2P)", "achieved": achieved, "peak": peak,

@@ -298,6 +298,9 @@ __global__ void k_seg_prep(const uint32_t* __restrict__ par_off, const uint32_t*
 // The tile's segments (from tile_seg, no search in global memory) and their table
 // (start, first high position, Gp, split rank) are staged in shared memory; each record
 // finds its segment by binary search there.
+#ifndef FMM2D_PARTITION_TWO_PASS
+#define FMM2D_PARTITION_TWO_PASS 0
+#endif
 constexpr int PT = 256, PI = 8, PTILE = PT * PI, PTILE_SHIFT = 11;
 static_assert(PTILE == (1 << PTILE_SHIFT), "tile size");
 constexpr int SEGMAX = 512;                          // larger tile spans: segment search in global memory
@@ -312,12 +315,16 @@ struct SplitArgs {
     const uint32_t* tile_seg;   // [tile] segment (relative to p0) of the tile's first position
     uint2* out;
     unsigned long long* tstate;
+    uint32_t* tile_cnt;         // two-pass mode: per tile high count (pass 1) / exclusive prefix (pass 2)
     uint32_t p0, p1;            // parent segments of the range
     uint32_t k0, k1;            // positions of the range (= par_off[p0], par_off[p1])
     uint32_t ntiles;
     int axis;                   // 0: compare rx, 1: compare ry
 };
 
+// MODE 0: one pass with the decoupled look-back; MODE 1: count pass (tile high counts);
+// MODE 2: scatter pass with the tiles' exclusive prefix (a CUB scan of the counts).
+template <int MODE>
 __global__ void __launch_bounds__(PT) k_partition(SplitArgs A)
 {
     typedef cub::BlockScan<uint32_t, PT> Scan;
@@ -404,8 +411,13 @@ __global__ void __launch_bounds__(PT) k_partition(SplitArgs A)
     }
     uint32_t excl, agg;
     Scan(scan_tmp).ExclusiveSum(cnt, excl, agg);
-    // decoupled look-back (warp 0)
-    if (tid < 32) {
+    if (MODE == 1) {
+        if (tid == 0) A.tile_cnt[tile] = agg;
+        return;
+    }
+    if (MODE == 2) {
+        if (tid == 0) s_prefix = A.tile_cnt[tile];
+    } else if (tid < 32) {       // decoupled look-back (warp 0)
         uint32_t prefix = 0;
         if (tile == 0) {
             if (tid == 0) atomicExch(&A.tstate[0], ST_PRE | agg);
@@ -751,7 +763,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
 
     // ---- scratch
     double2* zc;
-    uint32_t *k32a, *k32b, *u32a, *u32b, *hs, *Gp, *spl, *tseg;
+    uint32_t *k32a, *k32b, *u32a, *u32b, *hs, *Gp, *spl, *tseg, *tcnt, *tpre;
     uint64_t *vx, *vy, *v64a, *k64a, *k64b;
     uint2 *xl, *yl, *tmp;
     Bounds* bnd;
@@ -769,7 +781,8 @@ int build_tree(fmm2d_plan* P, const double2* z)
                                     (uint64_t*)nullptr, (int)n, 0, 64, st);
     cub::DeviceRadixSort::SortPairs(nullptr, sd, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                     (uint32_t*)nullptr, (int)n, 0, nbits, st);
-    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)npmax, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (int)std::max<int64_t>(npmax, ntiles), st);
     const size_t cub_bytes = std::max(std::max(s32, s64), std::max(sd, scan_bytes));
     std::vector<void*> tmp_ptrs;
     auto talloc = [&](void** p, size_t b) -> int {
@@ -796,6 +809,8 @@ int build_tree(fmm2d_plan* P, const double2* z)
         if ((rc = talloc((void**)&Gp, 4 * npmax))) break;
         if ((rc = talloc((void**)&spl, 4 * npmax))) break;
         if ((rc = talloc((void**)&tseg, 4 * (ntiles + 1)))) break;
+        if ((rc = talloc((void**)&tcnt, 4 * (ntiles + 1)))) break;
+        if ((rc = talloc((void**)&tpre, 4 * (ntiles + 1)))) break;
         if ((rc = talloc((void**)&tstate, 8 * ntiles))) break;
         if ((rc = talloc((void**)&xl, sizeof(uint2) * n))) break;
         if ((rc = talloc((void**)&yl, sizeof(uint2) * n))) break;
@@ -907,9 +922,21 @@ int build_tree(fmm2d_plan* P, const double2* z)
             A.k1 = k1;
             A.axis = axis;
             A.ntiles = (uint32_t)nt;
-            FMM2D_CUDA_TRY(cudaMemsetAsync(tstate, 0, 8 * nt, st));
-            k_partition<<<(unsigned)nt, PT, 0, st>>>(A);
+#if FMM2D_PARTITION_TWO_PASS
+            // count pass, scan of the tile counts, scatter pass (no look-back chain)
+            A.tile_cnt = tcnt;
+            k_partition<1><<<(unsigned)nt, PT, 0, st>>>(A);
             fmm2d::note_launch();
+            size_t b3 = cub_bytes;
+            FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, b3, tcnt, tpre, (int)nt, st));
+            A.tile_cnt = tpre;
+            k_partition<2><<<(unsigned)nt, PT, 0, st>>>(A);
+            fmm2d::note_launch();
+#else
+            FMM2D_CUDA_TRY(cudaMemsetAsync(tstate, 0, 8 * nt, st));
+            k_partition<0><<<(unsigned)nt, PT, 0, st>>>(A);
+            fmm2d::note_launch();
+#endif
             FMM2D_CUDA_TRY(cudaGetLastError());
             return 0;
         };
