@@ -355,24 +355,27 @@ inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / b
 // ---------------------------------------------------------------- r/R exchange (DESIGN R23)
 // P2L: the sources of the larger leaves in a leaf's P2L list go straight into
 // its local expansion: b_0 += m Log(c - z_j), b_l += -m / (l (z_j - c)^l) (c - z_j and
-// z_j - c each formed componentwise, R2).  One warp per leaf with P2L work: lanes over
-// the sources, coefficients in registers, fixed-order warp reduction, added to the local.
+// z_j - c each formed componentwise, R2).  One block of RR_T threads per leaf with P2L
+// work: warp w takes list entries w, w + RR_W, ...; lanes over each entry's sources;
+// coefficients in registers, a fixed-order shuffle reduction per warp, the warps'
+// partials summed in warp order in shared memory and added to the local.
+constexpr int RR_T = 128, RR_W = RR_T / 32;
+
 template <int P>
-__global__ void __launch_bounds__(128) k_rr_p2l(const uint32_t* __restrict__ leaves, int64_t nleaves,
-                                                const int64_t* __restrict__ off, const uint32_t* __restrict__ idx,
-                                                const uint32_t* __restrict__ boff, const double4* __restrict__ src,
-                                                const double* __restrict__ cx, const double* __restrict__ cy,
-                                                double2* __restrict__ loc)
+__global__ void __launch_bounds__(RR_T) k_rr_p2l(const uint32_t* __restrict__ leaves,
+                                                 const int64_t* __restrict__ off, const uint32_t* __restrict__ idx,
+                                                 const uint32_t* __restrict__ boff, const double4* __restrict__ src,
+                                                 const double* __restrict__ cx, const double* __restrict__ cy,
+                                                 double2* __restrict__ loc)
 {
-    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (w >= nleaves) return;
-    const uint32_t t = leaves[w];
+    __shared__ double2 part[RR_W][P + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t t = leaves[blockIdx.x];
     const double ctx = cx[t], cty = cy[t];
     double2 b[P + 1];
 #pragma unroll
     for (int l = 0; l <= P; ++l) b[l] = make_double2(0.0, 0.0);
-    for (int64_t q = off[t]; q < off[t + 1]; ++q) {
+    for (int64_t q = off[t] + warp; q < off[t + 1]; q += RR_W) {
         const uint32_t s = idx[q];
         for (uint32_t j = boff[s] + lane; j < boff[s + 1]; j += 32) {
             const double4 z = src[j];
@@ -399,44 +402,74 @@ __global__ void __launch_bounds__(128) k_rr_p2l(const uint32_t* __restrict__ lea
         }
     }
     if (lane == 0) {
-        double2* Lc = loc + (int64_t)t * (P + 1);
 #pragma unroll
-        for (int l = 0; l <= P; ++l) Lc[l] = cadd(Lc[l], b[l]);
+        for (int l = 0; l <= P; ++l) part[warp][l] = b[l];
+    }
+    __syncthreads();
+    if (threadIdx.x <= P) {
+        const int l = threadIdx.x;
+        double2 v = part[0][l];
+        for (int w = 1; w < RR_W; ++w) v = cadd(v, part[w][l]);
+        double2* Lc = loc + (int64_t)t * (P + 1);
+        Lc[l] = cadd(Lc[l], v);
     }
 }
 
 // M2P: the multipoles of the smaller leaves in a leaf's M2P list evaluated at
 // each of its points: a_0 Log(w) + sum_k a_k w^-k and a_0 / w - sum_k k a_k w^-(k+1),
-// w = z_i - c_s (componentwise), Horner in 1/w.  One block per leaf with M2P work; the
-// sums go to acc[i] (leaf order) and k_near adds them.
+// w = z_i - c_s (componentwise), Horner in 1/w.  One block per leaf with M2P work:
+// thread (point i, group g) takes list entries g, g + G, ...; the G partial sums of a
+// point are added in group order; the sums go to acc[i] (leaf order), k_near adds them.
 template <int P>
-__global__ void __launch_bounds__(128) k_rr_m2p(const uint32_t* __restrict__ leaves, const int64_t* __restrict__ off,
-                                                const uint32_t* __restrict__ idx, const uint32_t* __restrict__ boff,
-                                                const double4* __restrict__ src, const double* __restrict__ cx,
-                                                const double* __restrict__ cy, const double2* __restrict__ mp,
-                                                double4* __restrict__ acc)
+__global__ void __launch_bounds__(RR_T) k_rr_m2p(const uint32_t* __restrict__ leaves, const int64_t* __restrict__ off,
+                                                 const uint32_t* __restrict__ idx, const uint32_t* __restrict__ boff,
+                                                 const double4* __restrict__ src, const double* __restrict__ cx,
+                                                 const double* __restrict__ cy, const double2* __restrict__ mp,
+                                                 double4* __restrict__ acc)
 {
+    __shared__ double4 part[RR_T];
     const uint32_t t = leaves[blockIdx.x];
-    for (uint32_t i = boff[t] + threadIdx.x; i < boff[t + 1]; i += blockDim.x) {
-        const double4 z = src[i];
+    const uint32_t ts = boff[t];
+    const int nt = (int)(boff[t + 1] - ts);
+    const int per = min(nt, RR_T);                  // points per pass
+    const int G = RR_T / per;                       // list groups
+    const int ip = threadIdx.x % per, g = threadIdx.x / per;
+    for (int i0 = 0; i0 < nt; i0 += per) {
+        const int i = i0 + ip;
         double2 f = make_double2(0.0, 0.0), df = make_double2(0.0, 0.0);
-        for (int64_t q = off[t]; q < off[t + 1]; ++q) {
-            const uint32_t s = idx[q];
-            const double2* A = mp + (int64_t)s * (P + 1);
-            const double wx = z.x - cx[s], wy = z.y - cy[s];
-            const double iw2 = 1.0 / (wx * wx + wy * wy);
-            const double2 iw = make_double2(wx * iw2, -wy * iw2);
-            double2 h = A[P], dh = cscale(A[P], (double)P);
+        if (g < G && i < nt) {
+            const double4 z = src[ts + i];
+            for (int64_t q = off[t] + g; q < off[t + 1]; q += G) {
+                const uint32_t s = idx[q];
+                const double2* A = mp + (int64_t)s * (P + 1);
+                const double wx = z.x - cx[s], wy = z.y - cy[s];
+                const double iw2 = 1.0 / (wx * wx + wy * wy);
+                const double2 iw = make_double2(wx * iw2, -wy * iw2);
+                double2 h = A[P], dh = cscale(A[P], (double)P);
 #pragma unroll
-            for (int k = P - 1; k >= 1; --k) {
-                h = cadd(cmul(h, iw), A[k]);
-                dh = cadd(cmul(dh, iw), cscale(A[k], (double)k));
+                for (int k = P - 1; k >= 1; --k) {
+                    h = cadd(cmul(h, iw), A[k]);
+                    dh = cadd(cmul(dh, iw), cscale(A[k], (double)k));
+                }
+                const double2 lg = make_double2(0.5 * log(wx * wx + wy * wy), atan2(wy, wx));
+                f = cadd(f, cadd(cmul(A[0], lg), cmul(h, iw)));
+                df = cadd(df, csub(cmul(A[0], iw), cmul(dh, cmul(iw, iw))));
             }
-            const double2 lg = make_double2(0.5 * log(wx * wx + wy * wy), atan2(wy, wx));
-            f = cadd(f, cadd(cmul(A[0], lg), cmul(h, iw)));
-            df = cadd(df, csub(cmul(A[0], iw), cmul(dh, cmul(iw, iw))));
         }
-        acc[i] = make_double4(f.x, f.y, df.x, df.y);
+        __syncthreads();
+        part[threadIdx.x] = make_double4(f.x, f.y, df.x, df.y);
+        __syncthreads();
+        if (g == 0 && i < nt) {
+            double4 v = part[ip];
+            for (int gg = 1; gg < G; ++gg) {
+                const double4 u = part[gg * per + ip];
+                v.x += u.x;
+                v.y += u.y;
+                v.z += u.z;
+                v.w += u.w;
+            }
+            acc[ts + i] = v;
+        }
     }
 }
 
@@ -445,9 +478,9 @@ int rr_p2l_p(fmm2d_plan* Pl)
 {
     if (Pl->rr_np2l == 0) return 0;
     const int L = Pl->L;
-    k_rr_p2l<P><<<grid_for(Pl->rr_np2l * 32, 128), 128, 0, Pl->stream>>>(
-        Pl->rr_p2l_leaves, Pl->rr_np2l, Pl->rr_p2l.off, Pl->rr_p2l.idx, Pl->boff + Pl->obase[L], Pl->src,
-        Pl->cx + Pl->base[L], Pl->cy + Pl->base[L], Pl->local + Pl->base[L] * (P + 1));
+    k_rr_p2l<P><<<(unsigned)Pl->rr_np2l, RR_T, 0, Pl->stream>>>(
+        Pl->rr_p2l_leaves, Pl->rr_p2l.off, Pl->rr_p2l.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
+        Pl->cy + Pl->base[L], Pl->local + Pl->base[L] * (P + 1));
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     return 0;
@@ -458,7 +491,7 @@ int rr_m2p_p(fmm2d_plan* Pl)
 {
     if (Pl->rr_nm2p == 0) return 0;
     const int L = Pl->L;
-    k_rr_m2p<P><<<(unsigned)Pl->rr_nm2p, 128, 0, Pl->stream>>>(
+    k_rr_m2p<P><<<(unsigned)Pl->rr_nm2p, RR_T, 0, Pl->stream>>>(
         Pl->rr_m2p_leaves, Pl->rr_m2p.off, Pl->rr_m2p.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
         Pl->cy + Pl->base[L], Pl->mpole + Pl->base[L] * (P + 1), Pl->rr_acc);
     fmm2d::note_launch();

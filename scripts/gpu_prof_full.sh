@@ -10,6 +10,6 @@ CMD1="python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD1 > gpurun_out/ncu_launches.log 2>&1
 python tools/ncu_launch_summary.py gpurun_out/launches.csv > gpurun_out/launches_summary.txt 2>&1; head -12 gpurun_out/launches_summary.txt
 for K in k_near k_m2l k_partition k_tree_local k_finish; do
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -c 1 -o gpurun_out/prof_$K $CMD1 > gpurun_out/ncu_full_$K.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$K(<|\()" -c 1 -o gpurun_out/prof_$K $CMD1 > gpurun_out/ncu_full_$K.log 2>&1
 tail -1 gpurun_out/ncu_full_$K.log
 done
