@@ -538,7 +538,10 @@ int upward_top_p(fmm2d_plan* Pl)
 }
 
 template <int P>
-constexpr int m2l_split() { return P <= 20 ? 1 : (P <= 26 ? 2 : 3); }
+#ifndef FMM2D_M2L_SPLIT_P
+#define FMM2D_M2L_SPLIT_P 20      // p above this: the output coefficients over 2-3 threads
+#endif
+constexpr int m2l_split() { return P <= FMM2D_M2L_SPLIT_P ? 1 : (P <= 26 ? 2 : 3); }
 
 template <int P>
 int m2l_p(fmm2d_plan* Pl)

@@ -34,6 +34,14 @@ constexpr int NEAR_T = 128;
 #ifndef FMM2D_NEAR_SKIPBAR
 #define FMM2D_NEAR_SKIPBAR 1      // no barrier before the first chunk of a pass
 #endif
+#ifndef FMM2D_NEAR_TPT
+#define FMM2D_NEAR_TPT 2          // targets per thread (register blocking)
+#endif
+#ifndef FMM2D_NEAR_UNROLL
+#define FMM2D_NEAR_UNROLL 2       // source rows per unrolled iteration
+#endif
+constexpr int NEAR_TPT = FMM2D_NEAR_TPT;
+constexpr int NEAR_UNROLL = FMM2D_NEAR_UNROLL;
 #ifndef FMM2D_NEAR_LOG5
 #define FMM2D_NEAR_LOG5 1         // degree-5 log1p (absolute error < 2^-52: tests/test_fastmath.py)
 #endif
@@ -146,7 +154,7 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                                                  double2* __restrict__ phi, double2* __restrict__ dphi,
                                                  const int64_t* __restrict__ m2p_off, const double4* __restrict__ m2p_acc)
 {
-    __shared__ double4 S[NEAR_CHUNK];
+    __shared__ double4 S[(NEAR_CHUNK > NEAR_TPT * NEAR_T) ? NEAR_CHUNK : NEAR_TPT * NEAR_T];
     __shared__ fm::Tables T;
     double4(*red)[NEAR_T] = reinterpret_cast<double4(*)[NEAR_T]>(S);   // after the last chunk
     __shared__ int cstart[33];
@@ -168,16 +176,20 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
     load_tables(T, gtab);                    // (the first chunk's barriers cover it)
     const uint32_t ts = off[t], te = off[t + 1];
     const int nt = (int)(te - ts);
-    const int tile = NEAR_T / G;                 // target pairs per pass
-    for (int i0 = 0; i0 < nt; i0 += 2 * tile) {
+    const int tile = NEAR_T / G;                 // target tuples per pass
+    for (int i0 = 0; i0 < nt; i0 += NEAR_TPT * tile) {
         const int tp = tid % tile;
         const int g = tid / tile;
-        const int ni = min(2 * tile, nt - i0);   // targets in this pass
-        const bool active = (g < G) && (2 * tp < ni);
-        const int la = min(2 * tp, ni - 1), lb = min(2 * tp + 1, ni - 1);
-        const double4 A = src[ts + i0 + la];
-        const double4 B = src[ts + i0 + lb];
-        PairAcc aa, ab;
+        const int ni = min(NEAR_TPT * tile, nt - i0);   // targets in this pass
+        const bool active = (g < G) && (NEAR_TPT * tp < ni);
+        int la[NEAR_TPT];
+        double4 A[NEAR_TPT];
+        PairAcc acc[NEAR_TPT];
+#pragma unroll
+        for (int u = 0; u < NEAR_TPT; ++u) {
+            la[u] = min(NEAR_TPT * tp + u, ni - 1);
+            A[u] = src[ts + i0 + la[u]];
+        }
         for (int64_t q = q0; q < q1;) {
             if (q != q0 || !FMM2D_NEAR_SKIPBAR) __syncthreads();   // previous chunk consumed
             if (warp == 0) {
@@ -219,36 +231,38 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
             const int kend = min(total, kown + nt);
             if (active) {
                 // rows before the own leaf, then after it: no self pair possible
-#pragma unroll 2
+#pragma unroll NEAR_UNROLL
                 for (int k = g; k < kown; k += G) {
                     const double4 s = S[k];
-                    pair<REAL>(aa, A.x - s.x, A.y - s.y, s.z, s.w, T);
-                    pair<REAL>(ab, B.x - s.x, B.y - s.y, s.z, s.w, T);
+#pragma unroll
+                    for (int u = 0; u < NEAR_TPT; ++u) pair<REAL>(acc[u], A[u].x - s.x, A[u].y - s.y, s.z, s.w, T);
                 }
-#pragma unroll 2
+#pragma unroll NEAR_UNROLL
                 for (int k = first_in_class(kend, g, G); k < total; k += G) {
                     const double4 s = S[k];
-                    pair<REAL>(aa, A.x - s.x, A.y - s.y, s.z, s.w, T);
-                    pair<REAL>(ab, B.x - s.x, B.y - s.y, s.z, s.w, T);
+#pragma unroll
+                    for (int u = 0; u < NEAR_TPT; ++u) pair<REAL>(acc[u], A[u].x - s.x, A[u].y - s.y, s.z, s.w, T);
                 }
                 // own leaf: neutralise j == i
-                const int sa = kown + i0 + la, sb = kown + i0 + lb;
                 for (int k = first_in_class(kown, g, G); k < kend; k += G) {
                     const double4 s = S[k];
-                    const bool xa = (k == sa), xb = (k == sb);
-                    pair<REAL>(aa, xa ? 1.0 : A.x - s.x, xa ? 0.0 : A.y - s.y, xa ? 0.0 : s.z, xa ? 0.0 : s.w, T);
-                    pair<REAL>(ab, xb ? 1.0 : B.x - s.x, xb ? 0.0 : B.y - s.y, xb ? 0.0 : s.z, xb ? 0.0 : s.w, T);
+#pragma unroll
+                    for (int u = 0; u < NEAR_TPT; ++u) {
+                        const bool x = (k == kown + i0 + la[u]);
+                        pair<REAL>(acc[u], x ? 1.0 : A[u].x - s.x, x ? 0.0 : A[u].y - s.y, x ? 0.0 : s.z,
+                                   x ? 0.0 : s.w, T);
+                    }
                 }
             }
             q += nl;
         }
         __syncthreads();                          // chunk buffer free: reuse it for partial sums
-        red[0][tid] = pack(aa);
-        red[1][tid] = pack(ab);
+#pragma unroll
+        for (int u = 0; u < NEAR_TPT; ++u) red[u][tid] = pack(acc[u]);
         __syncthreads();
-        // finalize: 2*tile targets, thread k < ni handles target k (pair tp = k/2, slot k&1)
+        // finalize: NEAR_TPT*tile targets, thread k < ni handles target k (tuple k/TPT, slot k%TPT)
         for (int kk = tid; kk < ni; kk += NEAR_T) {
-            const int ptp = kk >> 1, slot = kk & 1;
+            const int ptp = kk / NEAR_TPT, slot = kk % NEAR_TPT;
             double4 acc = red[slot][ptp];
             for (int gg = 1; gg < G; ++gg) {
                 const double4 v = red[slot][gg * tile + ptp];
@@ -768,8 +782,8 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi)
         return 0;
     }
     if (P->stats.max_leaf <= NEAR_CHUNK) {
-        // target pairs per leaf, groups so that pairs * G <= 128
-        const int pairs = (std::max(1, P->stats.max_leaf) + 1) / 2;
+        // target tuples per leaf, groups so that tuples * G <= 128
+        const int pairs = (std::max(1, P->stats.max_leaf) + NEAR_TPT - 1) / NEAR_TPT;
         int G = NEAR_T / std::min(pairs, NEAR_T);
         if (G < 1) G = 1;
         const unsigned grid = (unsigned)(nl + P->near_nseg);
