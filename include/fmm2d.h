@@ -73,6 +73,11 @@ extern "C" {
                                       all four children of a box q interacts with q itself
                                       (cross-level M2L from level l-1) when Criterion 1
                                       holds for the pair (R25)                 */
+#define FMM2D_OVERLAP         0x80  /* evaluate the expansion chain (high-priority side stream)
+                                      concurrently with the P2P sums, then L2P + output; same
+                                      results bit for bit.  Measured slower on B200 (the
+                                      kernels' register footprints do not co-reside; DESIGN
+                                      6.4), so off by default                            */
 #define FMM2D_TREE_GLOBAL_ONLY 0x10 /* diagnostic: every split step in global memory (no
                                       on-chip finish of the deepest levels; same tree)  */
 
@@ -118,7 +123,8 @@ FMM2D_API int fmm2d_eval(fmm2d_plan* plan, const double* m, double* phi, double*
 
 /* fmm2d_eval, then synchronise and report the device time of each phase in
  * ms_out[0..7] (CUDA events on the plan's stream): 0 strength gather, 1 P2M+M2M,
- * 2 M2L (all levels), 3 L2L, 4 L2P+P2P+output, 5 total, 6..7 reserved.
+ * 2 M2L (all levels), 3 L2L (+ P2L), 4 L2P+P2P+output, 5 total, 6..7 reserved.
+ * The phases are run one after the other here (no overlap), so that each is timed alone.
  * Same arguments and errors as fmm2d_eval; ms_out may not be NULL. */
 FMM2D_API int fmm2d_eval_timed(fmm2d_plan* plan, const double* m, double* phi, double* dphi,
                                double* ms_out);

@@ -86,8 +86,12 @@ void fmm2d_free(fmm2d_plan* P)
 {
     if (!P) return;
     cudaSetDevice(P->device);
+    if (P->side) cudaStreamSynchronize(P->side);
     for (void* p : P->allocs) cudaFreeAsync(p, P->stream);
     cudaStreamSynchronize(P->stream);
+    if (P->side) cudaStreamDestroy(P->side);
+    if (P->ev_gather) cudaEventDestroy(P->ev_gather);
+    if (P->ev_exp) cudaEventDestroy(P->ev_exp);
     shard_free(P);
     delete P;
 }
@@ -122,7 +126,7 @@ static int plan_depth(int64_t n, const fmm2d_options* opt)
 // Stage 1 of a build: plan fields, partition, allocations, the tree (A0-A2).  For one
 // GPU it also runs the lists (A3).  Sharded plans continue in shard_build_rest.
 static int build_stage_tree(const double* z, int64_t n, const fmm2d_options* opt, int nranks, int rank,
-                            const void* nccl_id, fmm2d_plan** out)
+                            const void* nccl_id, fmm2d_plan** out, bool loopback = false)
 {
     *out = nullptr;
     const int L = plan_depth(n, opt);
@@ -190,6 +194,17 @@ static int build_stage_tree(const double* z, int64_t n, const fmm2d_options* opt
             FMM2D_TRY(build_lists(P));
             FMM2D_TRY(prepare_near_sym(P));
         }
+        // overlapped evaluation (DESIGN 6.4): not for loopback shards (one shared stream)
+        if ((P->flags & FMM2D_OVERLAP) && !loopback && P->L >= 1 && !P->sym &&
+            P->stats.max_leaf <= FMM2D_NEAR_CHUNK) {
+            int lo = 0, hi = 0;
+            FMM2D_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            FMM2D_CUDA_TRY(cudaStreamCreateWithPriority(&P->side, cudaStreamNonBlocking, hi));
+            FMM2D_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_gather, cudaEventDisableTiming));
+            FMM2D_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_exp, cudaEventDisableTiming));
+            FMM2D_TRY(dev_alloc(P, (void**)&P->nacc, sizeof(double4) * n));
+            P->overlap = true;
+        }
         FMM2D_CUDA_TRY(cudaEventRecord(e2, P->stream));
         FMM2D_CUDA_TRY(cudaEventSynchronize(e2));
         float a = 0, b = 0;
@@ -239,7 +254,7 @@ int fmm2d_build_shards(const double* z, int64_t n, const fmm2d_options* opt, int
     if (opt->flags & FMM2D_HOST_PTRS) return FMM2D_ENOTSUP;
     for (int i = 0; i < nshards; ++i) out[i] = nullptr;
     int rc = 0;
-    for (int i = 0; i < nshards && !rc; ++i) rc = build_stage_tree(z, n, opt, nshards, i, nullptr, &out[i]);
+    for (int i = 0; i < nshards && !rc; ++i) rc = build_stage_tree(z, n, opt, nshards, i, nullptr, &out[i], true);
     if (!rc && nshards > 1) rc = shard_build_rest(out, nshards);
     if (rc) {
         for (int i = 0; i < nshards; ++i) {
@@ -283,24 +298,45 @@ static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi
         if (sharded) FMM2D_TRY(shard_gather_halo(Ps[i], md));
     }
     if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[1], P0->stream));
-    for (int i = 0; i < np; ++i) FMM2D_TRY(run_upward(Ps[i]));
-    if (sharded) {
-        FMM2D_TRY(shard_comm_top(Ps, np));
-        for (int i = 0; i < np; ++i) {
-            FMM2D_TRY(run_upward_top(Ps[i]));
-            FMM2D_TRY(shard_pack_mp(Ps[i]));
+    // the expansion chain: P2M, M2M (+ halo exchange), M2L, L2L, P2L, M2P
+    auto expansions = [&]() -> int {
+        for (int i = 0; i < np; ++i) FMM2D_TRY(run_upward(Ps[i]));
+        if (sharded) {
+            FMM2D_TRY(shard_comm_top(Ps, np));
+            for (int i = 0; i < np; ++i) {
+                FMM2D_TRY(run_upward_top(Ps[i]));
+                FMM2D_TRY(shard_pack_mp(Ps[i]));
+            }
+            FMM2D_TRY(shard_comm_mp(Ps, np));
+            for (int i = 0; i < np; ++i) FMM2D_TRY(shard_unpack_mp(Ps[i]));
         }
-        FMM2D_TRY(shard_comm_mp(Ps, np));
-        for (int i = 0; i < np; ++i) FMM2D_TRY(shard_unpack_mp(Ps[i]));
+        if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[2], P0->stream));
+        for (int i = 0; i < np; ++i) FMM2D_TRY(run_m2l(Ps[i]));
+        if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[3], P0->stream));
+        for (int i = 0; i < np; ++i) FMM2D_TRY(run_downward(Ps[i]));
+        for (int i = 0; i < np; ++i) FMM2D_TRY(run_rr_p2l(Ps[i]));      // r/R exchange: into the locals
+        if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[4], P0->stream));
+        for (int i = 0; i < np; ++i) FMM2D_TRY(run_rr_m2p(Ps[i]));      // r/R exchange: M2P sums
+        return 0;
+    };
+    if (np == 1 && P0->overlap && !ev) {
+        // overlapped (DESIGN 6.4): the expansion chain on the high-priority side stream, the
+        // P2P sums on the plan's stream at the same time, then L2P + output (k_near_final)
+        cudaStream_t user = P0->stream;
+        FMM2D_CUDA_TRY(cudaEventRecord(P0->ev_gather, user));
+        FMM2D_CUDA_TRY(cudaStreamWaitEvent(P0->side, P0->ev_gather, 0));
+        P0->stream = P0->side;
+        const int rc = expansions();
+        P0->stream = user;
+        FMM2D_TRY(rc);
+        FMM2D_CUDA_TRY(cudaEventRecord(P0->ev_exp, P0->side));
+        FMM2D_TRY(run_near(P0, phid, dphid, 1));
+        FMM2D_CUDA_TRY(cudaStreamWaitEvent(user, P0->ev_exp, 0));
+        FMM2D_TRY(run_near(P0, phid, dphid, 2));
+    } else {
+        FMM2D_TRY(expansions());
+        for (int i = 0; i < np; ++i) FMM2D_TRY(run_near(Ps[i], phid, dphid, 0));
     }
-    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[2], P0->stream));
-    for (int i = 0; i < np; ++i) FMM2D_TRY(run_m2l(Ps[i]));
-    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[3], P0->stream));
-    for (int i = 0; i < np; ++i) FMM2D_TRY(run_downward(Ps[i]));
-    for (int i = 0; i < np; ++i) FMM2D_TRY(run_rr_p2l(Ps[i]));      // r/R exchange: into the locals
-    if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[4], P0->stream));
-    for (int i = 0; i < np; ++i) FMM2D_TRY(run_rr_m2p(Ps[i]));      // r/R exchange: M2P sums
-    for (int i = 0; i < np; ++i) FMM2D_TRY(run_near(Ps[i], phid, dphid));
     if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[5], P0->stream));
     if (host) {
         if (phi) FMM2D_CUDA_TRY(cudaMemcpyAsync(phi, phid, sizeof(double2) * n, cudaMemcpyDeviceToHost, P0->stream));

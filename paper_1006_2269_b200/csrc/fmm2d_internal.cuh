@@ -107,6 +107,12 @@ struct fmm2d_plan {
     double2* phistage = nullptr;
     double2* dphistage = nullptr;
     const void* tables = nullptr;       // fastmath tables (device, shared per device)
+    // overlapped eval: the expansion chain on a high-priority side stream while k_near's
+    // P2P runs on the plan's stream; k_near_final joins them
+    bool overlap = false;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_gather = nullptr, ev_exp = nullptr;
+    double4* nacc = nullptr;            // [n] P2P sums (leaf order)
     // symmetric near field (near.cu): each unordered leaf pair evaluated once
     bool sym = false;
     int sym_tile = 0, sym_npass = 0, sym_rows = 0, slot_w = 0;
@@ -132,7 +138,7 @@ int build_lists(fmm2d_plan* P);
 int run_upward(fmm2d_plan* P);
 int run_m2l(fmm2d_plan* P);
 int run_downward(fmm2d_plan* P);
-int run_near(fmm2d_plan* P, double2* phi, double2* dphi);
+int run_near(fmm2d_plan* P, double2* phi, double2* dphi, int mode);
 int prepare_near(fmm2d_plan* P);
 int prepare_near_sym(fmm2d_plan* P);
 int gather_strengths(fmm2d_plan* P, const double2* m);

@@ -152,7 +152,8 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                                                  const double* __restrict__ cy, const double2* __restrict__ loc,
                                                  const uint32_t* __restrict__ perm, const fm::Tables* __restrict__ gtab,
                                                  double2* __restrict__ phi, double2* __restrict__ dphi,
-                                                 const int64_t* __restrict__ m2p_off, const double4* __restrict__ m2p_acc)
+                                                 const int64_t* __restrict__ m2p_off, const double4* __restrict__ m2p_acc,
+                                                 double4* __restrict__ nacc)
 {
     __shared__ double4 S[(NEAR_CHUNK > NEAR_TPT * NEAR_T) ? NEAR_CHUNK : NEAR_TPT * NEAR_T];
     __shared__ fm::Tables T;
@@ -275,6 +276,10 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                 part[segi * part_w + i0 + kk] = acc;
                 continue;
             }
+            if (nacc) {                           // overlapped eval: P2P sums only (k_near_final adds L2P)
+                nacc[ts + i0 + kk] = acc;
+                continue;
+            }
             double4 f;                            // L2P (Horner) of the target
             {
                 const double4 me = src[ts + i0 + kk];
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(NEAR_T) k_near_combine(const uint32_t* __restr
                                                          const double* __restrict__ cy, const double2* __restrict__ loc,
                                                          const uint32_t* __restrict__ perm, double2* __restrict__ phi,
                                                          double2* __restrict__ dphi, const int64_t* __restrict__ m2p_off,
-                                                         const double4* __restrict__ m2p_acc)
+                                                         const double4* __restrict__ m2p_acc, double4* __restrict__ nacc)
 {
     const uint32_t t = leaves[blockIdx.x];
     const uint32_t ts = off[t], te = off[t + 1];
@@ -316,10 +321,48 @@ __global__ void __launch_bounds__(NEAR_T) k_near_combine(const uint32_t* __restr
             acc.z += v.z;
             acc.w += v.w;
         }
+        if (nacc) {                               // overlapped eval: P2P sums only
+            nacc[i] = acc;
+            continue;
+        }
         const double4 me = src[i];
         double4 f;
         l2p(loc + (int64_t)t * (p + 1), p, me.x - cx[t], me.y - cy[t], f.x, f.y, f.z, f.w);
         if (m2p_off && m2p_off[t + 1] > m2p_off[t]) {
+            const double4 g = m2p_acc[i];
+            f.x += g.x;
+            f.y += g.y;
+            f.z += g.z;
+            f.w += g.w;
+        }
+        const uint32_t o = perm[i];
+        if (phi) phi[o] = make_double2(acc.x + f.x, acc.y + f.y);
+        if (dphi) dphi[o] = make_double2(acc.z + f.z, acc.w + f.w);
+    }
+}
+
+// Overlapped evaluation (DESIGN 6.4): the P2P sums nacc (leaf order) + L2P + M2P, written
+// at the input positions.  One warp per target leaf, lanes over its points.
+__global__ void __launch_bounds__(NEAR_T) k_near_final(int64_t t0, int64_t nl, int p, const uint32_t* __restrict__ off,
+                                                       const double4* __restrict__ nacc, const double4* __restrict__ src,
+                                                       const double* __restrict__ cx, const double* __restrict__ cy,
+                                                       const double2* __restrict__ loc, const uint32_t* __restrict__ perm,
+                                                       double2* __restrict__ phi, double2* __restrict__ dphi,
+                                                       const int64_t* __restrict__ m2p_off,
+                                                       const double4* __restrict__ m2p_acc)
+{
+    const int64_t w = ((int64_t)blockIdx.x * NEAR_T + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nl) return;
+    const int64_t t = t0 + w;
+    const uint32_t ts = off[t], te = off[t + 1];
+    const bool m2p = m2p_off && m2p_off[t + 1] > m2p_off[t];
+    for (uint32_t i = ts + lane; i < te; i += 32) {
+        const double4 acc = nacc[i];
+        const double4 me = src[i];
+        double4 f;
+        l2p(loc + t * (p + 1), p, me.x - cx[t], me.y - cy[t], f.x, f.y, f.z, f.w);
+        if (m2p) {
             const double4 g = m2p_acc[i];
             f.x += g.x;
             f.y += g.y;
@@ -738,7 +781,9 @@ int prepare_near_sym(fmm2d_plan* P)
     return 0;
 }
 
-int run_near(fmm2d_plan* P, double2* phi, double2* dphi)
+// mode 0: the whole near field (P2P + L2P + M2P, outputs); mode 1: P2P sums only into
+// P->nacc (overlapped eval, before the expansions are done); mode 2: k_near_final.
+int run_near(fmm2d_plan* P, double2* phi, double2* dphi, int mode)
 {
     const int L = P->L;
     const int64_t t0 = P->box_lo(L), nl = P->box_hi(L) - t0;    // own target leaves
@@ -749,6 +794,14 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi)
     const bool real = (P->flags & FMM2D_REAL_STRENGTHS) != 0;
     const fm::Tables* tab = (const fm::Tables*)P->tables;
     const int64_t* m2p_off = (P->rr_nm2p > 0) ? P->rr_m2p.off : nullptr;     // r/R exchange
+    double4* nacc = (mode == 1) ? P->nacc : nullptr;
+    if (mode == 2) {
+        k_near_final<<<grid_for(nl * 32, NEAR_T), NEAR_T, 0, P->stream>>>(t0, nl, P->p, off, P->nacc, P->src, cx, cy,
+                                                                        loc, P->perm, phi, dphi, m2p_off, P->rr_acc);
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+        return 0;
+    }
     if (P->sym) {
         SymArgs A;
         A.off = off;
@@ -791,18 +844,18 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi)
             k_near<true><<<grid, NEAR_T, 0, P->stream>>>(G, P->p, t0, nl, P->near_seg_off, P->near_segs,
                                                         P->near_part, P->stats.max_leaf, off, P->near.off,
                                                         P->near.idx, P->src, cx, cy, loc, P->perm, tab, phi, dphi,
-                                                        m2p_off, P->rr_acc);
+                                                        m2p_off, P->rr_acc, nacc);
         else
             k_near<false><<<grid, NEAR_T, 0, P->stream>>>(G, P->p, t0, nl, P->near_seg_off, P->near_segs,
                                                          P->near_part, P->stats.max_leaf, off, P->near.off,
                                                          P->near.idx, P->src, cx, cy, loc, P->perm, tab, phi, dphi,
-                                                         m2p_off, P->rr_acc);
+                                                         m2p_off, P->rr_acc, nacc);
         if (P->near_nsplit > 0) {
             fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
             k_near_combine<<<(unsigned)P->near_nsplit, NEAR_T, 0, P->stream>>>(
                 P->near_split, P->near_seg_off, P->near_part, P->stats.max_leaf, P->p, off, P->src, cx, cy, loc,
-                P->perm, phi, dphi, m2p_off, P->rr_acc);
+                P->perm, phi, dphi, m2p_off, P->rr_acc, nacc);
         }
     } else {
         if (real)

@@ -339,3 +339,20 @@ def test_parent_merge_lists_and_eval_match_oracle(orc, name, n, theta, p):
     phi_o, dphi_o = op.eval(m, p)
     phi_g, dphi_g = _gpu_eval(gp, m)
     assert _nerr(phi_g, phi_o) <= TOL and _nerr(dphi_g, dphi_o) <= TOL
+
+
+@pytest.mark.parametrize("cfg,n,rr", [("C2", None, False), ("C3", 100_000, True), ("C3", 200_000, False)])
+def test_overlapped_eval_bit_identical(cfg, n, rr):
+    """FMM2D_OVERLAP runs the expansion chain on a side stream concurrently with the P2P
+    sums (DESIGN 6.4); the default runs them one after the other.  Same summation order:
+    bit-identical results (also with r/R exchange and split near lists)."""
+    from paper_1006_2269_b200 import Fmm2d
+    z, m = W.make_config(cfg, n=n)
+    zt, mt = torch.from_numpy(z).cuda(), torch.from_numpy(m).cuda()
+    out = []
+    for ov in (True, False):
+        plan = Fmm2d(zt, theta=0.5, p=17, leaf_target=35, overlap=ov, rr_exchange=rr)
+        phi, dphi = plan.eval(mt)
+        torch.cuda.synchronize()
+        out.append((phi, dphi))
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
