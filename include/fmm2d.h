@@ -78,6 +78,10 @@ extern "C" {
                                       results bit for bit.  Measured slower on B200 (the
                                       kernels' register footprints do not co-reside; DESIGN
                                       6.4), so off by default                            */
+#define FMM2D_GATHER_OUTPUT  0x100  /* multi-rank (NCCL) plans: every rank receives ALL entries
+                                      of Phi and Phi' (a sum all-reduce over the outputs,
+                                      each rank contributing its own sources; 2 x 16 n
+                                      bytes per evaluation).  One GPU / loopback: no effect */
 #define FMM2D_TREE_GLOBAL_ONLY 0x10 /* diagnostic: every split step in global memory (no
                                       on-chip finish of the deepest levels; same tree)  */
 
@@ -142,7 +146,8 @@ FMM2D_API int64_t fmm2d_launch_count(void);
  * the 128-byte ncclUniqueId made by fmm2d_nccl_unique_id on one rank and broadcast
  * (e.g. torch.distributed).  fmm2d_build is then collective (all ranks must call it),
  * and so is every fmm2d_eval: each rank passes the same full m and receives Phi, Phi'
- * at the input positions of the sources it owns (other entries are not written).
+ * at the input positions of the sources it owns (other entries are not written, unless
+ * FMM2D_GATHER_OUTPUT is set: then every rank receives all entries).
  * The library creates one NCCL communicator per distinct id and keeps it for the
  * life of the process; later builds with the same id (same nranks, same rank) reuse it.
  * The union over ranks equals the one-GPU result.  Errors: ENOTSUP (P not a power of

@@ -292,6 +292,11 @@ static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi
         phid = phi ? P0->phistage : nullptr;
         dphid = dphi ? P0->dphistage : nullptr;
     }
+    const bool gather_out = sharded && np == 1 && (P0->flags & FMM2D_GATHER_OUTPUT) && shard_has_comm(P0);
+    if (gather_out) {                                  // own entries written below, the rest summed in
+        if (phid) FMM2D_CUDA_TRY(cudaMemsetAsync(phid, 0, sizeof(double2) * n, P0->stream));
+        if (dphid) FMM2D_CUDA_TRY(cudaMemsetAsync(dphid, 0, sizeof(double2) * n, P0->stream));
+    }
     if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[0], P0->stream));
     for (int i = 0; i < np; ++i) {
         FMM2D_TRY(gather_strengths(Ps[i], md));
@@ -337,6 +342,7 @@ static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi
         FMM2D_TRY(expansions());
         for (int i = 0; i < np; ++i) FMM2D_TRY(run_near(Ps[i], phid, dphid, 0));
     }
+    if (gather_out) FMM2D_TRY(shard_gather_output(P0, phid, dphid));
     if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[5], P0->stream));
     if (host) {
         if (phi) FMM2D_CUDA_TRY(cudaMemcpyAsync(phi, phid, sizeof(double2) * n, cudaMemcpyDeviceToHost, P0->stream));

@@ -659,6 +659,21 @@ int shard_unpack_mp(fmm2d_plan* P)
 
 bool shard_has_comm(const fmm2d_plan* P) { return P->shard && P->shard->comm; }
 
+// FMM2D_GATHER_OUTPUT: every rank wrote its own sources' entries into zeroed outputs;
+// a sum all-reduce completes them on every rank (x + 0 = x exactly).  Loopback shards
+// already share one output array: nothing to do.
+int shard_gather_output(fmm2d_plan* P, double2* phi, double2* dphi)
+{
+    if (!shard_has_comm(P)) return 0;
+    NcclApi* A = nccl_api();
+    ncclComm_t c = (ncclComm_t)P->shard->comm;
+    FMM2D_NCCL_TRY(A->GroupStart());
+    if (phi) FMM2D_NCCL_TRY(A->AllReduce(phi, phi, 2 * (size_t)P->n, ncclDouble, ncclSum, c, P->stream));
+    if (dphi) FMM2D_NCCL_TRY(A->AllReduce(dphi, dphi, 2 * (size_t)P->n, ncclDouble, ncclSum, c, P->stream));
+    FMM2D_NCCL_TRY(A->GroupEnd());
+    return 0;
+}
+
 void shard_halo_sizes(const fmm2d_plan* P, int64_t* leaves, int64_t* mpoles, int64_t* exp_leaves, int64_t* exp_mp)
 {
     *leaves = P->shard ? P->shard->leaf.imp_tot : 0;
