@@ -25,6 +25,10 @@ Parity status of each oracle function (what pins it, see tests/test_oracle_*.py)
   parent merge  pinned (O8): list audit (each cross pair replaces exactly four
                 weak children and is itself well separated), exactly-once pair coverage,
                 the pass against the direct sum within the gate, fewer M2L pairs
+  midpoint tree pinned (O9, Fig. 2/4 baseline): equals the median tree on an aligned lattice
+                (both are the uniform quadtree), containment of every point in its
+                geometric cell, box counts = brute-force cell counts, exactly-once
+                coverage with empty boxes, the pass against the direct sum
   rr exchange   pinned (O7): predicate worked examples + the exchanged
                 geometric meaning, P2L closed form and P2L = M2L o P2M identity, M2P of a
                 single charge, conversion-list audit (exchanged holds, original fails,
@@ -153,7 +157,8 @@ class Plan:
     """Oracle tree + discs + lists for fixed (z, theta, L); ``eval(m, p)`` runs the
     evaluation pass.  Arrays are returned as numpy copies."""
 
-    def __init__(self, z, theta: float, L: int, rr_exchange: bool = False, parent_merge: bool = False):
+    def __init__(self, z, theta: float, L: int, rr_exchange: bool = False, parent_merge: bool = False,
+                 midpoint: bool = False):
         z = _c128(z)
         self.n = int(z.shape[0])
         self.theta = float(theta)
@@ -162,7 +167,8 @@ class Plan:
         self.parent_merge = bool(parent_merge)
         h = ctypes.c_void_p()
         rc = lib().oracle_build_ex(_dp(_as_f64(z)), self.n, self.theta, self.L,
-                                   (1 if rr_exchange else 0) | (2 if parent_merge else 0), ctypes.byref(h))
+                                   (1 if rr_exchange else 0) | (2 if parent_merge else 0) | (4 if midpoint else 0),
+                                   ctypes.byref(h))
         if rc:
             raise ValueError(f"oracle_build: {rc}")
         self._h = h
@@ -219,8 +225,9 @@ class Plan:
         return out
 
 
-def plan(z, theta: float, L: int, rr_exchange: bool = False, parent_merge: bool = False) -> Plan:
-    return Plan(z, theta, L, rr_exchange, parent_merge)
+def plan(z, theta: float, L: int, rr_exchange: bool = False, parent_merge: bool = False,
+         midpoint: bool = False) -> Plan:
+    return Plan(z, theta, L, rr_exchange, parent_merge, midpoint)
 
 
 def rr_exchange(cb, rb, cc, rc, theta) -> bool:

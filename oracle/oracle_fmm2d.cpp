@@ -19,6 +19,8 @@
  *   O6 branch conventions    DESIGN R2
  *   O7 r/R exchange          P:370-377 (optional; leaf level: P2L + M2P instead of P2P)
  *   O8 parent merge          P:364-370 (optional; cross-level M2L from a parent box)
+ *   O9 midpoint tree         Fig. 2, Fig. 4 baseline: geometric
+ *                            midpoint splits of the bounding square, empty boxes allowed
  * Floating point: compiled with -O2 -ffp-contract=off (no FMA contraction), no
  * fast-math; sqrt is IEEE correctly rounded.  OpenMP is used only across
  * independent boxes / targets, each of which is summed in a fixed order, so
@@ -137,6 +139,8 @@ struct oracle_plan {
      * separated from b; those children are then not in weak[l][b]. */
     int pm;
     std::vector<std::vector<std::vector<uint32_t>>> xweak;
+    /* O9: midpoint split policy (empty boxes possible: disc r = -1, centre 0) */
+    int midpoint;
     /* expansions from the last oracle_eval (diagnostics) */
     int p;
     std::vector<std::vector<cplx>> mpole, local;     /* per level: 4^l * (p+1)        */
@@ -204,6 +208,50 @@ static void build_tree(oracle_plan* P)
         std::sort(P->perm.data() + oL[b], P->perm.data() + oL[b + 1], byy);
 }
 
+/* O9: "standard midpoint adaptivity" (Fig. 2) as the uniform baseline of
+ * Fig. 4 ("a square and uniformly subdivided multipole mesh").  DESIGN R26:
+ * the root is the bounding square [x0, x0 + s) x [y0, y0 + s), s = max(x range, y range)
+ * (s = 1 if all points coincide); every box is split at its geometric midpoints, x then y,
+ * children 4b + 2 xside + yside as in O2, down to the same depth L.  A point's leaf is
+ * (ix, iy) = (floor((x - x0) * S), floor((y - y0) * S)) clamped to 2^L - 1, with
+ * S = 2^L / s (one correctly rounded division), interleaved x-high-first.  Inside a leaf
+ * the points keep ascending input index (the stable order).  Empty boxes are allowed. */
+static void build_tree_midpoint(oracle_plan* P)
+{
+    const int64_t n = P->n;
+    const int L = P->L;
+    double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+    for (int64_t i = 0; i < n; ++i) {
+        x0 = std::min(x0, P->x[i]); x1 = std::max(x1, P->x[i]);
+        y0 = std::min(y0, P->y[i]); y1 = std::max(y1, P->y[i]);
+    }
+    double side = std::max(x1 - x0, y1 - y0);
+    if (!(side > 0.0)) side = 1.0;
+    const double S = std::ldexp(1.0, L) / side;
+    const int64_t cmax = ((int64_t)1 << L) - 1;
+    std::vector<uint64_t> leaf(n);
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t ix = (int64_t)std::floor((P->x[i] - x0) * S);
+        int64_t iy = (int64_t)std::floor((P->y[i] - y0) * S);
+        ix = std::min(std::max(ix, (int64_t)0), cmax);
+        iy = std::min(std::max(iy, (int64_t)0), cmax);
+        uint64_t b = 0;
+        for (int j = L - 1; j >= 0; --j) b = 4 * b + 2 * ((ix >> j) & 1) + ((iy >> j) & 1);
+        leaf[i] = b;
+    }
+    P->perm.resize(n);
+    for (int64_t i = 0; i < n; ++i) P->perm[i] = (uint32_t)i;
+    std::stable_sort(P->perm.begin(), P->perm.end(), [&](uint32_t a, uint32_t b) { return leaf[a] < leaf[b]; });
+    P->off.assign(L + 1, std::vector<int64_t>());
+    P->off[L].assign(nboxes(L) + 1, 0);
+    for (int64_t i = 0; i < n; ++i) P->off[L][leaf[i] + 1] += 1;
+    for (int64_t b = 0; b < nboxes(L); ++b) P->off[L][b + 1] += P->off[L][b];
+    for (int l = L - 1; l >= 0; --l) {
+        P->off[l].assign(nboxes(l) + 1, 0);
+        for (int64_t b = 0; b <= nboxes(l); ++b) P->off[l][b] = P->off[L][b << (2 * (L - l))];
+    }
+}
+
 /* O3: the disc of a box (Criterion 1 asks for spheres containing the sets,
  * P:117-119).  DESIGN R8: centre = midpoint of the tight bounding box, radius
  * = the exact maximum distance from that centre to the box's points. */
@@ -220,6 +268,10 @@ static void build_discs(oracle_plan* P)
 #pragma omp parallel for schedule(dynamic, 64)
         for (int64_t b = 0; b < nb; ++b) {
             int64_t s = P->off[l][b], e = P->off[l][b + 1];
+            if (e == s) {                        /* O9: an empty box has no disc */
+                P->cx[l][b] = 0.0; P->cy[l][b] = 0.0; P->rad[l][b] = -1.0;
+                continue;
+            }
             double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
             for (int64_t k = s; k < e; ++k) {
                 uint32_t i = P->perm[k];
@@ -260,11 +312,12 @@ static void build_lists(oracle_plan* P)
 #pragma omp parallel for schedule(dynamic, 64)
         for (int64_t b = 0; b < nb; ++b) {
             int64_t parent = b / 4;
+            if (rr[b] < 0.0) continue;           /* O9: an empty box has no connections */
             for (uint32_t q : P->strong[l - 1][parent]) {
                 bool ws[4];
                 for (int64_t c = 4 * (int64_t)q; c < 4 * (int64_t)q + 4; ++c)
-                    ws[c - 4 * q] = (c != b) && oracle_well_separated(cx[b], cy[b], rr[b],
-                                                                      cx[c], cy[c], rr[c], P->theta);
+                    ws[c - 4 * q] = (c != b) && rr[c] >= 0.0 &&
+                                    oracle_well_separated(cx[b], cy[b], rr[b], cx[c], cy[c], rr[c], P->theta);
                 /* O8: "a box weakly coupled to all children of a parent box can
                  * often interact via the latter instead (whenever the theta-criterion with
                  * respect to that parent is true)".  The parent q is at level l-1. */
@@ -275,6 +328,7 @@ static void build_lists(oracle_plan* P)
                     continue;
                 }
                 for (int64_t c = 4 * (int64_t)q; c < 4 * (int64_t)q + 4; ++c) {
+                    if (rr[c] < 0.0) continue;   /* O9: empty candidates take no part */
                     if (ws[c - 4 * q]) P->weak[l][b].push_back((uint32_t)c);
                     else               P->strong[l][b].push_back((uint32_t)c);
                 }
@@ -321,13 +375,13 @@ int oracle_build(const double* z, int64_t n, double theta, int L, oracle_plan** 
     return oracle_build_ex(z, n, theta, L, 0, out);
 }
 
-/* flags bit 0: r/R exchange (O7), bit 1: parent merge (O8) */
+/* flags bit 0: r/R exchange (O7), bit 1: parent merge (O8), bit 2: midpoint tree (O9) */
 int oracle_build_ex(const double* z, int64_t n, double theta, int L, int flags, oracle_plan** out)
 {
     if (!out) return -1;
     *out = nullptr;
     if (n < 1 || !(theta > 0.0 && theta < 1.0) || L < 0 || L > 15) return -1;
-    if (n < nboxes(L)) return -1;               /* DESIGN R12: no empty boxes */
+    if (n < nboxes(L) && !(flags & 4)) return -1;   /* DESIGN R12: no empty boxes (median tree) */
     if (n >= ((int64_t)1 << 31)) return -1;
     for (int64_t i = 0; i < 2 * n; ++i) if (!std::isfinite(z[i])) return -2;
     oracle_plan* P = new (std::nothrow) oracle_plan();
@@ -341,7 +395,9 @@ int oracle_build_ex(const double* z, int64_t n, double theta, int L, int flags, 
     }
     P->rr = (flags & 1) ? 1 : 0;
     P->pm = (flags & 2) ? 1 : 0;
-    build_tree(P);
+    P->midpoint = (flags & 4) ? 1 : 0;
+    if (P->midpoint) build_tree_midpoint(P);
+    else build_tree(P);
     build_discs(P);
     build_lists(P);
     build_rr(P);
