@@ -82,6 +82,10 @@ extern "C" {
                                       of Phi and Phi' (a sum all-reduce over the outputs,
                                       each rank contributing its own sources; 2 x 16 n
                                       bytes per evaluation).  One GPU / loopback: no effect */
+#define FMM2D_MIDPOINT       0x200  /* the uniform baseline of Fig. 4: the bounding square split
+                                      at geometric midpoints ("standard midpoint
+                                      adaptivity", Fig. 2) instead of source medians; empty
+                                      boxes allowed (R26).  One GPU only        */
 #define FMM2D_TREE_GLOBAL_ONLY 0x10 /* diagnostic: every split step in global memory (no
                                       on-chip finish of the deepest levels; same tree)  */
 

@@ -114,7 +114,8 @@ static int plan_depth(int64_t n, const fmm2d_options* opt)
     int L;
     if (opt->nlevels >= 0) {
         L = opt->nlevels;
-        if (L > FMM2D_MAXL || n < nboxes(L)) return FMM2D_EINVAL;           // DESIGN R12
+        if (L > FMM2D_MAXL) return FMM2D_EINVAL;
+        if (n < nboxes(L) && !(opt->flags & FMM2D_MIDPOINT)) return FMM2D_EINVAL;   // DESIGN R12
     } else {
         if (opt->leaf_target < 1) return FMM2D_EINVAL;
         L = depth_rule(n, opt->leaf_target);
@@ -132,7 +133,8 @@ static int build_stage_tree(const double* z, int64_t n, const fmm2d_options* opt
     const int L = plan_depth(n, opt);
     if (L < 0) return L;
     if (nranks < 1 || rank < 0 || rank >= nranks) return FMM2D_EINVAL;
-    if (nranks > 1 && (opt->flags & FMM2D_RR_EXCHANGE)) return FMM2D_ENOTSUP;
+    if (nranks > 1 && (opt->flags & (FMM2D_RR_EXCHANGE | FMM2D_MIDPOINT))) return FMM2D_ENOTSUP;
+    if ((opt->flags & FMM2D_MIDPOINT) && L > 15) return FMM2D_EINVAL;          // 30-bit leaf keys
     if (nranks > 1) {                                   // partitionable? (before any device work)
         const int k = partition_level(nranks);
         if (k < 0 || L <= k) return FMM2D_ENOTSUP;

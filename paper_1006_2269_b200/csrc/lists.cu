@@ -54,6 +54,7 @@ __global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, c
     int64_t ncand = 4 * (poff[par + 1] - o0);
     double bx = cx[b], by = cy[b], br = r[b];
     int64_t nw = 0, ns = 0, nx = 0;
+    if (br < 0.0) ncand = 0;                 // empty box (midpoint tree): no connections
     int64_t wbase = FILL ? woff[b] : 0, sbase = FILL ? soff[b] : 0, xbase = (FILL && merge) ? xoff[b] : 0;
     unsigned lt = (1u << lane) - 1u;
     for (int64_t t0 = 0; t0 < ncand; t0 += 32) {
@@ -64,7 +65,8 @@ __global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, c
         if (valid) {
             q = pidx[o0 + (t >> 2)];
             c = 4u * q + (uint32_t)(t & 3);
-            ws = (c != (uint32_t)b) && well_separated(bx, by, br, cx[c], cy[c], r[c], theta);
+            valid = r[c] >= 0.0;                 // empty candidates (midpoint tree) take no part
+            ws = valid && (c != (uint32_t)b) && well_separated(bx, by, br, cx[c], cy[c], r[c], theta);
         }
         unsigned wm = __ballot_sync(0xffffffffu, valid && ws);
         bool merged = false;                        // my group of four merges into its parent q

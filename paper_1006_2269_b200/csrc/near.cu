@@ -738,7 +738,7 @@ int prepare_near_sym(fmm2d_plan* P)
     P->sym = false;
     const int L = P->L, ml = P->stats.max_leaf;
     if (L < 1 || ml > SYM_MAXLEAF || ml < 1 || !(P->flags & FMM2D_SYMMETRIC_P2P) || P->nranks > 1 ||
-        (P->flags & FMM2D_RR_EXCHANGE))
+        (P->flags & (FMM2D_RR_EXCHANGE | FMM2D_MIDPOINT)))
         return 0;
     cudaStream_t st = P->stream;
     const int64_t nl = nboxes(L);

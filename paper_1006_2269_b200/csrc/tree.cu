@@ -715,11 +715,163 @@ __global__ void __launch_bounds__(FIN_T) k_finish(const uint2* __restrict__ yl, 
     }
 }
 
-// r = sqrt_rn(max squared distance)
+// r = sqrt_rn(max squared distance); an empty box (midpoint tree) keeps r = -1
 __global__ void k_sqrt(double* __restrict__ r, int64_t nb)
 {
     int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < nb) r[b] = __dsqrt_rn(r[b]);
+    if (b < nb && r[b] >= 0.0) r[b] = __dsqrt_rn(r[b]);
+}
+
+// ---------------------------------------------------------------- midpoint tree (DESIGN R26)
+// The uniform baseline of Fig. 4: the bounding square split at geometric midpoints to
+// depth L (x then y, children 4b + 2 xside + yside), empty boxes allowed.  A point's leaf
+// is (floor((x - x0) S), floor((y - y0) S)) clamped, S = 2^L / side (host division),
+// interleaved x-high-first; leaves ascending, input order inside (stable sort).
+__device__ __forceinline__ uint32_t spread15(uint32_t v)
+{
+    v &= 0x7FFFu;
+    v = (v | (v << 8)) & 0x00FF00FFu;
+    v = (v | (v << 4)) & 0x0F0F0F0Fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+
+__global__ void k_mid_keys(const double2* __restrict__ zc, int64_t n, double x0, double y0, double S, int L,
+                           uint32_t* __restrict__ key, uint32_t* __restrict__ iota)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double2 v = zc[i];
+    const int64_t cmax = ((int64_t)1 << L) - 1;
+    int64_t ix = (int64_t)floor(__dmul_rn(__dsub_rn(v.x, x0), S));
+    int64_t iy = (int64_t)floor(__dmul_rn(__dsub_rn(v.y, y0), S));
+    ix = min(max(ix, (int64_t)0), cmax);
+    iy = min(max(iy, (int64_t)0), cmax);
+    key[i] = (spread15((uint32_t)ix) << 1) | spread15((uint32_t)iy);
+    iota[i] = (uint32_t)i;
+}
+
+// leaf offsets: off[b] = first sorted position with key >= b
+__global__ void k_mid_leaf_off(const uint32_t* __restrict__ skey, int64_t n, int64_t nl, uint32_t* __restrict__ off)
+{
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > nl) return;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)skey[mid] < b) lo = mid + 1;
+        else hi = mid;
+    }
+    off[b] = (uint32_t)lo;
+}
+
+__global__ void k_mid_level_off(const uint32_t* __restrict__ offL, int shift, int64_t nb, uint32_t* __restrict__ off)
+{
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b <= nb) off[b] = offL[b << shift];
+}
+
+__global__ void k_mid_rows(const uint32_t* __restrict__ sidx, const double2* __restrict__ zc, int64_t n,
+                           uint32_t* __restrict__ perm, double4* __restrict__ src)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t i = sidx[k];
+    const double2 v = zc[i];
+    perm[k] = i;
+    src[k] = make_double4(v.x, v.y, 0.0, 0.0);
+}
+
+// per box of every level: min / max of the orderable coordinate bits (segmented warp
+// reductions over the leaf-ordered points, one atomic per run)
+__global__ void __launch_bounds__(256) k_mid_bounds(const uint32_t* __restrict__ skey, const double4* __restrict__ src,
+                                                    int64_t n, int L, const int64_t* __restrict__ gbase,
+                                                    unsigned long long* __restrict__ bb)   // [4][nbox_total]
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool valid = k < n;
+    uint32_t leaf = valid ? skey[k] : 0u;
+    double4 v = valid ? src[k] : make_double4(0, 0, 0, 0);
+    const unsigned long long ox = orderable(v.x), oy = orderable(v.y);
+    const int64_t nbt = gbase[L + 1];
+    for (int l = L; l >= 0; --l) {
+        const uint32_t box = leaf >> (2 * (L - l));
+        unsigned long long a = ox, b = ox, c = oy, d = oy;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long a2 = __shfl_down_sync(0xffffffffu, a, o), b2 = __shfl_down_sync(0xffffffffu, b, o);
+            const unsigned long long c2 = __shfl_down_sync(0xffffffffu, c, o), d2 = __shfl_down_sync(0xffffffffu, d, o);
+            const uint32_t bv = __shfl_down_sync(0xffffffffu, box, o);
+            const bool vv = __shfl_down_sync(0xffffffffu, valid ? 1 : 0, o) != 0;
+            if (lane + o < 32 && vv && bv == box) {
+                a = min(a, a2);
+                b = max(b, b2);
+                c = min(c, c2);
+                d = max(d, d2);
+            }
+        }
+        const uint32_t bprev = __shfl_up_sync(0xffffffffu, box, 1);
+        if (valid && (lane == 0 || bprev != box)) {
+            const int64_t g = gbase[l] + box;
+            atomicMin(&bb[g], a);
+            atomicMax(&bb[nbt + g], b);
+            atomicMin(&bb[2 * nbt + g], c);
+            atomicMax(&bb[3 * nbt + g], d);
+        }
+    }
+}
+
+__global__ void k_mid_centres(const unsigned long long* __restrict__ bb, int64_t nbt, double* __restrict__ cx,
+                              double* __restrict__ cy, double* __restrict__ r)
+{
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nbt) return;
+    if (bb[g] == ~0ull) {                                     // no point: empty box
+        cx[g] = 0.0;
+        cy[g] = 0.0;
+        r[g] = -1.0;
+        return;
+    }
+    cx[g] = __dmul_rn(0.5, __dadd_rn(from_orderable(bb[g]), from_orderable(bb[nbt + g])));
+    cy[g] = __dmul_rn(0.5, __dadd_rn(from_orderable(bb[2 * nbt + g]), from_orderable(bb[3 * nbt + g])));
+    r[g] = 0.0;
+}
+
+// squared radii of every level (the sqrt follows in finish_radii)
+__global__ void __launch_bounds__(256) k_mid_radius(const uint32_t* __restrict__ skey, const double4* __restrict__ src,
+                                                    int64_t n, int L, const int64_t* __restrict__ gbase,
+                                                    const double* __restrict__ cx, const double* __restrict__ cy,
+                                                    double* __restrict__ r)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool valid = k < n;
+    const uint32_t leaf = valid ? skey[k] : 0u;
+    const double4 v = valid ? src[k] : make_double4(0, 0, 0, 0);
+    for (int l = L; l >= 0; --l) {
+        const uint32_t box = leaf >> (2 * (L - l));
+        const int64_t g = gbase[l] + box;
+        double d = valid ? rn_dist2(v.x, v.y, cx[g], cy[g]) : 0.0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double dv = __shfl_down_sync(0xffffffffu, d, o);
+            const uint32_t bv = __shfl_down_sync(0xffffffffu, box, o);
+            const bool vv = __shfl_down_sync(0xffffffffu, valid ? 1 : 0, o) != 0;
+            if (lane + o < 32 && vv && bv == box) d = fmax(d, dv);
+        }
+        const uint32_t bprev = __shfl_up_sync(0xffffffffu, box, 1);
+        if (valid && (lane == 0 || bprev != box))
+            atomicMax((unsigned long long*)(r + g), (unsigned long long)__double_as_longlong(d));
+    }
+}
+
+__global__ void k_mid_leaf_stats(const uint32_t* __restrict__ offL, int64_t nl, unsigned int* __restrict__ mm)
+{
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nl) return;
+    const unsigned int sz = offL[b + 1] - offL[b];
+    atomicMax(&mm[0], sz);
+    atomicMin(&mm[1], sz);
 }
 
 inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
@@ -736,8 +888,11 @@ int finish_radii(fmm2d_plan* P)
     return 0;
 }
 
+static int build_tree_midpoint(fmm2d_plan* P, const double2* z);
+
 int build_tree(fmm2d_plan* P, const double2* z)
 {
+    if (P->flags & FMM2D_MIDPOINT) return build_tree_midpoint(P, z);
     const int64_t n = P->n;
     const int L = P->L;
     cudaStream_t st = P->stream;
@@ -1013,6 +1168,117 @@ int build_tree(fmm2d_plan* P, const double2* z)
     };
     rc = body();
     tfree();
+    return rc;
+}
+
+// the midpoint tree (DESIGN R26): keys, one stable sort, offsets by search, discs by
+// segmented reductions over the leaf order
+static int build_tree_midpoint(fmm2d_plan* P, const double2* z)
+{
+    const int64_t n = P->n;
+    const int L = P->L;
+    cudaStream_t st = P->stream;
+    const int BS = 256;
+    const int64_t nl = nboxes(L), nbt = P->nbox_total;
+    P->obase.assign(L + 1, 0);
+    int64_t tot = 0;
+    for (int l = 0; l <= L; ++l) { P->obase[l] = tot; tot += nboxes(l) + 1; }
+    FMM2D_TRY(dev_alloc(P, (void**)&P->boff, sizeof(uint32_t) * tot));
+    double2* zc = nullptr;
+    uint32_t *key, *skey, *iota, *sidx;
+    unsigned long long* bb = nullptr;
+    int64_t* gbase = nullptr;
+    Bounds* bnd = nullptr;
+    unsigned int* mm = nullptr;
+    void* scratch = nullptr;
+    size_t sb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, sb, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int)n, 0, std::max(1, 2 * L), st);
+    std::vector<void*> tmp;
+    auto talloc = [&](void** p, size_t b) -> int {
+        if (cudaMallocAsync(p, b ? b : 16, st) != cudaSuccess) return FMM2D_ENOMEM;
+        tmp.push_back(*p);
+        return 0;
+    };
+    int rc = 0;
+    do {
+        if ((rc = talloc((void**)&zc, 16 * n))) break;
+        if ((rc = talloc((void**)&key, 4 * n))) break;
+        if ((rc = talloc((void**)&skey, 4 * n))) break;
+        if ((rc = talloc((void**)&iota, 4 * n))) break;
+        if ((rc = talloc((void**)&sidx, 4 * n))) break;
+        if ((rc = talloc((void**)&bb, 8 * 4 * nbt))) break;
+        if ((rc = talloc((void**)&gbase, 8 * (L + 2)))) break;
+        if ((rc = talloc((void**)&bnd, sizeof(Bounds)))) break;
+        if ((rc = talloc((void**)&mm, 8))) break;
+        if ((rc = talloc(&scratch, sb))) break;
+    } while (0);
+    auto body = [&]() -> int {
+        if (rc) return rc;
+        Bounds h;
+        h.xmin = h.ymin = ~0ull;
+        h.xmax = h.ymax = 0;
+        h.bad = 0;
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(bnd, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+        const unsigned g = (unsigned)std::min<int64_t>(grid_for(n, CT), 148 * 8);
+        k_canon<<<g, CT, 0, st>>>(z, n, zc, bnd);
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(&h, bnd, sizeof(h), cudaMemcpyDeviceToHost, st));
+        FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+        if (h.bad) return FMM2D_ENONFINITE;
+        auto host_from_orderable = [](unsigned long long k) {
+            uint64_t u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+            double d;
+            memcpy(&d, &u, 8);
+            return d;
+        };
+        const double x0 = host_from_orderable(h.xmin), x1 = host_from_orderable(h.xmax);
+        const double y0 = host_from_orderable(h.ymin), y1 = host_from_orderable(h.ymax);
+        double side = std::max(x1 - x0, y1 - y0);
+        if (!(side > 0.0)) side = 1.0;
+        const double S = std::ldexp(1.0, L) / side;
+        k_mid_keys<<<grid_for(n, BS), BS, 0, st>>>(zc, n, x0, y0, S, L, key, iota);
+        fmm2d::note_launch();
+        size_t s2 = sb;
+        FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, s2, key, skey, iota, sidx, (int)n, 0,
+                                                       std::max(1, 2 * L), st));
+        uint32_t* offL = P->boff + P->obase[L];
+        k_mid_leaf_off<<<grid_for(nl + 1, BS), BS, 0, st>>>(skey, n, nl, offL);
+        fmm2d::note_launch();
+        for (int l = 0; l < L; ++l) {
+            k_mid_level_off<<<grid_for(nboxes(l) + 1, BS), BS, 0, st>>>(offL, 2 * (L - l), nboxes(l),
+                                                                        P->boff + P->obase[l]);
+            fmm2d::note_launch();
+        }
+        k_mid_rows<<<grid_for(n, BS), BS, 0, st>>>(sidx, zc, n, P->perm, P->src);
+        fmm2d::note_launch();
+        std::vector<int64_t> hb(L + 2);
+        for (int l = 0; l <= L + 1; ++l) hb[l] = P->base[l];
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(gbase, hb.data(), 8 * (L + 2), cudaMemcpyHostToDevice, st));
+        FMM2D_CUDA_TRY(cudaMemsetAsync(bb, 0xFF, 8 * nbt, st));                    // min: ~0
+        FMM2D_CUDA_TRY(cudaMemsetAsync(bb + nbt, 0, 8 * nbt, st));                 // max: 0
+        FMM2D_CUDA_TRY(cudaMemsetAsync(bb + 2 * nbt, 0xFF, 8 * nbt, st));
+        FMM2D_CUDA_TRY(cudaMemsetAsync(bb + 3 * nbt, 0, 8 * nbt, st));
+        k_mid_bounds<<<grid_for(n, 256), 256, 0, st>>>(skey, P->src, n, L, gbase, bb);
+        fmm2d::note_launch();
+        k_mid_centres<<<grid_for(nbt, BS), BS, 0, st>>>(bb, nbt, P->cx, P->cy, P->r);
+        fmm2d::note_launch();
+        k_mid_radius<<<grid_for(n, 256), 256, 0, st>>>(skey, P->src, n, L, gbase, P->cx, P->cy, P->r);
+        fmm2d::note_launch();
+        unsigned int hmm[2] = {0u, 0xFFFFFFFFu};
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(mm, hmm, 8, cudaMemcpyHostToDevice, st));
+        k_mid_leaf_stats<<<grid_for(nl, BS), BS, 0, st>>>(offL, nl, mm);
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(hmm, mm, 8, cudaMemcpyDeviceToHost, st));
+        FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+        P->stats.max_leaf = (int)hmm[0];
+        P->stats.min_leaf = (int)hmm[1];
+        FMM2D_CUDA_TRY(cudaGetLastError());
+        if (P->nranks == 1) FMM2D_TRY(finish_radii(P));
+        return 0;
+    };
+    rc = body();
+    for (void* p : tmp) cudaFreeAsync(p, st);
     return rc;
 }
 

@@ -356,3 +356,24 @@ def test_overlapped_eval_bit_identical(cfg, n, rr):
         torch.cuda.synchronize()
         out.append((phi, dphi))
     assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+
+
+MID_CASES = [("C2", None, 0.5, 17), ("C3-100k", 100_000, 0.5, 17), ("C4-100k", 100_000, 0.5, 17),
+             ("C1-t.3-p8", None, 0.3, 8)]
+
+
+@pytest.mark.parametrize("name,n,theta,p", MID_CASES, ids=[c[0] for c in MID_CASES])
+def test_midpoint_tree_matches_oracle(orc, name, n, theta, p):
+    """FMM2D_MIDPOINT (Fig. 2 / Fig. 4 uniform baseline, DESIGN R26): permutation, offsets,
+    discs (empty boxes r = -1) and lists of every level bit-exact, Phi and Phi' within
+    1e-12 of the oracle pass on the same midpoint tree."""
+    from paper_1006_2269_b200 import Fmm2d
+    cfg = name.split("-")[0]
+    z, m = W.make_config(cfg, n=n)
+    L = orc.nlevels(len(z), 35)
+    op = orc.plan(z, theta, L, midpoint=True)
+    gp = Fmm2d(torch.from_numpy(z).cuda(), theta=theta, p=p, nlevels=L, midpoint=True)
+    _check_structure(gp, op, L)
+    phi_o, dphi_o = op.eval(m, p)
+    phi_g, dphi_g = _gpu_eval(gp, m)
+    assert _nerr(phi_g, phi_o) <= TOL and _nerr(dphi_g, dphi_o) <= TOL
