@@ -78,6 +78,21 @@ def positions(dist: str, n: int, rng: np.random.Generator) -> np.ndarray:
         r = rng.random(n)
         a = 2.0 * np.pi * rng.random(n)
         return r * np.cos(a) + 1j * (r * np.sin(a))
+    if dist.startswith("normal:") or dist.startswith("layer:"):
+        # Fig. 4: "a normal distribution with variance sigma^2 or ... a 'layer'
+        # distribution where the x-coordinate is uniformly distributed in [0,1], and the
+        # y-coordinate again is N(0, sigma^2)-distributed ... forced by rejection to fit
+        # exactly within the unit square" (clustering at the origin / the x-axis)
+        kind, sig = dist.split(":")
+        sig = float(sig)
+        out = np.empty(0, np.complex128)
+        while out.shape[0] < n:
+            k = 2 * (n - out.shape[0]) + 64
+            y = sig * rng.standard_normal(k)
+            x = sig * rng.standard_normal(k) if kind == "normal" else rng.random(k)
+            ok = (x >= 0) & (x <= 1) & (y >= 0) & (y <= 1)
+            out = np.concatenate([out, (x + 1j * y)[ok]])
+        return out[:n]
     raise ValueError(dist)
 
 
