@@ -36,15 +36,21 @@ __device__ __forceinline__ bool well_separated(double cbx, double cby, double rb
 // Parent merge (DESIGN R25; `merge`): a candidate group of four children of q
 // (four consecutive lanes) that are ALL weak to b, with Criterion 1 also true for (b, q)
 // itself (q's disc at level l-1: pcx, pcy, pr), becomes one cross-level entry q.
-template <bool FILL>
+// One pass per level: the entries go to per-box slots of a scratch array (capacity
+// 4 |S(parent)| per box -- the candidates -- at a closed-form slot start), with the
+// counts; k_compact_lists then packs them into the CSR lists after a scan of the counts.
+__device__ __forceinline__ int64_t cand_slot(const int64_t* __restrict__ poff, int64_t b)
+{
+    const int64_t par = b >> 2;
+    return 16 * poff[par] + 4 * (b & 3) * (poff[par + 1] - poff[par]);
+}
+
 __global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, const double* __restrict__ cy,
                         const double* __restrict__ r, double theta, const int64_t* __restrict__ poff,
-                        const uint32_t* __restrict__ pidx, int64_t* __restrict__ wcnt,
-                        int64_t* __restrict__ scnt, const int64_t* __restrict__ woff,
-                        const int64_t* __restrict__ soff, uint32_t* __restrict__ widx,
-                        uint32_t* __restrict__ sidx, bool merge, const double* __restrict__ pcx,
-                        const double* __restrict__ pcy, const double* __restrict__ pr, int64_t* __restrict__ xcnt,
-                        const int64_t* __restrict__ xoff, uint32_t* __restrict__ xidx)
+                        const uint32_t* __restrict__ pidx, int64_t* __restrict__ wcnt, int64_t* __restrict__ scnt,
+                        uint32_t* __restrict__ wtmp, uint32_t* __restrict__ stmp, bool merge,
+                        const double* __restrict__ pcx, const double* __restrict__ pcy, const double* __restrict__ pr,
+                        int64_t* __restrict__ xcnt, uint32_t* __restrict__ xtmp)
 {
     int64_t b = b0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     int lane = threadIdx.x & 31;
@@ -55,7 +61,7 @@ __global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, c
     double bx = cx[b], by = cy[b], br = r[b];
     int64_t nw = 0, ns = 0, nx = 0;
     if (br < 0.0) ncand = 0;                 // empty box (midpoint tree): no connections
-    int64_t wbase = FILL ? woff[b] : 0, sbase = FILL ? soff[b] : 0, xbase = (FILL && merge) ? xoff[b] : 0;
+    const int64_t slot = cand_slot(poff, b), xslot = slot / 4;
     unsigned lt = (1u << lane) - 1u;
     for (int64_t t0 = 0; t0 < ncand; t0 += 32) {
         int64_t t = t0 + lane;
@@ -79,24 +85,41 @@ __global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, c
         }
         unsigned sm = __ballot_sync(0xffffffffu, valid && !ws);
         unsigned xm = __ballot_sync(0xffffffffu, merged && (lane & 3) == 0);
-        if (FILL && valid) {
+        if (valid) {
             if (merged) {
-                if ((lane & 3) == 0) xidx[xbase + nx + __popc(xm & lt)] = q;
+                if ((lane & 3) == 0) xtmp[xslot + nx + __popc(xm & lt)] = q;
             } else if (ws) {
-                widx[wbase + nw + __popc(wm & lt)] = c;
+                wtmp[slot + nw + __popc(wm & lt)] = c;
             } else {
-                sidx[sbase + ns + __popc(sm & lt)] = c;
+                stmp[slot + ns + __popc(sm & lt)] = c;
             }
         }
         nw += __popc(wm);
         ns += __popc(sm);
         nx += __popc(xm);
     }
-    if (!FILL && lane == 0) {
+    if (lane == 0) {
         wcnt[b] = nw;
         scnt[b] = ns;
         if (merge) xcnt[b] = nx;
     }
+}
+
+// pack the slots into the CSR lists (warp per box)
+__global__ void k_compact_lists(int64_t b0, int64_t b1, const int64_t* __restrict__ poff,
+                                const uint32_t* __restrict__ wtmp, const uint32_t* __restrict__ stmp,
+                                const uint32_t* __restrict__ xtmp, const int64_t* __restrict__ woff,
+                                const int64_t* __restrict__ soff, const int64_t* __restrict__ xoff,
+                                uint32_t* __restrict__ widx, uint32_t* __restrict__ sidx, uint32_t* __restrict__ xidx)
+{
+    const int64_t b = b0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (b >= b1) return;
+    const int64_t slot = cand_slot(poff, b);
+    for (int64_t k = lane; k < woff[b + 1] - woff[b]; k += 32) widx[woff[b] + k] = wtmp[slot + k];
+    for (int64_t k = lane; k < soff[b + 1] - soff[b]; k += 32) sidx[soff[b] + k] = stmp[slot + k];
+    if (xoff)
+        for (int64_t k = lane; k < xoff[b + 1] - xoff[b]; k += 32) xidx[xoff[b] + k] = xtmp[slot / 4 + k];
 }
 
 // M2L work order of one level: inside each window of M2L_WIN consecutive boxes (tree
@@ -448,9 +471,13 @@ int build_lists(fmm2d_plan* P)
             const double* pcy = P->cy + P->base[l - 1];
             const double* pr = P->r + P->base[l - 1];
             unsigned grid = grid_for((b1 - b0) * 32, 256);
-            k_lists<false><<<grid, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w, cnt_s,
-                                                 nullptr, nullptr, nullptr, nullptr, merge, pcx, pcy, pr, cnt_x,
-                                                 nullptr, nullptr); fmm2d::note_launch();
+            uint32_t *wtmp = nullptr, *stmp = nullptr, *xtmp = nullptr;
+            const int64_t cap = 16 * PS.total;          // sum of the candidate counts of all boxes
+            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&wtmp, sizeof(uint32_t) * std::max<int64_t>(cap, 1), st));
+            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&stmp, sizeof(uint32_t) * std::max<int64_t>(cap, 1), st));
+            if (merge) FMM2D_CUDA_TRY(cudaMallocAsync((void**)&xtmp, sizeof(uint32_t) * std::max<int64_t>(cap / 4, 1), st));
+            k_lists<<<grid, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w, cnt_s, wtmp, stmp, merge,
+                                          pcx, pcy, pr, cnt_x, xtmp); fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
             size_t sb = scan_bytes;
             FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, cnt_w, W.off, (int)(nb + 1), st));
@@ -472,10 +499,12 @@ int build_lists(fmm2d_plan* P)
             FMM2D_TRY(dev_alloc(P, (void**)&W.idx, sizeof(uint32_t) * std::max<int64_t>(W.total, 1)));
             FMM2D_TRY(dev_alloc(P, (void**)&S.idx, sizeof(uint32_t) * std::max<int64_t>(S.total, 1)));
             if (merge) FMM2D_TRY(dev_alloc(P, (void**)&X.idx, sizeof(uint32_t) * std::max<int64_t>(X.total, 1)));
-            k_lists<true><<<grid, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, nullptr, nullptr,
-                                                W.off, S.off, W.idx, S.idx, merge, pcx, pcy, pr, nullptr, X.off,
-                                                X.idx); fmm2d::note_launch();
+            k_compact_lists<<<grid, 256, 0, st>>>(b0, b1, PS.off, wtmp, stmp, xtmp, W.off, S.off, merge ? X.off : nullptr,
+                                                  W.idx, S.idx, X.idx); fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
+            cudaFreeAsync(wtmp, st);
+            cudaFreeAsync(stmp, st);
+            if (xtmp) cudaFreeAsync(xtmp, st);
             P->stats.weak_pairs += W.total + X.total;
         }
         // M2L work order (k_m2l_keys)
