@@ -301,7 +301,14 @@ __global__ void k_seg_prep(const uint32_t* __restrict__ par_off, const uint32_t*
 #ifndef FMM2D_PARTITION_TWO_PASS
 #define FMM2D_PARTITION_TWO_PASS 0
 #endif
-constexpr int PT = 256, PI = 8, PTILE = PT * PI, PTILE_SHIFT = 11;
+#ifndef FMM2D_PART_PI
+#define FMM2D_PART_PI 8
+#endif
+#ifndef FMM2D_PART_PT
+#define FMM2D_PART_PT 256
+#endif
+constexpr int PT = FMM2D_PART_PT, PI = FMM2D_PART_PI, PTILE = PT * PI;
+constexpr int PTILE_SHIFT = (PTILE == 1024) ? 10 : (PTILE == 2048) ? 11 : (PTILE == 4096) ? 12 : 13;
 static_assert(PTILE == (1 << PTILE_SHIFT), "tile size");
 constexpr int SEGMAX = 512;                          // larger tile spans: segment search in global memory
 constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_MASK = 3ull << 62;

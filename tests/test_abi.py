@@ -80,3 +80,33 @@ def test_build_rejects_bad_sizes_and_nulls():
     o.nranks = 2                           # n = 4: a one-level tree has nothing below k = 1
     assert L.fmm2d_build(ctypes.c_void_p(z.ctypes.data), 4, ctypes.byref(o), ctypes.byref(h)) == -6
     assert not h.value
+
+
+def test_option_combinations_rejected_without_gpu():
+    """Partitioned builds: the r/R exchange and the midpoint tree are one-GPU options
+    (ENOTSUP, -6) -- checked before any device work."""
+    import paper_1006_2269_b200 as F
+    L = F.lib()
+    z = np.zeros(1000, np.complex128)
+    nid = ctypes.create_string_buffer(128)
+    for flag in (F.fmm2d.RR_EXCHANGE, F.fmm2d.MIDPOINT):
+        o = F.fmm2d.Options()
+        L.fmm2d_default_options(ctypes.byref(o))
+        o.nranks, o.rank, o.flags = 2, 0, flag
+        o.nccl_id = ctypes.cast(nid, ctypes.c_void_p)
+        h = ctypes.c_void_p()
+        assert L.fmm2d_build(ctypes.c_void_p(z.ctypes.data), 1000, ctypes.byref(o), ctypes.byref(h)) == -6
+        assert not h.value
+
+
+def test_flag_values_match_header():
+    import re
+    import paper_1006_2269_b200 as F
+    src = open(os.path.join(ROOT, "include", "fmm2d.h")).read()
+    flags = {k: int(v, 16) for k, v in re.findall(r"#define FMM2D_(\w+)\s+(0x[0-9a-fA-F]+)", src)}
+    for name in ("HOST_PTRS", "REAL_STRENGTHS", "SYMMETRIC_P2P", "TREE_KEY64", "TREE_GLOBAL_ONLY", "RR_EXCHANGE",
+                 "PARENT_MERGE", "OVERLAP", "GATHER_OUTPUT", "MIDPOINT"):
+        assert getattr(F.fmm2d, name) == flags[name], name
+    exports = {k: int(v) for k, v in re.findall(r"#define FMM2D_EXPORT_(\w+)\s+(\d+)", src)}
+    for name, v in exports.items():
+        assert getattr(F.fmm2d, "EXPORT_" + name) == v, name
