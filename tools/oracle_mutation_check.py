@@ -27,6 +27,23 @@ MUTATIONS = [
     ("y-split sorts by x", "std::sort(seg + h0, seg + nb, byy);", "std::sort(seg + h0, seg + nb, byx);"),
     ("P2P keeps self pair", "if (j == i) continue;                              /* j != i */", ""),
     ("L2P derivative index", "ds += (double)l * b[l] * wlm1;", "ds += (double)(l - 1) * b[l] * wlm1;"),
+    # O7 r/R exchange
+    ("P2L drops the minus sign", "b[l] -= ms[j] * ivl / (double)l;", "b[l] += ms[j] * ivl / (double)l;"),
+    ("exchanged criterion unswapped", "return (r < R) && (d > 0.0) && (r + theta * R <= theta * d);",
+     "return (r < R) && (d > 0.0) && (R + theta * r <= theta * d);"),
+    ("P2L into the larger box", "else if (rr[t] < rr[s]) P->p2l_in[t].push_back(s);",
+     "else if (rr[t] > rr[s]) P->p2l_in[t].push_back(s);"),
+    # O8 parent merge
+    ("merge without the parent criterion", "if (P->pm && l >= 2 && ws[0] && ws[1] && ws[2] && ws[3] &&\n"
+     "                    oracle_well_separated(", "if (P->pm && l >= 2 && ws[0] && ws[1] && ws[2] &&\n"
+     "                    oracle_well_separated("),
+    ("cross M2L from the wrong level", "m2l(P->mpole[l - 1].data() + (int64_t)q * P1, P->cx[l - 1][q], P->cy[l - 1][q],",
+     "m2l(P->mpole[l - 1].data() + (int64_t)q * P1, P->cx[l][q], P->cy[l][q],"),
+    # O9 midpoint tree
+    ("midpoint key y-high", "b = 4 * b + 2 * ((ix >> j) & 1) + ((iy >> j) & 1);",
+     "b = 4 * b + 2 * ((iy >> j) & 1) + ((ix >> j) & 1);"),
+    ("midpoint cell floor -> round", "int64_t ix = (int64_t)std::floor((P->x[i] - x0) * S);",
+     "int64_t ix = (int64_t)std::round((P->x[i] - x0) * S);"),
 ]
 
 
