@@ -113,47 +113,54 @@ __device__ __forceinline__ double key_scale(unsigned long long omin, unsigned lo
 
 // A0 (pass 2): the x-sort's keys (32-bit image of x, or the full orderable 64 bits)
 // and its payload {idx, 32-bit image of y} -- the y key rides along, so the y-sort's
-// input comes out of the x-sort in x order without a gather.
+// input comes out of the x-sort in x order without a gather.  The presort runs over
+// m points: all of them (sub == nullptr), or the ascending input indices sub[0..m) of
+// one level-k box of a partitioned build; its ranks are offset by roff (the box's first
+// leaf-order position), so every rank of the plan is a position.
 template <bool K64>
-__global__ void k_keys_x(const double2* __restrict__ zc, int64_t n, const Bounds* __restrict__ B,
-                         uint32_t* __restrict__ k32, uint64_t* __restrict__ k64, uint64_t* __restrict__ val)
+__global__ void k_keys_x(const double2* __restrict__ zc, const uint32_t* __restrict__ sub, int64_t m,
+                         const Bounds* __restrict__ B, uint32_t* __restrict__ k32, uint64_t* __restrict__ k64,
+                         uint64_t* __restrict__ val)
 {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    const uint32_t i = sub ? sub[t] : (uint32_t)t;
     double xmn, ymn;
     const double sx = key_scale(B->xmin, B->xmax, &xmn);
     const double sy = key_scale(B->ymin, B->ymax, &ymn);
     const double2 v = zc[i];
-    if (K64) k64[i] = orderable(v.x);
-    else k32[i] = key32(v.x, xmn, sx);
-    val[i] = (uint64_t)(uint32_t)i | ((uint64_t)key32(v.y, ymn, sy) << 32);
+    if (K64) k64[t] = orderable(v.x);
+    else k32[t] = key32(v.x, xmn, sx);
+    val[t] = (uint64_t)i | ((uint64_t)key32(v.y, ymn, sy) << 32);
 }
 
 // y-sort input in x order: key = 32-bit image of y, payload {x rank, idx}
-__global__ void k_prep_y(const uint64_t* __restrict__ vx, int64_t n, uint32_t* __restrict__ key,
+__global__ void k_prep_y(const uint64_t* __restrict__ vx, int64_t m, uint32_t roff, uint32_t* __restrict__ key,
                          uint64_t* __restrict__ val)
 {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
+    if (k >= m) return;
     const uint64_t v = vx[k];
     key[k] = (uint32_t)(v >> 32);
-    val[k] = (uint64_t)(uint32_t)k | (v << 32);          // {rx = k, idx}
+    val[k] = (uint64_t)(roff + (uint32_t)k) | (v << 32);          // {rx, idx}
 }
 
 // 64-bit fallback of the y-sort: input in idx order (so ties leave in idx order),
 // payload {x rank, idx}; the x ranks are scattered once (rare path)
-__global__ void k_scatter_rx(const uint64_t* __restrict__ vx, int64_t n, uint32_t* __restrict__ rx)
+__global__ void k_scatter_rx(const uint64_t* __restrict__ vx, int64_t m, uint32_t* __restrict__ rx)
 {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n) rx[(uint32_t)vx[k]] = (uint32_t)k;
+    if (k < m) rx[(uint32_t)vx[k]] = (uint32_t)k;
 }
-__global__ void k_keys_y64(const double2* __restrict__ zc, const uint32_t* __restrict__ rx, int64_t n,
-                           uint64_t* __restrict__ k64, uint64_t* __restrict__ val)
+__global__ void k_keys_y64(const double2* __restrict__ zc, const uint32_t* __restrict__ sub,
+                           const uint32_t* __restrict__ rx, int64_t m, uint32_t roff, uint64_t* __restrict__ k64,
+                           uint64_t* __restrict__ val)
 {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    k64[i] = orderable(zc[i].y);
-    val[i] = (uint64_t)rx[i] | ((uint64_t)(uint32_t)i << 32);
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    const uint32_t i = sub ? sub[t] : (uint32_t)t;
+    k64[t] = orderable(zc[i].y);
+    val[t] = (uint64_t)(roff + rx[i]) | ((uint64_t)i << 32);
 }
 
 // Runs of equal 32-bit keys are re-sorted by (c, idx) (insertion sort, exact
@@ -196,23 +203,23 @@ __global__ void k_fix_runs(const uint32_t* __restrict__ key, int64_t n, const do
     for (int a = 0; a < len; ++a) val[k + a] = pv[a];
 }
 
-// y-list and the x-ranks in y order (the key of the sort that inverts them)
-__global__ void k_make_ylist(const uint64_t* __restrict__ vy, int64_t n, uint2* __restrict__ yl,
+// y-list and the (local) x-ranks in y order (the key of the sort that inverts them)
+__global__ void k_make_ylist(const uint64_t* __restrict__ vy, int64_t m, uint32_t roff, uint2* __restrict__ yl,
                              uint32_t* __restrict__ keyd, uint32_t* __restrict__ iota)
 {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
+    if (k >= m) return;
     const uint32_t rx = (uint32_t)vy[k];
-    yl[k] = make_uint2(rx, (uint32_t)k);
-    keyd[k] = rx;
+    yl[k] = make_uint2(rx, roff + (uint32_t)k);
+    keyd[k] = rx - roff;
     iota[k] = (uint32_t)k;
 }
 
 // x-list from the y ranks in x order
-__global__ void k_make_xlist(const uint32_t* __restrict__ ryx, int64_t n, uint2* __restrict__ xl)
+__global__ void k_make_xlist(const uint32_t* __restrict__ ryx, int64_t m, uint32_t roff, uint2* __restrict__ xl)
 {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n) xl[k] = make_uint2((uint32_t)k, ryx[k]);
+    if (k < m) xl[k] = make_uint2(roff + (uint32_t)k, roff + ryx[k]);
 }
 
 // offsets of level 0
@@ -982,9 +989,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
         if ((rc = talloc(&scratch, cub_bytes))) break;
     } while (0);
     if (rc) { tfree(); return rc; }
-    // 64-bit keys of the fallback live in the (then unused) list buffers
-    k64a = reinterpret_cast<uint64_t*>(xl);
-    k64b = reinterpret_cast<uint64_t*>(yl);
+    k64a = k64b = nullptr;                  // 64-bit keys of the fallback: allocated when needed
 
     auto body = [&]() -> int {
         // ---- A0: validate, canonical coordinates, ranges
@@ -1002,58 +1007,80 @@ int build_tree(fmm2d_plan* P, const double2* z)
             FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
             if (h.bad) return FMM2D_ENONFINITE;
         }
-        // ---- presort: the (x, idx) order, then the (y, idx) order, as ranks (DESIGN 6.1)
+        // ---- presort: the (x, idx) order, then the (y, idx) order, as ranks (DESIGN 6.1),
+        // of m points (all, or one level-k box of a partitioned build: sub, roff, its bounds)
         const bool force64 = (P->flags & FMM2D_TREE_KEY64) != 0;
-        int h_ovf[2] = {0, 0};
-        FMM2D_CUDA_TRY(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), st));
-        size_t sb = cub_bytes;
-        if (!force64) {
-            // x: stable sort of 32-bit keys, payload {idx, y key}; equal-key runs fixed
-            k_keys_x<false><<<grid_for(n, BS), BS, 0, st>>>(zc, n, bnd, k32a, nullptr, v64a);
-            fmm2d::note_launch();
-            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, v64a, vx, (int)n, 0, 32, st));
-            k_fix_runs<<<grid_for(n, BS), BS, 0, st>>>(k32b, n, zc, 0, 0, vx, ovf);
-            fmm2d::note_launch();
-            FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_ovf[0], ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
-            FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
-        }
-        if (force64 || h_ovf[0]) {
-            // heavy ties in x: full 64-bit orderable keys (ties leave in idx order)
-            k_keys_x<true><<<grid_for(n, BS), BS, 0, st>>>(zc, n, bnd, nullptr, k64a, v64a);
+        auto presort = [&](const uint32_t* sub, int64_t m, uint32_t roff, const Bounds* bm) -> int {
+            if (m == 0) return 0;
+            int mbits = 1;
+            while (((int64_t)1 << mbits) < m) ++mbits;
+            uint64_t* vxm = vx + roff;
+            uint64_t* vym = vy + roff;
+            int h_ovf[2] = {0, 0};
+            FMM2D_CUDA_TRY(cudaMemsetAsync(ovf, 0, 2 * sizeof(int), st));
+            size_t sb = cub_bytes;
+            if (!force64) {
+                // x: stable sort of 32-bit keys, payload {idx, y key}; equal-key runs fixed
+                k_keys_x<false><<<grid_for(m, BS), BS, 0, st>>>(zc, sub, m, bm, k32a, nullptr, v64a);
+                fmm2d::note_launch();
+                FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, v64a, vxm, (int)m, 0, 32, st));
+                k_fix_runs<<<grid_for(m, BS), BS, 0, st>>>(k32b, m, zc, 0, 0, vxm, ovf);
+                fmm2d::note_launch();
+                FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_ovf[0], ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
+                FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+            }
+            uint64_t* k64buf = nullptr;
+            if (force64 || h_ovf[0]) {
+                // heavy ties in x: full 64-bit orderable keys (ties leave in idx order)
+                if (!k64buf) {
+                    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&k64buf, 16 * m, st));
+                    k64a = k64buf;
+                    k64b = k64buf + m;
+                }
+                k_keys_x<true><<<grid_for(m, BS), BS, 0, st>>>(zc, sub, m, bm, nullptr, k64a, v64a);
+                fmm2d::note_launch();
+                sb = cub_bytes;
+                FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k64a, k64b, v64a, vxm, (int)m, 0, 64, st));
+            }
+            if (!force64) {
+                // y: input in x order, key = y key, payload {x rank, idx}; runs fixed by (y, idx)
+                k_prep_y<<<grid_for(m, BS), BS, 0, st>>>(vxm, m, roff, k32a, v64a);
+                fmm2d::note_launch();
+                sb = cub_bytes;
+                FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, v64a, vym, (int)m, 0, 32, st));
+                k_fix_runs<<<grid_for(m, BS), BS, 0, st>>>(k32b, m, zc, 1, 32, vym, ovf + 1);
+                fmm2d::note_launch();
+                FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_ovf[1], ovf + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+                FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+            }
+            if (force64 || h_ovf[1]) {
+                // heavy ties in y: 64-bit keys over the input in idx order
+                if (!k64buf) {
+                    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&k64buf, 16 * m, st));
+                    k64a = k64buf;
+                    k64b = k64buf + m;
+                }
+                k_scatter_rx<<<grid_for(m, BS), BS, 0, st>>>(vxm, m, u32a);
+                fmm2d::note_launch();
+                k_keys_y64<<<grid_for(m, BS), BS, 0, st>>>(zc, sub, u32a, m, roff, k64a, v64a);
+                fmm2d::note_launch();
+                sb = cub_bytes;
+                FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k64a, k64b, v64a, vym, (int)m, 0, 64, st));
+            }
+            if (k64buf) cudaFreeAsync(k64buf, st);
+            FMM2D_CUDA_TRY(cudaGetLastError());
+            P->stats.tree_key64 |= (force64 || h_ovf[0] ? 1 : 0) + (force64 || h_ovf[1] ? 2 : 0);
+            // y-list {rx, k}; the y ranks in x order by one more sort (keys = local x ranks)
+            k_make_ylist<<<grid_for(m, BS), BS, 0, st>>>(vym, m, roff, yl + roff, k32a, u32a);
             fmm2d::note_launch();
             sb = cub_bytes;
-            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k64a, k64b, v64a, vx, (int)n, 0, 64, st));
-        }
-        if (!force64) {
-            // y: input in x order, key = y key, payload {x rank, idx}; runs fixed by (y, idx)
-            k_prep_y<<<grid_for(n, BS), BS, 0, st>>>(vx, n, k32a, v64a);
+            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, u32a, u32b, (int)m, 0, mbits, st));
+            k_make_xlist<<<grid_for(m, BS), BS, 0, st>>>(u32b, m, roff, xl + roff);
             fmm2d::note_launch();
-            sb = cub_bytes;
-            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, v64a, vy, (int)n, 0, 32, st));
-            k_fix_runs<<<grid_for(n, BS), BS, 0, st>>>(k32b, n, zc, 1, 32, vy, ovf + 1);
-            fmm2d::note_launch();
-            FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_ovf[1], ovf + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-            FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
-        }
-        if (force64 || h_ovf[1]) {
-            // heavy ties in y: 64-bit keys over the input in idx order
-            k_scatter_rx<<<grid_for(n, BS), BS, 0, st>>>(vx, n, u32a);
-            fmm2d::note_launch();
-            k_keys_y64<<<grid_for(n, BS), BS, 0, st>>>(zc, u32a, n, k64a, v64a);
-            fmm2d::note_launch();
-            sb = cub_bytes;
-            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k64a, k64b, v64a, vy, (int)n, 0, 64, st));
-        }
-        FMM2D_CUDA_TRY(cudaGetLastError());
-        P->stats.tree_key64 = (force64 || h_ovf[0] ? 1 : 0) + (force64 || h_ovf[1] ? 2 : 0);
-        // y-list {rx, k}; the y ranks in x order by one more sort (keys = x ranks)
-        k_make_ylist<<<grid_for(n, BS), BS, 0, st>>>(vy, n, yl, k32a, u32a);
-        fmm2d::note_launch();
-        sb = cub_bytes;
-        FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, u32a, u32b, (int)n, 0, nbits, st));
-        k_make_xlist<<<grid_for(n, BS), BS, 0, st>>>(u32b, n, xl);
-        fmm2d::note_launch();
-        FMM2D_CUDA_TRY(cudaGetLastError());
+            FMM2D_CUDA_TRY(cudaGetLastError());
+            return 0;
+        };
+        FMM2D_TRY(presort(nullptr, n, 0, bnd));
         k_bbox<<<1, 32, 0, st>>>(xl, yl, vx, vy, zc, P->boff + P->obase[0], 0, 1, P->cx + P->base[0],
                                  P->cy + P->base[0], P->r + P->base[0]);
         fmm2d::note_launch();
