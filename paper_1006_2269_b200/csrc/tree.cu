@@ -28,6 +28,11 @@
 //     writes the permutation, the source rows and every level's exact radius.
 // Every kernel works on a position range [k0, k1) of whole boxes, so a rank of a
 // sharded build continues below the top levels with its own subtrees only.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <utility>
 #include <cub/cub.cuh>
 
 #include "fmm2d_internal.cuh"
@@ -221,6 +226,217 @@ __global__ void k_make_xlist(const uint32_t* __restrict__ ryx, int64_t m, uint32
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < m) xl[k] = make_uint2(roff + (uint32_t)k, roff + ryx[k]);
 }
+
+// ---------------------------------------------------------------- partitioned build (DESIGN 8)
+// Levels 0..k-1 of a partitioned build without a full presort: the split record of every
+// (half-)box -- the first high record in (coordinate, idx) order -- is found by radix
+// selection over all points (replicated on every rank), then each rank presorts only the
+// points of its own level-k boxes.  A split record is {orderable 64-bit coordinate, idx};
+// "(c, i) >= record" is the high side.
+// FMM2D_TREE_TRACE=1: event times of the partitioned build's phases on stderr (diagnostics)
+struct PhaseTrace {
+    cudaStream_t st;
+    bool on;
+    std::vector<std::pair<std::string, cudaEvent_t>> ev;
+    explicit PhaseTrace(cudaStream_t s) : st(s), on(std::getenv("FMM2D_TREE_TRACE") != nullptr) {}
+    void mark(const std::string& name)
+    {
+        if (!on) return;
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        cudaEventRecord(e, st);
+        ev.emplace_back(name, e);
+    }
+    ~PhaseTrace()
+    {
+        if (!on || ev.empty()) return;
+        cudaEventSynchronize(ev.back().second);
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+            std::fprintf(stderr, "[fmm2d tree] %-28s %9.3f ms\n", ev[i].first.c_str(), ms);
+        }
+        for (auto& x : ev) cudaEventDestroy(x.second);
+    }
+};
+
+struct TopRec {
+    unsigned long long key;
+    uint32_t idx, pad;
+};
+
+__device__ __forceinline__ bool rec_ge(unsigned long long key, uint32_t idx, const TopRec& r)
+{
+    return key > r.key || (key == r.key && idx >= r.idx);
+}
+
+// the (half-)box of point (x, y, i) after `steps` split steps (x-split, y-split, ...),
+// given the records of those steps: xr[l][box], yr[l][half] packed level by level
+__device__ __forceinline__ uint32_t top_segment(double x, double y, uint32_t i, int steps,
+                                                const TopRec* __restrict__ recs, const int* __restrict__ roff)
+{
+    const unsigned long long kx = orderable(x), ky = orderable(y);
+    uint32_t seg = 0;
+    for (int st = 0; st < steps; ++st) {
+        const bool ax = (st & 1) != 0;                  // even steps: x-split, odd: y-split
+        const TopRec& r = recs[roff[st] + seg];
+        seg = 2 * seg + (rec_ge(ax ? ky : kx, i, r) ? 1u : 0u);
+    }
+    return seg;
+}
+
+// Selection state of one segment: the record sought is the want-th (in (key, idx) order)
+// of the segment's points inside the current range, which is split into SEL_BUCKETS buckets.
+//   mode 1: keys in [lo, lo + SEL_BUCKETS << shift), bucket (key - lo) >> shift
+//   mode 2: key == keyfix, idx in [lo, lo + SEL_BUCKETS << shift), bucket (idx - lo) >> shift
+//   mode 3 / 4: as 1 / 2, collect the points of bucket 0 (candidates); mode 0: idle
+struct SelSeg {
+    unsigned long long lo, keyfix;
+    int shift, mode;
+};
+constexpr int SEL_BITS = 12;
+constexpr int SEL_BUCKETS = 1 << SEL_BITS;   // per segment and pass (a 16 KB shared histogram)
+constexpr int SEL_SMEM_SEGS = 12;             // segments per pass that fit the shared histogram
+constexpr int SEL_COLLECT = 4096;             // a bucket this small is sorted on the host
+
+__device__ __forceinline__ int sel_bucket(const SelSeg& S, unsigned long long key, uint32_t i)
+{
+    unsigned long long v;
+    if (S.mode == 1 || S.mode == 3) {
+        if (key < S.lo) return -1;
+        v = (key - S.lo) >> S.shift;
+    } else if (S.mode == 2 || S.mode == 4) {
+        if (key != S.keyfix || (unsigned long long)i < S.lo) return -1;
+        v = ((unsigned long long)i - S.lo) >> S.shift;
+    } else {
+        return -1;
+    }
+    return v < (unsigned long long)SEL_BUCKETS ? (int)v : -1;
+}
+
+// histogram of the buckets of every segment in mode 1 / 2: persistent blocks, one shared
+// histogram per block (flushed with one global atomic per non-zero bin), or global atomics
+// when the segments' histograms do not fit (SMEM = false)
+template <bool SMEM>
+__global__ void __launch_bounds__(1024) k_top_hist(const double2* __restrict__ zc, int64_t n, int step,
+                                                   const TopRec* __restrict__ recs, const int* __restrict__ roff,
+                                                   const SelSeg* __restrict__ sel, int nseg,
+                                                   unsigned int* __restrict__ hist)
+{
+    extern __shared__ unsigned int shist[];
+    if (SMEM) {
+        for (int j = threadIdx.x; j < nseg * SEL_BUCKETS; j += blockDim.x) shist[j] = 0;
+        __syncthreads();
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 v = zc[i];
+        const uint32_t seg = top_segment(v.x, v.y, (uint32_t)i, step, recs, roff);
+        const SelSeg S = sel[seg];
+        if (S.mode != 1 && S.mode != 2) continue;
+        const int b = sel_bucket(S, orderable((step & 1) ? v.y : v.x), (uint32_t)i);
+        if (b < 0) continue;
+        if (SMEM)
+            atomicAdd(&shist[seg * SEL_BUCKETS + b], 1u);
+        else
+            atomicAdd(&hist[(int64_t)seg * SEL_BUCKETS + b], 1u);
+    }
+    if (SMEM) {
+        __syncthreads();
+        for (int j = threadIdx.x; j < nseg * SEL_BUCKETS; j += blockDim.x)
+            if (shist[j]) atomicAdd(&hist[j], shist[j]);
+    }
+}
+
+// the points of bucket 0 of every segment in mode 3 / 4: {key, idx} appended per segment
+__global__ void k_top_cand(const double2* __restrict__ zc, int64_t n, int step, const TopRec* __restrict__ recs,
+                           const int* __restrict__ roff, const SelSeg* __restrict__ sel,
+                           const int64_t* __restrict__ coff, unsigned int* __restrict__ ccnt, TopRec* __restrict__ cand)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double2 v = zc[i];
+    const uint32_t seg = top_segment(v.x, v.y, (uint32_t)i, step, recs, roff);
+    const SelSeg S = sel[seg];
+    if (S.mode != 3 && S.mode != 4) return;
+    const unsigned long long k = orderable((step & 1) ? v.y : v.x);
+    if (sel_bucket(S, k, (uint32_t)i) != 0) return;
+    const unsigned int at = atomicAdd(&ccnt[seg], 1u);
+    TopRec r;
+    r.key = k;
+    r.idx = (uint32_t)i;
+    r.pad = 0;
+    cand[coff[seg] + at] = r;
+}
+
+// level-k box of every point, and per level-k box the min / max orderable coordinates
+// (shared-memory reduction per block, one global atomic per block and box)
+__global__ void __launch_bounds__(256) k_top_box(const double2* __restrict__ zc, int64_t n, int steps,
+                                                 const TopRec* __restrict__ recs, const int* __restrict__ roff,
+                                                 int nbk, uint32_t* __restrict__ boxk,
+                                                 unsigned long long* __restrict__ bb)   // [4][nbk]
+{
+    __shared__ unsigned long long sb[4][256];
+    for (int j = threadIdx.x; j < 4 * nbk; j += 256) sb[j / nbk][j % nbk] = (j / nbk) & 1 ? 0ull : ~0ull;
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const double2 v = zc[i];
+        const uint32_t b = top_segment(v.x, v.y, (uint32_t)i, steps, recs, roff);
+        boxk[i] = b;
+        const unsigned long long kx = orderable(v.x), ky = orderable(v.y);
+        atomicMin(&sb[0][b], kx);
+        atomicMax(&sb[1][b], kx);
+        atomicMin(&sb[2][b], ky);
+        atomicMax(&sb[3][b], ky);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < nbk; j += 256) {
+        if (sb[0][j] != ~0ull) {
+            atomicMin(&bb[j], sb[0][j]);
+            atomicMax(&bb[nbk + j], sb[1][j]);
+            atomicMin(&bb[2 * nbk + j], sb[2][j]);
+            atomicMax(&bb[3 * nbk + j], sb[3][j]);
+        }
+    }
+}
+
+// discs of levels 0..k from the level-k boxes' bounds (a box's bounds are the union of its
+// descendants'); bounds of each level-k box also as the presort's key range (Bounds)
+__global__ void k_top_discs(const unsigned long long* __restrict__ bb, int k, double* __restrict__ cx,
+                            double* __restrict__ cy, double* __restrict__ r, Bounds* __restrict__ bnds)
+{
+    const int nbk = 1 << (2 * k);
+    int g = 0;                                        // global box id over levels 0..k
+    for (int l = 0; l <= k; ++l) {
+        const int nb = 1 << (2 * l), span = 1 << (2 * (k - l));
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+            unsigned long long a = ~0ull, c = 0, d = ~0ull, e = 0;
+            for (int q = b * span; q < (b + 1) * span; ++q) {
+                a = min(a, bb[q]);
+                c = max(c, bb[nbk + q]);
+                d = min(d, bb[2 * nbk + q]);
+                e = max(e, bb[3 * nbk + q]);
+            }
+            cx[g + b] = __dmul_rn(0.5, __dadd_rn(from_orderable(a), from_orderable(c)));
+            cy[g + b] = __dmul_rn(0.5, __dadd_rn(from_orderable(d), from_orderable(e)));
+            r[g + b] = 0.0;
+            if (l == k) {
+                bnds[b].xmin = a;
+                bnds[b].xmax = c;
+                bnds[b].ymin = d;
+                bnds[b].ymax = e;
+                bnds[b].bad = 0;
+            }
+        }
+        g += nb;
+    }
+}
+
+struct BoxIs {
+    const uint32_t* boxk;
+    uint32_t b;
+    __device__ __forceinline__ bool operator()(const uint32_t& i) const { return boxk[i] == b; }
+};
 
 // offsets of level 0
 __global__ void k_root_off(uint32_t* __restrict__ O, uint32_t n)
@@ -904,6 +1120,224 @@ int finish_radii(fmm2d_plan* P)
 
 static int build_tree_midpoint(fmm2d_plan* P, const double2* z);
 
+// Partitioned build, levels 0..k (DESIGN 8): split records by selection, level-k boxes and
+// their discs (replicated, identical on every rank), then the presort of each own level-k
+// box's points (ascending input index, ranks offset by the box's first position).
+template <class Presort>
+static int top_levels_sharded(fmm2d_plan* P, const double2* zc, const Bounds& hb_all, const std::vector<int64_t>& hbase,
+                              Presort& presort)
+{
+    cudaStream_t st = P->stream;
+    const int64_t n = P->n;
+    const int k = P->kpart;
+    const int nsteps = 2 * k;
+    const int BS = 256;
+    // segments of each step and their sizes (pure functions of n: host offsets)
+    std::vector<int> roff(nsteps + 1, 0);
+    std::vector<int64_t> seg_n, seg_hi;             // per step, per segment: size, first high index
+    auto bstart = [&](int l, int64_t b) -> int64_t {     // start of box b of level l (b = 4^l: n)
+        return (b >= ((int64_t)1 << (2 * l))) ? n : box_start_host(n, l, b);
+    };
+    for (int s = 0; s < nsteps; ++s) {
+        const int l = s / 2;
+        const int nseg = (s & 1) ? 2 << (2 * l) : 1 << (2 * l);
+        roff[s + 1] = roff[s] + nseg;
+        for (int g = 0; g < nseg; ++g) {
+            int64_t a, b;
+            if (s & 1) {                                // half g of level-l box g/2
+                const int64_t bs = bstart(l, g / 2), be = bstart(l, g / 2 + 1);
+                const int64_t sz = be - bs, h0 = sz - sz / 2;
+                a = (g & 1) ? bs + h0 : bs;
+                b = (g & 1) ? be : bs + h0;
+            } else {
+                a = bstart(l, g);
+                b = bstart(l, g + 1);
+            }
+            seg_n.push_back(b - a);
+            seg_hi.push_back((b - a) - (b - a) / 2);     // index of the first high record
+        }
+    }
+    TopRec* d_recs = nullptr;
+    int* d_roff = nullptr;
+    unsigned int *hist = nullptr, *ccnt = nullptr;
+    SelSeg* sel = nullptr;
+    int64_t* coff = nullptr;
+    TopRec* cand = nullptr;
+    uint32_t *boxk = nullptr, *sub = nullptr;
+    int64_t* d_nsel = nullptr;
+    unsigned long long* bb = nullptr;
+    Bounds* bnds = nullptr;
+    void* scratch = nullptr;
+    std::vector<void*> tmp;
+    auto talloc = [&](void** p, size_t b) -> int {
+        if (cudaMallocAsync(p, b ? b : 16, st) != cudaSuccess) return FMM2D_ENOMEM;
+        tmp.push_back(*p);
+        return 0;
+    };
+    const int maxseg = 2 << (2 * (k - 1));
+    const int nbk = 1 << (2 * k);
+    PhaseTrace tr(st);
+    tr.mark("start");
+    auto body = [&]() -> int {
+        FMM2D_TRY(talloc((void**)&d_recs, sizeof(TopRec) * std::max(1, roff[nsteps])));
+        FMM2D_TRY(talloc((void**)&d_roff, sizeof(int) * (nsteps + 1)));
+        FMM2D_TRY(talloc((void**)&hist, sizeof(unsigned int) * SEL_BUCKETS * maxseg));
+        FMM2D_TRY(talloc((void**)&sel, sizeof(SelSeg) * maxseg));
+        FMM2D_TRY(talloc((void**)&cand, sizeof(TopRec) * SEL_COLLECT * maxseg));
+        FMM2D_TRY(talloc((void**)&ccnt, sizeof(unsigned int) * maxseg));
+        FMM2D_TRY(talloc((void**)&coff, sizeof(int64_t) * maxseg));
+        FMM2D_TRY(talloc((void**)&boxk, sizeof(uint32_t) * n));
+        FMM2D_TRY(talloc((void**)&sub, sizeof(uint32_t) * n));
+        FMM2D_TRY(talloc((void**)&d_nsel, sizeof(int64_t)));
+        FMM2D_TRY(talloc((void**)&bb, sizeof(unsigned long long) * 4 * nbk));
+        FMM2D_TRY(talloc((void**)&bnds, sizeof(Bounds) * nbk));
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(d_roff, roff.data(), sizeof(int) * (nsteps + 1), cudaMemcpyHostToDevice, st));
+        std::vector<TopRec> h_recs(std::max(1, roff[nsteps]));
+        std::vector<unsigned int> h_hist((size_t)SEL_BUCKETS * maxseg);
+        std::vector<SelSeg> hs(maxseg);
+        std::vector<int64_t> want(maxseg), hcoff(maxseg), ccap(maxseg);
+        auto shift_for = [](unsigned long long range) {
+            int s = 0;
+            while (s < 63 && (range >> s) >= (unsigned long long)SEL_BUCKETS) ++s;
+            return s;
+        };
+        int64_t si = 0;                                  // index into seg_n / seg_hi
+        for (int s = 0; s < nsteps; ++s) {
+            const int nseg = roff[s + 1] - roff[s];
+            const unsigned long long gmin = (s & 1) ? hb_all.ymin : hb_all.xmin;
+            const unsigned long long gmax = (s & 1) ? hb_all.ymax : hb_all.xmax;
+            int nhist = 0;
+            for (int g = 0; g < nseg; ++g) {
+                want[g] = seg_hi[si + g];
+                hs[g].lo = gmin;
+                hs[g].keyfix = 0;
+                hs[g].shift = shift_for(gmax - gmin);
+                if (want[g] >= seg_n[si + g]) {          // no high record: every point is low
+                    hs[g].mode = 0;
+                    h_recs[roff[s] + g] = TopRec{~0ull, ~0u, 0u};
+                } else {
+                    hs[g].mode = 1;
+                    ++nhist;
+                }
+            }
+            // narrow each segment's range until its bucket holds at most SEL_COLLECT points
+            int npass = 0;
+            while (nhist > 0) {
+                ++npass;
+                FMM2D_CUDA_TRY(cudaMemcpyAsync(sel, hs.data(), sizeof(SelSeg) * nseg, cudaMemcpyHostToDevice, st));
+                FMM2D_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * SEL_BUCKETS * nseg, st));
+                if (nseg <= SEL_SMEM_SEGS) {
+                    const int sm = nseg * SEL_BUCKETS * 4;
+                    FMM2D_CUDA_TRY(cudaFuncSetAttribute(k_top_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+                    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(148, (n + 1023) / 1024));
+                    k_top_hist<true><<<g, 1024, sm, st>>>(zc, n, s, d_recs, d_roff, sel, nseg, hist);
+                } else {
+                    k_top_hist<false><<<grid_for(n, BS), BS, 0, st>>>(zc, n, s, d_recs, d_roff, sel, nseg, hist);
+                }
+                note_launch();
+                FMM2D_CUDA_TRY(cudaMemcpyAsync(h_hist.data(), hist, sizeof(unsigned int) * SEL_BUCKETS * nseg,
+                                               cudaMemcpyDeviceToHost, st));
+                FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+                nhist = 0;
+                for (int g = 0; g < nseg; ++g) {
+                    SelSeg& S = hs[g];
+                    if (S.mode != 1 && S.mode != 2) continue;
+                    const unsigned int* H = h_hist.data() + (size_t)g * SEL_BUCKETS;
+                    int64_t acc = 0;
+                    int b = 0;
+                    for (; b < SEL_BUCKETS; ++b) {
+                        if (acc + H[b] > want[g]) break;
+                        acc += H[b];
+                    }
+                    if (b == SEL_BUCKETS) return FMM2D_ECUDA;     // inconsistent counts (cannot happen)
+                    want[g] -= acc;
+                    S.lo += (unsigned long long)b << S.shift;
+                    if (H[b] <= (unsigned)SEL_COLLECT) {
+                        S.mode += 2;                              // collect bucket 0 of [lo, ...)
+                        ccap[g] = H[b];
+                    } else if (S.shift > SEL_BITS) {
+                        S.shift -= SEL_BITS;
+                        ++nhist;
+                    } else if (S.shift > 0) {
+                        S.shift = 0;
+                        ++nhist;
+                    } else if (S.mode == 1) {                     // one key, many points: select by idx
+                        S.mode = 2;
+                        S.keyfix = S.lo;
+                        S.lo = 0;
+                        S.shift = shift_for((unsigned long long)n);
+                        ++nhist;
+                    } else {
+                        return FMM2D_ECUDA;                       // one (key, idx) counted twice
+                    }
+                }
+            }
+            int64_t ctot = 0;
+            int ncol = 0;
+            for (int g = 0; g < nseg; ++g) {
+                hcoff[g] = ctot;
+                if (hs[g].mode >= 3) {
+                    ctot += ccap[g];
+                    ++ncol;
+                }
+            }
+            if (ncol > 0) {
+                FMM2D_CUDA_TRY(cudaMemcpyAsync(sel, hs.data(), sizeof(SelSeg) * nseg, cudaMemcpyHostToDevice, st));
+                FMM2D_CUDA_TRY(cudaMemcpyAsync(coff, hcoff.data(), sizeof(int64_t) * nseg, cudaMemcpyHostToDevice, st));
+                FMM2D_CUDA_TRY(cudaMemsetAsync(ccnt, 0, sizeof(unsigned int) * nseg, st));
+                k_top_cand<<<grid_for(n, BS), BS, 0, st>>>(zc, n, s, d_recs, d_roff, sel, coff, ccnt, cand);
+                note_launch();
+                std::vector<TopRec> hc(std::max<int64_t>(ctot, 1));
+                FMM2D_CUDA_TRY(cudaMemcpyAsync(hc.data(), cand, sizeof(TopRec) * ctot, cudaMemcpyDeviceToHost, st));
+                FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+                for (int g = 0; g < nseg; ++g) {
+                    if (hs[g].mode < 3) continue;
+                    const int64_t c0 = hcoff[g], c1 = c0 + ccap[g];
+                    std::sort(hc.begin() + c0, hc.begin() + c1, [](const TopRec& a, const TopRec& b) {
+                        return a.key < b.key || (a.key == b.key && a.idx < b.idx);
+                    });
+                    h_recs[roff[s] + g] = hc[c0 + want[g]];
+                }
+            }
+            FMM2D_CUDA_TRY(cudaMemcpyAsync(d_recs + roff[s], h_recs.data() + roff[s], sizeof(TopRec) * nseg,
+                                           cudaMemcpyHostToDevice, st));
+            si += nseg;
+            tr.mark("select step " + std::to_string(s) + " (" + std::to_string(npass) + " passes)");
+        }
+        // level-k boxes of all points, their bounds; discs of levels 0..k
+        std::vector<unsigned long long> hbb(4 * (size_t)nbk);
+        for (int j = 0; j < nbk; ++j) {
+            hbb[j] = ~0ull;
+            hbb[nbk + j] = 0;
+            hbb[2 * nbk + j] = ~0ull;
+            hbb[3 * nbk + j] = 0;
+        }
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(bb, hbb.data(), 8 * hbb.size(), cudaMemcpyHostToDevice, st));
+        k_top_box<<<grid_for(n, 256), 256, 0, st>>>(zc, n, nsteps, d_recs, d_roff, nbk, boxk, bb);
+        note_launch();
+        k_top_discs<<<1, 256, 0, st>>>(bb, k, P->cx, P->cy, P->r, bnds);
+        note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+        tr.mark("level-k boxes");
+        // presort of each own level-k box (its points in ascending input index)
+        size_t sb = 0;
+        cub::CountingInputIterator<uint32_t> it(0);
+        cub::DeviceSelect::If(nullptr, sb, it, sub, d_nsel, (int64_t)n, BoxIs{boxk, 0u}, st);
+        FMM2D_TRY(talloc(&scratch, sb));
+        for (int64_t R = P->own_lo(k); R < P->own_hi(k); ++R) {
+            size_t s2 = sb;
+            FMM2D_CUDA_TRY(cub::DeviceSelect::If(scratch, s2, it, sub, d_nsel, (int64_t)n, BoxIs{boxk, (uint32_t)R}, st));
+            const int64_t r0 = bstart(k, R), r1 = bstart(k, R + 1);
+            FMM2D_TRY(presort(sub, r1 - r0, (uint32_t)r0, bnds + R));
+            tr.mark("presort box " + std::to_string(R));
+        }
+        return 0;
+    };
+    const int rc = body();
+    for (void* p : tmp) cudaFreeAsync(p, st);
+    return rc;
+}
+
 int build_tree(fmm2d_plan* P, const double2* z)
 {
     if (P->flags & FMM2D_MIDPOINT) return build_tree_midpoint(P, z);
@@ -991,6 +1425,9 @@ int build_tree(fmm2d_plan* P, const double2* z)
     if (rc) { tfree(); return rc; }
     k64a = k64b = nullptr;                  // 64-bit keys of the fallback: allocated when needed
 
+    Bounds hall;                            // host copy of the global ranges (partitioned top levels)
+    PhaseTrace trb(st);
+    trb.mark("tree start");
     auto body = [&]() -> int {
         // ---- A0: validate, canonical coordinates, ranges
         {
@@ -1006,6 +1443,8 @@ int build_tree(fmm2d_plan* P, const double2* z)
             FMM2D_CUDA_TRY(cudaMemcpyAsync(&h, bnd, sizeof(h), cudaMemcpyDeviceToHost, st));
             FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
             if (h.bad) return FMM2D_ENONFINITE;
+            hall = h;
+            trb.mark("canon");
         }
         // ---- presort: the (x, idx) order, then the (y, idx) order, as ranks (DESIGN 6.1),
         // of m points (all, or one level-k box of a partitioned build: sub, roff, its bounds)
@@ -1080,10 +1519,17 @@ int build_tree(fmm2d_plan* P, const double2* z)
             FMM2D_CUDA_TRY(cudaGetLastError());
             return 0;
         };
-        FMM2D_TRY(presort(nullptr, n, 0, bnd));
-        k_bbox<<<1, 32, 0, st>>>(xl, yl, vx, vy, zc, P->boff + P->obase[0], 0, 1, P->cx + P->base[0],
-                                 P->cy + P->base[0], P->r + P->base[0]);
-        fmm2d::note_launch();
+        if (P->nranks == 1) {
+            FMM2D_TRY(presort(nullptr, n, 0, bnd));
+        } else {
+            FMM2D_TRY(top_levels_sharded(P, zc, hall, hbase, presort));
+        }
+        trb.mark("presort / top levels");
+        if (P->nranks == 1) {
+            k_bbox<<<1, 32, 0, st>>>(xl, yl, vx, vy, zc, P->boff + P->obase[0], 0, 1, P->cx + P->base[0],
+                                     P->cy + P->base[0], P->r + P->base[0]);
+            fmm2d::note_launch();
+        }
         // one split step: partition `list` inside the parent segments (par_off) [p0, p1),
         // positions [k0, k1), into the sub-segments sub_off, comparing ranks on `axis`
         // against `split`
@@ -1137,7 +1583,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
         for (int l = std::max(P->kpart, L - LLEV); l < L; ++l)
             if ((n + nboxes(l) - 1) / nboxes(l) <= LMAX) { l0 = l; break; }
         if (P->flags & FMM2D_TREE_GLOBAL_ONLY) l0 = L;
-        for (int l = 0; l < l0; ++l) {
+        for (int l = (P->nranks > 1 ? P->kpart : 0); l < l0; ++l) {   // partitioned: top levels done by selection
             const uint32_t* O = P->boff + P->obase[l];
             const uint32_t* H = P->boff + hbase[l];
             const uint32_t* C = P->boff + P->obase[l + 1];
@@ -1157,6 +1603,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
             fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
         }
+        trb.mark("global split levels");
         if (l0 < L) {
             LocalArgs A;
             A.yl = yl;
@@ -1198,6 +1645,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
         fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
         if (P->nranks == 1) FMM2D_TRY(finish_radii(P));
+        trb.mark("local levels + finish");
         return 0;
     };
     rc = body();

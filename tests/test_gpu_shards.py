@@ -113,3 +113,37 @@ def test_loopback_shards_with_parent_merge(orc):
         torch.cuda.synchronize()
         assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
         sh.close()
+
+
+@pytest.mark.parametrize("name", ["lattice-ties", "dups-negzero"])
+def test_loopback_shards_ties_and_duplicates(name):
+    """Split records found by selection with heavy ties (lattice, duplicates, -0) and the
+    per-box presort's 64-bit fallback: shards still equal the one-GPU result bit for bit."""
+    from paper_1006_2269_b200 import Fmm2d, LoopbackShards
+    if name == "lattice-ties":
+        z_np = W.lattice(8, 3, h=0.5, shuffle_seed=4)
+        L = 4
+    else:
+        rng = np.random.default_rng(12)
+        n = 20_000
+        # heavy ties in each coordinate (never two coincident points): x on a grid of 51
+        # values (-0.0 among them), a block of 600 with x = 0.5, then y = 0.25 on 300 of
+        # them with x moved off the tie
+        x = np.round(rng.random(n) * 50) / 50
+        y = rng.random(n)
+        x[:40] = -0.0
+        x[100:700] = 0.5
+        y[100:400] = 0.25
+        x[100:400] = np.arange(300) * 1e-6 + 0.5
+        z_np = x + 1j * y
+        L = 4
+    m_np = np.random.default_rng(1).uniform(-1, 1, z_np.shape[0]) + 0j
+    z, m = torch.from_numpy(z_np).cuda(), torch.from_numpy(m_np).cuda()
+    ref = Fmm2d(z, theta=0.5, p=12, nlevels=L)
+    a = ref.eval(m)
+    for P in (2, 8):
+        sh = LoopbackShards(z, P, theta=0.5, p=12, nlevels=L)
+        b = sh.eval(m)
+        torch.cuda.synchronize()
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+        sh.close()
