@@ -530,6 +530,12 @@ __global__ void k_seg_prep(const uint32_t* __restrict__ par_off, const uint32_t*
 #ifndef FMM2D_PART_PT
 #define FMM2D_PART_PT 256
 #endif
+// 1: the tile's records are regrouped in shared memory (lows, then highs, each in order)
+// and written with consecutive threads on consecutive destinations; 0: each thread
+// writes its own records (8-record stride across a warp)
+#ifndef FMM2D_PART_STAGED_OUT
+#define FMM2D_PART_STAGED_OUT 1
+#endif
 constexpr int PT = FMM2D_PART_PT, PI = FMM2D_PART_PI, PTILE = PT * PI;
 constexpr int PTILE_SHIFT = (PTILE == 1024) ? 10 : (PTILE == 2048) ? 11 : (PTILE == 4096) ? 12 : 13;
 static_assert(PTILE == (1 << PTILE_SHIFT), "tile size");
@@ -562,6 +568,9 @@ __global__ void __launch_bounds__(PT) k_partition(SplitArgs A)
     __shared__ uint32_t s_prefix;
     __shared__ __align__(16) uint2 stage[PTILE];
     __shared__ uint32_t s_off[SEGMAX + 1], s_hi[SEGMAX], s_gp[SEGMAX], s_split[SEGMAX];
+#if FMM2D_PART_STAGED_OUT
+    __shared__ uint32_t s_dst[PTILE];
+#endif
     const int tid = threadIdx.x;
     const uint32_t tile = blockIdx.x;
     const uint32_t kt = A.k0 + tile * (uint32_t)PTILE;
@@ -677,6 +686,12 @@ __global__ void __launch_bounds__(PT) k_partition(SplitArgs A)
     }
     __syncthreads();
     uint32_t g = s_prefix + excl;             // G(k) for the first item of this thread
+#if FMM2D_PART_STAGED_OUT
+    // every thread holds its records in registers (stage is free): lows at their rank
+    // among the tile's lows, highs after them at their rank among the tile's highs
+    uint32_t hl = excl;                       // highs before the item inside the tile
+    const uint32_t nlow = (uint32_t)nrec - agg;
+#endif
 #pragma unroll
     for (int u = 0; u < PI; ++u) {
         if (i0 + u < nrec) {
@@ -692,10 +707,21 @@ __global__ void __launch_bounds__(PT) k_partition(SplitArgs A)
             }
             const uint32_t hb = g - gp;       // highs before k inside its segment
             const uint32_t dst = f[u] ? hstart + hb : k - hb;
+#if FMM2D_PART_STAGED_OUT
+            const uint32_t loc = f[u] ? nlow + hl : (uint32_t)(i0 + u) - hl;
+            stage[loc] = r[u];
+            s_dst[loc] = dst;
+            hl += f[u];
+#else
             A.out[dst] = r[u];
+#endif
         }
         g += f[u];
     }
+#if FMM2D_PART_STAGED_OUT
+    __syncthreads();
+    for (int v = tid; v < nrec; v += PT) A.out[s_dst[v]] = stage[v];
+#endif
 }
 
 // The deepest levels in shared memory: once a box holds at most LMAX points, one CTA
