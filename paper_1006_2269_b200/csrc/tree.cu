@@ -897,10 +897,16 @@ __global__ void k_bbox(const uint2* __restrict__ xl, const uint2* __restrict__ y
 // Final order + A2 (part 2) for every level in one pass.  The final y-list is the
 // leaf order (leaves ascending, (y, idx) inside, R13): write perm and the source
 // rows, then r(box) = exact max distance (correctly rounded sqrt, no FMA) for the
-// box of every level containing the point: a block-wide max when the whole block
-// lies in one box (upper levels), else a segmented warp max; one atomicMax on the
-// bit pattern per segment (non-negative doubles order like their uint64 bits).
-constexpr int FIN_T = 256;
+// box of every level containing the point.  A block takes FIN_C chunks of FIN_T
+// consecutive positions (the gathers of all chunks in flight together).  Levels at which
+// the block's whole range lies in one box: per-thread then per-warp max, the warps'
+// maxima of all such levels combined after ONE barrier, one atomicMax per level and
+// block; other levels: a segmented warp max per chunk, one atomicMax per run (on the
+// bit pattern: non-negative doubles order like their uint64 bits).
+#ifndef FMM2D_FIN_C
+#define FMM2D_FIN_C 4
+#endif
+constexpr int FIN_T = 256, FIN_C = FMM2D_FIN_C, FIN_B = FIN_T * FIN_C;
 struct RadArgs {
     const double* cx[FMM2D_MAXL + 1];
     const double* cy[FMM2D_MAXL + 1];
@@ -912,61 +918,85 @@ __global__ void __launch_bounds__(FIN_T) k_finish(const uint2* __restrict__ yl, 
                                                   uint32_t lf0, uint32_t lf1, uint32_t* __restrict__ perm,
                                                   double4* __restrict__ src, RadArgs A)
 {
-    __shared__ uint32_t sleaf[FIN_T];
     __shared__ uint32_t s_lo, s_hi;
-    __shared__ double wmax[FIN_T / 32];
+    __shared__ double wmax[FMM2D_MAXL + 1][FIN_T / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t kb = k0 + blockIdx.x * FIN_T;
-    const uint32_t k = kb + tid;
-    const int nvalid = (int)min((uint32_t)FIN_T, k1 - kb);
-    const bool valid = k < k1;
+    const uint32_t kb = k0 + blockIdx.x * FIN_B;
+    const int nvalid = (int)min((uint32_t)FIN_B, k1 - kb);
     if (tid == 0) {
         const uint32_t lo = seg_search(offL, lf0, lf1, kb);
         s_lo = lo;
         s_hi = seg_search(offL, lo, lf1, kb + nvalid - 1) + 1;
     }
-    __syncthreads();
-    double x = 0.0, y = 0.0;
-    uint32_t leaf = 0;
-    if (valid) {
-        const uint32_t ry = yl[k].y;
-        leaf = seg_search(offL, s_lo, s_hi, k);
-        const uint32_t idx = (uint32_t)(vy[ry] >> 32);
-        const double2 zz = zc[idx];
-        x = zz.x;
-        y = zz.y;
-        perm[k] = idx;
-        src[k] = make_double4(x, y, 0.0, 0.0);
+    uint32_t ry[FIN_C], idx[FIN_C], leaf[FIN_C];
+    double x[FIN_C], y[FIN_C];
+#pragma unroll
+    for (int c = 0; c < FIN_C; ++c) {
+        const int i = c * FIN_T + tid;
+        ry[c] = i < nvalid ? yl[kb + i].y : 0u;
     }
-    sleaf[tid] = leaf;
+#pragma unroll
+    for (int c = 0; c < FIN_C; ++c) idx[c] = (c * FIN_T + tid < nvalid) ? (uint32_t)(vy[ry[c]] >> 32) : 0u;
+#pragma unroll
+    for (int c = 0; c < FIN_C; ++c) {
+        x[c] = y[c] = 0.0;
+        if (c * FIN_T + tid < nvalid) {
+            const double2 zz = zc[idx[c]];
+            x[c] = zz.x;
+            y[c] = zz.y;
+        }
+    }
     __syncthreads();
-    const uint32_t l0 = sleaf[0], l1 = sleaf[nvalid - 1];
+    const uint32_t l0 = s_lo, l1 = s_hi - 1;
+#pragma unroll
+    for (int c = 0; c < FIN_C; ++c) {
+        const int i = c * FIN_T + tid;
+        leaf[c] = 0;
+        if (i < nvalid) {
+            const uint32_t k = kb + i;
+            leaf[c] = seg_search(offL, l0, l1 + 1, k);
+            perm[k] = idx[c];
+            src[k] = make_double4(x[c], y[c], 0.0, 0.0);
+        }
+    }
     for (int l = L; l >= 0; --l) {
         const int sh = 2 * (L - l);
-        const uint32_t box = leaf >> sh;
-        double d = 0.0;
-        if (valid) d = rn_dist2(x, y, A.cx[l][box], A.cy[l][box]);     // squared; sqrt below
-        if ((l0 >> sh) == (l1 >> sh)) {                   // block-uniform (warp-uniform too)
+        if ((l0 >> sh) == (l1 >> sh)) {                   // block-uniform
+            const uint32_t box = l0 >> sh;
+            const double ccx = A.cx[l][box], ccy = A.cy[l][box];
+            double d = 0.0;
+#pragma unroll
+            for (int c = 0; c < FIN_C; ++c)
+                if (c * FIN_T + tid < nvalid) d = fmax(d, rn_dist2(x[c], y[c], ccx, ccy));   // squared
             for (int o = 16; o; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
-            if (lane == 0) wmax[warp] = d;
-            __syncthreads();
-            if (tid == 0) {
-                double m = wmax[0];
-                for (int w = 1; w < FIN_T / 32; ++w) m = fmax(m, wmax[w]);
-                atomicMax((unsigned long long*)(A.r[l] + (l0 >> sh)), (unsigned long long)__double_as_longlong(m));
-            }
-            __syncthreads();
+            if (lane == 0) wmax[l][warp] = d;
         } else {
-            // segmented max over lanes [lane, end of my box's run) (runs are contiguous)
-            for (int o = 1; o < 32; o <<= 1) {
-                const double dv = __shfl_down_sync(0xffffffffu, d, o);
-                const uint32_t bv = __shfl_down_sync(0xffffffffu, box, o);
-                const bool vv = __shfl_down_sync(0xffffffffu, valid ? 1 : 0, o) != 0;
-                if (lane + o < 32 && vv && bv == box) d = fmax(d, dv);
+#pragma unroll
+            for (int c = 0; c < FIN_C; ++c) {
+                const bool valid = c * FIN_T + tid < nvalid;
+                const uint32_t box = leaf[c] >> sh;
+                double d = 0.0;
+                if (valid) d = rn_dist2(x[c], y[c], A.cx[l][box], A.cy[l][box]);
+                // segmented max over lanes [lane, end of my box's run) (runs are contiguous)
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double dv = __shfl_down_sync(0xffffffffu, d, o);
+                    const uint32_t bv = __shfl_down_sync(0xffffffffu, box, o);
+                    const bool vv = __shfl_down_sync(0xffffffffu, valid ? 1 : 0, o) != 0;
+                    if (lane + o < 32 && vv && bv == box) d = fmax(d, dv);
+                }
+                const uint32_t bprev = __shfl_up_sync(0xffffffffu, box, 1);
+                if (valid && (lane == 0 || bprev != box))
+                    atomicMax((unsigned long long*)(A.r[l] + box), (unsigned long long)__double_as_longlong(d));
             }
-            const uint32_t bprev = __shfl_up_sync(0xffffffffu, box, 1);
-            if (valid && (lane == 0 || bprev != box))
-                atomicMax((unsigned long long*)(A.r[l] + box), (unsigned long long)__double_as_longlong(d));
+        }
+    }
+    __syncthreads();
+    if (tid <= L) {
+        const int l = tid, sh = 2 * (L - l);
+        if ((l0 >> sh) == (l1 >> sh)) {
+            double m = wmax[l][0];
+            for (int w = 1; w < FIN_T / 32; ++w) m = fmax(m, wmax[l][w]);
+            atomicMax((unsigned long long*)(A.r[l] + (l0 >> sh)), (unsigned long long)__double_as_longlong(m));
         }
     }
 }
@@ -1665,7 +1695,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
             A.r[l] = P->r + P->base[l];
         }
         const uint32_t nown = P->pos1 - P->pos0;
-        k_finish<<<grid_for(nown, FIN_T), FIN_T, 0, st>>>(yl, vy, zc, P->pos0, P->pos1, L,
+        k_finish<<<grid_for(nown, FIN_B), FIN_T, 0, st>>>(yl, vy, zc, P->pos0, P->pos1, L,
                                                           P->boff + P->obase[L], (uint32_t)P->box_lo(L),
                                                           (uint32_t)P->box_hi(L), P->perm, P->src, A);
         fmm2d::note_launch();
