@@ -131,7 +131,8 @@ FMM2D_API int fmm2d_eval(fmm2d_plan* plan, const double* m, double* phi, double*
 
 /* fmm2d_eval, then synchronise and report the device time of each phase in
  * ms_out[0..7] (CUDA events on the plan's stream): 0 strength gather, 1 P2M+M2M,
- * 2 M2L (all levels), 3 L2L (+ P2L), 4 L2P+P2P+output, 5 total, 6..7 reserved.
+ * 2 M2L (all levels), 3 L2L (+ r/R exchange: P2L, M2P), 4 L2P+P2P+output (k_near),
+ * 5 total, 6..7 reserved.
  * The phases are run one after the other here (no overlap), so that each is timed alone.
  * Same arguments and errors as fmm2d_eval; ms_out may not be NULL. */
 FMM2D_API int fmm2d_eval_timed(fmm2d_plan* plan, const double* m, double* phi, double* dphi,

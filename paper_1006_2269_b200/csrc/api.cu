@@ -322,8 +322,8 @@ static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi
         if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[3], P0->stream));
         for (int i = 0; i < np; ++i) FMM2D_TRY(run_downward(Ps[i]));
         for (int i = 0; i < np; ++i) FMM2D_TRY(run_rr_p2l(Ps[i]));      // r/R exchange: into the locals
-        if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[4], P0->stream));
         for (int i = 0; i < np; ++i) FMM2D_TRY(run_rr_m2p(Ps[i]));      // r/R exchange: M2P sums
+        if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[4], P0->stream));     // stage 4 = the near field alone
         return 0;
     };
     if (np == 1 && P0->overlap && !ev) {
