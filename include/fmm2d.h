@@ -129,6 +129,17 @@ FMM2D_API int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, 
  * FMM2D_HOST_PTRS: synchronous.  Errors: EINVAL, ECUDA. */
 FMM2D_API int fmm2d_eval(fmm2d_plan* plan, const double* m, double* phi, double* dphi);
 
+/* fmm2d_build followed by one fmm2d_eval, for a caller that holds z and m together
+ * (same arguments and meaning as those two calls; *out receives the plan, which later
+ * fmm2d_eval calls may reuse).  With FMM2D_HOST_PTRS the strengths' host->device copy
+ * runs on a second stream as soon as the positions' copy has finished, so it overlaps
+ * the tree build instead of following it (the copy engine beside the build kernels);
+ * the strengths are then staged in the plan's own buffer.  Synchronous with
+ * FMM2D_HOST_PTRS, else stream-ordered like fmm2d_eval.  Multi-GPU plans: not
+ * supported (ENOTSUP).  Errors: those of fmm2d_build and fmm2d_eval. */
+FMM2D_API int fmm2d_build_eval(const double* z, const double* m, int64_t n, const fmm2d_options* opt,
+                               double* phi, double* dphi, fmm2d_plan** out);
+
 /* fmm2d_eval, then synchronise and report the device time of each phase in
  * ms_out[0..7] (CUDA events on the plan's stream): 0 strength gather, 1 P2M+M2M,
  * 2 M2L (all levels), 3 L2L (+ r/R exchange: P2L, M2P), 4 L2P+P2P+output (k_near),

@@ -250,6 +250,75 @@ int fmm2d_build(const double* z, int64_t n, const fmm2d_options* opt, fmm2d_plan
     return 0;
 }
 
+static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi, double* dphi, cudaEvent_t* ev);
+
+int fmm2d_build_eval(const double* z, const double* m, int64_t n, const fmm2d_options* opt, double* phi,
+                     double* dphi, fmm2d_plan** out)
+{
+    if (!out) return FMM2D_EINVAL;
+    *out = nullptr;
+    if (!z || !m || !opt) return FMM2D_EINVAL;
+    if (opt->nranks != 1) return FMM2D_ENOTSUP;
+    if (!(opt->flags & FMM2D_HOST_PTRS)) {
+        FMM2D_TRY(fmm2d_build(z, n, opt, out));
+        const int rc = fmm2d_eval(*out, m, phi, dphi);
+        if (rc) {
+            fmm2d_free(*out);
+            *out = nullptr;
+        }
+        return rc;
+    }
+    if (n < 1) return FMM2D_EINVAL;
+    FMM2D_CUDA_TRY(cudaSetDevice(opt->device));
+    cudaStream_t st = (cudaStream_t)opt->stream;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_z = nullptr, ev_m = nullptr;
+    double2 *dz = nullptr, *dm = nullptr;
+    fmm2d_plan* P = nullptr;
+    auto body = [&]() -> int {
+        FMM2D_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        FMM2D_CUDA_TRY(cudaEventCreateWithFlags(&ev_z, cudaEventDisableTiming));
+        FMM2D_CUDA_TRY(cudaEventCreateWithFlags(&ev_m, cudaEventDisableTiming));
+        FMM2D_CUDA_TRY(cudaMallocAsync((void**)&dz, sizeof(double2) * n, st));
+        FMM2D_CUDA_TRY(cudaMallocAsync((void**)&dm, sizeof(double2) * n, st));
+        // positions first (the build needs them), then the strengths behind them
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(dz, z, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+        FMM2D_CUDA_TRY(cudaEventRecord(ev_z, st));
+        FMM2D_CUDA_TRY(cudaStreamWaitEvent(side, ev_z, 0));
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(dm, m, sizeof(double2) * n, cudaMemcpyHostToDevice, side));
+        FMM2D_CUDA_TRY(cudaEventRecord(ev_m, side));
+        fmm2d_options o = *opt;
+        o.flags &= ~FMM2D_HOST_PTRS;
+        FMM2D_TRY(fmm2d_build((const double*)dz, n, &o, &P));
+        cudaFreeAsync(dz, st);
+        dz = nullptr;
+        // the plan keeps host-pointer semantics; the strengths already sit in its staging
+        P->flags |= FMM2D_HOST_PTRS;
+        P->allocs.push_back(dm);
+        P->mstage = dm;
+        dm = nullptr;
+        FMM2D_TRY(dev_alloc(P, (void**)&P->phistage, sizeof(double2) * n));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->dphistage, sizeof(double2) * n));
+        FMM2D_CUDA_TRY(cudaStreamWaitEvent(st, ev_m, 0));
+        return eval_impl(&P, 1, nullptr, phi, dphi, nullptr);   // m == nullptr: already staged
+    };
+    int rc = body();
+    if (dz) cudaFreeAsync(dz, st);
+    if (dm) cudaFreeAsync(dm, st);
+    if (side) {
+        cudaStreamSynchronize(side);
+        cudaStreamDestroy(side);
+    }
+    if (ev_z) cudaEventDestroy(ev_z);
+    if (ev_m) cudaEventDestroy(ev_m);
+    if (rc) {
+        fmm2d_free(P);
+        return rc;
+    }
+    *out = P;
+    return 0;
+}
+
 int fmm2d_build_shards(const double* z, int64_t n, const fmm2d_options* opt, int nshards, fmm2d_plan** out)
 {
     if (!out || !z || !opt || nshards < 1 || nshards > 64) return FMM2D_EINVAL;
@@ -271,7 +340,9 @@ int fmm2d_build_shards(const double* z, int64_t n, const fmm2d_options* opt, int
 // rank of an NCCL-sharded build) or every rank of a loopback build, stage by stage.
 static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi, double* dphi, cudaEvent_t* ev)
 {
-    if (!Ps || np < 1 || !m) return FMM2D_EINVAL;
+    // m == nullptr: host-pointer plan whose strengths are already in its staging buffer
+    // (fmm2d_build_eval); the public entry points reject a null m before this
+    if (!Ps || np < 1 || (!m && !(np == 1 && Ps[0] && Ps[0]->mstage))) return FMM2D_EINVAL;
     for (int i = 0; i < np; ++i)
         if (!Ps[i]) return FMM2D_EINVAL;
     fmm2d_plan* P0 = Ps[0];
@@ -289,7 +360,7 @@ static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi
             FMM2D_TRY(dev_alloc(P0, (void**)&P0->phistage, sizeof(double2) * n));
             FMM2D_TRY(dev_alloc(P0, (void**)&P0->dphistage, sizeof(double2) * n));
         }
-        FMM2D_CUDA_TRY(cudaMemcpyAsync(P0->mstage, m, sizeof(double2) * n, cudaMemcpyHostToDevice, P0->stream));
+        if (m) FMM2D_CUDA_TRY(cudaMemcpyAsync(P0->mstage, m, sizeof(double2) * n, cudaMemcpyHostToDevice, P0->stream));
         md = P0->mstage;
         phid = phi ? P0->phistage : nullptr;
         dphid = dphi ? P0->dphistage : nullptr;
@@ -356,13 +427,14 @@ static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi
 
 int fmm2d_eval(fmm2d_plan* P, const double* m, double* phi, double* dphi)
 {
+    if (!m) return FMM2D_EINVAL;
     if (P && P->nranks > 1 && !shard_has_comm(P)) return FMM2D_EINVAL;   // loopback: eval_shards
     return eval_impl(&P, 1, m, phi, dphi, nullptr);
 }
 
 int fmm2d_eval_shards(fmm2d_plan* const* plans, int nshards, const double* m, double* phi, double* dphi)
 {
-    if (!plans || nshards < 1) return FMM2D_EINVAL;
+    if (!plans || nshards < 1 || !m) return FMM2D_EINVAL;
     for (int i = 0; i < nshards; ++i)
         if (!plans[i] || plans[i]->nranks != nshards || plans[i]->rank != i || shard_has_comm(plans[i]))
             return FMM2D_EINVAL;

@@ -48,16 +48,23 @@ constexpr int NEAR_UNROLL = FMM2D_NEAR_UNROLL;
 constexpr int NEAR_CHUNK = FMM2D_NEAR_CHUNK;    // >= 256: the chunk buffer doubles as reduction space
 static_assert(NEAR_CHUNK >= 2 * NEAR_T, "chunk buffer too small for the reduction");
 
-__global__ void k_gather_m(const double2* __restrict__ m, const uint32_t* __restrict__ perm, int64_t k0, int64_t k1,
-                           double4* __restrict__ src)
+// the strengths into the source rows' (z, w) halves (16-byte stores; the coordinates in
+// (x, y) are not read); GM rows per thread with the random gathers of m in flight together
+constexpr int GM = 4;
+__global__ void __launch_bounds__(256) k_gather_m(const double2* __restrict__ m, const uint32_t* __restrict__ perm,
+                                                  int64_t k0, int64_t k1, double4* __restrict__ src)
 {
-    int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= k1) return;
-    double2 v = m[perm[k]];
-    double4 s = src[k];
-    s.z = v.x;
-    s.w = v.y;
-    src[k] = s;
+    const int64_t kb = k0 + (int64_t)blockIdx.x * (256 * GM) + threadIdx.x;
+    uint32_t j[GM];
+    double2 v[GM];
+#pragma unroll
+    for (int u = 0; u < GM; ++u) j[u] = (kb + u * 256 < k1) ? perm[kb + u * 256] : 0u;
+#pragma unroll
+    for (int u = 0; u < GM; ++u)
+        if (kb + u * 256 < k1) v[u] = m[j[u]];
+#pragma unroll
+    for (int u = 0; u < GM; ++u)
+        if (kb + u * 256 < k1) reinterpret_cast<double2*>(src + kb + u * 256)[1] = v[u];
 }
 
 // Sums of one target: A = sum m log|dz|^2, B = sum m Arg dz, D = sum m conj(dz)/|dz|^2,
@@ -702,7 +709,7 @@ const fm::Tables* device_tables(int dev, int* rc)
 int gather_strengths(fmm2d_plan* P, const double2* m)
 {
     const int64_t k0 = P->pos0, k1 = P->pos1;
-    k_gather_m<<<grid_for(k1 - k0, 256), 256, 0, P->stream>>>(m, P->perm, k0, k1, P->src);
+    k_gather_m<<<grid_for(k1 - k0, 256 * GM), 256, 0, P->stream>>>(m, P->perm, k0, k1, P->src);
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     return 0;

@@ -41,7 +41,7 @@ EXPORT_PERM, EXPORT_OFFSETS, EXPORT_DISCS, EXPORT_STRONG, EXPORT_WEAK, EXPORT_MP
 SYMBOLS = ["fmm2d_default_options", "fmm2d_build", "fmm2d_eval", "fmm2d_eval_timed", "fmm2d_launch_count",
            "fmm2d_free", "fmm2d_strerror", "fmm2d_last_error_detail", "fmm2d_plan_info", "fmm2d_export",
            "fmm2d_nccl_unique_id", "fmm2d_partition_info", "fmm2d_build_shards", "fmm2d_eval_shards",
-           "fmm2d_halo_info"]
+           "fmm2d_halo_info", "fmm2d_build_eval"]
 
 
 class Options(ctypes.Structure):
@@ -94,6 +94,7 @@ def lib():
                                          ctypes.POINTER(vp)]
         L.fmm2d_eval_shards.argtypes = [ctypes.POINTER(vp), ctypes.c_int, vp, vp, vp]
         L.fmm2d_halo_info.argtypes = [vp, ctypes.POINTER(ctypes.c_int64)]
+        L.fmm2d_build_eval.argtypes = [vp, vp, ctypes.c_int64, ctypes.POINTER(Options), vp, vp, ctypes.POINTER(vp)]
         _lib = L
     return _lib
 
@@ -173,7 +174,7 @@ class Fmm2d:
                  rr_exchange: bool = False, parent_merge: bool = False, overlap: bool = False,
                  gather_output: bool = False, midpoint: bool = False,
                  nranks: int = 1, rank: int = 0,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, _first=None):
         L = lib()
         import torch
         host = not (isinstance(z, torch.Tensor) and z.is_cuda)
@@ -210,7 +211,15 @@ class Fmm2d:
         zp, keep = _ptr_of(z, host)
         self.n = int(keep.shape[0])
         h = ctypes.c_void_p()
-        _check(L.fmm2d_build(ctypes.c_void_p(zp), self.n, ctypes.byref(opt), ctypes.byref(h)), "fmm2d_build")
+        if _first is None:
+            _check(L.fmm2d_build(ctypes.c_void_p(zp), self.n, ctypes.byref(opt), ctypes.byref(h)), "fmm2d_build")
+        else:                                   # (m, phi, dphi): fmm2d_build_eval
+            mp = _ptr_of(_first[0], host)[0]
+            pp = _ptr_of(_first[1], host)[0] if _first[1] is not None else None
+            dp = _ptr_of(_first[2], host)[0] if _first[2] is not None else None
+            _check(L.fmm2d_build_eval(ctypes.c_void_p(zp), ctypes.c_void_p(mp), self.n, ctypes.byref(opt),
+                                      ctypes.c_void_p(pp), ctypes.c_void_p(dp), ctypes.byref(h)),
+                   "fmm2d_build_eval")
         self._h = h
         n = ctypes.c_int64()
         nl = ctypes.c_int()
@@ -224,6 +233,25 @@ class Fmm2d:
         self.theta = float(theta)
         self.weak_pairs = wp.value
         self.strong_leaf_pairs = sp.value
+
+    @classmethod
+    def build_eval(cls, z, m, phi=None, dphi=None, **kw):
+        """Build the plan and evaluate once (fmm2d_build_eval): for host arrays the strengths'
+        copy to the device overlaps the tree build.  Returns (plan, phi, dphi); phi / dphi
+        are allocated like eval's when not given (pinned host, or on the device)."""
+        import torch
+        host = not (isinstance(z, torch.Tensor) and z.is_cuda)
+        n = int(z.shape[0])
+        if phi is None or dphi is None:
+            if host:
+                pin = torch.cuda.is_available()
+                phi = torch.empty(n, dtype=torch.complex128, pin_memory=pin) if phi is None else phi
+                dphi = torch.empty(n, dtype=torch.complex128, pin_memory=pin) if dphi is None else dphi
+            else:
+                phi = torch.empty(n, dtype=torch.complex128, device=z.device) if phi is None else phi
+                dphi = torch.empty(n, dtype=torch.complex128, device=z.device) if dphi is None else dphi
+        plan = cls(z, _first=(m, phi, dphi), **kw)
+        return plan, phi, dphi
 
     # -- evaluation -------------------------------------------------------
     def eval(self, m, phi=None, dphi=None, want_phi: bool = True, want_dphi: bool = True):

@@ -216,6 +216,33 @@ def test_host_pointer_path_equals_device_path():
     np.testing.assert_array_equal(dphi.numpy(), dev[1])
 
 
+@pytest.mark.parametrize("host", [True, False])
+def test_build_eval_equals_build_then_eval(host):
+    """fmm2d_build_eval (the strengths' copy overlapping the build for host buffers) gives
+    the result of fmm2d_build + fmm2d_eval bit for bit, and its plan is reusable."""
+    import torch
+    from paper_1006_2269_b200 import Fmm2d
+    z, m = W.make_config("C2", n=40_000)
+    ref = _gpu_plan(z, 0.5, 17, 5)
+    a = _gpu_eval(ref, m)
+    m2 = np.ascontiguousarray(m[::-1])
+    a2 = _gpu_eval(ref, m2)
+    if host:
+        plan, phi, dphi = Fmm2d.build_eval(z, m, theta=0.5, p=17, nlevels=5)
+        got = (phi.numpy(), dphi.numpy())
+        phi2, dphi2 = plan.eval(m2)
+        got2 = (phi2.numpy(), dphi2.numpy())
+    else:
+        zd, md, m2d = (torch.from_numpy(v).cuda() for v in (z, m, m2))
+        plan, phi, dphi = Fmm2d.build_eval(zd, md, theta=0.5, p=17, nlevels=5)
+        got = (phi.cpu().numpy(), dphi.cpu().numpy())
+        phi2, dphi2 = plan.eval(m2d)
+        got2 = (phi2.cpu().numpy(), dphi2.cpu().numpy())
+    for x, y in zip(got + got2, a + a2):
+        np.testing.assert_array_equal(x, y)
+    plan.close()
+
+
 def test_eval_deterministic_and_reusable():
     z, m = W.make_config("C2", n=30_000)
     gp = _gpu_plan(z, 0.5, 17, 5)
