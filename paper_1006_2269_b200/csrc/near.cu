@@ -38,7 +38,7 @@ constexpr int NEAR_T = 128;
 #define FMM2D_NEAR_TPT 2          // targets per thread (register blocking)
 #endif
 #ifndef FMM2D_NEAR_UNROLL
-#define FMM2D_NEAR_UNROLL 2       // source rows per unrolled iteration
+#define FMM2D_NEAR_UNROLL 1       // source rows per unrolled iteration (1: measured best at C5)
 #endif
 constexpr int NEAR_TPT = FMM2D_NEAR_TPT;
 constexpr int NEAR_UNROLL = FMM2D_NEAR_UNROLL;
