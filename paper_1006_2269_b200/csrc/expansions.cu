@@ -17,6 +17,7 @@
 // below the machine balance).  Every kernel is templated on p so the coefficient
 // vectors live in registers.
 #include "fmm2d_internal.cuh"
+#include "fastmath.cuh"
 
 namespace fmm2d {
 
@@ -358,17 +359,29 @@ inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / b
 // z_j - c each formed componentwise, R2).  One block of RR_T threads per leaf with P2L
 // work: warp w takes list entries w, w + RR_W, ...; lanes over each entry's sources;
 // coefficients in registers, a fixed-order shuffle reduction per warp, the warps'
-// partials summed in warp order in shared memory and added to the local.
+// partials summed in warp order in shared memory and added to the local.  Per source:
+// log|.|, Arg and 1/|.|^2 by the table-driven routines of fastmath.cuh (tables in shared
+// memory, as in k_near), t_l = m iv^l by one complex product per l, b_l -= t_l / l.
 constexpr int RR_T = 128, RR_W = RR_T / 32;
+
+__device__ __forceinline__ void rr_load_tables(fm::Tables& T, const fm::Tables* __restrict__ g)
+{
+    const double2* gs = reinterpret_cast<const double2*>(g);
+    double2* ss = reinterpret_cast<double2*>(&T);
+    for (int k = threadIdx.x; k < (int)(sizeof(fm::Tables) / 16); k += blockDim.x) ss[k] = gs[k];
+}
 
 template <int P>
 __global__ void __launch_bounds__(RR_T) k_rr_p2l(const uint32_t* __restrict__ leaves,
                                                  const int64_t* __restrict__ off, const uint32_t* __restrict__ idx,
                                                  const uint32_t* __restrict__ boff, const double4* __restrict__ src,
                                                  const double* __restrict__ cx, const double* __restrict__ cy,
-                                                 double2* __restrict__ loc)
+                                                 double2* __restrict__ loc, const fm::Tables* __restrict__ gtab)
 {
     __shared__ double2 part[RR_W][P + 1];
+    __shared__ fm::Tables T;
+    rr_load_tables(T, gtab);
+    __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t t = leaves[blockIdx.x];
     const double ctx = cx[t], cty = cy[t];
@@ -381,16 +394,19 @@ __global__ void __launch_bounds__(RR_T) k_rr_p2l(const uint32_t* __restrict__ le
             const double4 z = src[j];
             const double2 m = make_double2(z.z, z.w);
             const double ux = ctx - z.x, uy = cty - z.y;              // c - z_j
-            const double2 lg = make_double2(0.5 * log(ux * ux + uy * uy), atan2(uy, ux));
+            const double r2 = fma(ux, ux, uy * uy);
+            const double2 lg = make_double2(0.5 * fm::log_pos(r2, T.lg), fm::arg_t(ux, uy, T.at));
             b[0] = cadd(b[0], cmul(m, lg));
             const double vx = z.x - ctx, vy = z.y - cty;              // z_j - c
-            const double iv2 = 1.0 / (vx * vx + vy * vy);
+            const double iv2 = fm::rcp(fma(vx, vx, vy * vy));
             const double2 iv = make_double2(vx * iv2, -vy * iv2);
-            double2 ivl = iv;
+            double2 tl = m;
 #pragma unroll
             for (int l = 1; l <= P; ++l) {
-                b[l] = csub(b[l], cscale(cmul(m, ivl), 1.0 / l));
-                if (l < P) ivl = cmul(ivl, iv);
+                tl = cmul(tl, iv);                                     // m iv^l
+                const double c = -1.0 / l;
+                b[l].x = fma(c, tl.x, b[l].x);
+                b[l].y = fma(c, tl.y, b[l].y);
             }
         }
     }
@@ -416,18 +432,23 @@ __global__ void __launch_bounds__(RR_T) k_rr_p2l(const uint32_t* __restrict__ le
 }
 
 // M2P: the multipoles of the smaller leaves in a leaf's M2P list evaluated at
-// each of its points: a_0 Log(w) + sum_k a_k w^-k and a_0 / w - sum_k k a_k w^-(k+1),
-// w = z_i - c_s (componentwise), Horner in 1/w.  One block per leaf with M2P work:
-// thread (point i, group g) takes list entries g, g + G, ...; the G partial sums of a
-// point are added in group order; the sums go to acc[i] (leaf order), k_near adds them.
+// each of its points: Phi += a_0 Log(w) + sum_k a_k x^k and Phi' += a_0 x - x^2 sum_k k a_k
+// x^(k-1), w = z_i - c_s (componentwise), x = 1/w.  Both sums from one Horner pass over
+// H(x) = sum_k a_k x^(k-1) and its derivative (sum_k k a_k x^(k-1) = H + x H').  One
+// block per leaf with M2P work: thread (point i, group g) takes list entries g, g + G, ...;
+// the G partial sums of a point are added in group order; the sums go to acc[i] (leaf
+// order), k_near adds them.  log|w|, Arg w, 1/|w|^2: fastmath.cuh, tables in shared memory.
 template <int P>
 __global__ void __launch_bounds__(RR_T) k_rr_m2p(const uint32_t* __restrict__ leaves, const int64_t* __restrict__ off,
                                                  const uint32_t* __restrict__ idx, const uint32_t* __restrict__ boff,
                                                  const double4* __restrict__ src, const double* __restrict__ cx,
                                                  const double* __restrict__ cy, const double2* __restrict__ mp,
-                                                 double4* __restrict__ acc)
+                                                 double4* __restrict__ acc, const fm::Tables* __restrict__ gtab)
 {
     __shared__ double4 part[RR_T];
+    __shared__ fm::Tables T;
+    rr_load_tables(T, gtab);
+    __syncthreads();
     const uint32_t t = leaves[blockIdx.x];
     const uint32_t ts = boff[t];
     const int nt = (int)(boff[t + 1] - ts);
@@ -443,17 +464,19 @@ __global__ void __launch_bounds__(RR_T) k_rr_m2p(const uint32_t* __restrict__ le
                 const uint32_t s = idx[q];
                 const double2* A = mp + (int64_t)s * (P + 1);
                 const double wx = z.x - cx[s], wy = z.y - cy[s];
-                const double iw2 = 1.0 / (wx * wx + wy * wy);
-                const double2 iw = make_double2(wx * iw2, -wy * iw2);
-                double2 h = A[P], dh = cscale(A[P], (double)P);
+                const double r2 = fma(wx, wx, wy * wy);
+                const double iw2 = fm::rcp(r2);
+                const double2 x = make_double2(wx * iw2, -wy * iw2);
+                double2 h = A[P], dh = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int k = P - 1; k >= 1; --k) {
-                    h = cadd(cmul(h, iw), A[k]);
-                    dh = cadd(cmul(dh, iw), cscale(A[k], (double)k));
+                    dh = cadd(cmul(dh, x), h);              // H'
+                    h = cadd(cmul(h, x), A[k]);             // H
                 }
-                const double2 lg = make_double2(0.5 * log(wx * wx + wy * wy), atan2(wy, wx));
-                f = cadd(f, cadd(cmul(A[0], lg), cmul(h, iw)));
-                df = cadd(df, csub(cmul(A[0], iw), cmul(dh, cmul(iw, iw))));
+                const double2 d = cadd(h, cmul(x, dh));     // sum_k k a_k x^(k-1)
+                const double2 lg = make_double2(0.5 * fm::log_pos(r2, T.lg), fm::arg_t(wx, wy, T.at));
+                f = cadd(f, cadd(cmul(A[0], lg), cmul(h, x)));
+                df = cadd(df, csub(cmul(A[0], x), cmul(d, cmul(x, x))));
             }
         }
         __syncthreads();
@@ -480,7 +503,7 @@ int rr_p2l_p(fmm2d_plan* Pl)
     const int L = Pl->L;
     k_rr_p2l<P><<<(unsigned)Pl->rr_np2l, RR_T, 0, Pl->stream>>>(
         Pl->rr_p2l_leaves, Pl->rr_p2l.off, Pl->rr_p2l.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
-        Pl->cy + Pl->base[L], Pl->local + Pl->base[L] * (P + 1));
+        Pl->cy + Pl->base[L], Pl->local + Pl->base[L] * (P + 1), static_cast<const fm::Tables*>(Pl->tables));
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     return 0;
@@ -493,7 +516,7 @@ int rr_m2p_p(fmm2d_plan* Pl)
     const int L = Pl->L;
     k_rr_m2p<P><<<(unsigned)Pl->rr_nm2p, RR_T, 0, Pl->stream>>>(
         Pl->rr_m2p_leaves, Pl->rr_m2p.off, Pl->rr_m2p.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
-        Pl->cy + Pl->base[L], Pl->mpole + Pl->base[L] * (P + 1), Pl->rr_acc);
+        Pl->cy + Pl->base[L], Pl->mpole + Pl->base[L] * (P + 1), Pl->rr_acc, static_cast<const fm::Tables*>(Pl->tables));
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     return 0;
