@@ -435,9 +435,12 @@ __global__ void __launch_bounds__(RR_T) k_rr_p2l(const uint32_t* __restrict__ le
 // each of its points: Phi += a_0 Log(w) + sum_k a_k x^k and Phi' += a_0 x - x^2 sum_k k a_k
 // x^(k-1), w = z_i - c_s (componentwise), x = 1/w.  Both sums from one Horner pass over
 // H(x) = sum_k a_k x^(k-1) and its derivative (sum_k k a_k x^(k-1) = H + x H').  One
-// block per leaf with M2P work: thread (point i, group g) takes list entries g, g + G, ...;
-// the G partial sums of a point are added in group order; the sums go to acc[i] (leaf
-// order), k_near adds them.  log|w|, Arg w, 1/|w|^2: fastmath.cuh, tables in shared memory.
+// block per leaf with M2P work: the list's multipoles and centres are staged in shared
+// memory in chunks of RR_CH entries (coalesced loads by the whole block); thread (point i,
+// group g) takes the chunk's entries g, g + G, ...; the G partial sums of a point are
+// added in group order; the sums go to acc[i] (leaf order), k_near adds them.  log|w|,
+// Arg w, 1/|w|^2: fastmath.cuh, tables in shared memory.
+constexpr int RR_CH = 32;
 template <int P>
 __global__ void __launch_bounds__(RR_T) k_rr_m2p(const uint32_t* __restrict__ leaves, const int64_t* __restrict__ off,
                                                  const uint32_t* __restrict__ idx, const uint32_t* __restrict__ boff,
@@ -445,38 +448,52 @@ __global__ void __launch_bounds__(RR_T) k_rr_m2p(const uint32_t* __restrict__ le
                                                  const double* __restrict__ cy, const double2* __restrict__ mp,
                                                  double4* __restrict__ acc, const fm::Tables* __restrict__ gtab)
 {
+    constexpr int E = P + 2;                        // per entry: P + 1 coefficients, the centre
     __shared__ double4 part[RR_T];
+    __shared__ double2 sA[RR_CH * E];
     __shared__ fm::Tables T;
     rr_load_tables(T, gtab);
-    __syncthreads();
     const uint32_t t = leaves[blockIdx.x];
     const uint32_t ts = boff[t];
     const int nt = (int)(boff[t + 1] - ts);
+    const int64_t q0 = off[t], q1 = off[t + 1];
     const int per = min(nt, RR_T);                  // points per pass
     const int G = RR_T / per;                       // list groups
     const int ip = threadIdx.x % per, g = threadIdx.x / per;
     for (int i0 = 0; i0 < nt; i0 += per) {
         const int i = i0 + ip;
+        const bool act = g < G && i < nt;
         double2 f = make_double2(0.0, 0.0), df = make_double2(0.0, 0.0);
-        if (g < G && i < nt) {
-            const double4 z = src[ts + i];
-            for (int64_t q = off[t] + g; q < off[t + 1]; q += G) {
-                const uint32_t s = idx[q];
-                const double2* A = mp + (int64_t)s * (P + 1);
-                const double wx = z.x - cx[s], wy = z.y - cy[s];
-                const double r2 = fma(wx, wx, wy * wy);
-                const double iw2 = fm::rcp(r2);
-                const double2 x = make_double2(wx * iw2, -wy * iw2);
-                double2 h = A[P], dh = make_double2(0.0, 0.0);
+        double4 z = make_double4(0.0, 0.0, 0.0, 0.0);
+        if (act) z = src[ts + i];
+        for (int64_t qc = q0; qc < q1; qc += RR_CH) {
+            const int nch = (int)min((int64_t)RR_CH, q1 - qc);
+            __syncthreads();                        // previous chunk consumed (and the tables)
+            for (int e = threadIdx.x; e < nch * E; e += RR_T) {
+                const int j = e / E, k = e - j * E;
+                const uint32_t s = idx[qc + j];
+                sA[e] = (k <= P) ? mp[(int64_t)s * (P + 1) + k] : make_double2(cx[s], cy[s]);
+            }
+            __syncthreads();
+            if (act) {
+                for (int j = g; j < nch; j += G) {
+                    const double2* A = sA + j * E;
+                    const double2 c = A[P + 1];
+                    const double wx = z.x - c.x, wy = z.y - c.y;
+                    const double r2 = fma(wx, wx, wy * wy);
+                    const double iw2 = fm::rcp(r2);
+                    const double2 x = make_double2(wx * iw2, -wy * iw2);
+                    double2 h = A[P], dh = make_double2(0.0, 0.0);
 #pragma unroll
-                for (int k = P - 1; k >= 1; --k) {
-                    dh = cadd(cmul(dh, x), h);              // H'
-                    h = cadd(cmul(h, x), A[k]);             // H
+                    for (int k = P - 1; k >= 1; --k) {
+                        dh = cadd(cmul(dh, x), h);          // H'
+                        h = cadd(cmul(h, x), A[k]);         // H
+                    }
+                    const double2 d = cadd(h, cmul(x, dh)); // sum_k k a_k x^(k-1)
+                    const double2 lg = make_double2(0.5 * fm::log_pos(r2, T.lg), fm::arg_t(wx, wy, T.at));
+                    f = cadd(f, cadd(cmul(A[0], lg), cmul(h, x)));
+                    df = cadd(df, csub(cmul(A[0], x), cmul(d, cmul(x, x))));
                 }
-                const double2 d = cadd(h, cmul(x, dh));     // sum_k k a_k x^(k-1)
-                const double2 lg = make_double2(0.5 * fm::log_pos(r2, T.lg), fm::arg_t(wx, wy, T.at));
-                f = cadd(f, cadd(cmul(A[0], lg), cmul(h, x)));
-                df = cadd(df, csub(cmul(A[0], x), cmul(d, cmul(x, x))));
             }
         }
         __syncthreads();
