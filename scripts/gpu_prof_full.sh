@@ -9,7 +9,9 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 CMD1="python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD1 > gpurun_out/ncu_launches.log 2>&1
 python tools/ncu_launch_summary.py gpurun_out/launches.csv > gpurun_out/launches_summary.txt 2>&1; head -12 gpurun_out/launches_summary.txt
-for K in k_near k_m2l k_partition k_tree_local k_finish; do
-timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$K(<|\()" -c 1 -o gpurun_out/prof_$K $CMD1 > gpurun_out/ncu_full_$K.log 2>&1
+# mangled-name regexes (the demangled "k_m2l" also matches k_m2l_keys)
+for K in 6k_nearI 5k_m2lI 11k_partitionI 12k_tree_local 8k_finish; do
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k "regex:$K" -c 1 -o gpurun_out/prof_$K $CMD1 > gpurun_out/ncu_full_$K.log 2>&1
 tail -1 gpurun_out/ncu_full_$K.log
+python tools/ncu_brief.py gpurun_out/prof_$K.ncu-rep > gpurun_out/brief_$K.txt 2>&1
 done
