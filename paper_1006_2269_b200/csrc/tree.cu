@@ -34,6 +34,7 @@
 #include <string>
 #include <utility>
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "fmm2d_internal.cuh"
 
@@ -218,6 +219,22 @@ __global__ void k_make_ylist(const uint64_t* __restrict__ vy, int64_t m, uint32_
     yl[k] = make_uint2(rx, roff + (uint32_t)k);
     keyd[k] = rx - roff;
     iota[k] = (uint32_t)k;
+}
+
+// 1: the x-list by a direct scatter xl[rx] = {rx, ry} inside k_make_ylist (one random
+// 8-byte write per point); 0: by one more radix sort of the x ranks (k_make_xlist)
+#ifndef FMM2D_PRESORT_SCATTER
+#define FMM2D_PRESORT_SCATTER 1
+#endif
+__global__ void k_make_lists(const uint64_t* __restrict__ vy, int64_t m, uint32_t roff, uint2* __restrict__ yl,
+                             uint2* __restrict__ xl)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const uint32_t rx = (uint32_t)vy[k];
+    const uint2 r = make_uint2(rx, roff + (uint32_t)k);
+    yl[k] = r;
+    xl[rx - roff] = r;
 }
 
 // x-list from the y ranks in x order
@@ -1377,7 +1394,7 @@ static int top_levels_sharded(fmm2d_plan* P, const double2* zc, const Bounds& hb
         tr.mark("level-k boxes");
         // presort of each own level-k box (its points in ascending input index)
         size_t sb = 0;
-        cub::CountingInputIterator<uint32_t> it(0);
+        thrust::counting_iterator<uint32_t> it(0);
         cub::DeviceSelect::If(nullptr, sb, it, sub, d_nsel, (int64_t)n, BoxIs{boxk, 0u}, st);
         FMM2D_TRY(talloc(&scratch, sb));
         for (int64_t R = P->own_lo(k); R < P->own_hi(k); ++R) {
@@ -1565,13 +1582,19 @@ int build_tree(fmm2d_plan* P, const double2* z)
             if (k64buf) cudaFreeAsync(k64buf, st);
             FMM2D_CUDA_TRY(cudaGetLastError());
             P->stats.tree_key64 |= (force64 || h_ovf[0] ? 1 : 0) + (force64 || h_ovf[1] ? 2 : 0);
-            // y-list {rx, k}; the y ranks in x order by one more sort (keys = local x ranks)
-            k_make_ylist<<<grid_for(m, BS), BS, 0, st>>>(vym, m, roff, yl + roff, k32a, u32a);
-            fmm2d::note_launch();
-            sb = cub_bytes;
-            FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, u32a, u32b, (int)m, 0, mbits, st));
-            k_make_xlist<<<grid_for(m, BS), BS, 0, st>>>(u32b, m, roff, xl + roff);
-            fmm2d::note_launch();
+            if (FMM2D_PRESORT_SCATTER) {
+                // y-list {rx, ry} in y order, and the same records scattered to x order
+                k_make_lists<<<grid_for(m, BS), BS, 0, st>>>(vym, m, roff, yl + roff, xl + roff);
+                fmm2d::note_launch();
+            } else {
+                // y-list {rx, k}; the y ranks in x order by one more sort (keys = local x ranks)
+                k_make_ylist<<<grid_for(m, BS), BS, 0, st>>>(vym, m, roff, yl + roff, k32a, u32a);
+                fmm2d::note_launch();
+                sb = cub_bytes;
+                FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, u32a, u32b, (int)m, 0, mbits, st));
+                k_make_xlist<<<grid_for(m, BS), BS, 0, st>>>(u32b, m, roff, xl + roff);
+                fmm2d::note_launch();
+            }
             FMM2D_CUDA_TRY(cudaGetLastError());
             return 0;
         };
