@@ -10,6 +10,10 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/fmm2d.h"
@@ -164,6 +168,33 @@ int upload_binomials(int p);
 // count of this library's own kernel launches (reported by bench.py as gpu_launches)
 void note_launch();
 int64_t launch_count();
+
+// FMM2D_TREE_TRACE=1: event times of the build's phases on stderr (diagnostics only)
+struct PhaseTrace {
+    cudaStream_t st;
+    bool on;
+    std::vector<std::pair<std::string, cudaEvent_t>> ev;
+    explicit PhaseTrace(cudaStream_t s) : st(s), on(std::getenv("FMM2D_TREE_TRACE") != nullptr) {}
+    void mark(const std::string& name)
+    {
+        if (!on) return;
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        cudaEventRecord(e, st);
+        ev.emplace_back(name, e);
+    }
+    ~PhaseTrace()
+    {
+        if (!on || ev.empty()) return;
+        cudaEventSynchronize(ev.back().second);
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+            std::fprintf(stderr, "[fmm2d tree] %-28s %9.3f ms\n", ev[i].first.c_str(), ms);
+        }
+        for (auto& x : ev) cudaEventDestroy(x.second);
+    }
+};
 
 }  // namespace fmm2d
 

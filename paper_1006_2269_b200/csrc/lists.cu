@@ -442,6 +442,8 @@ int build_lists(fmm2d_plan* P)
     FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt_s, sizeof(int64_t) * (nbmax + 1), st));
     FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt_x, sizeof(int64_t) * (nbmax + 1), st));
     FMM2D_CUDA_TRY(cudaMallocAsync(&scratch, scan_bytes, st));
+    PhaseTrace tr(st);
+    tr.mark("lists start");
     auto body = [&]() -> int {
         const bool merge_on = (P->flags & FMM2D_PARENT_MERGE) != 0;
         for (int l = 1; l <= L; ++l) {
@@ -506,6 +508,7 @@ int build_lists(fmm2d_plan* P)
             cudaFreeAsync(stmp, st);
             if (xtmp) cudaFreeAsync(xtmp, st);
             P->stats.weak_pairs += W.total + X.total;
+            tr.mark("lists level " + std::to_string(l));
         }
         // M2L work order (k_m2l_keys)
         {
@@ -558,6 +561,7 @@ int build_lists(fmm2d_plan* P)
         P->stats.strong_leaf_pairs = P->strong[L].total;
         const int64_t t0 = P->box_lo(L), t1 = P->box_hi(L);
         P->near = P->strong[L];                     // the direct pairs (all strong pairs unless r/R exchange)
+        tr.mark("m2l order + long lists");
         if (P->flags & FMM2D_RR_EXCHANGE) FMM2D_TRY(build_rr_lists(P));
         unsigned long long* d_tot = (unsigned long long*)cnt_w;   // reuse scratch
         FMM2D_CUDA_TRY(cudaMemsetAsync(d_tot, 0, 2 * sizeof(unsigned long long), st));
@@ -569,7 +573,9 @@ int build_lists(fmm2d_plan* P)
         FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
         P->stats.p2p_pairs = (int64_t)h_tot[0];
         // long near lists: segments for k_near (only if some list exceeds the split size)
+        tr.mark("rr lists + pair count");
         if (P->stats.max_leaf <= FMM2D_NEAR_CHUNK && h_tot[1] > FMM2D_NEAR_SPLIT) FMM2D_TRY(build_near_segments(P));
+        tr.mark("near segments");
         return 0;
     };
     int rc = body();

@@ -250,33 +250,6 @@ __global__ void k_make_xlist(const uint32_t* __restrict__ ryx, int64_t m, uint32
 // selection over all points (replicated on every rank), then each rank presorts only the
 // points of its own level-k boxes.  A split record is {orderable 64-bit coordinate, idx};
 // "(c, i) >= record" is the high side.
-// FMM2D_TREE_TRACE=1: event times of the partitioned build's phases on stderr (diagnostics)
-struct PhaseTrace {
-    cudaStream_t st;
-    bool on;
-    std::vector<std::pair<std::string, cudaEvent_t>> ev;
-    explicit PhaseTrace(cudaStream_t s) : st(s), on(std::getenv("FMM2D_TREE_TRACE") != nullptr) {}
-    void mark(const std::string& name)
-    {
-        if (!on) return;
-        cudaEvent_t e;
-        if (cudaEventCreate(&e) != cudaSuccess) return;
-        cudaEventRecord(e, st);
-        ev.emplace_back(name, e);
-    }
-    ~PhaseTrace()
-    {
-        if (!on || ev.empty()) return;
-        cudaEventSynchronize(ev.back().second);
-        for (size_t i = 1; i < ev.size(); ++i) {
-            float ms = 0;
-            cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
-            std::fprintf(stderr, "[fmm2d tree] %-28s %9.3f ms\n", ev[i].first.c_str(), ms);
-        }
-        for (auto& x : ev) cudaEventDestroy(x.second);
-    }
-};
-
 struct TopRec {
     unsigned long long key;
     uint32_t idx, pad;
