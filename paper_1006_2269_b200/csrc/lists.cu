@@ -10,10 +10,11 @@
 // Criterion 1: well separated iff R + theta r <= theta d (readings
 // R9-R11: d > 0 required, non-strict, no FMA, exact operation order).
 //
-// GPU formulation: one warp per box; the candidate list (children of the parent's
-// strong list, in ascending order) is walked 32 at a time, each lane evaluates the
-// predicate, and ballot/popc compaction writes weak and strong entries in candidate
-// order (so lists come out ascending, R13).  Count pass -> scan -> fill pass.
+// GPU formulation: one warp per parent box (its four children share the candidate list:
+// the children of the parent's strong list, in ascending order), walked 32 candidates at a
+// time; each lane evaluates the predicate against the four children, and ballot/popc
+// compaction writes weak and strong entries in candidate order (so lists come out
+// ascending, R13) into per-box slots; a scan of the counts and a compaction pass follow.
 #include <cub/cub.cuh>
 
 #include "fmm2d_internal.cuh"
@@ -45,6 +46,9 @@ __device__ __forceinline__ int64_t cand_slot(const int64_t* __restrict__ poff, i
     return 16 * poff[par] + 4 * (b & 3) * (poff[par + 1] - poff[par]);
 }
 
+// One warp per PARENT: its four children share the candidate list (the children of the
+// parent's strong list), so each candidate's disc is loaded once and tested against the four
+// children; per child the ballots and slots are those of the box-per-warp formulation.
 __global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, const double* __restrict__ cy,
                         const double* __restrict__ r, double theta, const int64_t* __restrict__ poff,
                         const uint32_t* __restrict__ pidx, int64_t* __restrict__ wcnt, int64_t* __restrict__ scnt,
@@ -52,56 +56,91 @@ __global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, c
                         const double* __restrict__ pcx, const double* __restrict__ pcy, const double* __restrict__ pr,
                         int64_t* __restrict__ xcnt, uint32_t* __restrict__ xtmp)
 {
-    int64_t b = b0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    int lane = threadIdx.x & 31;
-    if (b >= b1) return;
-    int64_t par = b >> 2;
-    int64_t o0 = poff[par];
-    int64_t ncand = 4 * (poff[par + 1] - o0);
-    double bx = cx[b], by = cy[b], br = r[b];
-    int64_t nw = 0, ns = 0, nx = 0;
-    if (br < 0.0) ncand = 0;                 // empty box (midpoint tree): no connections
-    const int64_t slot = cand_slot(poff, b), xslot = slot / 4;
-    unsigned lt = (1u << lane) - 1u;
+    const int64_t par = (b0 >> 2) + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (4 * par >= b1) return;
+    const int64_t o0 = poff[par];
+    const int64_t ncand = 4 * (poff[par + 1] - o0);
+    double bx[4], by[4], br[4];
+    bool live[4], conn[4];
+    int64_t slot[4], nw[4], ns[4], nx[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t b = 4 * par + j;
+        live[j] = b >= b0 && b < b1;
+        bx[j] = by[j] = br[j] = 0.0;
+        if (live[j]) {
+            bx[j] = cx[b];
+            by[j] = cy[b];
+            br[j] = r[b];
+        }
+        conn[j] = live[j] && br[j] >= 0.0;          // empty box (midpoint tree): no connections
+        slot[j] = cand_slot(poff, b);
+        nw[j] = ns[j] = nx[j] = 0;
+    }
+    const unsigned lt = (1u << lane) - 1u;
     for (int64_t t0 = 0; t0 < ncand; t0 += 32) {
-        int64_t t = t0 + lane;
+        const int64_t t = t0 + lane;
         bool valid = t < ncand;
         uint32_t c = 0, q = 0;
-        bool ws = false;
+        double ccx = 0.0, ccy = 0.0, crr = 0.0, qx = 0.0, qy = 0.0, qr = 0.0;
         if (valid) {
             q = pidx[o0 + (t >> 2)];
             c = 4u * q + (uint32_t)(t & 3);
-            valid = r[c] >= 0.0;                 // empty candidates (midpoint tree) take no part
-            ws = valid && (c != (uint32_t)b) && well_separated(bx, by, br, cx[c], cy[c], r[c], theta);
-        }
-        unsigned wm = __ballot_sync(0xffffffffu, valid && ws);
-        bool merged = false;                        // my group of four merges into its parent q
-        if (merge) {
-            const bool all4 = ((wm >> (lane & ~3)) & 0xFu) == 0xFu;
-            bool mq = false;
-            if (all4 && (lane & 3) == 0) mq = well_separated(bx, by, br, pcx[q], pcy[q], pr[q], theta);
-            merged = __shfl_sync(0xffffffffu, mq ? 1 : 0, lane & ~3) != 0;
-            wm = __ballot_sync(0xffffffffu, valid && ws && !merged);
-        }
-        unsigned sm = __ballot_sync(0xffffffffu, valid && !ws);
-        unsigned xm = __ballot_sync(0xffffffffu, merged && (lane & 3) == 0);
-        if (valid) {
-            if (merged) {
-                if ((lane & 3) == 0) xtmp[xslot + nx + __popc(xm & lt)] = q;
-            } else if (ws) {
-                wtmp[slot + nw + __popc(wm & lt)] = c;
-            } else {
-                stmp[slot + ns + __popc(sm & lt)] = c;
+            ccx = cx[c];
+            ccy = cy[c];
+            crr = r[c];
+            valid = crr >= 0.0;                      // empty candidates (midpoint tree) take no part
+            if (merge && (lane & 3) == 0) {
+                qx = pcx[q];
+                qy = pcy[q];
+                qr = pr[q];
             }
         }
-        nw += __popc(wm);
-        ns += __popc(sm);
-        nx += __popc(xm);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (!conn[j]) continue;                  // warp-uniform
+            const uint32_t b = (uint32_t)(4 * par + j);
+            const bool ws = valid && (c != b) && well_separated(bx[j], by[j], br[j], ccx, ccy, crr, theta);
+            unsigned wm = __ballot_sync(0xffffffffu, valid && ws);
+            bool merged = false;                    // my group of four merges into its parent q
+            if (merge) {
+                const bool all4 = ((wm >> (lane & ~3)) & 0xFu) == 0xFu;
+                bool mq = false;
+                if (all4 && (lane & 3) == 0) mq = well_separated(bx[j], by[j], br[j], qx, qy, qr, theta);
+                merged = __shfl_sync(0xffffffffu, mq ? 1 : 0, lane & ~3) != 0;
+                wm = __ballot_sync(0xffffffffu, valid && ws && !merged);
+            }
+            const unsigned sm = __ballot_sync(0xffffffffu, valid && !ws);
+            const unsigned xm = __ballot_sync(0xffffffffu, merged && (lane & 3) == 0);
+            if (valid) {
+                if (merged) {
+                    if ((lane & 3) == 0) xtmp[slot[j] / 4 + nx[j] + __popc(xm & lt)] = q;
+                } else if (ws) {
+                    wtmp[slot[j] + nw[j] + __popc(wm & lt)] = c;
+                } else {
+                    stmp[slot[j] + ns[j] + __popc(sm & lt)] = c;
+                }
+            }
+            nw[j] += __popc(wm);
+            ns[j] += __popc(sm);
+            nx[j] += __popc(xm);
+        }
     }
-    if (lane == 0) {
-        wcnt[b] = nw;
-        scnt[b] = ns;
-        if (merge) xcnt[b] = nx;
+    if (lane < 4 && live[lane]) {
+        const int64_t b = 4 * par + lane;
+        // (register arrays indexed by lane: select instead of local memory)
+        int64_t w = nw[0], sct = ns[0], x = nx[0];
+#pragma unroll
+        for (int j = 1; j < 4; ++j)
+            if (lane == j) {
+                w = nw[j];
+                sct = ns[j];
+                x = nx[j];
+            }
+        wcnt[b] = w;
+        scnt[b] = sct;
+        if (merge) xcnt[b] = x;
     }
 }
 
@@ -473,12 +512,13 @@ int build_lists(fmm2d_plan* P)
             const double* pcy = P->cy + P->base[l - 1];
             const double* pr = P->r + P->base[l - 1];
             unsigned grid = grid_for((b1 - b0) * 32, 256);
+            const unsigned grid4 = grid_for((((b1 + 3) >> 2) - (b0 >> 2)) * 32, 256);   // warp per parent
             uint32_t *wtmp = nullptr, *stmp = nullptr, *xtmp = nullptr;
             const int64_t cap = 16 * PS.total;          // sum of the candidate counts of all boxes
             FMM2D_CUDA_TRY(cudaMallocAsync((void**)&wtmp, sizeof(uint32_t) * std::max<int64_t>(cap, 1), st));
             FMM2D_CUDA_TRY(cudaMallocAsync((void**)&stmp, sizeof(uint32_t) * std::max<int64_t>(cap, 1), st));
             if (merge) FMM2D_CUDA_TRY(cudaMallocAsync((void**)&xtmp, sizeof(uint32_t) * std::max<int64_t>(cap / 4, 1), st));
-            k_lists<<<grid, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w, cnt_s, wtmp, stmp, merge,
+            k_lists<<<grid4, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w, cnt_s, wtmp, stmp, merge,
                                           pcx, pcy, pr, cnt_x, xtmp); fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
             size_t sb = scan_bytes;
