@@ -17,7 +17,6 @@
 // below the machine balance).  Every kernel is templated on p so the coefficient
 // vectors live in registers.
 #include "fmm2d_internal.cuh"
-#include "fastmath.cuh"
 
 namespace fmm2d {
 
@@ -353,192 +352,6 @@ __global__ void __launch_bounds__(128) k_l2l(int64_t c0, int64_t c1, const doubl
 
 inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
-// ---------------------------------------------------------------- r/R exchange (DESIGN R23)
-// P2L: the sources of the larger leaves in a leaf's P2L list go straight into
-// its local expansion: b_0 += m Log(c - z_j), b_l += -m / (l (z_j - c)^l) (c - z_j and
-// z_j - c each formed componentwise, R2).  One block of RR_T threads per leaf with P2L
-// work: warp w takes list entries w, w + RR_W, ...; lanes over each entry's sources;
-// coefficients in registers, a fixed-order shuffle reduction per warp, the warps'
-// partials summed in warp order in shared memory and added to the local.  Per source:
-// log|.|, Arg and 1/|.|^2 by the table-driven routines of fastmath.cuh (tables in shared
-// memory, as in k_near), t_l = m iv^l by one complex product per l, b_l -= t_l / l.
-constexpr int RR_T = 128, RR_W = RR_T / 32;
-
-__device__ __forceinline__ void rr_load_tables(fm::Tables& T, const fm::Tables* __restrict__ g)
-{
-    const double2* gs = reinterpret_cast<const double2*>(g);
-    double2* ss = reinterpret_cast<double2*>(&T);
-    for (int k = threadIdx.x; k < (int)(sizeof(fm::Tables) / 16); k += blockDim.x) ss[k] = gs[k];
-}
-
-template <int P>
-__global__ void __launch_bounds__(RR_T) k_rr_p2l(const uint32_t* __restrict__ leaves,
-                                                 const int64_t* __restrict__ off, const uint32_t* __restrict__ idx,
-                                                 const uint32_t* __restrict__ boff, const double4* __restrict__ src,
-                                                 const double* __restrict__ cx, const double* __restrict__ cy,
-                                                 double2* __restrict__ loc, const fm::Tables* __restrict__ gtab)
-{
-    __shared__ double2 part[RR_W][P + 1];
-    __shared__ fm::Tables T;
-    rr_load_tables(T, gtab);
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t t = leaves[blockIdx.x];
-    const double ctx = cx[t], cty = cy[t];
-    double2 b[P + 1];
-#pragma unroll
-    for (int l = 0; l <= P; ++l) b[l] = make_double2(0.0, 0.0);
-    for (int64_t q = off[t] + warp; q < off[t + 1]; q += RR_W) {
-        const uint32_t s = idx[q];
-        for (uint32_t j = boff[s] + lane; j < boff[s + 1]; j += 32) {
-            const double4 z = src[j];
-            const double2 m = make_double2(z.z, z.w);
-            const double ux = ctx - z.x, uy = cty - z.y;              // c - z_j
-            const double r2 = fma(ux, ux, uy * uy);
-            const double2 lg = make_double2(0.5 * fm::log_pos(r2, T.lg), fm::arg_t(ux, uy, T.at));
-            b[0] = cadd(b[0], cmul(m, lg));
-            const double vx = z.x - ctx, vy = z.y - cty;              // z_j - c
-            const double iv2 = fm::rcp(fma(vx, vx, vy * vy));
-            const double2 iv = make_double2(vx * iv2, -vy * iv2);
-            double2 tl = m;
-#pragma unroll
-            for (int l = 1; l <= P; ++l) {
-                tl = cmul(tl, iv);                                     // m iv^l
-                const double c = -1.0 / l;
-                b[l].x = fma(c, tl.x, b[l].x);
-                b[l].y = fma(c, tl.y, b[l].y);
-            }
-        }
-    }
-#pragma unroll
-    for (int l = 0; l <= P; ++l) {
-        for (int o = 16; o; o >>= 1) {
-            b[l].x += __shfl_xor_sync(0xffffffffu, b[l].x, o);
-            b[l].y += __shfl_xor_sync(0xffffffffu, b[l].y, o);
-        }
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int l = 0; l <= P; ++l) part[warp][l] = b[l];
-    }
-    __syncthreads();
-    if (threadIdx.x <= P) {
-        const int l = threadIdx.x;
-        double2 v = part[0][l];
-        for (int w = 1; w < RR_W; ++w) v = cadd(v, part[w][l]);
-        double2* Lc = loc + (int64_t)t * (P + 1);
-        Lc[l] = cadd(Lc[l], v);
-    }
-}
-
-// M2P: the multipoles of the smaller leaves in a leaf's M2P list evaluated at
-// each of its points: Phi += a_0 Log(w) + sum_k a_k x^k and Phi' += a_0 x - x^2 sum_k k a_k
-// x^(k-1), w = z_i - c_s (componentwise), x = 1/w.  Both sums from one Horner pass over
-// H(x) = sum_k a_k x^(k-1) and its derivative (sum_k k a_k x^(k-1) = H + x H').  One
-// block per leaf with M2P work: the list's multipoles and centres are staged in shared
-// memory in chunks of RR_CH entries (coalesced loads by the whole block); thread (point i,
-// group g) takes the chunk's entries g, g + G, ...; the G partial sums of a point are
-// added in group order; the sums go to acc[i] (leaf order), k_near adds them.  log|w|,
-// Arg w, 1/|w|^2: fastmath.cuh, tables in shared memory.
-constexpr int RR_CH = 32;
-template <int P>
-__global__ void __launch_bounds__(RR_T) k_rr_m2p(const uint32_t* __restrict__ leaves, const int64_t* __restrict__ off,
-                                                 const uint32_t* __restrict__ idx, const uint32_t* __restrict__ boff,
-                                                 const double4* __restrict__ src, const double* __restrict__ cx,
-                                                 const double* __restrict__ cy, const double2* __restrict__ mp,
-                                                 double4* __restrict__ acc, const fm::Tables* __restrict__ gtab)
-{
-    constexpr int E = P + 2;                        // per entry: P + 1 coefficients, the centre
-    __shared__ double4 part[RR_T];
-    __shared__ double2 sA[RR_CH * E];
-    __shared__ fm::Tables T;
-    rr_load_tables(T, gtab);
-    const uint32_t t = leaves[blockIdx.x];
-    const uint32_t ts = boff[t];
-    const int nt = (int)(boff[t + 1] - ts);
-    const int64_t q0 = off[t], q1 = off[t + 1];
-    const int per = min(nt, RR_T);                  // points per pass
-    const int G = RR_T / per;                       // list groups
-    const int ip = threadIdx.x % per, g = threadIdx.x / per;
-    for (int i0 = 0; i0 < nt; i0 += per) {
-        const int i = i0 + ip;
-        const bool act = g < G && i < nt;
-        double2 f = make_double2(0.0, 0.0), df = make_double2(0.0, 0.0);
-        double4 z = make_double4(0.0, 0.0, 0.0, 0.0);
-        if (act) z = src[ts + i];
-        for (int64_t qc = q0; qc < q1; qc += RR_CH) {
-            const int nch = (int)min((int64_t)RR_CH, q1 - qc);
-            __syncthreads();                        // previous chunk consumed (and the tables)
-            for (int e = threadIdx.x; e < nch * E; e += RR_T) {
-                const int j = e / E, k = e - j * E;
-                const uint32_t s = idx[qc + j];
-                sA[e] = (k <= P) ? mp[(int64_t)s * (P + 1) + k] : make_double2(cx[s], cy[s]);
-            }
-            __syncthreads();
-            if (act) {
-                for (int j = g; j < nch; j += G) {
-                    const double2* A = sA + j * E;
-                    const double2 c = A[P + 1];
-                    const double wx = z.x - c.x, wy = z.y - c.y;
-                    const double r2 = fma(wx, wx, wy * wy);
-                    const double iw2 = fm::rcp(r2);
-                    const double2 x = make_double2(wx * iw2, -wy * iw2);
-                    double2 h = A[P], dh = make_double2(0.0, 0.0);
-#pragma unroll
-                    for (int k = P - 1; k >= 1; --k) {
-                        dh = cadd(cmul(dh, x), h);          // H'
-                        h = cadd(cmul(h, x), A[k]);         // H
-                    }
-                    const double2 d = cadd(h, cmul(x, dh)); // sum_k k a_k x^(k-1)
-                    const double2 lg = make_double2(0.5 * fm::log_pos(r2, T.lg), fm::arg_t(wx, wy, T.at));
-                    f = cadd(f, cadd(cmul(A[0], lg), cmul(h, x)));
-                    df = cadd(df, csub(cmul(A[0], x), cmul(d, cmul(x, x))));
-                }
-            }
-        }
-        __syncthreads();
-        part[threadIdx.x] = make_double4(f.x, f.y, df.x, df.y);
-        __syncthreads();
-        if (g == 0 && i < nt) {
-            double4 v = part[ip];
-            for (int gg = 1; gg < G; ++gg) {
-                const double4 u = part[gg * per + ip];
-                v.x += u.x;
-                v.y += u.y;
-                v.z += u.z;
-                v.w += u.w;
-            }
-            acc[ts + i] = v;
-        }
-    }
-}
-
-template <int P>
-int rr_p2l_p(fmm2d_plan* Pl)
-{
-    if (Pl->rr_np2l == 0) return 0;
-    const int L = Pl->L;
-    k_rr_p2l<P><<<(unsigned)Pl->rr_np2l, RR_T, 0, Pl->stream>>>(
-        Pl->rr_p2l_leaves, Pl->rr_p2l.off, Pl->rr_p2l.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
-        Pl->cy + Pl->base[L], Pl->local + Pl->base[L] * (P + 1), static_cast<const fm::Tables*>(Pl->tables));
-    fmm2d::note_launch();
-    FMM2D_CUDA_TRY(cudaGetLastError());
-    return 0;
-}
-
-template <int P>
-int rr_m2p_p(fmm2d_plan* Pl)
-{
-    if (Pl->rr_nm2p == 0) return 0;
-    const int L = Pl->L;
-    k_rr_m2p<P><<<(unsigned)Pl->rr_nm2p, RR_T, 0, Pl->stream>>>(
-        Pl->rr_m2p_leaves, Pl->rr_m2p.off, Pl->rr_m2p.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
-        Pl->cy + Pl->base[L], Pl->mpole + Pl->base[L] * (P + 1), Pl->rr_acc, static_cast<const fm::Tables*>(Pl->tables));
-    fmm2d::note_launch();
-    FMM2D_CUDA_TRY(cudaGetLastError());
-    return 0;
-}
-
 // P2M of the own leaves, then M2M for parent levels L-1 .. lstop (own parents; the
 // replicated levels above the partition level are done by upward_top_p)
 template <int P>
@@ -667,17 +480,6 @@ int run_upward_top(fmm2d_plan* P)
     switch (P->p) { FMM2D_P_CASES(upward_top_p) default: return FMM2D_EINVAL; }
 }
 
-int run_rr_p2l(fmm2d_plan* P)
-{
-    if (!(P->flags & FMM2D_RR_EXCHANGE)) return 0;
-    switch (P->p) { FMM2D_P_CASES(rr_p2l_p) default: return FMM2D_EINVAL; }
-}
-
-int run_rr_m2p(fmm2d_plan* P)
-{
-    if (!(P->flags & FMM2D_RR_EXCHANGE)) return 0;
-    switch (P->p) { FMM2D_P_CASES(rr_m2p_p) default: return FMM2D_EINVAL; }
-}
 
 int run_m2l(fmm2d_plan* P)
 {

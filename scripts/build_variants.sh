@@ -9,7 +9,7 @@ for v in "$@"; do
   nvcc -O3 -std=c++17 $ARCH -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden $v \
        -c paper_1006_2269_b200/csrc/$stem.cu -o build/var_$name/$stem.o
   objs=""
-  for o in api expansions lists near shard tree; do
+  for o in api expansions lists near rr shard tree; do
     if [ "$o" = "$stem" ]; then objs="$objs build/var_$name/$stem.o"; else objs="$objs build/$o.o"; fi
   done
   nvcc $ARCH -shared -o build/var_$name/libfmm2d.so $objs
