@@ -20,7 +20,17 @@
 
 namespace fmm2d {
 
-__constant__ double c_m2l[(FMM2D_PMAX + 1) * (FMM2D_PMAX + 1)];   // [l][k] = C(l+k-1, k-1)
+// M2L transition matrix C(l+k-1, k-1), l = 0..p, k = 1..p, at [l * M2L_CS + k - 1 + M2L_KOFF]
+// (the layout changes which uniform constant loads the compiler emits: measured per layout)
+#ifndef FMM2D_M2L_CS
+#define FMM2D_M2L_CS 33
+#endif
+#ifndef FMM2D_M2L_KOFF
+#define FMM2D_M2L_KOFF 1
+#endif
+constexpr int M2L_CS = FMM2D_M2L_CS, M2L_KOFF = FMM2D_M2L_KOFF;
+static_assert(M2L_CS + M2L_KOFF >= FMM2D_PMAX + 1, "row stride of the M2L matrix");
+__constant__ double c_m2l[(FMM2D_PMAX + 1) * M2L_CS + M2L_KOFF];
 __constant__ double c_pas[(FMM2D_PMAX + 1) * (FMM2D_PMAX + 1)];   // [a][b] = C(a, b)
 
 // exact binomials in 64-bit integers (C(63,31) < 2^64), correctly rounded to double
@@ -41,12 +51,13 @@ int upload_binomials(int p)
     if (uploaded_for_device == dev) return 0;
     (void)p;
     const int S = FMM2D_PMAX + 1;
-    std::vector<double> m2l(S * S, 0.0), pas(S * S, 0.0);
+    std::vector<double> m2l(S * M2L_CS + M2L_KOFF, 0.0), pas(S * S, 0.0);
     for (int l = 0; l <= FMM2D_PMAX; ++l)
-        for (int k = 1; k <= FMM2D_PMAX; ++k) m2l[l * S + k] = (double)binom_u64(l + k - 1, k - 1);
+        for (int k = 1; k <= FMM2D_PMAX; ++k)
+            m2l[l * M2L_CS + k - 1 + M2L_KOFF] = (double)binom_u64(l + k - 1, k - 1);
     for (int a = 0; a <= FMM2D_PMAX; ++a)
         for (int b = 0; b <= a; ++b) pas[a * S + b] = (double)binom_u64(a, b);
-    FMM2D_CUDA_TRY(cudaMemcpyToSymbol(c_m2l, m2l.data(), sizeof(double) * S * S));
+    FMM2D_CUDA_TRY(cudaMemcpyToSymbol(c_m2l, m2l.data(), sizeof(double) * m2l.size()));
     FMM2D_CUDA_TRY(cudaMemcpyToSymbol(c_pas, pas.data(), sizeof(double) * S * S));
     uploaded_for_device = dev;
     return 0;
@@ -178,7 +189,7 @@ __device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, double ctx
         double2 beta = make_double2(0.0, 0.0);
 #pragma unroll
         for (int k = 1; k <= P; ++k) {
-            const double c = c_m2l[l * S1 + k];
+            const double c = c_m2l[l * M2L_CS + k - 1 + M2L_KOFF];
             beta.x = fma(c, al[k].x, beta.x);
             beta.y = fma(c, al[k].y, beta.y);
         }
