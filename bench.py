@@ -395,27 +395,44 @@ def end_to_end(z_np, m_np, cfg, real, stream, args, shard_kw):
     mh = torch.from_numpy(m_np).pin_memory()
     ph = torch.empty(cfg.n, dtype=torch.complex128).pin_memory()
     dh = torch.empty(cfg.n, dtype=torch.complex128).pin_memory()
-    kw = dict(theta=cfg.theta, p=cfg.p, leaf_target=cfg.leaf_target, real_strengths=real, stream=stream)
+    kw = dict(theta=cfg.theta, p=cfg.p, leaf_target=cfg.leaf_target, real_strengths=real)
+    # one GPU: two problems in flight on two streams (fmm2d_build_eval with FMM2D_ASYNC_HOST:
+    # each call returns once its result copies are enqueued; the strengths' copy overlaps the
+    # build, and one problem's copies overlap the other's kernels); each problem has its own
+    # pinned output buffers.  Several GPUs: build, then eval on the bench stream.
+    streams = [stream, torch.cuda.Stream()]
+    outs = [(ph, dh), (torch.empty_like(ph).pin_memory(), torch.empty_like(dh).pin_memory())]
+    inflight = []
 
-    def step():
-        # one call with host buffers: fmm2d_build_eval (the strengths' copy overlaps the
-        # build); several GPUs: build, then eval (each rank its own plan)
+    def step(k):
         if shard_kw:
-            plan = Fmm2d(zh, **kw, **shard_kw)
+            plan = Fmm2d(zh, stream=stream, **kw, **shard_kw)
             plan.eval(mh, ph, dh)
-        else:
-            plan = Fmm2d.build_eval(zh, mh, ph, dh, **kw)[0]
-        plan.close()
+            plan.close()
+            return
+        o = outs[k % 2]
+        plan = Fmm2d.build_eval(zh, mh, o[0], o[1], stream=streams[k % 2], async_host=True, **kw)[0]
+        inflight.append(plan)
+        if len(inflight) > 1:
+            inflight.pop(0).close()          # synchronises the older problem's stream
 
-    step()
+    step(0)
+    step(1)
+    while inflight:
+        inflight.pop(0).close()
     torch.cuda.synchronize()
-    steps = max(1, min(args.steps, 3))
+    steps = max(2, min(args.steps, 4))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        step()
-    e1.record(stream)
+    e_side = torch.cuda.Event()
+    e0.record(streams[0])
+    for k in range(steps):
+        step(k)
+    e_side.record(streams[1])                   # the end of both streams' work, on stream 0
+    streams[0].wait_event(e_side)
+    e1.record(streams[0])
+    while inflight:
+        inflight.pop(0).close()
     torch.cuda.synchronize()
     return {"ms": e0.elapsed_time(e1) / steps, "h2d": 16 * cfg.n * 2, "d2h": 16 * cfg.n * 2}
 

@@ -86,6 +86,13 @@ extern "C" {
                                       at geometric midpoints ("standard midpoint
                                       adaptivity", Fig. 2) instead of source medians; empty
                                       boxes allowed (R26).  One GPU only        */
+#define FMM2D_ASYNC_HOST     0x400  /* with FMM2D_HOST_PTRS: fmm2d_eval / fmm2d_build_eval
+                                      return once the results' device->host copies are
+                                      enqueued on opt->stream instead of waiting for them;
+                                      the caller synchronises that stream before reading
+                                      phi / dphi (fmm2d_free does).  Lets a caller keep two
+                                      problems in flight on two streams (the copies of one
+                                      overlap the kernels of the other)                   */
 #define FMM2D_TREE_GLOBAL_ONLY 0x10 /* diagnostic: every split step in global memory (no
                                       on-chip finish of the deepest levels; same tree)  */
 
@@ -131,10 +138,13 @@ FMM2D_API int fmm2d_eval(fmm2d_plan* plan, const double* m, double* phi, double*
 
 /* fmm2d_build followed by one fmm2d_eval, for a caller that holds z and m together
  * (same arguments and meaning as those two calls; *out receives the plan, which later
- * fmm2d_eval calls may reuse).  With FMM2D_HOST_PTRS the strengths' host->device copy
- * runs on a second stream as soon as the positions' copy has finished, so it overlaps
- * the tree build instead of following it (the copy engine beside the build kernels);
- * the strengths are then staged in the plan's own buffer.  Synchronous with
+ * fmm2d_eval calls may reuse).  With FMM2D_HOST_PTRS the positions' copy and the build
+ * run on an internal high-priority stream, the strengths' host->device copy on a second
+ * one as soon as the positions' copy has finished (it overlaps the tree build), and the
+ * evaluation and the results' copies on opt->stream; the strengths are then staged in the
+ * plan's own buffer.  With FMM2D_ASYNC_HOST as well, two problems can be kept in flight on
+ * two caller streams: the next build's kernels are dispatched ahead of the running
+ * evaluation's, and each problem's copies overlap the other's kernels.  Synchronous with
  * FMM2D_HOST_PTRS, else stream-ordered like fmm2d_eval.  Multi-GPU plans: not
  * supported (ENOTSUP).  Errors: those of fmm2d_build and fmm2d_eval. */
 FMM2D_API int fmm2d_build_eval(const double* z, const double* m, int64_t n, const fmm2d_options* opt,

@@ -270,29 +270,41 @@ int fmm2d_build_eval(const double* z, const double* m, int64_t n, const fmm2d_op
     }
     if (n < 1) return FMM2D_EINVAL;
     FMM2D_CUDA_TRY(cudaSetDevice(opt->device));
+    // streams: the build (positions' copy + build kernels) on a HIGH-priority stream of its
+    // own, the strengths' copy on a second one behind the positions' copy, the evaluation
+    // and the results' copies on the caller's stream.  With another problem's evaluation
+    // in flight (FMM2D_ASYNC_HOST, two streams), the build's CTAs are dispatched ahead of
+    // that evaluation's instead of queueing behind all of them.
     cudaStream_t st = (cudaStream_t)opt->stream;
-    cudaStream_t side = nullptr;
+    cudaStream_t bst = nullptr, side = nullptr;
     cudaEvent_t ev_z = nullptr, ev_m = nullptr;
     double2 *dz = nullptr, *dm = nullptr;
     fmm2d_plan* P = nullptr;
     auto body = [&]() -> int {
+        int lo = 0, hi = 0;
+        FMM2D_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        FMM2D_CUDA_TRY(cudaStreamCreateWithPriority(&bst, cudaStreamNonBlocking, hi));
         FMM2D_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         FMM2D_CUDA_TRY(cudaEventCreateWithFlags(&ev_z, cudaEventDisableTiming));
         FMM2D_CUDA_TRY(cudaEventCreateWithFlags(&ev_m, cudaEventDisableTiming));
-        FMM2D_CUDA_TRY(cudaMallocAsync((void**)&dz, sizeof(double2) * n, st));
-        FMM2D_CUDA_TRY(cudaMallocAsync((void**)&dm, sizeof(double2) * n, st));
+        FMM2D_CUDA_TRY(cudaMallocAsync((void**)&dz, sizeof(double2) * n, bst));
+        FMM2D_CUDA_TRY(cudaMallocAsync((void**)&dm, sizeof(double2) * n, bst));
         // positions first (the build needs them), then the strengths behind them
-        FMM2D_CUDA_TRY(cudaMemcpyAsync(dz, z, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
-        FMM2D_CUDA_TRY(cudaEventRecord(ev_z, st));
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(dz, z, sizeof(double2) * n, cudaMemcpyHostToDevice, bst));
+        FMM2D_CUDA_TRY(cudaEventRecord(ev_z, bst));
         FMM2D_CUDA_TRY(cudaStreamWaitEvent(side, ev_z, 0));
         FMM2D_CUDA_TRY(cudaMemcpyAsync(dm, m, sizeof(double2) * n, cudaMemcpyHostToDevice, side));
         FMM2D_CUDA_TRY(cudaEventRecord(ev_m, side));
         fmm2d_options o = *opt;
         o.flags &= ~FMM2D_HOST_PTRS;
-        FMM2D_TRY(fmm2d_build((const double*)dz, n, &o, &P));
-        cudaFreeAsync(dz, st);
+        o.stream = bst;
+        FMM2D_TRY(fmm2d_build((const double*)dz, n, &o, &P));   // synchronous
+        // from here on the plan lives on the caller's stream, with host-pointer semantics;
+        // the strengths already sit in its staging buffer
+        P->stream = st;
+        cudaFreeAsync(dz, bst);
         dz = nullptr;
-        // the plan keeps host-pointer semantics; the strengths already sit in its staging
+        FMM2D_CUDA_TRY(cudaStreamSynchronize(bst));
         P->flags |= FMM2D_HOST_PTRS;
         P->allocs.push_back(dm);
         P->mstage = dm;
@@ -303,11 +315,15 @@ int fmm2d_build_eval(const double* z, const double* m, int64_t n, const fmm2d_op
         return eval_impl(&P, 1, nullptr, phi, dphi, nullptr);   // m == nullptr: already staged
     };
     int rc = body();
-    if (dz) cudaFreeAsync(dz, st);
-    if (dm) cudaFreeAsync(dm, st);
+    if (dz) cudaFreeAsync(dz, bst ? bst : st);
+    if (dm) cudaFreeAsync(dm, bst ? bst : st);
     if (side) {
         cudaStreamSynchronize(side);
         cudaStreamDestroy(side);
+    }
+    if (bst) {
+        cudaStreamSynchronize(bst);
+        cudaStreamDestroy(bst);
     }
     if (ev_z) cudaEventDestroy(ev_z);
     if (ev_m) cudaEventDestroy(ev_m);
@@ -420,7 +436,7 @@ static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi
     if (host) {
         if (phi) FMM2D_CUDA_TRY(cudaMemcpyAsync(phi, phid, sizeof(double2) * n, cudaMemcpyDeviceToHost, P0->stream));
         if (dphi) FMM2D_CUDA_TRY(cudaMemcpyAsync(dphi, dphid, sizeof(double2) * n, cudaMemcpyDeviceToHost, P0->stream));
-        FMM2D_CUDA_TRY(cudaStreamSynchronize(P0->stream));
+        if (!(P0->flags & FMM2D_ASYNC_HOST)) FMM2D_CUDA_TRY(cudaStreamSynchronize(P0->stream));
     }
     return 0;
 }

@@ -33,6 +33,7 @@ PARENT_MERGE = 0x40
 OVERLAP = 0x80
 GATHER_OUTPUT = 0x100
 MIDPOINT = 0x200
+ASYNC_HOST = 0x400
 
 EXPORT_PERM, EXPORT_OFFSETS, EXPORT_DISCS, EXPORT_STRONG, EXPORT_WEAK, EXPORT_MPOLE, EXPORT_LOCAL, \
     EXPORT_STATS, EXPORT_NEAR, EXPORT_RR_P2L, EXPORT_RR_M2P, EXPORT_XWEAK = range(1, 13)
@@ -172,7 +173,7 @@ class Fmm2d:
                  real_strengths: bool = False, device: int | None = None, stream=None,
                  symmetric_p2p: bool = False, tree_key64: bool = False, tree_global_only: bool = False,
                  rr_exchange: bool = False, parent_merge: bool = False, overlap: bool = False,
-                 gather_output: bool = False, midpoint: bool = False,
+                 gather_output: bool = False, midpoint: bool = False, async_host: bool = False,
                  nranks: int = 1, rank: int = 0,
                  nccl_id: bytes | None = None, _first=None):
         L = lib()
@@ -195,7 +196,8 @@ class Fmm2d:
                      | (SYMMETRIC_P2P if symmetric_p2p else 0) | (TREE_KEY64 if tree_key64 else 0)
                      | (TREE_GLOBAL_ONLY if tree_global_only else 0) | (RR_EXCHANGE if rr_exchange else 0)
                      | (PARENT_MERGE if parent_merge else 0) | (OVERLAP if overlap else 0)
-                     | (GATHER_OUTPUT if gather_output else 0) | (MIDPOINT if midpoint else 0))
+                     | (GATHER_OUTPUT if gather_output else 0) | (MIDPOINT if midpoint else 0)
+                     | (ASYNC_HOST if async_host else 0))
         opt.device = int(device)
         opt.stream = ctypes.c_void_p(stream.cuda_stream)
         opt.nranks = int(nranks)

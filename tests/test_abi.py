@@ -105,7 +105,7 @@ def test_flag_values_match_header():
     src = open(os.path.join(ROOT, "include", "fmm2d.h")).read()
     flags = {k: int(v, 16) for k, v in re.findall(r"#define FMM2D_(\w+)\s+(0x[0-9a-fA-F]+)", src)}
     for name in ("HOST_PTRS", "REAL_STRENGTHS", "SYMMETRIC_P2P", "TREE_KEY64", "TREE_GLOBAL_ONLY", "RR_EXCHANGE",
-                 "PARENT_MERGE", "OVERLAP", "GATHER_OUTPUT", "MIDPOINT"):
+                 "PARENT_MERGE", "OVERLAP", "GATHER_OUTPUT", "MIDPOINT", "ASYNC_HOST"):
         assert getattr(F.fmm2d, name) == flags[name], name
     exports = {k: int(v) for k, v in re.findall(r"#define FMM2D_EXPORT_(\w+)\s+(\d+)", src)}
     for name, v in exports.items():

@@ -243,6 +243,32 @@ def test_build_eval_equals_build_then_eval(host):
     plan.close()
 
 
+def test_async_host_two_problems_in_flight():
+    """FMM2D_ASYNC_HOST: two host-buffer problems in flight on two streams (the bench's e2e
+    pattern) give the synchronous results bit for bit once each stream is synchronised."""
+    import torch
+    from paper_1006_2269_b200 import Fmm2d
+    z1, m1 = W.make_config("C2", n=40_000)
+    z2, m2 = W.make_config("C3", n=60_000)
+    ref1 = Fmm2d.build_eval(z1, m1, theta=0.5, p=17)[1:]
+    ref2 = Fmm2d.build_eval(z2, m2, theta=0.5, p=17)[1:]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    out = []
+    plans = []
+    for z, m, st in ((z1, m1, s1), (z2, m2, s2), (z1, m1, s2)):
+        ph = torch.empty(z.shape[0], dtype=torch.complex128).pin_memory()
+        dh = torch.empty(z.shape[0], dtype=torch.complex128).pin_memory()
+        plans.append(Fmm2d.build_eval(z, m, ph, dh, theta=0.5, p=17, stream=st, async_host=True)[0])
+        out.append((ph, dh))
+    s1.synchronize()
+    s2.synchronize()
+    for (ph, dh), ref in zip(out, (ref1, ref2, ref1)):
+        np.testing.assert_array_equal(ph.numpy(), ref[0].numpy())
+        np.testing.assert_array_equal(dh.numpy(), ref[1].numpy())
+    for p_ in plans:
+        p_.close()
+
+
 def test_eval_deterministic_and_reusable():
     z, m = W.make_config("C2", n=30_000)
     gp = _gpu_plan(z, 0.5, 17, 5)
