@@ -45,10 +45,10 @@ static uint64_t binom_u64(int a, int b)
 
 int upload_binomials(int p)
 {
-    static int uploaded_for_device = -1;
+    static bool uploaded[64] = {false};           // per device (__constant__ data is per device)
     int dev = 0;
     FMM2D_CUDA_TRY(cudaGetDevice(&dev));
-    if (uploaded_for_device == dev) return 0;
+    if (dev >= 0 && dev < 64 && uploaded[dev]) return 0;
     (void)p;
     const int S = FMM2D_PMAX + 1;
     std::vector<double> m2l(S * M2L_CS + M2L_KOFF, 0.0), pas(S * S, 0.0);
@@ -59,7 +59,7 @@ int upload_binomials(int p)
         for (int b = 0; b <= a; ++b) pas[a * S + b] = (double)binom_u64(a, b);
     FMM2D_CUDA_TRY(cudaMemcpyToSymbol(c_m2l, m2l.data(), sizeof(double) * m2l.size()));
     FMM2D_CUDA_TRY(cudaMemcpyToSymbol(c_pas, pas.data(), sizeof(double) * S * S));
-    uploaded_for_device = dev;
+    if (dev >= 0 && dev < 64) uploaded[dev] = true;
     return 0;
 }
 
