@@ -206,6 +206,23 @@ def test_eval_root_only_equals_direct(orc):
     assert _nerr(phi_g, phi_d) <= 1e-13 and _nerr(dphi_g, dphi_d) <= 1e-13
 
 
+@pytest.mark.parametrize("n,L", [(1, 0), (2, 0), (3, 0), (4, 1), (5, 1), (16, 2)])
+def test_eval_tiny_inputs_match_direct(orc, n, L):
+    """Degenerate sizes: one point (empty sum: Phi = Phi' = 0), a pair, one point per leaf
+    (every leaf-level box is its own near list), forced levels on tiny inputs.  Against the
+    oracle: Phi and Phi'; against the direct sum: Re Phi and Phi' (real strengths: the FMM
+    branch of Im Phi is not the principal-branch sum's, DESIGN R2)."""
+    z, m = W.make("uniform", n, "real", seed=100 + n)
+    phi_g, dphi_g = _gpu_eval(_gpu_plan(z, 0.5, 17, L), m)
+    if n == 1:
+        assert np.all(phi_g == 0) and np.all(dphi_g == 0)
+        return
+    phi_o, dphi_o = orc.plan(z, 0.5, L).eval(m, 17)
+    assert _nerr(phi_g, phi_o) <= TOL and _nerr(dphi_g, dphi_o) <= TOL
+    phi_d, dphi_d = orc.direct(z, m)
+    assert _nerr(phi_g.real, phi_d.real) <= 1e-6 and _nerr(dphi_g, dphi_d) <= 1e-6
+
+
 def test_host_pointer_path_equals_device_path():
     from paper_1006_2269_b200 import Fmm2d
     z, m = W.make_config("C1")
