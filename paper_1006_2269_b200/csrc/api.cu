@@ -5,6 +5,7 @@
 // far-to-local shifts along the weak pattern, downward shifts, and the direct
 // near field at the finest level.
 #include <atomic>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -275,16 +276,29 @@ int fmm2d_build_eval(const double* z, const double* m, int64_t n, const fmm2d_op
     // and the results' copies on the caller's stream.  With another problem's evaluation
     // in flight (FMM2D_ASYNC_HOST, two streams), the build's CTAs are dispatched ahead of
     // that evaluation's instead of queueing behind all of them.
+    // The two internal streams are created once per device and kept: allocations made on
+    // them are then reused from the memory pool call after call (a fresh stream per call
+    // made the pool grow now and then, a host stall of tens of ms).
     cudaStream_t st = (cudaStream_t)opt->stream;
     cudaStream_t bst = nullptr, side = nullptr;
     cudaEvent_t ev_z = nullptr, ev_m = nullptr;
     double2 *dz = nullptr, *dm = nullptr;
     fmm2d_plan* P = nullptr;
     auto body = [&]() -> int {
-        int lo = 0, hi = 0;
-        FMM2D_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        FMM2D_CUDA_TRY(cudaStreamCreateWithPriority(&bst, cudaStreamNonBlocking, hi));
-        FMM2D_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        static std::mutex mu;
+        static cudaStream_t cache_b[64] = {nullptr}, cache_s[64] = {nullptr};
+        if (opt->device < 0 || opt->device >= 64) return FMM2D_EINVAL;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!cache_b[opt->device]) {
+                int lo = 0, hi = 0;
+                FMM2D_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+                FMM2D_CUDA_TRY(cudaStreamCreateWithPriority(&cache_b[opt->device], cudaStreamNonBlocking, hi));
+                FMM2D_CUDA_TRY(cudaStreamCreateWithFlags(&cache_s[opt->device], cudaStreamNonBlocking));
+            }
+            bst = cache_b[opt->device];
+            side = cache_s[opt->device];
+        }
         FMM2D_CUDA_TRY(cudaEventCreateWithFlags(&ev_z, cudaEventDisableTiming));
         FMM2D_CUDA_TRY(cudaEventCreateWithFlags(&ev_m, cudaEventDisableTiming));
         FMM2D_CUDA_TRY(cudaMallocAsync((void**)&dz, sizeof(double2) * n, bst));
@@ -317,14 +331,8 @@ int fmm2d_build_eval(const double* z, const double* m, int64_t n, const fmm2d_op
     int rc = body();
     if (dz) cudaFreeAsync(dz, bst ? bst : st);
     if (dm) cudaFreeAsync(dm, bst ? bst : st);
-    if (side) {
-        cudaStreamSynchronize(side);
-        cudaStreamDestroy(side);
-    }
-    if (bst) {
-        cudaStreamSynchronize(bst);
-        cudaStreamDestroy(bst);
-    }
+    if (side) cudaStreamSynchronize(side);               // the strengths' copy (kept streams)
+    if (bst) cudaStreamSynchronize(bst);
     if (ev_z) cudaEventDestroy(ev_z);
     if (ev_m) cudaEventDestroy(ev_m);
     if (rc) {
