@@ -161,6 +161,8 @@ int shard_pack_mp(fmm2d_plan* P);
 int shard_comm_mp(fmm2d_plan* const* Ps, int np);
 int shard_unpack_mp(fmm2d_plan* P);
 bool shard_has_comm(const fmm2d_plan* P);
+int shard_allreduce_sum_u32(fmm2d_plan* P, unsigned int* buf, size_t count);
+int shard_allgather_inplace(fmm2d_plan* P, void* base, size_t bytes_per_rank);
 int shard_gather_output(fmm2d_plan* P, double2* phi, double2* dphi);
 void shard_halo_sizes(const fmm2d_plan* P, int64_t* leaves, int64_t* mpoles, int64_t* exp_leaves, int64_t* exp_mp);
 int nccl_unique_id(void* out);

@@ -659,6 +659,26 @@ int shard_unpack_mp(fmm2d_plan* P)
 
 bool shard_has_comm(const fmm2d_plan* P) { return P->shard && P->shard->comm; }
 
+// Collectives of the partitioned build's top-level selection (tree.cu) on the plan's stream.
+int shard_allreduce_sum_u32(fmm2d_plan* P, unsigned int* buf, size_t count)
+{
+    if (!shard_has_comm(P)) return 0;
+    FMM2D_NCCL_TRY(nccl_api()->AllReduce(buf, buf, count, ncclUint32, ncclSum, (ncclComm_t)P->shard->comm,
+                                         P->stream));
+    return 0;
+}
+
+// block r (bytes_per_rank bytes at base + r bytes_per_rank) of every rank to every rank;
+// the caller's own block is already in place
+int shard_allgather_inplace(fmm2d_plan* P, void* base, size_t bytes_per_rank)
+{
+    if (!shard_has_comm(P)) return 0;
+    char* b = static_cast<char*>(base);
+    FMM2D_NCCL_TRY(nccl_api()->AllGather(b + bytes_per_rank * P->rank, b, bytes_per_rank, ncclChar,
+                                         (ncclComm_t)P->shard->comm, P->stream));
+    return 0;
+}
+
 // FMM2D_GATHER_OUTPUT: every rank wrote its own sources' entries into zeroed outputs;
 // a sum all-reduce completes them on every rank (x + 0 = x exactly).  Loopback shards
 // already share one output array: nothing to do.

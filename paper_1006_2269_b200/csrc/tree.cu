@@ -308,7 +308,7 @@ __device__ __forceinline__ int sel_bucket(const SelSeg& S, unsigned long long ke
 // histogram per block (flushed with one global atomic per non-zero bin), or global atomics
 // when the segments' histograms do not fit (SMEM = false)
 template <bool SMEM>
-__global__ void __launch_bounds__(1024) k_top_hist(const double2* __restrict__ zc, int64_t n, int step,
+__global__ void __launch_bounds__(1024) k_top_hist(const double2* __restrict__ zc, int64_t i0, int64_t n, int step,
                                                    const TopRec* __restrict__ recs, const int* __restrict__ roff,
                                                    const SelSeg* __restrict__ sel, int nseg,
                                                    unsigned int* __restrict__ hist)
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(1024) k_top_hist(const double2* __restrict__ z
         for (int j = threadIdx.x; j < nseg * SEL_BUCKETS; j += blockDim.x) shist[j] = 0;
         __syncthreads();
     }
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double2 v = zc[i];
         const uint32_t seg = top_segment(v.x, v.y, (uint32_t)i, step, recs, roff);
         const SelSeg S = sel[seg];
@@ -338,11 +338,11 @@ __global__ void __launch_bounds__(1024) k_top_hist(const double2* __restrict__ z
 }
 
 // the points of bucket 0 of every segment in mode 3 / 4: {key, idx} appended per segment
-__global__ void k_top_cand(const double2* __restrict__ zc, int64_t n, int step, const TopRec* __restrict__ recs,
-                           const int* __restrict__ roff, const SelSeg* __restrict__ sel,
+__global__ void k_top_cand(const double2* __restrict__ zc, int64_t i0, int64_t n, int step,
+                           const TopRec* __restrict__ recs, const int* __restrict__ roff, const SelSeg* __restrict__ sel,
                            const int64_t* __restrict__ coff, unsigned int* __restrict__ ccnt, TopRec* __restrict__ cand)
 {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double2 v = zc[i];
     const uint32_t seg = top_segment(v.x, v.y, (uint32_t)i, step, recs, roff);
@@ -1222,6 +1222,17 @@ static int top_levels_sharded(fmm2d_plan* P, const double2* zc, const Bounds& hb
     };
     const int maxseg = 2 << (2 * (k - 1));
     const int nbk = 1 << (2 * k);
+    // Sliced selection: with NCCL every rank counts (histogram passes) and collects
+    // (candidate pass) over its own slice [n r / R, n (r+1) / R) of the input only; the
+    // histograms are summed by an all-reduce and the candidate blocks all-gathered, so every
+    // rank sees the global counts and candidates.  Loopback with FMM2D_SEL_SLICED=1 runs the
+    // same slices one after the other into the same buffers (the emulation the tests use);
+    // otherwise one pass over all points.
+    const int R = P->nranks, myrank = P->rank;
+    const bool nccl = shard_has_comm(P);
+    const bool emul = !nccl && std::getenv("FMM2D_SEL_SLICED") != nullptr;
+    const int nblk = (nccl || emul) ? R : 1;              // candidate blocks (one per slice)
+    auto slice_lo = [&](int r) { return n * r / R; };
     PhaseTrace tr(st);
     tr.mark("start");
     auto body = [&]() -> int {
@@ -1229,8 +1240,8 @@ static int top_levels_sharded(fmm2d_plan* P, const double2* zc, const Bounds& hb
         FMM2D_TRY(talloc((void**)&d_roff, sizeof(int) * (nsteps + 1)));
         FMM2D_TRY(talloc((void**)&hist, sizeof(unsigned int) * SEL_BUCKETS * maxseg));
         FMM2D_TRY(talloc((void**)&sel, sizeof(SelSeg) * maxseg));
-        FMM2D_TRY(talloc((void**)&cand, sizeof(TopRec) * SEL_COLLECT * maxseg));
-        FMM2D_TRY(talloc((void**)&ccnt, sizeof(unsigned int) * maxseg));
+        FMM2D_TRY(talloc((void**)&cand, sizeof(TopRec) * SEL_COLLECT * maxseg * nblk));
+        FMM2D_TRY(talloc((void**)&ccnt, sizeof(unsigned int) * maxseg * nblk));
         FMM2D_TRY(talloc((void**)&coff, sizeof(int64_t) * maxseg));
         FMM2D_TRY(talloc((void**)&boxk, sizeof(uint32_t) * n));
         FMM2D_TRY(talloc((void**)&sub, sizeof(uint32_t) * n));
@@ -1272,15 +1283,27 @@ static int top_levels_sharded(fmm2d_plan* P, const double2* zc, const Bounds& hb
                 ++npass;
                 FMM2D_CUDA_TRY(cudaMemcpyAsync(sel, hs.data(), sizeof(SelSeg) * nseg, cudaMemcpyHostToDevice, st));
                 FMM2D_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * SEL_BUCKETS * nseg, st));
-                if (nseg <= SEL_SMEM_SEGS) {
-                    const int sm = nseg * SEL_BUCKETS * 4;
-                    FMM2D_CUDA_TRY(cudaFuncSetAttribute(k_top_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-                    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(148, (n + 1023) / 1024));
-                    k_top_hist<true><<<g, 1024, sm, st>>>(zc, n, s, d_recs, d_roff, sel, nseg, hist);
+                auto hist_pass = [&](int64_t a, int64_t b) -> int {
+                    if (b <= a) return 0;
+                    if (nseg <= SEL_SMEM_SEGS) {
+                        const int sm = nseg * SEL_BUCKETS * 4;
+                        FMM2D_CUDA_TRY(cudaFuncSetAttribute(k_top_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+                        const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(148, (b - a + 1023) / 1024));
+                        k_top_hist<true><<<g, 1024, sm, st>>>(zc, a, b, s, d_recs, d_roff, sel, nseg, hist);
+                    } else {
+                        k_top_hist<false><<<grid_for(b - a, BS), BS, 0, st>>>(zc, a, b, s, d_recs, d_roff, sel, nseg, hist);
+                    }
+                    note_launch();
+                    return 0;
+                };
+                if (nccl) {
+                    FMM2D_TRY(hist_pass(slice_lo(myrank), slice_lo(myrank + 1)));
+                    FMM2D_TRY(shard_allreduce_sum_u32(P, hist, (size_t)SEL_BUCKETS * nseg));
+                } else if (emul) {
+                    for (int r = 0; r < R; ++r) FMM2D_TRY(hist_pass(slice_lo(r), slice_lo(r + 1)));
                 } else {
-                    k_top_hist<false><<<grid_for(n, BS), BS, 0, st>>>(zc, n, s, d_recs, d_roff, sel, nseg, hist);
+                    FMM2D_TRY(hist_pass(0, n));
                 }
-                note_launch();
                 FMM2D_CUDA_TRY(cudaMemcpyAsync(h_hist.data(), hist, sizeof(unsigned int) * SEL_BUCKETS * nseg,
                                                cudaMemcpyDeviceToHost, st));
                 FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1328,21 +1351,51 @@ static int top_levels_sharded(fmm2d_plan* P, const double2* zc, const Bounds& hb
                 }
             }
             if (ncol > 0) {
+                // candidate block r (slice r, or everything when not sliced): entries of
+                // segment g at [blk r + coff_g, + count[r][g])
+                const int64_t bstride = (int64_t)SEL_COLLECT * maxseg;
                 FMM2D_CUDA_TRY(cudaMemcpyAsync(sel, hs.data(), sizeof(SelSeg) * nseg, cudaMemcpyHostToDevice, st));
                 FMM2D_CUDA_TRY(cudaMemcpyAsync(coff, hcoff.data(), sizeof(int64_t) * nseg, cudaMemcpyHostToDevice, st));
-                FMM2D_CUDA_TRY(cudaMemsetAsync(ccnt, 0, sizeof(unsigned int) * nseg, st));
-                k_top_cand<<<grid_for(n, BS), BS, 0, st>>>(zc, n, s, d_recs, d_roff, sel, coff, ccnt, cand);
-                note_launch();
-                std::vector<TopRec> hc(std::max<int64_t>(ctot, 1));
-                FMM2D_CUDA_TRY(cudaMemcpyAsync(hc.data(), cand, sizeof(TopRec) * ctot, cudaMemcpyDeviceToHost, st));
+                FMM2D_CUDA_TRY(cudaMemsetAsync(ccnt, 0, sizeof(unsigned int) * maxseg * nblk, st));
+                auto cand_pass = [&](int blk, int64_t a, int64_t b) {
+                    if (b > a)
+                        k_top_cand<<<grid_for(b - a, BS), BS, 0, st>>>(zc, a, b, s, d_recs, d_roff, sel, coff,
+                                                                       ccnt + (int64_t)blk * maxseg,
+                                                                       cand + (int64_t)blk * bstride);
+                    note_launch();
+                };
+                if (nccl) {
+                    cand_pass(myrank, slice_lo(myrank), slice_lo(myrank + 1));
+                    FMM2D_TRY(shard_allgather_inplace(P, cand, sizeof(TopRec) * bstride));
+                    FMM2D_TRY(shard_allgather_inplace(P, ccnt, sizeof(unsigned int) * maxseg));
+                } else if (emul) {
+                    for (int r = 0; r < R; ++r) cand_pass(r, slice_lo(r), slice_lo(r + 1));
+                } else {
+                    cand_pass(0, 0, n);
+                }
+                FMM2D_CUDA_TRY(cudaGetLastError());
+                std::vector<TopRec> hc((size_t)std::max<int64_t>(ctot, 1) * nblk);
+                std::vector<unsigned int> hcnt((size_t)maxseg * nblk);
+                for (int r = 0; r < nblk; ++r)
+                    FMM2D_CUDA_TRY(cudaMemcpyAsync(hc.data() + (size_t)r * std::max<int64_t>(ctot, 1),
+                                                   cand + (int64_t)r * bstride, sizeof(TopRec) * ctot,
+                                                   cudaMemcpyDeviceToHost, st));
+                FMM2D_CUDA_TRY(cudaMemcpyAsync(hcnt.data(), ccnt, sizeof(unsigned int) * maxseg * nblk,
+                                               cudaMemcpyDeviceToHost, st));
                 FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+                std::vector<TopRec> seg;
                 for (int g = 0; g < nseg; ++g) {
                     if (hs[g].mode < 3) continue;
-                    const int64_t c0 = hcoff[g], c1 = c0 + ccap[g];
-                    std::sort(hc.begin() + c0, hc.begin() + c1, [](const TopRec& a, const TopRec& b) {
+                    seg.clear();
+                    for (int r = 0; r < nblk; ++r) {
+                        const TopRec* b0 = hc.data() + (size_t)r * std::max<int64_t>(ctot, 1) + hcoff[g];
+                        seg.insert(seg.end(), b0, b0 + hcnt[(size_t)r * maxseg + g]);
+                    }
+                    if ((int64_t)seg.size() != ccap[g]) return FMM2D_ECUDA;   // counts and candidates disagree
+                    std::sort(seg.begin(), seg.end(), [](const TopRec& a, const TopRec& b) {
                         return a.key < b.key || (a.key == b.key && a.idx < b.idx);
                     });
-                    h_recs[roff[s] + g] = hc[c0 + want[g]];
+                    h_recs[roff[s] + g] = seg[want[g]];
                 }
             }
             FMM2D_CUDA_TRY(cudaMemcpyAsync(d_recs + roff[s], h_recs.data() + roff[s], sizeof(TopRec) * nseg,

@@ -147,3 +147,31 @@ def test_loopback_shards_ties_and_duplicates(name):
         torch.cuda.synchronize()
         assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
         sh.close()
+
+
+@pytest.mark.parametrize("case", ["uniform-300k", "C3-200k", "ties-200k"])
+def test_loopback_shards_sliced_selection(monkeypatch, case):
+    """FMM2D_SEL_SLICED=1: the top-level selection counted and collected slice by slice (the
+    NCCL path's per-rank slices, summed / gathered as its all-reduce and all-gather would) --
+    shards still equal the one-GPU result bit for bit."""
+    from paper_1006_2269_b200 import Fmm2d, LoopbackShards
+    monkeypatch.setenv("FMM2D_SEL_SLICED", "1")
+    rng = np.random.default_rng(33)
+    if case == "uniform-300k":
+        z_np = rng.random(300_000) + 1j * rng.random(300_000)
+    elif case == "C3-200k":
+        z_np, _ = W.make_config("C3", n=200_000)
+    else:
+        n = 200_000
+        z_np = np.round(rng.random(n) * 8) / 8 + 1j * rng.random(n)      # 9 distinct x values
+    m_np = rng.uniform(-1, 1, z_np.shape[0]) + 0j
+    z, m = torch.from_numpy(z_np).cuda(), torch.from_numpy(m_np).cuda()
+    ref = Fmm2d(z, theta=0.5, p=12, leaf_target=40)
+    a = ref.eval(m)
+    for P in (2, 4, 8):
+        sh = LoopbackShards(z, P, theta=0.5, p=12, leaf_target=40)
+        b = sh.eval(m)
+        torch.cuda.synchronize()
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+        sh.close()
+    ref.close()
