@@ -224,8 +224,17 @@ __global__ void k_make_ylist(const uint64_t* __restrict__ vy, int64_t m, uint32_
 // 1: the x-list by a direct scatter xl[rx] = {rx, ry} inside k_make_ylist (one random
 // 8-byte write per point); 0: by one more radix sort of the x ranks (k_make_xlist)
 #ifndef FMM2D_PRESORT_SCATTER
-#define FMM2D_PRESORT_SCATTER 1
+#define FMM2D_PRESORT_SCATTER 2
 #endif
+// 2: the records first bucketed by the top 8 bits of their x rank (one stable radix pass),
+// then scattered: each bucket's destinations form one window of the x-list small enough to
+// stay in L2, so the 8-byte writes merge into whole sectors there instead of in DRAM
+__global__ void k_scatter_xlist(const uint32_t* __restrict__ key, const uint32_t* __restrict__ val, int64_t m,
+                                uint32_t roff, uint2* __restrict__ xl)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < m) xl[key[k]] = make_uint2(roff + key[k], roff + val[k]);
+}
 __global__ void k_make_lists(const uint64_t* __restrict__ vy, int64_t m, uint32_t roff, uint2* __restrict__ yl,
                              uint2* __restrict__ xl)
 {
@@ -1608,7 +1617,16 @@ int build_tree(fmm2d_plan* P, const double2* z)
             if (k64buf) cudaFreeAsync(k64buf, st);
             FMM2D_CUDA_TRY(cudaGetLastError());
             P->stats.tree_key64 |= (force64 || h_ovf[0] ? 1 : 0) + (force64 || h_ovf[1] ? 2 : 0);
-            if (FMM2D_PRESORT_SCATTER) {
+            if (FMM2D_PRESORT_SCATTER == 2) {
+                // y-list {rx, ry}; local x ranks bucketed by their top 8 bits, then scattered
+                k_make_ylist<<<grid_for(m, BS), BS, 0, st>>>(vym, m, roff, yl + roff, k32a, u32a);
+                fmm2d::note_launch();
+                sb = cub_bytes;
+                FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, u32a, u32b, (int)m,
+                                                               std::max(0, mbits - 8), mbits, st));
+                k_scatter_xlist<<<grid_for(m, BS), BS, 0, st>>>(k32b, u32b, m, roff, xl + roff);
+                fmm2d::note_launch();
+            } else if (FMM2D_PRESORT_SCATTER == 1) {
                 // y-list {rx, ry} in y order, and the same records scattered to x order
                 k_make_lists<<<grid_for(m, BS), BS, 0, st>>>(vym, m, roff, yl + roff, xl + roff);
                 fmm2d::note_launch();
