@@ -268,7 +268,10 @@ __device__ __forceinline__ void m2l_target_warp(const M2LArgs& A, int64_t g, int
 #ifndef FMM2D_M2L_MINB
 #define FMM2D_M2L_MINB 2
 #endif
-constexpr int M2L_T = 128;
+#ifndef FMM2D_M2L_T
+#define FMM2D_M2L_T 128
+#endif
+constexpr int M2L_T = FMM2D_M2L_T;
 
 // threads: NS consecutive warps share 32 target boxes; warp-uniform part index.
 // (Tried and measured slower at p = 17 on B200: accumulators in shared memory, and a
