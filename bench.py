@@ -49,6 +49,9 @@ NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 # bounded CPU sample of a workload for the oracle: the C5 recipe at L = 8 (same leaf occupancy,
 # 23.8 points per leaf), build + eval passes repeated up to about 10 s of host work
 CPU_SAMPLE_N = 1_562_500
+# end-to-end line: problems in flight on as many streams (FMM2D_ASYNC_HOST); the oldest is
+# synchronised (its result copies complete) when a new one is issued beyond this count
+E2E_IN_FLIGHT = int(os.environ.get("FMM2D_E2E_IN_FLIGHT", "3"))
 CPU_SAMPLE_SECONDS = 10.0
 
 
@@ -409,8 +412,10 @@ def end_to_end(z_np, m_np, cfg, real, stream, args, shard_kw):
     # each call returns once its result copies are enqueued; the strengths' copy overlaps the
     # build, and one problem's copies overlap the other's kernels); each problem has its own
     # pinned output buffers.  Several GPUs: build, then eval on the bench stream.
-    streams = [stream, torch.cuda.Stream()]
-    outs = [(ph, dh), (torch.empty_like(ph).pin_memory(), torch.empty_like(dh).pin_memory())]
+    NF = E2E_IN_FLIGHT
+    streams = [stream] + [torch.cuda.Stream() for _ in range(NF - 1)]
+    outs = [(ph, dh)] + [(torch.empty_like(ph).pin_memory(), torch.empty_like(dh).pin_memory())
+                         for _ in range(NF - 1)]
     inflight = []
 
     def step(k):
@@ -419,26 +424,27 @@ def end_to_end(z_np, m_np, cfg, real, stream, args, shard_kw):
             plan.eval(mh, ph, dh)
             plan.close()
             return
-        o = outs[k % 2]
-        plan = Fmm2d.build_eval(zh, mh, o[0], o[1], stream=streams[k % 2], async_host=True, **kw)[0]
+        o = outs[k % NF]
+        plan = Fmm2d.build_eval(zh, mh, o[0], o[1], stream=streams[k % NF], async_host=True, **kw)[0]
         inflight.append(plan)
-        if len(inflight) > 1:
-            inflight.pop(0).close()          # synchronises the older problem's stream
+        if len(inflight) > NF - 1:
+            inflight.pop(0).close()          # synchronises the oldest problem's stream
 
-    step(0)
-    step(1)
+    for k in range(NF):
+        step(k)
     while inflight:
         inflight.pop(0).close()
     torch.cuda.synchronize()
     steps = max(2, min(args.steps, 4))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e_side = torch.cuda.Event()
     e0.record(streams[0])
     for k in range(steps):
         step(k)
-    e_side.record(streams[1])                   # the end of both streams' work, on stream 0
-    streams[0].wait_event(e_side)
+    for st_ in streams[1:]:                     # the end of every stream's work, on stream 0
+        e_side = torch.cuda.Event()
+        e_side.record(st_)
+        streams[0].wait_event(e_side)
     e1.record(streams[0])
     while inflight:
         inflight.pop(0).close()
