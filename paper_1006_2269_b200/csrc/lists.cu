@@ -46,6 +46,68 @@ __device__ __forceinline__ int64_t cand_slot(const int64_t* __restrict__ poff, i
     return 16 * poff[par] + 4 * (b & 3) * (poff[par + 1] - poff[par]);
 }
 
+// One warp per box (used where the parents' strong lists are long: one warp per parent would
+// serialise four long candidate walks)
+__global__ void k_lists_box(int64_t b0, int64_t b1, const double* __restrict__ cx, const double* __restrict__ cy,
+                        const double* __restrict__ r, double theta, const int64_t* __restrict__ poff,
+                        const uint32_t* __restrict__ pidx, int64_t* __restrict__ wcnt, int64_t* __restrict__ scnt,
+                        uint32_t* __restrict__ wtmp, uint32_t* __restrict__ stmp, bool merge,
+                        const double* __restrict__ pcx, const double* __restrict__ pcy, const double* __restrict__ pr,
+                        int64_t* __restrict__ xcnt, uint32_t* __restrict__ xtmp)
+{
+    int64_t b = b0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    int lane = threadIdx.x & 31;
+    if (b >= b1) return;
+    int64_t par = b >> 2;
+    int64_t o0 = poff[par];
+    int64_t ncand = 4 * (poff[par + 1] - o0);
+    double bx = cx[b], by = cy[b], br = r[b];
+    int64_t nw = 0, ns = 0, nx = 0;
+    if (br < 0.0) ncand = 0;                 // empty box (midpoint tree): no connections
+    const int64_t slot = cand_slot(poff, b), xslot = slot / 4;
+    unsigned lt = (1u << lane) - 1u;
+    for (int64_t t0 = 0; t0 < ncand; t0 += 32) {
+        int64_t t = t0 + lane;
+        bool valid = t < ncand;
+        uint32_t c = 0, q = 0;
+        bool ws = false;
+        if (valid) {
+            q = pidx[o0 + (t >> 2)];
+            c = 4u * q + (uint32_t)(t & 3);
+            valid = r[c] >= 0.0;                 // empty candidates (midpoint tree) take no part
+            ws = valid && (c != (uint32_t)b) && well_separated(bx, by, br, cx[c], cy[c], r[c], theta);
+        }
+        unsigned wm = __ballot_sync(0xffffffffu, valid && ws);
+        bool merged = false;                        // my group of four merges into its parent q
+        if (merge) {
+            const bool all4 = ((wm >> (lane & ~3)) & 0xFu) == 0xFu;
+            bool mq = false;
+            if (all4 && (lane & 3) == 0) mq = well_separated(bx, by, br, pcx[q], pcy[q], pr[q], theta);
+            merged = __shfl_sync(0xffffffffu, mq ? 1 : 0, lane & ~3) != 0;
+            wm = __ballot_sync(0xffffffffu, valid && ws && !merged);
+        }
+        unsigned sm = __ballot_sync(0xffffffffu, valid && !ws);
+        unsigned xm = __ballot_sync(0xffffffffu, merged && (lane & 3) == 0);
+        if (valid) {
+            if (merged) {
+                if ((lane & 3) == 0) xtmp[xslot + nx + __popc(xm & lt)] = q;
+            } else if (ws) {
+                wtmp[slot + nw + __popc(wm & lt)] = c;
+            } else {
+                stmp[slot + ns + __popc(sm & lt)] = c;
+            }
+        }
+        nw += __popc(wm);
+        ns += __popc(sm);
+        nx += __popc(xm);
+    }
+    if (lane == 0) {
+        wcnt[b] = nw;
+        scnt[b] = ns;
+        if (merge) xcnt[b] = nx;
+    }
+}
+
 // One warp per PARENT: its four children share the candidate list (the children of the
 // parent's strong list), so each candidate's disc is loaded once and tested against the four
 // children; per child the ballots and slots are those of the box-per-warp formulation.
@@ -518,8 +580,15 @@ int build_lists(fmm2d_plan* P)
             FMM2D_CUDA_TRY(cudaMallocAsync((void**)&wtmp, sizeof(uint32_t) * std::max<int64_t>(cap, 1), st));
             FMM2D_CUDA_TRY(cudaMallocAsync((void**)&stmp, sizeof(uint32_t) * std::max<int64_t>(cap, 1), st));
             if (merge) FMM2D_CUDA_TRY(cudaMallocAsync((void**)&xtmp, sizeof(uint32_t) * std::max<int64_t>(cap / 4, 1), st));
-            k_lists<<<grid4, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w, cnt_s, wtmp, stmp, merge,
-                                          pcx, pcy, pr, cnt_x, xtmp); fmm2d::note_launch();
+            // per parent while the parents' strong lists are short (C5: ~11), per box when long
+            const int64_t npar = ((b1 + 3) >> 2) - (b0 >> 2);
+            if (PS.total <= 32 * std::max<int64_t>(npar, 1))
+                k_lists<<<grid4, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w, cnt_s, wtmp, stmp,
+                                              merge, pcx, pcy, pr, cnt_x, xtmp);
+            else
+                k_lists_box<<<grid, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w, cnt_s, wtmp, stmp,
+                                                  merge, pcx, pcy, pr, cnt_x, xtmp);
+            fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
             size_t sb = scan_bytes;
             FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, cnt_w, W.off, (int)(nb + 1), st));
