@@ -545,6 +545,8 @@ int build_lists(fmm2d_plan* P)
     FMM2D_CUDA_TRY(cudaMallocAsync(&scratch, scan_bytes, st));
     PhaseTrace tr(st);
     tr.mark("lists start");
+    uint32_t *wtmp = nullptr, *stmp = nullptr, *xtmp = nullptr;
+    int64_t tmp_cap = 0;
     auto body = [&]() -> int {
         const bool merge_on = (P->flags & FMM2D_PARENT_MERGE) != 0;
         for (int l = 1; l <= L; ++l) {
@@ -575,11 +577,19 @@ int build_lists(fmm2d_plan* P)
             const double* pr = P->r + P->base[l - 1];
             unsigned grid = grid_for((b1 - b0) * 32, 256);
             const unsigned grid4 = grid_for((((b1 + 3) >> 2) - (b0 >> 2)) * 32, 256);   // warp per parent
-            uint32_t *wtmp = nullptr, *stmp = nullptr, *xtmp = nullptr;
             const int64_t cap = 16 * PS.total;          // sum of the candidate counts of all boxes
-            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&wtmp, sizeof(uint32_t) * std::max<int64_t>(cap, 1), st));
-            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&stmp, sizeof(uint32_t) * std::max<int64_t>(cap, 1), st));
-            if (merge) FMM2D_CUDA_TRY(cudaMallocAsync((void**)&xtmp, sizeof(uint32_t) * std::max<int64_t>(cap / 4, 1), st));
+            // slot buffers kept across levels and grown geometrically (few, large pool
+            // allocations instead of three fresh ones per level)
+            if (cap > tmp_cap) {
+                if (wtmp) cudaFreeAsync(wtmp, st);
+                if (stmp) cudaFreeAsync(stmp, st);
+                if (xtmp) cudaFreeAsync(xtmp, st);
+                wtmp = stmp = xtmp = nullptr;
+                tmp_cap = std::max<int64_t>(cap, 2 * tmp_cap);
+                FMM2D_CUDA_TRY(cudaMallocAsync((void**)&wtmp, sizeof(uint32_t) * tmp_cap, st));
+                FMM2D_CUDA_TRY(cudaMallocAsync((void**)&stmp, sizeof(uint32_t) * tmp_cap, st));
+                FMM2D_CUDA_TRY(cudaMallocAsync((void**)&xtmp, sizeof(uint32_t) * (tmp_cap / 4 + 1), st));
+            }
             // per parent while the parents' strong lists are short (C5: ~11), per box when long
             const int64_t npar = ((b1 + 3) >> 2) - (b0 >> 2);
             if (PS.total <= 32 * std::max<int64_t>(npar, 1))
@@ -613,9 +623,7 @@ int build_lists(fmm2d_plan* P)
             k_compact_lists<<<grid, 256, 0, st>>>(b0, b1, PS.off, wtmp, stmp, xtmp, W.off, S.off, merge ? X.off : nullptr,
                                                   W.idx, S.idx, X.idx); fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
-            cudaFreeAsync(wtmp, st);
-            cudaFreeAsync(stmp, st);
-            if (xtmp) cudaFreeAsync(xtmp, st);
+
             P->stats.weak_pairs += W.total + X.total;
             tr.mark("lists level " + std::to_string(l));
         }
@@ -688,6 +696,9 @@ int build_lists(fmm2d_plan* P)
         return 0;
     };
     int rc = body();
+    if (wtmp) cudaFreeAsync(wtmp, st);
+    if (stmp) cudaFreeAsync(stmp, st);
+    if (xtmp) cudaFreeAsync(xtmp, st);
     cudaFreeAsync(cnt_w, st);
     cudaFreeAsync(cnt_s, st);
     cudaFreeAsync(cnt_x, st);
