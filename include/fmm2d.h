@@ -159,6 +159,13 @@ FMM2D_API int fmm2d_build_eval(const double* z, const double* m, int64_t n, cons
 FMM2D_API int fmm2d_eval_timed(fmm2d_plan* plan, const double* m, double* phi, double* dphi,
                                double* ms_out);
 
+/* Grow the stream-ordered memory pool of `device` (the default pool, from which every plan
+ * and every temporary buffer of this library is allocated, and which keeps freed memory) to
+ * hold at least `bytes`, once, outside any timed or latency-critical section: later builds
+ * then reuse memory instead of mapping fresh pages (hundreds of ms for tens of GB).  A
+ * serving setup step; optional.  Synchronous.  Errors: EINVAL, ENOMEM, ECUDA. */
+FMM2D_API int fmm2d_reserve(int device, size_t bytes);
+
 /* Number of kernels this library has launched since it was loaded (all plans and
  * threads; CUB's internal launches are not counted). */
 FMM2D_API int64_t fmm2d_launch_count(void);

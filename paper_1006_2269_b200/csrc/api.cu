@@ -525,6 +525,36 @@ int fmm2d_partition_info(int64_t n, const fmm2d_options* opt, int nranks, int ra
 
 int64_t fmm2d_launch_count(void) { return launch_count(); }
 
+int fmm2d_reserve(int device, size_t bytes)
+{
+    if (device < 0) return FMM2D_EINVAL;
+    FMM2D_CUDA_TRY(cudaSetDevice(device));
+    cudaMemPool_t pool;
+    FMM2D_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;                       // keep freed memory (as every build does)
+    FMM2D_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    uint64_t have = 0;
+    FMM2D_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have));
+    if (have >= bytes) return 0;
+    cudaStream_t st = nullptr;
+    FMM2D_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    void* p = nullptr;
+    const cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    if (e == cudaSuccess) cudaFreeAsync(p, st);
+    const cudaError_t e2 = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fmm2d_set_last_cuda_error(e, "cudaMallocAsync (reserve)", __FILE__, __LINE__);
+        return FMM2D_ENOMEM;
+    }
+    if (e2 != cudaSuccess) {
+        fmm2d_set_last_cuda_error(e2, "cudaStreamSynchronize (reserve)", __FILE__, __LINE__);
+        return FMM2D_ECUDA;
+    }
+    return 0;
+}
+
 int fmm2d_halo_info(const fmm2d_plan* P, int64_t* info)
 {
     if (!P || !info) return FMM2D_EINVAL;

@@ -42,7 +42,7 @@ EXPORT_PERM, EXPORT_OFFSETS, EXPORT_DISCS, EXPORT_STRONG, EXPORT_WEAK, EXPORT_MP
 SYMBOLS = ["fmm2d_default_options", "fmm2d_build", "fmm2d_eval", "fmm2d_eval_timed", "fmm2d_launch_count",
            "fmm2d_free", "fmm2d_strerror", "fmm2d_last_error_detail", "fmm2d_plan_info", "fmm2d_export",
            "fmm2d_nccl_unique_id", "fmm2d_partition_info", "fmm2d_build_shards", "fmm2d_eval_shards",
-           "fmm2d_halo_info", "fmm2d_build_eval"]
+           "fmm2d_halo_info", "fmm2d_build_eval", "fmm2d_reserve"]
 
 
 class Options(ctypes.Structure):
@@ -96,6 +96,7 @@ def lib():
         L.fmm2d_eval_shards.argtypes = [ctypes.POINTER(vp), ctypes.c_int, vp, vp, vp]
         L.fmm2d_halo_info.argtypes = [vp, ctypes.POINTER(ctypes.c_int64)]
         L.fmm2d_build_eval.argtypes = [vp, vp, ctypes.c_int64, ctypes.POINTER(Options), vp, vp, ctypes.POINTER(vp)]
+        L.fmm2d_reserve.argtypes = [ctypes.c_int, ctypes.c_size_t]
         _lib = L
     return _lib
 
@@ -160,6 +161,15 @@ def _ptr_of(a, host: bool):
         raise TypeError("device plans need CUDA tensors")
     arr = np.ascontiguousarray(a, dtype=np.complex128)
     return arr.ctypes.data, arr
+
+
+def reserve_pool(nbytes: int, device: int | None = None) -> None:
+    """fmm2d_reserve: grow the device's stream-ordered memory pool (which the library's plans
+    allocate from and keep) to at least nbytes, once, outside any timed section."""
+    import torch
+    if device is None:
+        device = torch.cuda.current_device()
+    _check(lib().fmm2d_reserve(int(device), int(nbytes)), "fmm2d_reserve")
 
 
 class Fmm2d:

@@ -1,0 +1,36 @@
+make -s all > /dev/null 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -p no:cacheprovider -k "eval_matches" 2>&1 | tail -1
+timeout 600 python - <<'PY'
+import sys, time, ctypes; sys.path.insert(0,'.')
+import torch, workloads as W
+from paper_1006_2269_b200 import Fmm2d
+c=W.CONFIGS["C5"]; z_np,m_np=W.make_config("C5")
+zh=torch.from_numpy(z_np).pin_memory(); mh=torch.from_numpy(m_np).pin_memory()
+NF=3
+outs=[(torch.empty(c.n,dtype=torch.complex128).pin_memory(), torch.empty(c.n,dtype=torch.complex128).pin_memory()) for _ in range(NF)]
+streams=[torch.cuda.current_stream()]+[torch.cuda.Stream() for _ in range(NF-1)]
+kw=dict(theta=c.theta,p=c.p,leaf_target=c.leaf_target,real_strengths=True)
+if len(sys.argv) > 0 and "grow" in sys.argv[-1:]:
+    pass
+p=Fmm2d.build_eval(zh,mh,outs[0][0],outs[0][1],**kw)[0]; p.close()     # sets the pool's release threshold
+rt=ctypes.CDLL("libcudart.so.12") if False else None
+import glob, os
+cands=glob.glob("/usr/local/cuda/lib64/libcudart.so*")
+rt=ctypes.CDLL(sorted(cands)[-1])
+ptr=ctypes.c_void_p()
+t0=time.perf_counter()
+e=rt.cudaMallocAsync(ctypes.byref(ptr), ctypes.c_size_t(100<<30), ctypes.c_void_p(0)); rt.cudaFreeAsync(ptr, ctypes.c_void_p(0)); rt.cudaDeviceSynchronize()
+print("pool pre-grow 100 GB: err %d, %.1f ms" % (e, (time.perf_counter()-t0)*1e3))
+T0=time.perf_counter()
+def t(): return (time.perf_counter()-T0)*1e3
+inflight=[]
+for k in range(12):
+    a=t()
+    plan=Fmm2d.build_eval(zh,mh,outs[k%NF][0],outs[k%NF][1],stream=streams[k%NF],async_host=True,**kw)[0]
+    b=t(); inflight.append(plan)
+    if len(inflight)>NF-1: inflight.pop(0).close()
+    d=t()
+    print("step %2d: build_eval %7.1f  close %6.1f   total %7.1f" % (k, b-a, d-b, d), flush=True)
+while inflight: inflight.pop(0).close()
+torch.cuda.synchronize(); print("end %.1f" % t())
+PY

@@ -286,6 +286,19 @@ def test_async_host_two_problems_in_flight():
         p_.close()
 
 
+def test_reserve_pool_then_build():
+    """fmm2d_reserve grows the memory pool once; builds afterwards work as before."""
+    import torch
+    from paper_1006_2269_b200 import Fmm2d, reserve_pool
+    reserve_pool(1 << 30)
+    reserve_pool(1 << 20)                               # already large enough: no-op
+    z, m = W.make_config("C2", n=20_000)
+    a = Fmm2d.build_eval(z, m, theta=0.5, p=17, nlevels=5)[1:]
+    b = _gpu_eval(_gpu_plan(z, 0.5, 17, 5), m)
+    np.testing.assert_array_equal(a[0].numpy(), b[0])
+    np.testing.assert_array_equal(a[1].numpy(), b[1])
+
+
 def test_eval_deterministic_and_reusable():
     z, m = W.make_config("C2", n=30_000)
     gp = _gpu_plan(z, 0.5, 17, 5)
