@@ -16,6 +16,7 @@
 // by z0^-l -- fused per pair in registers (no HBM staging: 2.25 flop/B would be
 // below the machine balance).  Every kernel is templated on p so the coefficient
 // vectors live in registers.
+#include <mutex>
 #include "fmm2d_internal.cuh"
 
 namespace fmm2d {
@@ -46,8 +47,10 @@ static uint64_t binom_u64(int a, int b)
 int upload_binomials(int p)
 {
     static bool uploaded[64] = {false};           // per device (__constant__ data is per device)
+    static std::mutex mu;
     int dev = 0;
     FMM2D_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
     if (dev >= 0 && dev < 64 && uploaded[dev]) return 0;
     (void)p;
     const int S = FMM2D_PMAX + 1;

@@ -18,6 +18,7 @@
 // result is stored at the input position perm[i].
 // Leaves larger than NEAR_CHUNK (only when nlevels forces a shallow tree) take
 // k_near_wide, which reads sources straight from global memory.
+#include <mutex>
 #include <cub/cub.cuh>
 
 #include "fastmath.cuh"
@@ -684,11 +685,13 @@ inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / b
 const fm::Tables* device_tables(int dev, int* rc)
 {
     static const fm::Tables* cache[64] = {nullptr};
+    static std::mutex mu;                            // plans may be built from several threads
     *rc = 0;
     if (dev < 0 || dev >= 64) {
         *rc = FMM2D_EINVAL;
         return nullptr;
     }
+    std::lock_guard<std::mutex> lk(mu);
     if (cache[dev]) return cache[dev];
     static fm::Tables h;
     fm::make_tables(&h);
