@@ -108,10 +108,13 @@ __global__ void k_lists_box(int64_t b0, int64_t b1, const double* __restrict__ c
     }
 }
 
+#ifndef FMM2D_LISTS_MINB
+#define FMM2D_LISTS_MINB 3            // 80 registers: 3 blocks of 256 per SM (measured best at C5)
+#endif
 // One warp per PARENT: its four children share the candidate list (the children of the
 // parent's strong list), so each candidate's disc is loaded once and tested against the four
 // children; per child the ballots and slots are those of the box-per-warp formulation.
-__global__ void k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, const double* __restrict__ cy,
+__global__ void __launch_bounds__(256, FMM2D_LISTS_MINB) k_lists(int64_t b0, int64_t b1, const double* __restrict__ cx, const double* __restrict__ cy,
                         const double* __restrict__ r, double theta, const int64_t* __restrict__ poff,
                         const uint32_t* __restrict__ pidx, int64_t* __restrict__ wcnt, int64_t* __restrict__ scnt,
                         uint32_t* __restrict__ wtmp, uint32_t* __restrict__ stmp, bool merge,
