@@ -532,6 +532,9 @@ __global__ void k_seg_prep(const uint32_t* __restrict__ par_off, const uint32_t*
 // 1: the tile's records are regrouped in shared memory (lows, then highs, each in order)
 // and written with consecutive threads on consecutive destinations; 0: each thread
 // writes its own records (8-record stride across a warp)
+#ifndef FMM2D_PART_MINB
+#define FMM2D_PART_MINB 5             // 48 registers, 5 tiles per SM (measured best at C5)
+#endif
 #ifndef FMM2D_PART_STAGED_OUT
 #define FMM2D_PART_STAGED_OUT 1
 #endif
@@ -560,7 +563,7 @@ struct SplitArgs {
 // MODE 0: one pass with the decoupled look-back; MODE 1: count pass (tile high counts);
 // MODE 2: scatter pass with the tiles' exclusive prefix (a CUB scan of the counts).
 template <int MODE>
-__global__ void __launch_bounds__(PT) k_partition(SplitArgs A)
+__global__ void __launch_bounds__(PT, FMM2D_PART_MINB) k_partition(SplitArgs A)
 {
     typedef cub::BlockScan<uint32_t, PT> Scan;
     __shared__ typename Scan::TempStorage scan_tmp;
