@@ -343,28 +343,49 @@ __global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l_long(M2LArgs A, c
 
 // ---------------------------------------------------------------- L2L (A8)
 template <int P>
+__host__ __device__ constexpr int l2l_block() { return (P + 2) * 16 * 128 <= 48 * 1024 ? 128 : 64; }   // children per block
+
+template <int P>
 __global__ void __launch_bounds__(128) k_l2l(int64_t c0, int64_t c1, const double* __restrict__ cxp,
                                              const double* __restrict__ cyp, const double* __restrict__ cxc,
                                              const double* __restrict__ cyc, const double2* __restrict__ lpar,
                                              double2* __restrict__ lch)
 {
-    int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= c1) return;
-    int64_t b = c >> 2;
-    const double2* B = lpar + b * (P + 1);
-    double2 d[P + 1];
-#pragma unroll
-    for (int k = 0; k <= P; ++k) d[k] = B[k];
-    const double2 h = make_double2(cxc[c] - cxp[b], cyc[c] - cyp[b]);
-    // Taylor shift: d_k = sum_{l>=k} b_l C(l,k) h^{l-k}
-#pragma unroll
-    for (int i = 0; i < P; ++i) {
-#pragma unroll
-        for (int j = P - 1; j >= i; --j) d[j] = cadd(d[j], cmul(h, d[j + 1]));
+    // the block's children's locals (contiguous) move through shared memory with coalesced
+    // 16-byte accesses; each thread's row is padded by one entry (bank spread)
+    constexpr int W = P + 2, NB = l2l_block<P>();
+    __shared__ double2 sl[NB * W];
+    const int64_t cb = c0 + (int64_t)blockIdx.x * NB;
+    const int nc = (int)min((int64_t)NB, c1 - cb);
+    double2* g = lch + cb * (P + 1);
+    for (int e = threadIdx.x; e < nc * (P + 1); e += NB) {
+        const int i = e / (P + 1), k = e - i * (P + 1);
+        sl[i * W + k] = g[e];
     }
-    double2* out = lch + c * (P + 1);
+    __syncthreads();
+    const int64_t c = cb + threadIdx.x;
+    if (threadIdx.x < nc) {
+        const int64_t b = c >> 2;
+        const double2* B = lpar + b * (P + 1);
+        double2 d[P + 1];
 #pragma unroll
-    for (int k = 0; k <= P; ++k) out[k] = cadd(out[k], d[k]);
+        for (int k = 0; k <= P; ++k) d[k] = B[k];
+        const double2 h = make_double2(cxc[c] - cxp[b], cyc[c] - cyp[b]);
+        // Taylor shift: d_k = sum_{l>=k} b_l C(l,k) h^{l-k}
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+#pragma unroll
+            for (int j = P - 1; j >= i; --j) d[j] = cadd(d[j], cmul(h, d[j + 1]));
+        }
+        double2* out = sl + threadIdx.x * W;
+#pragma unroll
+        for (int k = 0; k <= P; ++k) out[k] = cadd(out[k], d[k]);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nc * (P + 1); e += NB) {
+        const int i = e / (P + 1), k = e - i * (P + 1);
+        g[e] = sl[i * W + k];
+    }
 }
 
 inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
@@ -464,7 +485,7 @@ int downward_p(fmm2d_plan* Pl)
     cudaStream_t st = Pl->stream;
     for (int l = 2; l <= Pl->L; ++l) {
         const int64_t c0 = Pl->box_lo(l), c1 = Pl->box_hi(l);
-        k_l2l<P><<<grid_for(c1 - c0, 128), 128, 0, st>>>(
+        k_l2l<P><<<grid_for(c1 - c0, l2l_block<P>()), l2l_block<P>(), 0, st>>>(
             c0, c1, Pl->cx + Pl->base[l - 1], Pl->cy + Pl->base[l - 1], Pl->cx + Pl->base[l], Pl->cy + Pl->base[l],
             Pl->local + Pl->base[l - 1] * (P + 1), Pl->local + Pl->base[l] * (P + 1)); fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
