@@ -78,6 +78,10 @@ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 
+// children per block of k_m2m / k_l2l (their expansions staged in shared memory, <= 48 KB)
+template <int P>
+__host__ __device__ constexpr int l2l_block() { return (P + 2) * 16 * 128 <= 48 * 1024 ? 128 : 64; }
+
 // ---------------------------------------------------------------- P2M (A4)
 template <int P>
 __global__ void __launch_bounds__(128) k_p2m(int64_t b0, int64_t b1, const uint32_t* __restrict__ off,
@@ -114,35 +118,61 @@ __global__ void __launch_bounds__(128) k_m2m(int64_t b0, int64_t b1, const doubl
                                              const double* __restrict__ cyc, const double2* __restrict__ mc,
                                              double2* __restrict__ mpar)
 {
-    int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= b1) return;
-    double2 acc[P + 1];
+    // one thread per CHILD (32 parents per block): the children's multipoles in and the
+    // parents' out through shared memory with coalesced accesses; the four shifted children
+    // are added by the parent's lane in child order 0, 1, 2, 3 (the sequential order)
+    constexpr int W = P + 2, NB = l2l_block<P>();
+    __shared__ double2 sm[NB * W];
+    const int64_t cb = 4 * b0 + (int64_t)blockIdx.x * NB;               // first child of the block
+    const int nc = (int)min((int64_t)NB, 4 * b1 - cb);
+    const double2* g = mc + cb * (P + 1);
+    for (int e = threadIdx.x; e < nc * (P + 1); e += NB) {
+        const int i = e / (P + 1), k = e - i * (P + 1);
+        sm[i * W + k] = g[e];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, q = threadIdx.x & 3;
+    const int64_t c = cb + threadIdx.x, b = c >> 2;
+    const bool act = threadIdx.x < nc;
+    double2 t[P + 1];
 #pragma unroll
-    for (int k = 0; k <= P; ++k) acc[k] = make_double2(0.0, 0.0);
-    const double px = cxp[b], py = cyp[b];
-    for (int q = 0; q < 4; ++q) {
-        int64_t c = 4 * b + q;
-        const double2* A = mc + c * (P + 1);
-        double2 a[P + 1];
-#pragma unroll
-        for (int k = 0; k <= P; ++k) a[k] = A[k];
-        double2 z0 = make_double2(cxc[c] - px, cyc[c] - py);
-        acc[0] = cadd(acc[0], a[0]);
+    for (int k = 0; k <= P; ++k) t[k] = make_double2(0.0, 0.0);
+    if (act) {
+        const double2* a = sm + threadIdx.x * W;
+        const double2 z0 = make_double2(cxc[c] - cxp[b], cyc[c] - cyp[b]);
+        const double2 a0 = a[0];
+        t[0] = a0;
         double2 zl = make_double2(1.0, 0.0);
 #pragma unroll
         for (int l = 1; l <= P; ++l) {
             zl = cmul(zl, z0);                          // z0^l
             // Horner in z0: sum_{k=1..l} C(l-1,k-1) a_k z0^{l-k}
-            double2 t = cscale(a[1], c_pas[(l - 1) * S1 + 0]);
+            double2 u = cscale(a[1], c_pas[(l - 1) * S1 + 0]);
 #pragma unroll
-            for (int k = 2; k <= l; ++k) t = cadd(cmul(t, z0), cscale(a[k], c_pas[(l - 1) * S1 + (k - 1)]));
-            t = csub(t, cscale(cmul(a[0], zl), 1.0 / l));
-            acc[l] = cadd(acc[l], t);
+            for (int k = 2; k <= l; ++k) u = cadd(cmul(u, z0), cscale(a[k], c_pas[(l - 1) * S1 + (k - 1)]));
+            t[l] = csub(u, cscale(cmul(a0, zl), 1.0 / l));
         }
     }
-    double2* out = mpar + b * (P + 1);
+    __syncthreads();                                 // children consumed: sm reused for parents
+    const int base = lane & ~3;
 #pragma unroll
-    for (int k = 0; k <= P; ++k) out[k] = acc[k];
+    for (int k = 0; k <= P; ++k) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const double x = __shfl_sync(0xffffffffu, t[k].x, base + j);
+            const double y = __shfl_sync(0xffffffffu, t[k].y, base + j);
+            acc = cadd(acc, make_double2(x, y));
+        }
+        if (q == 0 && act) sm[(threadIdx.x >> 2) * W + k] = acc;
+    }
+    __syncthreads();
+    const int np = (nc + 3) >> 2;
+    double2* o = mpar + (cb >> 2) * (P + 1);
+    for (int e = threadIdx.x; e < np * (P + 1); e += NB) {
+        const int i = e / (P + 1), k = e - i * (P + 1);
+        o[e] = sm[i * W + k];
+    }
 }
 
 // ---------------------------------------------------------------- M2L (A6/A7)
@@ -343,9 +373,6 @@ __global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l_long(M2LArgs A, c
 
 // ---------------------------------------------------------------- L2L (A8)
 template <int P>
-__host__ __device__ constexpr int l2l_block() { return (P + 2) * 16 * 128 <= 48 * 1024 ? 128 : 64; }   // children per block
-
-template <int P>
 __global__ void __launch_bounds__(128) k_l2l(int64_t c0, int64_t c1, const double* __restrict__ cxp,
                                              const double* __restrict__ cyp, const double* __restrict__ cxc,
                                              const double* __restrict__ cyc, const double2* __restrict__ lpar,
@@ -404,7 +431,7 @@ int upward_p(fmm2d_plan* Pl)
     FMM2D_CUDA_TRY(cudaGetLastError());
     for (int l = L - 1; l >= Pl->kpart; --l) {
         const int64_t b0 = Pl->own_lo(l), b1 = Pl->own_hi(l);
-        k_m2m<P><<<grid_for(b1 - b0, 128), 128, 0, st>>>(
+        k_m2m<P><<<grid_for(4 * (b1 - b0), l2l_block<P>()), l2l_block<P>(), 0, st>>>(
             b0, b1, Pl->cx + Pl->base[l], Pl->cy + Pl->base[l], Pl->cx + Pl->base[l + 1], Pl->cy + Pl->base[l + 1],
             Pl->mpole + Pl->base[l + 1] * (P + 1), Pl->mpole + Pl->base[l] * (P + 1)); fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
@@ -420,7 +447,7 @@ int upward_top_p(fmm2d_plan* Pl)
     cudaStream_t st = Pl->stream;
     for (int l = Pl->kpart - 1; l >= 0; --l) {
         const int64_t nb = nboxes(l);
-        k_m2m<P><<<grid_for(nb, 128), 128, 0, st>>>(
+        k_m2m<P><<<grid_for(4 * nb, l2l_block<P>()), l2l_block<P>(), 0, st>>>(
             0, nb, Pl->cx + Pl->base[l], Pl->cy + Pl->base[l], Pl->cx + Pl->base[l + 1], Pl->cy + Pl->base[l + 1],
             Pl->mpole + Pl->base[l + 1] * (P + 1), Pl->mpole + Pl->base[l] * (P + 1)); fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
