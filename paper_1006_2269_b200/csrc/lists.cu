@@ -226,6 +226,39 @@ __global__ void k_compact_lists(int64_t b0, int64_t b1, const int64_t* __restric
         for (int64_t k = lane; k < xoff[b + 1] - xoff[b]; k += 32) xidx[xoff[b] + k] = xtmp[slot / 4 + k];
 }
 
+// pack the slots into the CSR lists: one warp per parent, its four children's slot regions
+// (contiguous, 4|S(parent)| entries each) into their (contiguous) CSR ranges; each list is
+// copied as one flat range over the four children
+__global__ void k_compact_lists4(int64_t b0, int64_t b1, const int64_t* __restrict__ poff,
+                                const uint32_t* __restrict__ wtmp, const uint32_t* __restrict__ stmp,
+                                const uint32_t* __restrict__ xtmp, const int64_t* __restrict__ woff,
+                                const int64_t* __restrict__ soff, const int64_t* __restrict__ xoff,
+                                uint32_t* __restrict__ widx, uint32_t* __restrict__ sidx, uint32_t* __restrict__ xidx)
+{
+    const int64_t par = (b0 >> 2) + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (4 * par >= b1) return;
+    const int64_t c0 = max(4 * par, b0), c1 = min(4 * par + 4, b1);    // own children
+    const int64_t reg = 4 * (poff[par + 1] - poff[par]);                 // slot region per child
+    const int64_t base = cand_slot(poff, c0);
+    auto copy = [&](const int64_t* __restrict__ off, const uint32_t* __restrict__ tmp, uint32_t* __restrict__ idx,
+                    int64_t rg, int64_t bs) {
+        const int64_t o0 = off[c0], tot = off[c1] - o0;
+        int64_t j = c0, jstart = 0, jend = off[c0 + 1] - o0;         // child of output entry k
+        for (int64_t k = lane; k < tot; k += 32) {
+            while (k >= jend) {
+                ++j;
+                jstart = jend;
+                jend = off[j + 1] - o0;
+            }
+            idx[o0 + k] = tmp[bs + (j - c0) * rg + (k - jstart)];
+        }
+    };
+    copy(woff, wtmp, widx, reg, base);
+    copy(soff, stmp, sidx, reg, base);
+    if (xoff) copy(xoff, xtmp, xidx, reg / 4, base / 4);
+}
+
 // M2L work order of one level: inside each window of M2L_WIN consecutive boxes (tree
 // order: neighbouring targets share source multipoles in cache), targets by descending
 // weak-list length (clamped to 255), so the 32 targets of a warp walk lists of nearly
@@ -623,8 +656,13 @@ int build_lists(fmm2d_plan* P)
             FMM2D_TRY(dev_alloc(P, (void**)&W.idx, sizeof(uint32_t) * std::max<int64_t>(W.total, 1)));
             FMM2D_TRY(dev_alloc(P, (void**)&S.idx, sizeof(uint32_t) * std::max<int64_t>(S.total, 1)));
             if (merge) FMM2D_TRY(dev_alloc(P, (void**)&X.idx, sizeof(uint32_t) * std::max<int64_t>(X.total, 1)));
-            k_compact_lists<<<grid, 256, 0, st>>>(b0, b1, PS.off, wtmp, stmp, xtmp, W.off, S.off, merge ? X.off : nullptr,
-                                                  W.idx, S.idx, X.idx); fmm2d::note_launch();
+            if (PS.total <= 16 * std::max<int64_t>(npar, 1))      // short lists: a warp per parent
+                k_compact_lists4<<<grid4, 256, 0, st>>>(b0, b1, PS.off, wtmp, stmp, xtmp, W.off, S.off,
+                                                        merge ? X.off : nullptr, W.idx, S.idx, X.idx);
+            else
+                k_compact_lists<<<grid, 256, 0, st>>>(b0, b1, PS.off, wtmp, stmp, xtmp, W.off, S.off,
+                                                      merge ? X.off : nullptr, W.idx, S.idx, X.idx);
+            fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
 
             P->stats.weak_pairs += W.total + X.total;
