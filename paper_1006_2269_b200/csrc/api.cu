@@ -395,8 +395,12 @@ static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi
         if (dphid) FMM2D_CUDA_TRY(cudaMemsetAsync(dphid, 0, sizeof(double2) * n, P0->stream));
     }
     if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[0], P0->stream));
+    // the own sources' strengths: gathered by P2M (which reads the same rows) unless the near
+    // field runs concurrently with the expansions (overlap mode needs the rows first)
+    const bool overlapped = np == 1 && P0->overlap && !ev;
     for (int i = 0; i < np; ++i) {
-        FMM2D_TRY(gather_strengths(Ps[i], md));
+        Ps[i]->m_fused = overlapped ? nullptr : md;
+        if (overlapped) FMM2D_TRY(gather_strengths(Ps[i], md));
         if (sharded) FMM2D_TRY(shard_gather_halo(Ps[i], md));
     }
     if (ev) FMM2D_CUDA_TRY(cudaEventRecord(ev[1], P0->stream));

@@ -84,9 +84,13 @@ __host__ __device__ constexpr int l2l_block() { return (P + 2) * 16 * 128 <= 48 
 
 // ---------------------------------------------------------------- P2M (A4)
 template <int P>
+// m != nullptr: the strengths are gathered here (m[perm[j]], input order) and written into
+// the rows' (z, w) halves for the near field -- the rows' sectors are in cache from the
+// coordinate read, so the 16-byte writes merge there
 __global__ void __launch_bounds__(128) k_p2m(int64_t b0, int64_t b1, const uint32_t* __restrict__ off,
-                                             const double4* __restrict__ src, const double* __restrict__ cx,
-                                             const double* __restrict__ cy, double2* __restrict__ mp)
+                                             double4* __restrict__ src, const double* __restrict__ cx,
+                                             const double* __restrict__ cy, double2* __restrict__ mp,
+                                             const double2* __restrict__ mg, const uint32_t* __restrict__ perm)
 {
     int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= b1) return;
@@ -98,6 +102,10 @@ __global__ void __launch_bounds__(128) k_p2m(int64_t b0, int64_t b1, const uint3
         double4 s = src[j];
         double2 w = make_double2(s.x - c0, s.y - c1);
         double2 m = make_double2(s.z, s.w);
+        if (mg) {
+            m = mg[perm[j]];
+            reinterpret_cast<double2*>(src + j)[1] = m;
+        }
         a[0] = cadd(a[0], m);
         double2 wk = m;                                 // m w^k, k = 1..P
 #pragma unroll
@@ -426,7 +434,9 @@ int upward_p(fmm2d_plan* Pl)
     const int L = Pl->L;
     const int64_t l0 = Pl->box_lo(L), l1 = Pl->box_hi(L);
     k_p2m<P><<<grid_for(l1 - l0, 128), 128, 0, st>>>(l0, l1, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
-                                                    Pl->cy + Pl->base[L], Pl->mpole + Pl->base[L] * (P + 1));
+                                                    Pl->cy + Pl->base[L], Pl->mpole + Pl->base[L] * (P + 1),
+                                                    Pl->m_fused, Pl->perm);
+    Pl->m_fused = nullptr;
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     for (int l = L - 1; l >= Pl->kpart; --l) {

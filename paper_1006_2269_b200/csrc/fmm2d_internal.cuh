@@ -108,6 +108,9 @@ struct fmm2d_plan {
     double2* local = nullptr;           // [nbox_total][p+1]
     // staging for FMM2D_HOST_PTRS
     double2* mstage = nullptr;
+    // strengths (input order) whose gather into the source rows is left to P2M, which reads
+    // those rows anyway (set by eval_impl for one evaluation; nullptr: rows already hold m)
+    const double2* m_fused = nullptr;
     double2* phistage = nullptr;
     double2* dphistage = nullptr;
     const void* tables = nullptr;       // fastmath tables (device, shared per device)
