@@ -11,14 +11,15 @@
  * splits, theta-criterion connectivity (Criterion 1, P:115-123;
  * rule P:343-353), upward P2M/M2M, M2L along the weak lists, downward L2L,
  * and L2P + direct P2P along the strong leaf lists.  Readings of
- * points the paper leaves open are DESIGN.md section 2 (R1..R22).
+ * points the paper leaves open are DESIGN.md section 2 (R1..R26).
  *
  * Conventions for every entry point:
  *   - Complex arrays are interleaved float64 pairs (re, im), length 2*n doubles,
  *     in INPUT order (index j of z, m, phi, dphi refers to the same source).
  *   - Pointers are CUDA device pointers on opt.stream unless FMM2D_HOST_PTRS is set
  *     in opt.flags, in which case they are host pointers (pinned memory gives the
- *     fastest copies) and the call returns after the results are in host memory.
+ *     fastest copies) and the call returns after the results are in host memory
+ *     (with FMM2D_ASYNC_HOST: once their copies are enqueued on opt.stream).
  *   - Return 0 on success, a negative FMM2D_E* code on error; nothing aborts or
  *     exits.  On error the outputs are unspecified and an existing plan is unchanged.
  *   - There is no CPU fallback: every numeric step runs in the library's CUDA kernels.
