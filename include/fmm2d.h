@@ -160,12 +160,18 @@ FMM2D_API int fmm2d_build_eval(const double* z, const double* m, int64_t n, cons
 FMM2D_API int fmm2d_eval_timed(fmm2d_plan* plan, const double* m, double* phi, double* dphi,
                                double* ms_out);
 
-/* Grow the stream-ordered memory pool of `device` (the default pool, from which every plan
- * and every temporary buffer of this library is allocated, and which keeps freed memory) to
- * hold at least `bytes`, once, outside any timed or latency-critical section: later builds
- * then reuse memory instead of mapping fresh pages (hundreds of ms for tens of GB).  A
- * serving setup step; optional.  Synchronous.  Errors: EINVAL, ENOMEM, ECUDA. */
+/* Grow the library's stream-ordered memory pool on `device` to hold at least `bytes`, once,
+ * outside any timed or latency-critical section.  Every plan and every temporary buffer of
+ * this library is allocated from this pool: one per device, owned by the library (never the
+ * device's default pool, whose attributes are left alone), created on first use, and it keeps
+ * freed memory, so later builds reuse it instead of mapping fresh pages (hundreds of ms for
+ * tens of GB).  A serving setup step; optional.  Synchronous.  Errors: EINVAL, ENOMEM, ECUDA. */
 FMM2D_API int fmm2d_reserve(int device, size_t bytes);
+
+/* Give the memory the library's pool on `device` holds but no live plan uses back to the
+ * device, down to keep_bytes (cudaMemPoolTrimTo), e.g. before handing the GPU to another
+ * allocator.  Synchronises the device first.  Errors: EINVAL, ECUDA. */
+FMM2D_API int fmm2d_pool_trim(int device, size_t keep_bytes);
 
 /* Number of kernels this library has launched since it was loaded (all plans and
  * threads; CUB's internal launches are not counted). */

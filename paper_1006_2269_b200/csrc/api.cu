@@ -30,11 +30,45 @@ static std::atomic<int64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+cudaMemPool_t lib_pool(int device)
+{
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {nullptr};
+    if (device < 0 || device >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[device]) {
+        cudaMemPoolProps props;
+        memset(&props, 0, sizeof(props));
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+        // keep freed memory for the next build / evaluation (no page mapping in a timed path);
+        // fmm2d_pool_trim gives it back
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        pools[device] = pool;
+    }
+    return pools[device];
+}
+
+cudaError_t pool_malloc(void** ptr, size_t bytes, cudaStream_t st)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    cudaMemPool_t pool = lib_pool(dev);
+    if (!pool) return cudaErrorMemoryAllocation;
+    return cudaMallocFromPoolAsync(ptr, bytes ? bytes : 16, pool, st);
+}
+
 int dev_alloc(fmm2d_plan* P, void** ptr, size_t bytes)
 {
     *ptr = nullptr;
     if (bytes == 0) bytes = 16;
-    cudaError_t e = cudaMallocAsync(ptr, bytes, P->stream);
+    cudaError_t e = fmm2d::pool_malloc((void**)ptr, bytes, P->stream);
     if (e != cudaSuccess) {
         fmm2d_set_last_cuda_error(e, "cudaMallocAsync", __FILE__, __LINE__);
         *ptr = nullptr;
@@ -163,14 +197,6 @@ static int build_stage_tree(const double* z, int64_t n, const fmm2d_options* opt
         FMM2D_CUDA_TRY(cudaEventCreate(&e1));
         FMM2D_CUDA_TRY(cudaEventCreate(&e2));
         FMM2D_CUDA_TRY(cudaEventRecord(e0, P->stream));
-        // keep freed pool memory for the next build/eval (no OS round trips)
-        {
-            cudaMemPool_t pool;
-            if (cudaDeviceGetDefaultMemPool(&pool, P->device) == cudaSuccess) {
-                uint64_t thr = UINT64_MAX;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-            }
-        }
         FMM2D_TRY(upload_binomials(P->p));
         FMM2D_TRY(prepare_near(P));
         const int64_t nb = P->nbox_total;
@@ -185,7 +211,7 @@ static int build_stage_tree(const double* z, int64_t n, const fmm2d_options* opt
         const double2* zd = (const double2*)z;
         double2* zstage = nullptr;
         if (P->flags & FMM2D_HOST_PTRS) {
-            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&zstage, sizeof(double2) * n, P->stream));
+            FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&zstage, sizeof(double2) * n, P->stream));
             FMM2D_CUDA_TRY(cudaMemcpyAsync(zstage, z, sizeof(double2) * n, cudaMemcpyHostToDevice, P->stream));
             zd = zstage;
         }
@@ -301,8 +327,8 @@ int fmm2d_build_eval(const double* z, const double* m, int64_t n, const fmm2d_op
         }
         FMM2D_CUDA_TRY(cudaEventCreateWithFlags(&ev_z, cudaEventDisableTiming));
         FMM2D_CUDA_TRY(cudaEventCreateWithFlags(&ev_m, cudaEventDisableTiming));
-        FMM2D_CUDA_TRY(cudaMallocAsync((void**)&dz, sizeof(double2) * n, bst));
-        FMM2D_CUDA_TRY(cudaMallocAsync((void**)&dm, sizeof(double2) * n, bst));
+        FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&dz, sizeof(double2) * n, bst));
+        FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&dm, sizeof(double2) * n, bst));
         // positions first (the build needs them), then the strengths behind them
         FMM2D_CUDA_TRY(cudaMemcpyAsync(dz, z, sizeof(double2) * n, cudaMemcpyHostToDevice, bst));
         FMM2D_CUDA_TRY(cudaEventRecord(ev_z, bst));
@@ -533,17 +559,15 @@ int fmm2d_reserve(int device, size_t bytes)
 {
     if (device < 0) return FMM2D_EINVAL;
     FMM2D_CUDA_TRY(cudaSetDevice(device));
-    cudaMemPool_t pool;
-    FMM2D_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
-    uint64_t thr = UINT64_MAX;                       // keep freed memory (as every build does)
-    FMM2D_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    cudaMemPool_t pool = lib_pool(device);           // keeps freed memory (the library's own pool)
+    if (!pool) return FMM2D_ECUDA;
     uint64_t have = 0;
     FMM2D_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have));
     if (have >= bytes) return 0;
     cudaStream_t st = nullptr;
     FMM2D_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     void* p = nullptr;
-    const cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    const cudaError_t e = fmm2d::pool_malloc((void**)&p, bytes, st);
     if (e == cudaSuccess) cudaFreeAsync(p, st);
     const cudaError_t e2 = cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
@@ -556,6 +580,17 @@ int fmm2d_reserve(int device, size_t bytes)
         fmm2d_set_last_cuda_error(e2, "cudaStreamSynchronize (reserve)", __FILE__, __LINE__);
         return FMM2D_ECUDA;
     }
+    return 0;
+}
+
+int fmm2d_pool_trim(int device, size_t keep_bytes)
+{
+    if (device < 0) return FMM2D_EINVAL;
+    FMM2D_CUDA_TRY(cudaSetDevice(device));
+    cudaMemPool_t pool = lib_pool(device);
+    if (!pool) return FMM2D_ECUDA;
+    FMM2D_CUDA_TRY(cudaDeviceSynchronize());        // frees enqueued on any stream have completed
+    FMM2D_CUDA_TRY(cudaMemPoolTrimTo(pool, keep_bytes));
     return 0;
 }
 

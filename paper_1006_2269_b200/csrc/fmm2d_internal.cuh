@@ -136,6 +136,11 @@ struct fmm2d_plan {
 namespace fmm2d {
 
 int dev_alloc(fmm2d_plan* P, void** ptr, size_t bytes);
+// Every device allocation of the library comes from ONE library-owned stream-ordered pool per
+// device (created on first use, release threshold = keep everything), never from the device's
+// default pool, whose attributes the library leaves alone (fmm2d_release_pool trims it).
+cudaMemPool_t lib_pool(int device);
+cudaError_t pool_malloc(void** ptr, size_t bytes, cudaStream_t st);
 
 // build steps (tree.cu, lists.cu)
 int build_tree(fmm2d_plan* P, const double2* z_dev);

@@ -445,8 +445,8 @@ static int build_rr_lists(fmm2d_plan* P)
     void* scratch = nullptr;
     size_t sb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, sb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(nl + 1), st);
-    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt, sizeof(int64_t) * 3 * (nl + 1), st));
-    FMM2D_CUDA_TRY(cudaMallocAsync(&scratch, sb, st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&cnt, sizeof(int64_t) * 3 * (nl + 1), st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&scratch, sb, st));
     auto body = [&]() -> int {
         FMM2D_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * 3 * (nl + 1), st));
         const unsigned grid = grid_for((t1 - t0) * 32, 256);
@@ -504,8 +504,8 @@ static int build_near_segments(fmm2d_plan* P)
     void* scratch = nullptr;
     size_t sb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, sb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(nl + 1), st);
-    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt, sizeof(int64_t) * (nl + 1), st));
-    FMM2D_CUDA_TRY(cudaMallocAsync(&scratch, sb, st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&cnt, sizeof(int64_t) * (nl + 1), st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&scratch, sb, st));
     auto body = [&]() -> int {
         FMM2D_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (nl + 1), st));
         k_near_segs<false><<<grid_for((t1 - t0) * 32, 256), 256, 0, st>>>(t0, t1, P->near.off, P->near.idx, boff,
@@ -575,10 +575,10 @@ int build_lists(fmm2d_plan* P)
     void* scratch = nullptr;
     size_t scan_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)(nbmax + 1), st);
-    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt_w, sizeof(int64_t) * (nbmax + 1), st));
-    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt_s, sizeof(int64_t) * (nbmax + 1), st));
-    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt_x, sizeof(int64_t) * (nbmax + 1), st));
-    FMM2D_CUDA_TRY(cudaMallocAsync(&scratch, scan_bytes, st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&cnt_w, sizeof(int64_t) * (nbmax + 1), st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&cnt_s, sizeof(int64_t) * (nbmax + 1), st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&cnt_x, sizeof(int64_t) * (nbmax + 1), st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&scratch, scan_bytes, st));
     PhaseTrace tr(st);
     tr.mark("lists start");
     uint32_t *wtmp = nullptr, *stmp = nullptr, *xtmp = nullptr;
@@ -622,9 +622,9 @@ int build_lists(fmm2d_plan* P)
                 if (xtmp) cudaFreeAsync(xtmp, st);
                 wtmp = stmp = xtmp = nullptr;
                 tmp_cap = std::max<int64_t>(cap, 2 * tmp_cap);
-                FMM2D_CUDA_TRY(cudaMallocAsync((void**)&wtmp, sizeof(uint32_t) * tmp_cap, st));
-                FMM2D_CUDA_TRY(cudaMallocAsync((void**)&stmp, sizeof(uint32_t) * tmp_cap, st));
-                FMM2D_CUDA_TRY(cudaMallocAsync((void**)&xtmp, sizeof(uint32_t) * (tmp_cap / 4 + 1), st));
+                FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&wtmp, sizeof(uint32_t) * tmp_cap, st));
+                FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&stmp, sizeof(uint32_t) * tmp_cap, st));
+                FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&xtmp, sizeof(uint32_t) * (tmp_cap / 4 + 1), st));
             }
             // per parent while the parents' strong lists are short (C5: ~11), per box when long
             const int64_t npar = ((b1 + 3) >> 2) - (b0 >> 2);
@@ -679,10 +679,10 @@ int build_lists(fmm2d_plan* P)
             size_t sb = 0;
             cub::DeviceRadixSort::SortPairs(nullptr, sb, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                             (uint32_t*)nullptr, (int)nbmax, 0, 32, st);
-            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&k0, sizeof(uint32_t) * nbmax, st));
-            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&k1, sizeof(uint32_t) * nbmax, st));
-            FMM2D_CUDA_TRY(cudaMallocAsync((void**)&v0, sizeof(uint32_t) * std::max<int64_t>(tot, nbmax), st));
-            FMM2D_CUDA_TRY(cudaMallocAsync(&sc, std::max<size_t>(sb, 16), st));
+            FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&k0, sizeof(uint32_t) * nbmax, st));
+            FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&k1, sizeof(uint32_t) * nbmax, st));
+            FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&v0, sizeof(uint32_t) * std::max<int64_t>(tot, nbmax), st));
+            FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&sc, std::max<size_t>(sb, 16), st));
             int64_t o = 0;
             for (int l = 1; l <= L; ++l) {
                 const int64_t b0 = P->box_lo(l), b1 = P->box_hi(l), nb = b1 - b0;

@@ -767,8 +767,8 @@ int prepare_near_sym(fmm2d_plan* P)
     void* scratch = nullptr;
     size_t sb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, sb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(nl + 1), st);
-    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&cnt, sizeof(int64_t) * (nl + 1), st));
-    FMM2D_CUDA_TRY(cudaMallocAsync(&scratch, sb, st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&cnt, sizeof(int64_t) * (nl + 1), st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&scratch, sb, st));
     k_to_i64<<<grid_for(nl + 1, 256), 256, 0, st>>>(P->sym_selfpos, nl, cnt);
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scratch, sb, cnt, P->sym_lower, (int)(nl + 1), st));

@@ -372,9 +372,9 @@ static int compact_requests(fmm2d_plan* P, const uint8_t* need, int64_t nitems, 
     cub::CountingInputIterator<uint32_t> it(0);
     OwnerIs pred{need, 1};
     cub::DeviceSelect::If(nullptr, sb, it, (uint32_t*)nullptr, (int64_t*)nullptr, (int64_t)nitems, pred, st);
-    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&tmp, sizeof(uint32_t) * std::max<int64_t>(nitems, 1), st));
-    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&d_num, sizeof(int64_t) * R, st));
-    FMM2D_CUDA_TRY(cudaMallocAsync(&scratch, std::max<size_t>(sb, 16), st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&tmp, sizeof(uint32_t) * std::max<int64_t>(nitems, 1), st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&d_num, sizeof(int64_t) * R, st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&scratch, std::max<size_t>(sb, 16), st));
     int64_t tot = 0;
     std::vector<int64_t> h(R, 0);
     auto body = [&]() -> int {
@@ -410,7 +410,7 @@ static int halo_requests(fmm2d_plan* P)
     Shard* S = P->shard;
     const int64_t nl = nboxes(L);
     uint8_t* need = nullptr;
-    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&need, std::max<int64_t>(P->nbox_total, nl), st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&need, std::max<int64_t>(P->nbox_total, nl), st));
     auto body = [&]() -> int {
         // leaves of the own strong lists (level L)
         FMM2D_CUDA_TRY(cudaMemsetAsync(need, 0, nl, st));

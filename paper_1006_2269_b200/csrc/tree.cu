@@ -1228,7 +1228,7 @@ static int top_levels_sharded(fmm2d_plan* P, const double2* zc, const Bounds& hb
     void* scratch = nullptr;
     std::vector<void*> tmp;
     auto talloc = [&](void** p, size_t b) -> int {
-        if (cudaMallocAsync(p, b ? b : 16, st) != cudaSuccess) return FMM2D_ENOMEM;
+        if (fmm2d::pool_malloc((void**)p, b ? b : 16, st) != cudaSuccess) return FMM2D_ENOMEM;
         tmp.push_back(*p);
         return 0;
     };
@@ -1500,7 +1500,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
     const size_t cub_bytes = std::max(std::max(s32, s64), std::max(sd, scan_bytes));
     std::vector<void*> tmp_ptrs;
     auto talloc = [&](void** p, size_t b) -> int {
-        cudaError_t e = cudaMallocAsync(p, b ? b : 16, st);
+        cudaError_t e = fmm2d::pool_malloc((void**)p, b ? b : 16, st);
         if (e != cudaSuccess) return FMM2D_ENOMEM;
         tmp_ptrs.push_back(*p);
         return 0;
@@ -1583,7 +1583,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
             if (force64 || h_ovf[0]) {
                 // heavy ties in x: full 64-bit orderable keys (ties leave in idx order)
                 if (!k64buf) {
-                    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&k64buf, 16 * m, st));
+                    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&k64buf, 16 * m, st));
                     k64a = k64buf;
                     k64b = k64buf + m;
                 }
@@ -1606,7 +1606,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
             if (force64 || h_ovf[1]) {
                 // heavy ties in y: 64-bit keys over the input in idx order
                 if (!k64buf) {
-                    FMM2D_CUDA_TRY(cudaMallocAsync((void**)&k64buf, 16 * m, st));
+                    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&k64buf, 16 * m, st));
                     k64a = k64buf;
                     k64b = k64buf + m;
                 }
@@ -1804,7 +1804,7 @@ static int build_tree_midpoint(fmm2d_plan* P, const double2* z)
                                     (uint32_t*)nullptr, (int)n, 0, std::max(1, 2 * L), st);
     std::vector<void*> tmp;
     auto talloc = [&](void** p, size_t b) -> int {
-        if (cudaMallocAsync(p, b ? b : 16, st) != cudaSuccess) return FMM2D_ENOMEM;
+        if (fmm2d::pool_malloc((void**)p, b ? b : 16, st) != cudaSuccess) return FMM2D_ENOMEM;
         tmp.push_back(*p);
         return 0;
     };

@@ -42,7 +42,7 @@ EXPORT_PERM, EXPORT_OFFSETS, EXPORT_DISCS, EXPORT_STRONG, EXPORT_WEAK, EXPORT_MP
 SYMBOLS = ["fmm2d_default_options", "fmm2d_build", "fmm2d_eval", "fmm2d_eval_timed", "fmm2d_launch_count",
            "fmm2d_free", "fmm2d_strerror", "fmm2d_last_error_detail", "fmm2d_plan_info", "fmm2d_export",
            "fmm2d_nccl_unique_id", "fmm2d_partition_info", "fmm2d_build_shards", "fmm2d_eval_shards",
-           "fmm2d_halo_info", "fmm2d_build_eval", "fmm2d_reserve"]
+           "fmm2d_halo_info", "fmm2d_build_eval", "fmm2d_reserve", "fmm2d_pool_trim"]
 
 
 class Options(ctypes.Structure):
@@ -97,6 +97,7 @@ def lib():
         L.fmm2d_halo_info.argtypes = [vp, ctypes.POINTER(ctypes.c_int64)]
         L.fmm2d_build_eval.argtypes = [vp, vp, ctypes.c_int64, ctypes.POINTER(Options), vp, vp, ctypes.POINTER(vp)]
         L.fmm2d_reserve.argtypes = [ctypes.c_int, ctypes.c_size_t]
+        L.fmm2d_pool_trim.argtypes = [ctypes.c_int, ctypes.c_size_t]
         _lib = L
     return _lib
 
@@ -145,8 +146,11 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def _ptr_of(a, host: bool):
-    """(pointer, keepalive) of a complex128 array: torch tensor (cuda or pinned cpu) or numpy."""
+def _ptr_of(a, host: bool, out: bool = False):
+    """(pointer, keepalive) of a complex128 array: torch tensor (cuda or pinned cpu) or numpy.
+    The caller keeps the keepalive bound until the C call (and, for asynchronous host plans,
+    the stream) is done with the pointer.  Outputs (out=True) must already be contiguous
+    complex128: a converted temporary would receive the results instead of the caller's array."""
     try:
         import torch
         if isinstance(a, torch.Tensor):
@@ -160,6 +164,8 @@ def _ptr_of(a, host: bool):
     if not host:
         raise TypeError("device plans need CUDA tensors")
     arr = np.ascontiguousarray(a, dtype=np.complex128)
+    if out and not (isinstance(a, np.ndarray) and np.shares_memory(arr, a)):
+        raise TypeError("outputs must be contiguous complex128 arrays (no conversion copy)")
     return arr.ctypes.data, arr
 
 
@@ -170,6 +176,14 @@ def reserve_pool(nbytes: int, device: int | None = None) -> None:
     if device is None:
         device = torch.cuda.current_device()
     _check(lib().fmm2d_reserve(int(device), int(nbytes)), "fmm2d_reserve")
+
+
+def pool_trim(keep_bytes: int = 0, device: int | None = None) -> None:
+    """fmm2d_pool_trim: return the library pool's unused memory to the device."""
+    import torch
+    if device is None:
+        device = torch.cuda.current_device()
+    _check(lib().fmm2d_pool_trim(int(device), int(keep_bytes)), "fmm2d_pool_trim")
 
 
 class Fmm2d:
@@ -219,6 +233,7 @@ class Fmm2d:
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
             opt.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
         self.nranks, self.rank = int(nranks), int(rank)
+        self.async_host = bool(async_host)
         self._opt = opt
         zp, keep = _ptr_of(z, host)
         self.n = int(keep.shape[0])
@@ -226,9 +241,11 @@ class Fmm2d:
         if _first is None:
             _check(L.fmm2d_build(ctypes.c_void_p(zp), self.n, ctypes.byref(opt), ctypes.byref(h)), "fmm2d_build")
         else:                                   # (m, phi, dphi): fmm2d_build_eval
-            mp = _ptr_of(_first[0], host)[0]
-            pp = _ptr_of(_first[1], host)[0] if _first[1] is not None else None
-            dp = _ptr_of(_first[2], host)[0] if _first[2] is not None else None
+            mp, mkeep = _ptr_of(_first[0], host)
+            pp, pkeep = _ptr_of(_first[1], host, out=True) if _first[1] is not None else (None, None)
+            dp, dkeep = _ptr_of(_first[2], host, out=True) if _first[2] is not None else (None, None)
+            if host and (opt.flags & ASYNC_HOST):
+                self._inflight = (keep, mkeep, pkeep, dkeep)   # read by the streams after the call returns
             _check(L.fmm2d_build_eval(ctypes.c_void_p(zp), ctypes.c_void_p(mp), self.n, ctypes.byref(opt),
                                       ctypes.c_void_p(pp), ctypes.c_void_p(dp), ctypes.byref(h)),
                    "fmm2d_build_eval")
@@ -268,7 +285,10 @@ class Fmm2d:
     # -- evaluation -------------------------------------------------------
     def eval(self, m, phi=None, dphi=None, want_phi: bool = True, want_dphi: bool = True):
         """Phi(z_i), Phi'(z_i) in input order.  Device plans: complex128 CUDA tensors,
-        asynchronous on the plan's stream.  Host plans: numpy/pinned arrays, synchronous."""
+        asynchronous on the plan's stream.  Host plans: numpy/pinned arrays, synchronous --
+        except with async_host=True (FMM2D_ASYNC_HOST, a property of the plan, also when it
+        came from build_eval), where the call returns once the copies are enqueued and the
+        results are valid after ``plan.stream.synchronize()``."""
         import torch
         if self._h is None:
             raise RuntimeError("plan freed")
@@ -284,20 +304,23 @@ class Fmm2d:
                 phi = torch.empty(self.n, dtype=torch.complex128, device=dev)
             if want_dphi and dphi is None:
                 dphi = torch.empty(self.n, dtype=torch.complex128, device=dev)
-        pp = _ptr_of(phi, self.host)[0] if phi is not None else None
-        dp = _ptr_of(dphi, self.host)[0] if dphi is not None else None
+        pp, pkeep = _ptr_of(phi, self.host, out=True) if phi is not None else (None, None)
+        dp, dkeep = _ptr_of(dphi, self.host, out=True) if dphi is not None else (None, None)
         _check(lib().fmm2d_eval(self._h, ctypes.c_void_p(mp), ctypes.c_void_p(pp), ctypes.c_void_p(dp)),
                "fmm2d_eval")
+        if self.host and self.async_host:
+            self._inflight = (mkeep, pkeep, dkeep)     # the stream still reads / writes them
         return phi, dphi
 
     def eval_timed(self, m, phi, dphi) -> dict:
         """eval into preallocated outputs, synchronise, return per-phase device ms."""
         t = (ctypes.c_double * 8)()
-        mp = _ptr_of(m, self.host)[0]
-        pp = _ptr_of(phi, self.host)[0] if phi is not None else None
-        dp = _ptr_of(dphi, self.host)[0] if dphi is not None else None
+        mp, mkeep = _ptr_of(m, self.host)
+        pp, pkeep = _ptr_of(phi, self.host, out=True) if phi is not None else (None, None)
+        dp, dkeep = _ptr_of(dphi, self.host, out=True) if dphi is not None else (None, None)
         _check(lib().fmm2d_eval_timed(self._h, ctypes.c_void_p(mp), ctypes.c_void_p(pp), ctypes.c_void_p(dp), t),
                "fmm2d_eval_timed")
+        del mkeep, pkeep, dkeep
         return {"gather_ms": t[0], "upward_ms": t[1], "m2l_ms": t[2], "downward_ms": t[3], "near_ms": t[4],
                 "eval_ms": t[5]}
 

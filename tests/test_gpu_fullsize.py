@@ -1,20 +1,26 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
 
-Full-size outputs cannot all be recomputed by the oracle, so:
-  - C3 (1e6, clusters) and C4 (1e7, curve): tree, discs and lists bit-exact against the
-    oracle's tree/list builder (cheap at these sizes), plus sampled outputs against the
-    oracle's long-double direct sum;
-  - C5 (1e8, the metric's workload): sampled outputs against the direct sum, and
-    properties that hold at any size (perm is a bijection, leaf sizes floor/ceil(N/4^L),
-    finite outputs).
+  - C5 recipe at N = 1e7: the whole problem against the oracle -- tree, discs and lists of
+    every level bit-exact, Phi and Phi' over all N within 1e-12 normwise and pointwise
+    (floor 1e-3 max|ref|, tests/fullparity.py);
+  - C5 (1e8, the metric's workload): the same whole-problem comparison (all 12 levels, all
+    1e8 outputs; ~10 min of oracle time on the GPU box's cores) when FMM2D_FULL_C5=1 -- its
+    log is committed under profiles/ (tools/full_parity.py); always: sampled outputs against
+    the direct sum and properties that hold at any size (perm is a bijection, leaf sizes
+    floor/ceil(N/4^L), finite outputs);
+  - C3 (1e6, clusters) and C4 (1e7, curve): tree, discs and lists of every level bit-exact
+    against the oracle, plus sampled outputs against the oracle's long-double direct sum.
 The direct-sum gate is BJ's: Re Phi (real m) within 1e-6 normwise and Phi' within the
 paper's a-priori law theta^{p+1}/(1-theta)^2 over the sampled targets.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
 
 import workloads as W
+from fullparity import compare
 
 pytestmark = pytest.mark.gpu
 
@@ -73,7 +79,7 @@ def test_c4_full_structure_and_sampled(orc):
     c, z, m, plan, phi, dphi = _run("C4")
     assert plan.L == 9
     op = orc.plan(z, c.theta, plan.L)
-    _structure_equal(plan, op, plan.L, [0, 3, 6, plan.L])
+    _structure_equal(plan, op, plan.L, range(plan.L + 1))
     _sampled_direct(orc, z, m, phi, dphi, c.theta, c.p, M=32, seed=401)
 
 
@@ -87,3 +93,34 @@ def test_c5_full_sampled_and_properties(orc):
     assert sizes.min() == n // 4 ** plan.L and sizes.max() == -(-n // 4 ** plan.L)
     assert torch.isfinite(torch.view_as_real(phi)).all() and torch.isfinite(torch.view_as_real(dphi)).all()
     _sampled_direct(orc, z, m, phi, dphi, c.theta, c.p, M=16, seed=501)
+
+
+TOL = 1e-12
+
+
+def _assert_whole(r):
+    assert r["levels_compared"] == list(range(r["L"] + 1))
+    for k in ("phi", "dphi"):
+        assert r[k]["norm"] <= TOL, (k, r[k])
+        assert r[k]["point"] <= TOL, (k, r[k])
+
+
+def test_c5_recipe_1e7_whole_problem_vs_oracle(orc):
+    """C5's recipe (uniform, real m, theta = .5, p = 17, leaf target 40) at N = 1e7, L = 9:
+    every level's structure bit-exact and all 1e7 outputs within 1e-12 of the oracle FMM."""
+    c = W.CONFIGS["C5"]
+    z, m = W.make_config("C5", n=10_000_000)
+    L = orc.nlevels(len(z), c.leaf_target)
+    assert L == 9
+    _assert_whole(compare(z, m, c.theta, c.p, L, real=True))
+
+
+@pytest.mark.skipif(os.environ.get("FMM2D_FULL_C5") != "1",
+                    reason="set FMM2D_FULL_C5=1 (~10 min oracle); log: profiles/r02/full_parity_c5.json")
+def test_c5_whole_problem_vs_oracle(orc):
+    """BJ configs[4] itself (N = 1e8, L = 11, 12 levels): the bench's workload, whole problem."""
+    c = W.CONFIGS["C5"]
+    z, m = W.make_config("C5")
+    L = orc.nlevels(len(z), c.leaf_target)
+    assert L == 11
+    _assert_whole(compare(z, m, c.theta, c.p, L, real=True))

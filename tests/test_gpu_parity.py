@@ -14,6 +14,7 @@ import pytest
 import torch
 
 import workloads as W
+from fullparity import errors as _errors
 
 pytestmark = pytest.mark.gpu
 
@@ -62,6 +63,9 @@ STRUCT_CASES = [
     ("C4-200k", lambda: W.make_config("C4", n=200_000), 0.5, None),
     ("lattice-ties", lambda: (W.lattice(6, 4, h=0.5, shuffle_seed=2), None), 0.5, 4),
     ("ragged-7777", lambda: W.make("uniform", 7777, seed=3), 0.5, 3),
+    # level-1 weak pairs (DESIGN R15): four tight clusters, one per level-1 box
+    ("corners-t.5", lambda: W.make("corners", 2000, seed=31), 0.5, 2),
+    ("corners-t.3", lambda: W.make("corners", 40_000, seed=32), 0.3, 4),
 ]
 
 
@@ -155,6 +159,30 @@ def test_eval_matches_oracle(orc, name, cfg, n, theta, p):
     assert np.isfinite(phi_g).all() and np.isfinite(dphi_g).all()
     e1, e2 = _nerr(phi_g, phi_o), _nerr(dphi_g, dphi_o)
     assert e1 <= TOL and e2 <= TOL, (e1, e2)
+    # pointwise, with the floor 1e-3 max|ref| (tests/fullparity.py)
+    p1, p2 = _errors(phi_g, phi_o), _errors(dphi_g, dphi_o)
+    assert p1["point"] <= TOL and p2["point"] <= TOL, (p1, p2)
+
+
+@pytest.mark.parametrize("n,theta,L", [(2000, 0.5, 2), (40_000, 0.3, 4), (40_000, 0.5, 4)])
+def test_eval_level1_weak_pairs(orc, n, theta, L):
+    """Level-1 M2L carries the whole inter-cluster field (corners input, DESIGN R15): the GPU
+    lists hold the 12 level-1 weak pairs, the outputs match the oracle within 1e-12 and the
+    direct sum within BJ's gate."""
+    z, m = W.make("corners", n, "real", seed=33)
+    gp = _gpu_plan(z, theta, 17, L, real=True)
+    op = orc.plan(z, theta, L)
+    _check_structure(gp, op, L)
+    assert len(gp.list(1, "weak")[1]) == 12
+    phi_o, dphi_o = op.eval(m, 17)
+    phi_g, dphi_g = _gpu_eval(gp, m)
+    assert _nerr(phi_g, phi_o) <= TOL and _nerr(dphi_g, dphi_o) <= TOL
+    lo = gp.expansions(1, "local")
+    assert np.abs(lo - op.expansions(1, "local")).max() <= 1e-12 * np.abs(op.expansions(1, "local")).max()
+    t = W.sample_targets(n, 200, seed=34)
+    phi_d, dphi_d = orc.direct(z, m, targets=t)
+    assert _nerr(phi_g[t].real, phi_d.real) <= 1e-6
+    assert _nerr(dphi_g[t], dphi_d) <= orc.error_bound(theta, 17)
 
 
 def test_eval_real_strength_flag_matches(orc):

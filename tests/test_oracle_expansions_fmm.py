@@ -208,6 +208,34 @@ def test_fmm_input_order_invariance(orc):
     assert _nerr(phi2, phi[perm]) < 1e-13 and _nerr(dphi2, dphi[perm]) < 1e-13
 
 
+@pytest.mark.parametrize("theta,L", [(0.5, 2), (0.3, 3)])
+def test_fmm_level1_weak_pairs_vs_direct(orc, theta, L):
+    """Level-1 M2L (DESIGN R15): "for each box b, the strong connections S(p) of its parent ...
+    recursively defines the connectivity for the whole tree" applies from level 1
+    (P:343-351), and the far-to-local shifts follow the weak pattern on every level
+    (P:356-357).  Four tight clusters at the corners of a square: every level-1 box is one
+    cluster and all 12 ordered level-1 pairs are weak, so the whole inter-cluster field goes
+    through level-1 M2L; skipping that level leaves O(1) errors."""
+    z, m = W.make("corners", 2000, "real", seed=31)
+    P = orc.plan(z, theta, L)
+    off1, idx1 = P.list(1, "weak")
+    assert len(idx1) == 12 and all(len(P.list(l, "weak")[1]) == 0 for l in (2,))
+    phi_d, dphi_d = orc.direct(z, m)
+    phi, dphi = P.eval(m, 17)
+    assert _nerr(phi.real, phi_d.real) <= 1e-6
+    assert _nerr(dphi, dphi_d) <= orc.error_bound(theta, 17)
+    # the level-1 locals hold the field of the three other clusters: evaluate the local of
+    # box 0 at its own points and compare with the direct sum over the other clusters
+    loc1 = P.expansions(1, "local")
+    cx, cy, _ = P.discs(1)
+    perm, off = P.perm(), P.offsets(1)
+    pts = perm[off[0]:off[1]]
+    other = np.setdiff1d(np.arange(len(z)), pts)
+    ph_l, dph_l = orc.l2p(loc1[0], cx[0] + 1j * cy[0], 17, z[pts])
+    ref = np.array([np.sum(m[other] / (z[i] - z[other])) for i in pts])
+    assert _nerr(dph_l, ref) <= 1e-10
+
+
 def test_fmm_root_only_is_direct_sum(orc):
     """L = 0: the root is strong to itself, everything is P2P."""
     z, m = W.make("uniform", 60, "phase", seed=27)

@@ -151,7 +151,7 @@ def _ancestor(leaf_of, l, L):
 
 @pytest.mark.parametrize("dist,n,L,theta", [
     ("uniform", 1500, 3, 0.5), ("clusters", 1500, 3, 0.3), ("curve", 1500, 3, 0.7),
-    ("uniform", 700, 4, 0.5)])
+    ("uniform", 700, 4, 0.5), ("corners", 1200, 3, 0.5)])
 def test_lists_exactly_once_coverage(orc, dist, n, L, theta):
     """Every ordered pair (i, j), i != j, is accounted for exactly once: by one
     ancestor weak pair or by the leaf strong pair."""

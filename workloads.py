@@ -67,6 +67,15 @@ def positions(dist: str, n: int, rng: np.random.Generator) -> np.ndarray:
         t = rng.random(n)
         e = 1e-4 * rng.standard_normal((n, 2))
         return (t + e[:, 0]) + 1j * (0.1 * np.sin(8.0 * np.pi * t) + e[:, 1])
+    if dist.startswith("corners"):
+        # four tight Gaussian clusters (sigma = 1e-3, or "corners:<sigma>") at the corners
+        # of the square [0.2, 0.8]^2, point i in cluster (i mod 4): with N divisible by 4
+        # every level-1 box of the median tree is exactly one cluster, so the level-1 boxes
+        # are weakly coupled and level-1 M2L carries the whole far field
+        sig = float(dist.split(":")[1]) if ":" in dist else 1e-3
+        centres = np.array([[0.2, 0.2], [0.2, 0.8], [0.8, 0.2], [0.8, 0.8]])
+        xy = centres[np.arange(n) % 4] + sig * rng.standard_normal((n, 2))
+        return xy[:, 0] + 1j * xy[:, 1]
     if dist == "disc":
         # Fig. 3 (i): uniform in the unit disc
         r = np.sqrt(rng.random(n))
