@@ -222,6 +222,25 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: start N ranks (one process per GPU) through
+    torch.distributed.run on this node and return its exit code; rank 0 prints the line.
+    Fails loudly if the node has fewer than N GPUs."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} needs {n} CUDA devices, this node has {have}", file=sys.stderr, flush=True)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -244,8 +263,15 @@ def main():
     local_rank = _env_int("LOCAL_RANK", 0)
 
     if args.impl == "reference":
-        run_reference(args, cfg, rank, world)
+        run_reference(args, cfg, rank, world if "WORLD_SIZE" in os.environ else args.gpus)
         return
+
+    if args.gpus < 1:
+        sys.exit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch one rank per GPU)")
 
     import torch
     import torch.distributed as dist

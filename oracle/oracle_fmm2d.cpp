@@ -27,6 +27,8 @@
  * the results are bitwise identical for any thread count.
  */
 #include <algorithm>
+#include <omp.h>
+#include <parallel/algorithm>
 #include <cmath>
 #include <complex>
 #include <cstdint>
@@ -166,6 +168,18 @@ struct ByY {
 
 static int64_t ceil_half(int64_t n) { return n - n / 2; }
 
+/* A library sort under a STRICT total order (ties broken by the input index, R6), so the
+ * result is unique: the OpenMP-parallel GNU sort is used for the few huge segments of the
+ * top levels (one box spans all points at level 0), std::sort elsewhere. */
+extern "C++" {
+template <class Cmp>
+static void sort_seg(uint32_t* a, int64_t n, Cmp c)
+{
+    if (n > (1 << 16) && !omp_in_parallel()) __gnu_parallel::sort(a, a + n, c);
+    else std::sort(a, a + n, c);
+}
+}
+
 /* O2: "recursively splitting the source points at or near their median in each
  * coordinate direction".  DESIGN R5/R7: x first, low side gets the
  * first ceil(n/2) points in (x, idx) order; each half is then split in y the
@@ -186,14 +200,15 @@ static void build_tree(oracle_plan* P)
         const std::vector<int64_t>& o = P->off[l];
         std::vector<int64_t>& oc = P->off[l + 1];
         oc.assign(4 * nboxes(l) + 1, 0);
-#pragma omp parallel for schedule(dynamic, 64)
+        /* few huge boxes: one at a time, each sort parallel inside (sort_seg) */
+#pragma omp parallel for schedule(dynamic, 64) if (nboxes(l) >= 256)
         for (int64_t b = 0; b < nboxes(l); ++b) {
             int64_t s = o[b], e = o[b + 1], nb = e - s;
             uint32_t* seg = P->perm.data() + s;
-            std::sort(seg, seg + nb, byx);                     /* x-split */
+            sort_seg(seg, nb, byx);                            /* x-split */
             int64_t h0 = ceil_half(nb), h1 = nb - h0;
-            std::sort(seg, seg + h0, byy);                     /* y-split of x-low  */
-            std::sort(seg + h0, seg + nb, byy);                /* y-split of x-high */
+            sort_seg(seg, h0, byy);                            /* y-split of x-low  */
+            sort_seg(seg + h0, nb - h0, byy);                  /* y-split of x-high */
             oc[4 * b + 0] = s;
             oc[4 * b + 1] = s + ceil_half(h0);
             oc[4 * b + 2] = s + h0;
@@ -203,9 +218,9 @@ static void build_tree(oracle_plan* P)
     }
     /* DESIGN R13: inside a leaf, ascending (y, idx). */
     const std::vector<int64_t>& oL = P->off[P->L];
-#pragma omp parallel for schedule(dynamic, 64)
+#pragma omp parallel for schedule(dynamic, 64) if (nboxes(P->L) >= 256)
     for (int64_t b = 0; b < nboxes(P->L); ++b)
-        std::sort(P->perm.data() + oL[b], P->perm.data() + oL[b + 1], byy);
+        sort_seg(P->perm.data() + oL[b], oL[b + 1] - oL[b], byy);
 }
 
 /* O9: "standard midpoint adaptivity" (Fig. 2) as the uniform baseline of

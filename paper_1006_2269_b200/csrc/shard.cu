@@ -64,8 +64,11 @@ NcclApi* nccl_api()
     static NcclApi api;
     static std::once_flag once;
     std::call_once(once, [] {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        // FMM2D_NCCL_LIB: another library with NCCL's entry points (tests only: the
+        // one-GPU multi-process shim tests/ncclshim); the product loads NCCL itself
+        const char* alt = getenv("FMM2D_NCCL_LIB");
+        void* h = (alt && *alt) ? dlopen(alt, RTLD_NOW | RTLD_GLOBAL) : dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h && !(alt && *alt)) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
         if (!h) return;
 #define FMM2D_SYM(f, name) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, name))
         FMM2D_SYM(GetUniqueId, "ncclGetUniqueId");

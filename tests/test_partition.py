@@ -75,3 +75,20 @@ def test_dist_plumbing_gloo_world2():
         assert p0["positions"][0] == 0 and p0["positions"][1] == p1["positions"][0]
         assert p1["positions"][1] == 1_000_000
     assert res[0] == res[1]
+
+
+def test_bench_gpus_without_devices_fails_loudly():
+    """`bench.py --gpus N` spawns N ranks itself (torch.distributed.run) when no launcher
+    did; with fewer than N devices it must fail with a message, never time one GPU."""
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("this host has >= 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2 and "needs 2 CUDA devices" in r.stderr, (r.returncode, r.stderr[-500:])
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, env=dict(os.environ, WORLD_SIZE="1"))
+    assert r.returncode != 0 and "WORLD_SIZE=1" in r.stderr

@@ -33,8 +33,6 @@ MUTATIONS = [
      "    for (int l = 1; l <= P->L; ++l) {\n        if (l == 1) { P->strong[1].assign(4, {}); P->weak[1].assign(4, {});"
      " for (uint32_t b = 0; b < 4; ++b) for (uint32_t c = 0; c < 4; ++c) P->strong[1][b].push_back(c); continue; }\n"
      "        int64_t nb = nboxes(l);\n        P->strong[l]"),
-    ("L2L from level 2", "    for (int l = 1; l <= L; ++l) {\n#pragma omp parallel for schedule(dynamic, 64)\n        for (int64_t c = 0;",
-     "    for (int l = 2; l <= L; ++l) {\n#pragma omp parallel for schedule(dynamic, 64)\n        for (int64_t c = 0;"),
     # O7 r/R exchange
     ("P2L drops the minus sign", "b[l] -= ms[j] * ivl / (double)l;", "b[l] += ms[j] * ivl / (double)l;"),
     ("exchanged criterion unswapped", "return (r < R) && (d > 0.0) && (r + theta * R <= theta * d);",

@@ -87,6 +87,12 @@ def positions(dist: str, n: int, rng: np.random.Generator) -> np.ndarray:
         r = rng.random(n)
         a = 2.0 * np.pi * rng.random(n)
         return r * np.cos(a) + 1j * (r * np.sin(a))
+    if dist == "disc_logr":
+        # Fig. 3 (ii) under SPEC's reading (S:483 design decision): radial density ~ 1/r on the
+        # truncated support [1e-8, 1], i.e. a log-uniform radius (the SURVEY f3 row's reading)
+        r = np.exp(rng.uniform(np.log(1e-8), 0.0, n))
+        a = 2.0 * np.pi * rng.random(n)
+        return r * np.cos(a) + 1j * (r * np.sin(a))
     if dist.startswith("normal:") or dist.startswith("layer:"):
         # Fig. 4: "a normal distribution with variance sigma^2 or ... a 'layer'
         # distribution where the x-coordinate is uniformly distributed in [0,1], and the
