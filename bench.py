@@ -171,6 +171,52 @@ def k_near_traffic(cfg, default_cfg):
         return None, None
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+ONE_THREAD_N = 390_625          # C5 recipe at L = 7: the same leaf occupancy (23.8), one pass
+
+
+def oracle_one_thread(cfg):
+    """The oracle on ONE host thread (OMP_NUM_THREADS=1, a child process): one build + eval
+    of the C5 recipe at N = 390,625 (same leaf occupancy), points/s."""
+    code = ("import sys, time; sys.path.insert(0, %r); import oracle, workloads as W; "
+            "z, m = W.make(%r, %d, %r, seed=W.SEED_BASE + 78); L = oracle.nlevels(%d, %d); "
+            "t = time.perf_counter(); P = oracle.plan(z, %r, L); P.eval(m, %d); "
+            "print(time.perf_counter() - t)") % (ROOT, cfg.dist, ONE_THREAD_N, cfg.strengths, ONE_THREAD_N,
+                                                  cfg.leaf_target, cfg.theta, cfg.p)
+    try:
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                           env=dict(os.environ, OMP_NUM_THREADS="1"))
+        dt = float(r.stdout.strip().splitlines()[-1])
+    except Exception as e:                       # report, never fail the bench line over it
+        return {"error": str(e)[:200]}
+    return {"value": ONE_THREAD_N / dt, "unit": "points/s", "cores": 1, "seconds": dt,
+            "sample": f"{cfg.dist} N={ONE_THREAD_N} (same leaf occupancy as {cfg.name}), one build+eval"}
+
+
+def parity_record(default_cfg):
+    """The committed whole-problem parity log of the bench's own configuration (C5)."""
+    if not default_cfg:
+        return None
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02", "full_parity_C5.json")))
+    except Exception:
+        return None
+    return {"source": "profiles/r02/full_parity_C5.json (tools/full_parity.py; tests/test_gpu_fullsize.py)",
+            "levels_bit_exact": len(d["levels_compared"]), "list_entries_bit_exact": d["entries_compared"],
+            "phi_normwise": d["phi"]["norm"], "phi_pointwise": d["phi"]["point"],
+            "dphi_normwise": d["dphi"]["norm"], "dphi_pointwise": d["dphi"]["point"],
+            "pointwise_floor": f"{d['pt_floor']:g} max|ref|", "bar": 1e-12}
+
+
 def cpu_baseline(cfg, seconds_hint=True):
     """Oracle (plain C++ + OpenMP) on a bounded sample of the same workload."""
     import oracle
@@ -187,8 +233,10 @@ def cpu_baseline(cfg, seconds_hint=True):
         passes += 1
     cores = _env_int("OMP_NUM_THREADS", os.cpu_count() or 1)
     return {"value": n * passes / dt, "unit": "points/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"{cfg.dist} N={n} (L={L}, same leaf occupancy as {cfg.name}), theta={cfg.theta}, "
-                      f"p={cfg.p}: {passes} build+eval passes, {dt:.1f} s"}
+                      f"p={cfg.p}: {passes} build+eval passes, {dt:.1f} s",
+            "one_thread": oracle_one_thread(cfg)}
 
 
 def run_reference(args, cfg, rank, world):
@@ -377,8 +425,14 @@ def main():
             t = torch.tensor([e2e["ms"]], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e["ms"] = float(t.item())
+        single = e2e.get("single_ms")
         e2e = {"value": cfg.n / (e2e["ms"] / 1e3), "unit": "points/s",
-               "h2d_bytes_per_step": e2e["h2d"] * world, "d2h_bytes_per_step": e2e["d2h"] * world}
+               "h2d_bytes_per_step": e2e["h2d"] * world, "d2h_bytes_per_step": e2e["d2h"] * world,
+               "mode": (f"{E2E_IN_FLIGHT} problems in flight (fmm2d_build_eval, FMM2D_ASYNC_HOST, one stream each)"
+                        if not shard_kw else "one problem at a time (build, then eval)")}
+        if single is not None:
+            e2e["single_call"] = {"value": cfg.n / (single / 1e3), "unit": "points/s", "ms": single,
+                                  "mode": "one synchronous fmm2d_build_eval at a time (host buffers, latency)"}
 
     launches_per_step = phase["launches"]
     if rank == 0:
@@ -398,6 +452,7 @@ def main():
                 "clocks": clk.summary(), "e2e": e2e,
                 "stats": {"weak_pairs": weak_pairs, "p2p_pairs": pairs, "min_leaf": st.get("min_leaf"),
                           "max_leaf": st.get("max_leaf")}}
+        line["parity"] = parity_record(args.config == "C5" and not args.n)
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(cfg)
         print(json.dumps(line), flush=True)
@@ -481,7 +536,17 @@ def end_to_end(z_np, m_np, cfg, real, stream, args, shard_kw):
     while inflight:
         inflight.pop(0).close()
     torch.cuda.synchronize()
-    return {"ms": e0.elapsed_time(e1) / steps, "h2d": 16 * cfg.n * 2, "d2h": 16 * cfg.n * 2}
+    out = {"ms": e0.elapsed_time(e1) / steps, "h2d": 16 * cfg.n * 2, "d2h": 16 * cfg.n * 2}
+    if not shard_kw:
+        # latency: one synchronous problem at a time through the same call (no overlap across calls)
+        reps = 3
+        e0.record(stream)
+        for _ in range(reps):
+            Fmm2d.build_eval(zh, mh, ph, dh, stream=stream, **kw)[0].close()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out["single_ms"] = e0.elapsed_time(e1) / reps
+    return out
 
 
 if __name__ == "__main__":

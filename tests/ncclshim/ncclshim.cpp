@@ -67,6 +67,7 @@ struct Op {
 
 int g_group = 0;
 std::vector<Op> g_ops;
+Comm* g_comm = nullptr;                   // the process's communicator (one per process here)
 std::atomic<long> g_calls{0};
 
 size_t type_size(ncclDataType_t t)
@@ -127,8 +128,9 @@ void reduce_typed(void* acc, const void* v, size_t bytes, ncclDataType_t t, nccl
 // run a batch of operations of one communicator: deposits, barrier, withdrawals, barrier
 ncclResult_t run_ops(std::vector<Op>& ops)
 {
-    if (ops.empty()) return ncclSuccess;
-    Comm* c = ops[0].comm;
+    // an empty group still takes part in both barriers (the peers' groups may not be empty)
+    Comm* c = ops.empty() ? g_comm : ops[0].comm;
+    if (!c) return ncclSuccess;
     for (const Op& o : ops)
         if (o.comm != c) return ncclInvalidUsage;        // one communicator per group here
     const int R = c->nranks, me = c->rank;
@@ -208,6 +210,7 @@ ncclResult_t ncclGetUniqueId(ncclUniqueId* id)
 ncclResult_t ncclCommInitRank(ncclComm_t* out, int nranks, ncclUniqueId id, int rank)
 {
     if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks) return ncclInvalidArgument;
+    if (getenv("FMM2D_NCCLSHIM_DEBUG")) fprintf(stderr, "ncclshim: init rank %d of %d\n", rank, nranks);
     Comm* c = new Comm();
     c->nranks = nranks;
     c->rank = rank;
@@ -240,6 +243,7 @@ ncclResult_t ncclCommInitRank(ncclComm_t* out, int nranks, ncclUniqueId id, int 
     }
     barrier(c);
     g_calls.fetch_add(1);
+    g_comm = c;
     *out = (ncclComm_t)c;
     return ncclSuccess;
 }
