@@ -43,9 +43,25 @@ import numpy as np  # noqa: E402
 import workloads as W  # noqa: E402
 
 METRIC = "FMM evaluated points/sec at 1/2/4/8 B200 (θ=0.5, p=17) and % FP64 roofline"
-P2P_FLOPS_PER_PAIR = 105.0        # SURVEY 8(d) working estimate (algorithmic, per ordered pair)
 M2L_FLOPS_PER_PAIR = 1450.0       # SURVEY 8(d), p = 17
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+CENSUS = os.path.join(ROOT, "profiles", "r02", "fp64_census.json")
+
+
+def census():
+    try:
+        return json.load(open(CENSUS))
+    except Exception:
+        return {}
+
+
+def p2p_flops_per_pair():
+    """SURVEY 8(d)'s convention: each transcendental at its libdevice FP64 instruction cost,
+    measured once by ncu on a microbenchmark (tools/p2p_census.cu): 2 DFMA + DADD + DMUL per
+    pair of the library-math pair body (128 at C5-like |dz|).  Falls back to the survey's
+    working estimate 105 if the census is missing."""
+    c = census().get("libdevice_pair", {})
+    return float(c.get("flops_per_pair", 105.0)), (CENSUS if c else "SURVEY 8(d) working estimate")
 # bounded CPU sample of a workload for the oracle: the C5 recipe at L = 8 (same leaf occupancy,
 # 23.8 points per leaf), build + eval passes repeated up to about 10 s of host work
 CPU_SAMPLE_N = 1_562_500
@@ -63,8 +79,10 @@ def _env_int(k, d):
 
 
 def fp64_peak():
-    """(TFLOP/s, source).  MEASURED_PEAKS.json if it has an FP64 entry, else our own
-    DFMA microbenchmark result profiles/fp64_peak.json, else the nominal figure."""
+    """(TFLOP/s, source).  MEASURED_PEAKS.json if it has an FP64 entry; else, for a path bound
+    by plain FP64 ALU work, the peak derived from the unit counts and clock (B200_PROFILING.md:
+    148 SMs, 64 FP64 lanes each, 1.965 GHz clocks.max.sm) = 37.2 TFLOP/s.  The measured DFMA
+    loop and cuBLAS DGEMM figures are reported beside it (roofline.peaks)."""
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         for k in ("fp64_tflops", "fp64_tflops_sustained"):
@@ -72,12 +90,7 @@ def fp64_peak():
                 return float(mp[k]), "MEASURED_PEAKS.json:" + k
     except Exception:
         pass
-    try:
-        fp = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
-        return float(fp["dfma_tflops"]), "profiles/fp64_peak.json (DFMA microbenchmark, measured)"
-    except Exception:
-        pass
-    return NOMINAL_FP64_TFLOPS, "nominal 148 SM x 64 DFMA x 2 x 1.965 GHz"
+    return NOMINAL_FP64_TFLOPS, "derived: 148 SM x 64 FP64 lanes x 2 flop x 1.965 GHz (unit counts and clock)"
 
 
 class ClockSampler:
@@ -402,18 +415,29 @@ def main():
     peak, peak_src = fp64_peak()
     pairs = st.get("p2p_pairs", 0.0)
     near_ms = phase["near_ms"]
-    achieved = pairs * P2P_FLOPS_PER_PAIR / (near_ms / 1e3) / 1e12
+    fpp, fpp_src = p2p_flops_per_pair()
+    achieved = pairs * fpp / (near_ms / 1e3) / 1e12
     traffic, traffic_src = k_near_traffic(cfg, args.config == "C5" and not args.n and world == 1
                                           and not args.rr_exchange and not args.parent_merge
                                           and not args.symmetric_p2p)
     nleaf = 4 ** L if L else 1
     algo_bytes = 32.0 * cfg.n * 2 + 4.0 * cfg.n + 288.0 * nleaf        # rows in, Phi/Phi' out, perm, locals
+    cen = census()
     roof = {"bound": "alu", "kernel": "k_near (P2P+L2P)", "achieved": achieved, "peak": peak,
             "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
             "algorithmic_bytes_per_launch": algo_bytes,
-            "flops_per_launch": pairs * P2P_FLOPS_PER_PAIR, "pairs_per_launch": pairs,
+            "flops_per_launch": pairs * fpp, "pairs_per_launch": pairs,
             "peak_source": peak_src,
-            "flop_convention": f"{P2P_FLOPS_PER_PAIR:.0f} FP64 flop per ordered P2P pair (SURVEY 8(d))"}
+            "flop_convention": f"{fpp:g} FP64 flop per ordered P2P pair: the libdevice pair body's executed "
+                               f"2 DFMA + DADD + DMUL, ncu census ({fpp_src}; SURVEY 8(d))",
+            "peaks": cen.get("peaks_tflops")}
+    kn = cen.get("k_near")
+    if kn and "flops_per_pair" in kn:
+        ex = pairs * kn["flops_per_pair"] / (near_ms / 1e3) / 1e12
+        roof["executed"] = {"flops_per_pair": kn["flops_per_pair"], "tflops": ex, "frac_of_peak": ex / peak,
+                            "fp64_pipe_pct": kn.get("fp64_pipe_pct"), "source": CENSUS,
+                            "note": "the kernel's own executed FP64 flops (table-driven log/Arg/rcp need fewer "
+                                    "than libdevice's); the FP64-pipe utilisation is clock-independent"}
     weak_pairs = st.get("weak_pairs", 0.0)
     m2l_tf = weak_pairs * M2L_FLOPS_PER_PAIR / (phase["m2l_ms"] / 1e3) / 1e12 if phase["m2l_ms"] > 0 else 0.0
 

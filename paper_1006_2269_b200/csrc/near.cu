@@ -232,7 +232,11 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                 const uint32_t lf = sidx[q + l];
                 const uint32_t s0 = off[lf];
                 const int c0 = cstart[l], sz = cstart[l + 1] - c0;
+#ifndef FMM2D_NEAR_EXP_NOSTAGE
                 for (int e = lane; e < sz; e += 32) S[c0 + e] = src[s0 + e];
+#else
+                (void)s0; (void)c0; (void)sz;              // timing experiment only: rows not staged
+#endif
             }
             __syncthreads();
             const int total = cstart[nl];
@@ -289,10 +293,14 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                 continue;
             }
             double4 f;                            // L2P (Horner) of the target
+#ifndef FMM2D_NEAR_EXP_NOL2P
             {
                 const double4 me = src[ts + i0 + kk];
                 l2p(loc + t * (p + 1), p, me.x - cx[t], me.y - cy[t], f.x, f.y, f.z, f.w);
             }
+#else
+            f = make_double4(0.0, 0.0, 0.0, 0.0);    // timing experiment only
+#endif
             if (m2p_off && m2p_off[t + 1] > m2p_off[t]) {      // r/R exchange: M2P sums
                 const double4 g = m2p_acc[ts + i0 + kk];
                 f.x += g.x;
@@ -300,7 +308,11 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                 f.z += g.z;
                 f.w += g.w;
             }
+#ifndef FMM2D_NEAR_EXP_NOSTORE
             const uint32_t o = perm[ts + i0 + kk];
+#else
+            const uint32_t o = ts + i0 + kk;         // timing experiment only: leaf order, no scatter
+#endif
             if (phi) phi[o] = make_double2(acc.x + f.x, acc.y + f.y);
             if (dphi) dphi[o] = make_double2(acc.z + f.z, acc.w + f.w);
         }

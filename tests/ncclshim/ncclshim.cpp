@@ -150,6 +150,7 @@ ncclResult_t run_ops(std::vector<Op>& ops)
             soff[o.peer] += o.bytes;
         }
     }
+    SHIM_CUDA(cudaDeviceSynchronize());                   // device-to-device cudaMemcpy may return early
     barrier(c);
     // withdrawals from the peers' staging
     boff = 0;
