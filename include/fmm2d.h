@@ -173,6 +173,12 @@ FMM2D_API int fmm2d_reserve(int device, size_t bytes);
  * allocator.  Synchronises the device first.  Errors: EINVAL, ECUDA. */
 FMM2D_API int fmm2d_pool_trim(int device, size_t keep_bytes);
 
+/* The library pool's device memory in use now and its high-water mark since the last reset
+ * (cudaMemPoolAttrUsedMemCurrent / UsedMemHigh), in bytes; reset != 0 restarts the
+ * high-water mark.  Diagnostics (per-rank memory of a partitioned build).  Errors: EINVAL,
+ * ECUDA. */
+FMM2D_API int fmm2d_pool_usage(int device, int64_t* used, int64_t* high, int reset);
+
 /* Number of kernels this library has launched since it was loaded (all plans and
  * threads; CUB's internal launches are not counted). */
 FMM2D_API int64_t fmm2d_launch_count(void);
@@ -243,7 +249,7 @@ FMM2D_API int fmm2d_plan_info(const fmm2d_plan* plan, int64_t* n, int* nlevels, 
 #define FMM2D_EXPORT_WEAK        5  /* l      int64[4^l+1] offsets then uint32[] idx  */
 #define FMM2D_EXPORT_MPOLE       6  /* l      complex128[4^l][p+1] (after an eval)    */
 #define FMM2D_EXPORT_LOCAL       7  /* l      complex128[4^l][p+1] (after an eval)    */
-#define FMM2D_EXPORT_STATS       8  /* -      double[16]: see fmm2d_api.cu            */
+#define FMM2D_EXPORT_STATS       8  /* -      double[16]: see api.cu (15: device bytes held) */
 #define FMM2D_EXPORT_NEAR        9  /* L      int64[4^L+1] offsets then uint32[]: direct pairs */
 #define FMM2D_EXPORT_RR_P2L     10  /* L      same layout: P2L sources of each leaf (r/R exch.) */
 #define FMM2D_EXPORT_RR_M2P     11  /* L      same layout: M2P sources of each leaf (r/R exch.) */

@@ -75,6 +75,7 @@ int dev_alloc(fmm2d_plan* P, void** ptr, size_t bytes)
         return FMM2D_ENOMEM;
     }
     P->allocs.push_back(*ptr);
+    P->stats.dev_bytes += (int64_t)bytes;
     return 0;
 }
 
@@ -201,13 +202,28 @@ static int build_stage_tree(const double* z, int64_t n, const fmm2d_options* opt
         FMM2D_TRY(prepare_near(P));
         const int64_t nb = P->nbox_total;
         const int P1 = P->p + 1;
-        FMM2D_TRY(dev_alloc(P, (void**)&P->perm, sizeof(uint32_t) * n));
-        FMM2D_TRY(dev_alloc(P, (void**)&P->src, sizeof(double4) * n));
+        // leaf-ordered rows and input indices of the own positions [pos0, pos1) only (one
+        // GPU: all n); src / perm are virtual bases indexed by the global position
+        const int64_t nown = (int64_t)P->pos1 - (int64_t)P->pos0;
+        FMM2D_TRY(dev_alloc(P, (void**)&P->perm, sizeof(uint32_t) * nown));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->src, sizeof(double4) * nown));
+        P->perm -= P->pos0;
+        P->src -= P->pos0;
         FMM2D_TRY(dev_alloc(P, (void**)&P->cx, sizeof(double) * nb));
         FMM2D_TRY(dev_alloc(P, (void**)&P->cy, sizeof(double) * nb));
         FMM2D_TRY(dev_alloc(P, (void**)&P->r, sizeof(double) * nb));
-        FMM2D_TRY(dev_alloc(P, (void**)&P->mpole, sizeof(double2) * nb * P1));
-        FMM2D_TRY(dev_alloc(P, (void**)&P->local, sizeof(double2) * nb * P1));
+        // expansions of the stored boxes of every level (replicated levels: all, below: own)
+        int64_t sbase[FMM2D_MAXL + 2], stot = 0;
+        for (int l = 0; l <= L; ++l) {
+            sbase[l] = stot;
+            stot += P->box_hi(l) - P->box_lo(l);
+        }
+        FMM2D_TRY(dev_alloc(P, (void**)&P->mpole, sizeof(double2) * stot * P1));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->local, sizeof(double2) * stot * P1));
+        for (int l = 0; l <= L; ++l) {
+            P->mpl[l] = P->mpole + (sbase[l] - P->box_lo(l)) * P1;
+            P->lcl[l] = P->local + (sbase[l] - P->box_lo(l)) * P1;
+        }
         const double2* zd = (const double2*)z;
         double2* zstage = nullptr;
         if (P->flags & FMM2D_HOST_PTRS) {
@@ -231,7 +247,8 @@ static int build_stage_tree(const double* z, int64_t n, const fmm2d_options* opt
             FMM2D_CUDA_TRY(cudaStreamCreateWithPriority(&P->side, cudaStreamNonBlocking, hi));
             FMM2D_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_gather, cudaEventDisableTiming));
             FMM2D_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_exp, cudaEventDisableTiming));
-            FMM2D_TRY(dev_alloc(P, (void**)&P->nacc, sizeof(double4) * n));
+            FMM2D_TRY(dev_alloc(P, (void**)&P->nacc, sizeof(double4) * ((int64_t)P->pos1 - P->pos0)));
+            P->nacc -= P->pos0;                 // virtual base, like src
             P->overlap = true;
         }
         FMM2D_CUDA_TRY(cudaEventRecord(e2, P->stream));
@@ -594,6 +611,24 @@ int fmm2d_pool_trim(int device, size_t keep_bytes)
     return 0;
 }
 
+int fmm2d_pool_usage(int device, int64_t* used, int64_t* high, int reset)
+{
+    if (device < 0 || !used || !high) return FMM2D_EINVAL;
+    FMM2D_CUDA_TRY(cudaSetDevice(device));
+    cudaMemPool_t pool = lib_pool(device);
+    if (!pool) return FMM2D_ECUDA;
+    uint64_t u = 0, h = 0;
+    FMM2D_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &u));
+    FMM2D_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &h));
+    *used = (int64_t)u;
+    *high = (int64_t)h;
+    if (reset) {
+        uint64_t z = 0;
+        FMM2D_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &z));
+    }
+    return 0;
+}
+
 int fmm2d_halo_info(const fmm2d_plan* P, int64_t* info)
 {
     if (!P || !info) return FMM2D_EINVAL;
@@ -630,7 +665,7 @@ static int copy_out(const void* dsrc, void* dst, size_t bytes, size_t* cap, size
  * 5 strong leaf pairs, 6 min leaf size, 7 max leaf size, 8 t_build_ms, 9 t_tree_ms,
  * 10 t_lists_ms, 11 number of boxes (all levels), 12 kernel launches of this library
  * since it was loaded (all plans), 13 ordered P2P pairs (j != i) of one eval, 14 axes presorted
- * with 64-bit keys (bit 0 x, bit 1 y), 15 reserved. */
+ * with 64-bit keys (bit 0 x, bit 1 y), 15 device bytes the plan holds. */
 int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* bytes)
 {
     if (!P || !bytes) return FMM2D_EINVAL;
@@ -681,7 +716,12 @@ int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* by
     size_t off = 0, cap = *bytes;
     cudaStream_t st = P->stream;
     switch (what) {
-        case FMM2D_EXPORT_PERM: FMM2D_TRY(copy_out(P->perm, dst, need, &cap, &off, st)); break;
+        case FMM2D_EXPORT_PERM:                  // sharded plans: the own positions (the rest 0)
+            memset(dst, 0, need);
+            FMM2D_CUDA_TRY(cudaMemcpyAsync((uint32_t*)dst + P->pos0, P->perm + P->pos0,
+                                           sizeof(uint32_t) * (P->pos1 - P->pos0), cudaMemcpyDeviceToHost, st));
+            off = need;
+            break;
         case FMM2D_EXPORT_OFFSETS: {
             std::vector<uint32_t> h(nb + 1);
             FMM2D_CUDA_TRY(cudaMemcpyAsync(h.data(), P->boff + P->obase[level], sizeof(uint32_t) * (nb + 1),
@@ -717,9 +757,13 @@ int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* by
             }
             break;
         case FMM2D_EXPORT_MPOLE:
-        case FMM2D_EXPORT_LOCAL: {
-            const double2* E = (what == FMM2D_EXPORT_MPOLE) ? P->mpole : P->local;
-            FMM2D_TRY(copy_out(E + P->base[level] * (P->p + 1), dst, need, &cap, &off, st));
+        case FMM2D_EXPORT_LOCAL: {              // sharded plans: the stored boxes (the rest 0)
+            const double2* E = (what == FMM2D_EXPORT_MPOLE) ? P->mpl[level] : P->lcl[level];
+            const int64_t b0 = P->box_lo(level), b1 = P->box_hi(level), P1 = P->p + 1;
+            memset(dst, 0, need);
+            FMM2D_CUDA_TRY(cudaMemcpyAsync((double2*)dst + b0 * P1, E + b0 * P1, sizeof(double2) * (b1 - b0) * P1,
+                                           cudaMemcpyDeviceToHost, st));
+            off = need;
             break;
         }
         case FMM2D_EXPORT_STATS: {
@@ -733,6 +777,7 @@ int fmm2d_export(const fmm2d_plan* P, int what, int level, void* dst, size_t* by
             s[12] = (double)launch_count();
             s[13] = (double)P->stats.p2p_pairs;
             s[14] = (double)P->stats.tree_key64;
+            s[15] = (double)P->stats.dev_bytes;
             off = need;
             break;
         }

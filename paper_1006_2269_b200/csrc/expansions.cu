@@ -32,6 +32,7 @@ namespace fmm2d {
 constexpr int M2L_CS = FMM2D_M2L_CS, M2L_KOFF = FMM2D_M2L_KOFF;
 static_assert(M2L_CS + M2L_KOFF >= FMM2D_PMAX + 1, "row stride of the M2L matrix");
 __constant__ double c_m2l[(FMM2D_PMAX + 1) * M2L_CS + M2L_KOFF];
+
 __constant__ double c_pas[(FMM2D_PMAX + 1) * (FMM2D_PMAX + 1)];   // [a][b] = C(a, b)
 
 // exact binomials in 64-bit integers (C(63,31) < 2^64), correctly rounded to double
@@ -61,6 +62,7 @@ int upload_binomials(int p)
     for (int a = 0; a <= FMM2D_PMAX; ++a)
         for (int b = 0; b <= a; ++b) pas[a * S + b] = (double)binom_u64(a, b);
     FMM2D_CUDA_TRY(cudaMemcpyToSymbol(c_m2l, m2l.data(), sizeof(double) * m2l.size()));
+
     FMM2D_CUDA_TRY(cudaMemcpyToSymbol(c_pas, pas.data(), sizeof(double) * S * S));
     if (dev >= 0 && dev < 64) uploaded[dev] = true;
     return 0;
@@ -196,17 +198,22 @@ struct M2LArgs {
     int L;
     const double* cx;
     const double* cy;
-    const double2* mpole;
-    double2* local;
+    // per level: stored expansions (level-local box b at mpl[l] + b (p+1)) and the stored
+    // range [slo, shi) -- one GPU: every box; other sources are imported (mhalo + hmap)
+    const double2* mpl[FMM2D_MAXL + 1];
+    double2* lcl[FMM2D_MAXL + 1];
+    int64_t slo[FMM2D_MAXL + 1], shi[FMM2D_MAXL + 1];
+    const double2* mhalo;
+    const uint32_t* hmap;             // [global box id] import slot
 };
 
-// One weak pair: the multipole of source box s (global id) into coefficients l in
-// [L0, L1) of the local about (ctx, cty), accumulated into acc.
+// One weak pair: the multipole M of source box s (global id, for its centre) into
+// coefficients l in [L0, L1) of the local about (ctx, cty), accumulated into acc.
 template <int P, int L0, int L1>
-__device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, double ctx, double cty, double2 (&acc)[L1 - L0])
+__device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, const double2* __restrict__ M, double ctx,
+                                         double cty, double2 (&acc)[L1 - L0])
 {
     const double csx = A.cx[s], csy = A.cy[s];
-    const double2* M = A.mpole + s * (P + 1);
     // z0 = c_s - c_t and 1/z0
     const double dx = csx - ctx, dy = csy - cty;
     const double r2 = dx * dx + dy * dy;
@@ -263,8 +270,14 @@ __device__ __forceinline__ void m2l_accum(const M2LArgs& A, int64_t g, int lev, 
     const int64_t wbase = A.base[lev], xbase = lev > 0 ? A.base[lev - 1] : 0;
     const double ctx = A.cx[g], cty = A.cy[g];
     for (int64_t j = ja; j < jb; j += js) {
-        const int64_t s = (j < nw) ? wbase + widx[w0 + j] : xbase + xidx[x0 + (j - nw)];
-        m2l_pair<P, L0, L1>(A, s, ctx, cty, acc);
+        const bool cross = j >= nw;
+        const int sl = cross ? lev - 1 : lev;                       // the source's level
+        const uint32_t bs = cross ? xidx[x0 + (j - nw)] : widx[w0 + j];
+        const int64_t s = (cross ? xbase : wbase) + bs;
+        // stored multipole (own / replicated box), or an imported one (sharded plans' halo)
+        const double2* M = (bs >= A.slo[sl] && bs < A.shi[sl]) ? A.mpl[sl] + (int64_t)bs * (P + 1)
+                                                              : A.mhalo + (int64_t)A.hmap[s] * (P + 1);
+        m2l_pair<P, L0, L1>(A, s, M, ctx, cty, acc);
     }
 }
 
@@ -277,7 +290,7 @@ __device__ __forceinline__ void m2l_target(const M2LArgs& A, int64_t g, int lev)
 #pragma unroll
     for (int l = 0; l < L1 - L0; ++l) acc[l] = make_double2(0.0, 0.0);
     m2l_accum<P, L0, L1>(A, g, lev, b, 0, 1, acc);
-    double2* out = A.local + g * (P + 1);
+    double2* out = A.lcl[lev] + b * (P + 1);
 #pragma unroll
     for (int l = L0; l < L1; ++l) out[l] = acc[l - L0];
 }
@@ -300,7 +313,7 @@ __device__ __forceinline__ void m2l_target_warp(const M2LArgs& A, int64_t g, int
         }
     }
     if (lane == 0) {
-        double2* out = A.local + g * (P + 1);
+        double2* out = A.lcl[lev] + b * (P + 1);
 #pragma unroll
         for (int l = L0; l < L1; ++l) out[l] = acc[l - L0];
     }
@@ -434,7 +447,7 @@ int upward_p(fmm2d_plan* Pl)
     const int L = Pl->L;
     const int64_t l0 = Pl->box_lo(L), l1 = Pl->box_hi(L);
     k_p2m<P><<<grid_for(l1 - l0, 128), 128, 0, st>>>(l0, l1, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
-                                                    Pl->cy + Pl->base[L], Pl->mpole + Pl->base[L] * (P + 1),
+                                                    Pl->cy + Pl->base[L], Pl->mpl[L],
                                                     Pl->m_fused, Pl->perm);
     Pl->m_fused = nullptr;
     fmm2d::note_launch();
@@ -443,7 +456,7 @@ int upward_p(fmm2d_plan* Pl)
         const int64_t b0 = Pl->own_lo(l), b1 = Pl->own_hi(l);
         k_m2m<P><<<grid_for(4 * (b1 - b0), l2l_block<P>()), l2l_block<P>(), 0, st>>>(
             b0, b1, Pl->cx + Pl->base[l], Pl->cy + Pl->base[l], Pl->cx + Pl->base[l + 1], Pl->cy + Pl->base[l + 1],
-            Pl->mpole + Pl->base[l + 1] * (P + 1), Pl->mpole + Pl->base[l] * (P + 1)); fmm2d::note_launch();
+            Pl->mpl[l + 1], Pl->mpl[l]); fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
     }
     return 0;
@@ -459,7 +472,7 @@ int upward_top_p(fmm2d_plan* Pl)
         const int64_t nb = nboxes(l);
         k_m2m<P><<<grid_for(4 * nb, l2l_block<P>()), l2l_block<P>(), 0, st>>>(
             0, nb, Pl->cx + Pl->base[l], Pl->cy + Pl->base[l], Pl->cx + Pl->base[l + 1], Pl->cy + Pl->base[l + 1],
-            Pl->mpole + Pl->base[l + 1] * (P + 1), Pl->mpole + Pl->base[l] * (P + 1)); fmm2d::note_launch();
+            Pl->mpl[l + 1], Pl->mpl[l]); fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
     }
     return 0;
@@ -498,8 +511,14 @@ int m2l_p(fmm2d_plan* Pl)
     A.L = L;
     A.cx = Pl->cx;
     A.cy = Pl->cy;
-    A.mpole = Pl->mpole;
-    A.local = Pl->local;
+    for (int l = 0; l <= L; ++l) {
+        A.mpl[l] = Pl->mpl[l];
+        A.lcl[l] = Pl->lcl[l];
+        A.slo[l] = Pl->box_lo(l);
+        A.shi[l] = Pl->box_hi(l);
+    }
+    A.mhalo = Pl->mhalo;
+    A.hmap = Pl->hmap;
     // level-0 local is zero (no M2L at the root)
     FMM2D_CUDA_TRY(cudaMemsetAsync(Pl->local, 0, sizeof(double2) * (P + 1), st));
     constexpr int NS = m2l_split<P>();
@@ -524,7 +543,7 @@ int downward_p(fmm2d_plan* Pl)
         const int64_t c0 = Pl->box_lo(l), c1 = Pl->box_hi(l);
         k_l2l<P><<<grid_for(c1 - c0, l2l_block<P>()), l2l_block<P>(), 0, st>>>(
             c0, c1, Pl->cx + Pl->base[l - 1], Pl->cy + Pl->base[l - 1], Pl->cx + Pl->base[l], Pl->cy + Pl->base[l],
-            Pl->local + Pl->base[l - 1] * (P + 1), Pl->local + Pl->base[l] * (P + 1)); fmm2d::note_launch();
+            Pl->lcl[l - 1], Pl->lcl[l]); fmm2d::note_launch();
         FMM2D_CUDA_TRY(cudaGetLastError());
     }
     return 0;

@@ -51,6 +51,7 @@ struct Stats {
     int64_t weak_pairs = 0, strong_leaf_pairs = 0, p2p_pairs = 0;
     int max_leaf = 0, min_leaf = 0;
     int tree_key64 = 0;                // axes presorted with 64-bit keys (bit 0 x, bit 1 y)
+    int64_t dev_bytes = 0;             // device memory the plan holds (its allocations)
 };
 
 }  // namespace fmm2d
@@ -103,9 +104,24 @@ struct fmm2d_plan {
     uint32_t* near_split = nullptr;     // split leaves
     double4* near_part = nullptr;       // [segments][max_leaf] partial sums
     int64_t near_nseg = 0, near_nsplit = 0;
-    // expansions
-    double2* mpole = nullptr;           // [nbox_total][p+1]
-    double2* local = nullptr;           // [nbox_total][p+1]
+    // expansions.  Storage per level: every box of the replicated levels l <= kpart, the own
+    // boxes [own_lo(l), own_hi(l)) of the levels below (one GPU: every box of every level, in
+    // global box order, so mpole + g (p+1) is box g).  mpl[l] / lcl[l] point such that
+    // mpl[l] + b (p+1) is level-l box b for every STORED b (a per-level virtual base).
+    double2* mpole = nullptr;           // storage (one GPU: [nbox_total][p+1])
+    double2* local = nullptr;
+    double2* mpl[FMM2D_MAXL + 1] = {};
+    double2* lcl[FMM2D_MAXL + 1] = {};
+    // sharded plans: halo multipoles live in the import buffer (shard->mp.recv, slot = import
+    // order); hmap[global box id] = the slot of an imported box
+    const double2* mhalo = nullptr;
+    uint32_t* hmap = nullptr;
+    // sharded plans: source rows / input indices of the own positions only (src, perm are
+    // virtual bases: src[k] valid for k in [pos0, pos1)); halo leaves' rows in hsrc / hperm,
+    // leaf lf of the halo at hsrc + lmap[lf] (lmap = ~0 for every other leaf)
+    double4* hsrc = nullptr;
+    uint32_t* hperm = nullptr;
+    uint32_t* lmap = nullptr;
     // staging for FMM2D_HOST_PTRS
     double2* mstage = nullptr;
     // strengths (input order) whose gather into the source rows is left to P2M, which reads

@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                                                  const uint32_t* __restrict__ perm, const fm::Tables* __restrict__ gtab,
                                                  double2* __restrict__ phi, double2* __restrict__ dphi,
                                                  const int64_t* __restrict__ m2p_off, const double4* __restrict__ m2p_acc,
-                                                 double4* __restrict__ nacc)
+                                                 double4* __restrict__ nacc, const uint32_t* __restrict__ lmap,
+                                                 const double4* __restrict__ hsrc)
 {
     __shared__ double4 S[(NEAR_CHUNK > NEAR_TPT * NEAR_T) ? NEAR_CHUNK : NEAR_TPT * NEAR_T];
     __shared__ fm::Tables T;
@@ -230,12 +231,14 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
             const int nl = cinfo[0];
             for (int l = warp; l < nl; l += NEAR_T / 32) {
                 const uint32_t lf = sidx[q + l];
-                const uint32_t s0 = off[lf];
+                // own / replicated leaf: rows at its position; halo leaf (sharded plans): in hsrc
+                const uint32_t hm = lmap ? lmap[lf] : 0xFFFFFFFFu;
+                const double4* __restrict__ sp = (hm != 0xFFFFFFFFu) ? hsrc + hm : src + off[lf];
                 const int c0 = cstart[l], sz = cstart[l + 1] - c0;
 #ifndef FMM2D_NEAR_EXP_NOSTAGE
-                for (int e = lane; e < sz; e += 32) S[c0 + e] = src[s0 + e];
+                for (int e = lane; e < sz; e += 32) S[c0 + e] = sp[e];
 #else
-                (void)s0; (void)c0; (void)sz;              // timing experiment only: rows not staged
+                (void)sp; (void)c0; (void)sz;              // timing experiment only: rows not staged
 #endif
             }
             __syncthreads();
@@ -405,7 +408,9 @@ __global__ void __launch_bounds__(NEAR_T) k_near_wide(int p, int64_t t0, const u
                                                       const uint32_t* __restrict__ perm,
                                                       const fm::Tables* __restrict__ gtab, double2* __restrict__ phi,
                                                       double2* __restrict__ dphi, const int64_t* __restrict__ m2p_off,
-                                                      const double4* __restrict__ m2p_acc)
+                                                      const double4* __restrict__ m2p_acc,
+                                                      const uint32_t* __restrict__ lmap,
+                                                      const double4* __restrict__ hsrc)
 {
     __shared__ fm::Tables T;
     load_tables(T, gtab);
@@ -417,9 +422,11 @@ __global__ void __launch_bounds__(NEAR_T) k_near_wide(int p, int64_t t0, const u
         PairAcc acc;
         for (int64_t q = soff[t]; q < soff[t + 1]; ++q) {
             const uint32_t lf = sidx[q];
+            const uint32_t hm = lmap ? lmap[lf] : 0xFFFFFFFFu;
+            const double4* __restrict__ sp = (hm != 0xFFFFFFFFu) ? hsrc + hm - off[lf] : src;   // indexed by position
             for (uint32_t j = off[lf]; j < off[lf + 1]; ++j) {
-                const double4 s = src[j];
-                const bool self = (j == i);
+                const double4 s = sp[j];
+                const bool self = (j == i) && (hm == 0xFFFFFFFFu);
                 pair<REAL>(acc, self ? 1.0 : me.x - s.x, self ? 0.0 : me.y - s.y, self ? 0.0 : s.z,
                            self ? 0.0 : s.w, T);
             }
@@ -811,7 +818,7 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi, int mode)
     const int64_t t0 = P->box_lo(L), nl = P->box_hi(L) - t0;    // own target leaves
     const double* cx = P->cx + P->base[L];
     const double* cy = P->cy + P->base[L];
-    const double2* loc = P->local + P->base[L] * (P->p + 1);
+    const double2* loc = P->lcl[L];
     const uint32_t* off = P->boff + P->obase[L];
     const bool real = (P->flags & FMM2D_REAL_STRENGTHS) != 0;
     const fm::Tables* tab = (const fm::Tables*)P->tables;
@@ -866,12 +873,12 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi, int mode)
             k_near<true><<<grid, NEAR_T, 0, P->stream>>>(G, P->p, t0, nl, P->near_seg_off, P->near_segs,
                                                         P->near_part, P->stats.max_leaf, off, P->near.off,
                                                         P->near.idx, P->src, cx, cy, loc, P->perm, tab, phi, dphi,
-                                                        m2p_off, P->rr_acc, nacc);
+                                                        m2p_off, P->rr_acc, nacc, P->lmap, P->hsrc);
         else
             k_near<false><<<grid, NEAR_T, 0, P->stream>>>(G, P->p, t0, nl, P->near_seg_off, P->near_segs,
                                                          P->near_part, P->stats.max_leaf, off, P->near.off,
                                                          P->near.idx, P->src, cx, cy, loc, P->perm, tab, phi, dphi,
-                                                         m2p_off, P->rr_acc, nacc);
+                                                         m2p_off, P->rr_acc, nacc, P->lmap, P->hsrc);
         if (P->near_nsplit > 0) {
             fmm2d::note_launch();
             FMM2D_CUDA_TRY(cudaGetLastError());
@@ -883,11 +890,11 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi, int mode)
         if (real)
             k_near_wide<true><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, t0, off, P->near.off, P->near.idx,
                                                                      P->src, cx, cy, loc, P->perm, tab, phi, dphi,
-                                                                     m2p_off, P->rr_acc);
+                                                                     m2p_off, P->rr_acc, P->lmap, P->hsrc);
         else
             k_near_wide<false><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, t0, off, P->near.off, P->near.idx,
                                                                       P->src, cx, cy, loc, P->perm, tab, phi, dphi,
-                                                                      m2p_off, P->rr_acc);
+                                                                      m2p_off, P->rr_acc, P->lmap, P->hsrc);
     }
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());

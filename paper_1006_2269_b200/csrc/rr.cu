@@ -184,7 +184,7 @@ int rr_p2l_p(fmm2d_plan* Pl)
     const int L = Pl->L;
     k_rr_p2l<P><<<(unsigned)Pl->rr_np2l, RR_T, 0, Pl->stream>>>(
         Pl->rr_p2l_leaves, Pl->rr_p2l.off, Pl->rr_p2l.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
-        Pl->cy + Pl->base[L], Pl->local + Pl->base[L] * (P + 1), static_cast<const fm::Tables*>(Pl->tables));
+        Pl->cy + Pl->base[L], Pl->lcl[L], static_cast<const fm::Tables*>(Pl->tables));
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     return 0;
@@ -197,7 +197,7 @@ int rr_m2p_p(fmm2d_plan* Pl)
     const int L = Pl->L;
     k_rr_m2p<P><<<(unsigned)Pl->rr_nm2p, RR_T, 0, Pl->stream>>>(
         Pl->rr_m2p_leaves, Pl->rr_m2p.off, Pl->rr_m2p.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
-        Pl->cy + Pl->base[L], Pl->mpole + Pl->base[L] * (P + 1), Pl->rr_acc, static_cast<const fm::Tables*>(Pl->tables));
+        Pl->cy + Pl->base[L], Pl->mpl[L], Pl->rr_acc, static_cast<const fm::Tables*>(Pl->tables));
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     return 0;

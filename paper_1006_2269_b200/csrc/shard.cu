@@ -190,57 +190,68 @@ __global__ void k_pack_rows(const uint32_t* __restrict__ ids, int64_t cnt, int s
     }
 }
 
+// the imported rows of halo leaf e (slot e of `slot` rows) into the halo row store; the
+// leaf's map entry lmap[leaf] = its first row there
 __global__ void k_unpack_rows(const uint32_t* __restrict__ ids, int64_t cnt, int slot, const uint32_t* __restrict__ off,
-                              const Row* __restrict__ in, double4* __restrict__ src, uint32_t* __restrict__ perm)
+                              const Row* __restrict__ in, double4* __restrict__ hsrc, uint32_t* __restrict__ hperm,
+                              uint32_t* __restrict__ lmap)
 {
     const int64_t e = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (e >= cnt) return;
-    const uint32_t s = ids[e], s0 = off[s], sz = off[s + 1] - s0;
+    const uint32_t s = ids[e], sz = off[s + 1] - off[s];
+    if (lane == 0) lmap[s] = (uint32_t)(e * slot);
     for (uint32_t j = lane; j < sz; j += 32) {
         const Row r = in[e * slot + j];
-        src[s0 + j] = make_double4(r.x, r.y, 0.0, 0.0);
-        perm[s0 + j] = r.idx;
+        hsrc[e * slot + j] = make_double4(r.x, r.y, 0.0, 0.0);
+        hperm[e * slot + j] = r.idx;
     }
 }
 
 // strengths of the halo leaves, gathered locally through the imported input indices
-__global__ void k_gather_halo(const uint32_t* __restrict__ ids, int64_t cnt, const uint32_t* __restrict__ off,
-                              const uint32_t* __restrict__ perm, const double2* __restrict__ m,
-                              double4* __restrict__ src)
+__global__ void k_gather_halo(const uint32_t* __restrict__ ids, int64_t cnt, int slot, const uint32_t* __restrict__ off,
+                              const uint32_t* __restrict__ hperm, const double2* __restrict__ m,
+                              double4* __restrict__ hsrc)
 {
     const int64_t e = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (e >= cnt) return;
-    const uint32_t s = ids[e], s0 = off[s], sz = off[s + 1] - s0;
+    const uint32_t s = ids[e], sz = off[s + 1] - off[s];
     for (uint32_t j = lane; j < sz; j += 32) {
-        const double2 v = m[perm[s0 + j]];
-        double4 r = src[s0 + j];
+        const double2 v = m[hperm[e * slot + j]];
+        double4 r = hsrc[e * slot + j];
         r.z = v.x;
         r.w = v.y;
-        src[s0 + j] = r;
+        hsrc[e * slot + j] = r;
     }
 }
 
-// multipoles (P1 complex each) by global box id: pack (gather) / unpack (scatter)
-__global__ void k_pack_mp(const uint32_t* __restrict__ ids, int64_t cnt, int P1, const double2* __restrict__ mp,
+// the stored expansions of every level (level l's box b at mp[l] + b P1) by global box id
+struct LevelPtrs {
+    const double2* mp[FMM2D_MAXL + 1];
+    int64_t base[FMM2D_MAXL + 2];
+    int L;
+};
+
+// exported multipoles (own boxes, P1 complex each) by global box id into the send buffer
+__global__ void k_pack_mp(const uint32_t* __restrict__ ids, int64_t cnt, int P1, LevelPtrs M,
                           double2* __restrict__ out)
 {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= cnt * P1) return;
     const int64_t e = t / P1;
     const int k = (int)(t - e * P1);
-    out[t] = mp[(int64_t)ids[e] * P1 + k];
+    const int64_t g = ids[e];
+    int l = 0;
+    while (l < M.L && g >= M.base[l + 1]) ++l;
+    out[t] = M.mp[l][(g - M.base[l]) * P1 + k];
 }
 
-__global__ void k_unpack_mp(const uint32_t* __restrict__ ids, int64_t cnt, int P1, const double2* __restrict__ in,
-                            double2* __restrict__ mp)
+// import slot of every imported box (the receive buffer is the halo multipoles' store)
+__global__ void k_halo_map(const uint32_t* __restrict__ ids, int64_t cnt, uint32_t* __restrict__ hmap)
 {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= cnt * P1) return;
-    const int64_t e = t / P1;
-    const int k = (int)(t - e * P1);
-    mp[(int64_t)ids[e] * P1 + k] = in[t];
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < cnt) hmap[ids[e]] = (uint32_t)e;
 }
 
 __global__ void k_max_into(double* __restrict__ dst, const double* __restrict__ src, int64_t n)
@@ -513,15 +524,33 @@ static int pack_rows(fmm2d_plan* P)
     return 0;
 }
 
+// the halo stores (rows + input indices of the imported leaves, the imported multipoles'
+// slots) -- allocated for the import counts only, never for all n points / all boxes
 static int unpack_rows(fmm2d_plan* P)
 {
     const XSet& X = P->shard->leaf;
-    if (X.imp_tot == 0) return 0;
-    const uint32_t* off = P->boff + P->obase[P->L];
-    k_unpack_rows<<<grid_for(X.imp_tot * 32, 256), 256, 0, P->stream>>>(X.imp_ids, X.imp_tot, P->shard->slot, off,
-                                                                       (const Row*)X.recv, P->src, P->perm);
-    note_launch();
-    FMM2D_CUDA_TRY(cudaGetLastError());
+    const int slot = P->shard->slot;
+    const int64_t nl = nboxes(P->L);
+    FMM2D_TRY(dev_alloc(P, (void**)&P->lmap, sizeof(uint32_t) * nl));
+    FMM2D_CUDA_TRY(cudaMemsetAsync(P->lmap, 0xFF, sizeof(uint32_t) * nl, P->stream));
+    FMM2D_TRY(dev_alloc(P, (void**)&P->hsrc, sizeof(double4) * std::max<int64_t>(X.imp_tot * slot, 1)));
+    FMM2D_TRY(dev_alloc(P, (void**)&P->hperm, sizeof(uint32_t) * std::max<int64_t>(X.imp_tot * slot, 1)));
+    if (X.imp_tot > 0) {
+        const uint32_t* off = P->boff + P->obase[P->L];
+        k_unpack_rows<<<grid_for(X.imp_tot * 32, 256), 256, 0, P->stream>>>(X.imp_ids, X.imp_tot, slot, off,
+                                                                           (const Row*)X.recv, P->hsrc, P->hperm,
+                                                                           P->lmap);
+        note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    }
+    const XSet& Y = P->shard->mp;
+    FMM2D_TRY(dev_alloc(P, (void**)&P->hmap, sizeof(uint32_t) * std::max<int64_t>(P->nbox_total, 1)));
+    if (Y.imp_tot > 0) {
+        k_halo_map<<<grid_for(Y.imp_tot, 256), 256, 0, P->stream>>>(Y.imp_ids, Y.imp_tot, P->hmap);
+        note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    }
+    P->mhalo = (const double2*)Y.recv;
     return 0;
 }
 
@@ -617,8 +646,8 @@ int shard_gather_halo(fmm2d_plan* P, const double2* m)
     const XSet& X = P->shard->leaf;
     if (X.imp_tot == 0) return 0;
     const uint32_t* off = P->boff + P->obase[P->L];
-    k_gather_halo<<<grid_for(X.imp_tot * 32, 256), 256, 0, P->stream>>>(X.imp_ids, X.imp_tot, off, P->perm, m,
-                                                                       P->src);
+    k_gather_halo<<<grid_for(X.imp_tot * 32, 256), 256, 0, P->stream>>>(X.imp_ids, X.imp_tot, P->shard->slot, off,
+                                                                       P->hperm, m, P->hsrc);
     note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     return 0;
@@ -630,8 +659,7 @@ int shard_comm_top(fmm2d_plan* const* Ps, int np)
     fmm2d_plan* P0 = Ps[0];
     const int k = P0->kpart;
     const size_t part = sizeof(double2) * (P0->p + 1) * (size_t)(nboxes(k) / P0->nranks);
-    const int64_t b = P0->base[k] * (P0->p + 1);
-    return allgather_inplace(Ps, np, part, [b](fmm2d_plan* P) { return (void*)(P->mpole + b); });
+    return allgather_inplace(Ps, np, part, [k](fmm2d_plan* P) { return (void*)P->mpl[k]; });   // level k: all boxes stored
 }
 
 int shard_pack_mp(fmm2d_plan* P)
@@ -639,8 +667,11 @@ int shard_pack_mp(fmm2d_plan* P)
     const XSet& X = P->shard->mp;
     if (X.exp_tot == 0) return 0;
     const int P1 = P->p + 1;
-    k_pack_mp<<<grid_for(X.exp_tot * P1, 256), 256, 0, P->stream>>>(X.exp_ids, X.exp_tot, P1, P->mpole,
-                                                                    (double2*)X.send);
+    LevelPtrs M;
+    M.L = P->L;
+    for (int l = 0; l <= P->L; ++l) M.mp[l] = P->mpl[l];
+    for (int l = 0; l <= P->L + 1; ++l) M.base[l] = P->base[l];
+    k_pack_mp<<<grid_for(X.exp_tot * P1, 256), 256, 0, P->stream>>>(X.exp_ids, X.exp_tot, P1, M, (double2*)X.send);
     note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     return 0;
@@ -648,15 +679,10 @@ int shard_pack_mp(fmm2d_plan* P)
 
 int shard_comm_mp(fmm2d_plan* const* Ps, int np) { return exchange(Ps, np, &Shard::mp, false); }
 
+// the imported multipoles stay in the receive buffer, which M2L reads through hmap
 int shard_unpack_mp(fmm2d_plan* P)
 {
-    const XSet& X = P->shard->mp;
-    if (X.imp_tot == 0) return 0;
-    const int P1 = P->p + 1;
-    k_unpack_mp<<<grid_for(X.imp_tot * P1, 256), 256, 0, P->stream>>>(X.imp_ids, X.imp_tot, P1,
-                                                                      (const double2*)X.recv, P->mpole);
-    note_launch();
-    FMM2D_CUDA_TRY(cudaGetLastError());
+    (void)P;
     return 0;
 }
 

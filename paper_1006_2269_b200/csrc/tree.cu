@@ -1486,15 +1486,19 @@ int build_tree(fmm2d_plan* P, const double2* z)
     void* scratch = nullptr;
     size_t s32 = 0, s64 = 0, sd = 0, scan_bytes = 0;
     const int64_t npmax = (L > 0) ? 2 * nboxes(L - 1) : 1;        // parents of the widest step
-    const int64_t ntiles = (n + PTILE - 1) / PTILE;
+    // a partitioned build keeps only its own positions [pos0, pos1) in the position-indexed
+    // arrays (virtual bases), and presorts one own level-k box at a time (at most mmax points)
+    const int64_t nown = (int64_t)P->pos1 - (int64_t)P->pos0;
+    const int64_t mmax = (P->nranks == 1) ? n : (n + nboxes(P->kpart) - 1) / nboxes(P->kpart);
+    const int64_t ntiles = (nown + PTILE - 1) / PTILE;
     int nbits = 1;
-    while (((int64_t)1 << nbits) < n) ++nbits;
+    while (((int64_t)1 << nbits) < mmax) ++nbits;
     cub::DeviceRadixSort::SortPairs(nullptr, s32, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint64_t*)nullptr,
-                                    (uint64_t*)nullptr, (int)n, 0, 32, st);
+                                    (uint64_t*)nullptr, (int)mmax, 0, 32, st);
     cub::DeviceRadixSort::SortPairs(nullptr, s64, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint64_t*)nullptr,
-                                    (uint64_t*)nullptr, (int)n, 0, 64, st);
+                                    (uint64_t*)nullptr, (int)mmax, 0, 64, st);
     cub::DeviceRadixSort::SortPairs(nullptr, sd, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                    (uint32_t*)nullptr, (int)n, 0, nbits, st);
+                                    (uint32_t*)nullptr, (int)mmax, 0, nbits, st);
     cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                   (int)std::max<int64_t>(npmax, ntiles), st);
     const size_t cub_bytes = std::max(std::max(s32, s64), std::max(sd, scan_bytes));
@@ -1512,13 +1516,13 @@ int build_tree(fmm2d_plan* P, const double2* z)
     int rc = 0;
     do {
         if ((rc = talloc((void**)&zc, 16 * n))) break;
-        if ((rc = talloc((void**)&k32a, 4 * n))) break;
-        if ((rc = talloc((void**)&k32b, 4 * n))) break;
-        if ((rc = talloc((void**)&u32a, 4 * n))) break;
-        if ((rc = talloc((void**)&u32b, 4 * n))) break;
-        if ((rc = talloc((void**)&v64a, 8 * n))) break;
-        if ((rc = talloc((void**)&vx, 8 * n))) break;
-        if ((rc = talloc((void**)&vy, 8 * n))) break;
+        if ((rc = talloc((void**)&k32a, 4 * mmax))) break;
+        if ((rc = talloc((void**)&k32b, 4 * mmax))) break;
+        if ((rc = talloc((void**)&u32a, 4 * n))) break;       // also x ranks by input index (64-bit y path)
+        if ((rc = talloc((void**)&u32b, 4 * mmax))) break;
+        if ((rc = talloc((void**)&v64a, 8 * mmax))) break;
+        if ((rc = talloc((void**)&vx, 8 * nown))) break;
+        if ((rc = talloc((void**)&vy, 8 * nown))) break;
         if ((rc = talloc((void**)&hs, 4 * npmax))) break;
         if ((rc = talloc((void**)&Gp, 4 * npmax))) break;
         if ((rc = talloc((void**)&spl, 4 * npmax))) break;
@@ -1526,14 +1530,19 @@ int build_tree(fmm2d_plan* P, const double2* z)
         if ((rc = talloc((void**)&tcnt, 4 * (ntiles + 1)))) break;
         if ((rc = talloc((void**)&tpre, 4 * (ntiles + 1)))) break;
         if ((rc = talloc((void**)&tstate, 8 * ntiles))) break;
-        if ((rc = talloc((void**)&xl, sizeof(uint2) * n))) break;
-        if ((rc = talloc((void**)&yl, sizeof(uint2) * n))) break;
-        if ((rc = talloc((void**)&tmp, sizeof(uint2) * n))) break;
+        if ((rc = talloc((void**)&xl, sizeof(uint2) * nown))) break;
+        if ((rc = talloc((void**)&yl, sizeof(uint2) * nown))) break;
+        if ((rc = talloc((void**)&tmp, sizeof(uint2) * nown))) break;
         if ((rc = talloc((void**)&bnd, sizeof(Bounds)))) break;
         if ((rc = talloc((void**)&ovf, 2 * sizeof(int)))) break;
         if ((rc = talloc(&scratch, cub_bytes))) break;
     } while (0);
     if (rc) { tfree(); return rc; }
+    vx -= P->pos0;                          // position-indexed: virtual bases
+    vy -= P->pos0;
+    xl -= P->pos0;
+    yl -= P->pos0;
+    tmp -= P->pos0;
     k64a = k64b = nullptr;                  // 64-bit keys of the fallback: allocated when needed
 
     Bounds hall;                            // host copy of the global ranges (partitioned top levels)

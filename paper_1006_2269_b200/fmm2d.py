@@ -42,7 +42,7 @@ EXPORT_PERM, EXPORT_OFFSETS, EXPORT_DISCS, EXPORT_STRONG, EXPORT_WEAK, EXPORT_MP
 SYMBOLS = ["fmm2d_default_options", "fmm2d_build", "fmm2d_eval", "fmm2d_eval_timed", "fmm2d_launch_count",
            "fmm2d_free", "fmm2d_strerror", "fmm2d_last_error_detail", "fmm2d_plan_info", "fmm2d_export",
            "fmm2d_nccl_unique_id", "fmm2d_partition_info", "fmm2d_build_shards", "fmm2d_eval_shards",
-           "fmm2d_halo_info", "fmm2d_build_eval", "fmm2d_reserve", "fmm2d_pool_trim"]
+           "fmm2d_halo_info", "fmm2d_build_eval", "fmm2d_reserve", "fmm2d_pool_trim", "fmm2d_pool_usage"]
 
 
 class Options(ctypes.Structure):
@@ -98,6 +98,8 @@ def lib():
         L.fmm2d_build_eval.argtypes = [vp, vp, ctypes.c_int64, ctypes.POINTER(Options), vp, vp, ctypes.POINTER(vp)]
         L.fmm2d_reserve.argtypes = [ctypes.c_int, ctypes.c_size_t]
         L.fmm2d_pool_trim.argtypes = [ctypes.c_int, ctypes.c_size_t]
+        L.fmm2d_pool_usage.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                                       ctypes.c_int]
         _lib = L
     return _lib
 
@@ -184,6 +186,16 @@ def pool_trim(keep_bytes: int = 0, device: int | None = None) -> None:
     if device is None:
         device = torch.cuda.current_device()
     _check(lib().fmm2d_pool_trim(int(device), int(keep_bytes)), "fmm2d_pool_trim")
+
+
+def pool_usage(reset: bool = False, device: int | None = None) -> tuple:
+    """fmm2d_pool_usage: (bytes in use, high-water bytes) of the library pool on `device`."""
+    import torch
+    if device is None:
+        device = torch.cuda.current_device()
+    u, h = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().fmm2d_pool_usage(int(device), ctypes.byref(u), ctypes.byref(h), int(reset)), "fmm2d_pool_usage")
+    return u.value, h.value
 
 
 class Fmm2d:
@@ -368,7 +380,7 @@ class Fmm2d:
     def stats(self) -> dict:
         s = np.frombuffer(self._export(EXPORT_STATS), np.float64)
         keys = ["n", "L", "p", "theta", "weak_pairs", "strong_leaf_pairs", "min_leaf", "max_leaf",
-                "t_build_ms", "t_tree_ms", "t_lists_ms", "nboxes", "launches", "p2p_pairs", "tree_key64"]
+                "t_build_ms", "t_tree_ms", "t_lists_ms", "nboxes", "launches", "p2p_pairs", "tree_key64", "dev_bytes"]
         return {k: float(v) for k, v in zip(keys, s)}
 
     def close(self):
