@@ -315,6 +315,7 @@ def main():
     ap.add_argument("--rr-exchange", action="store_true", help="FMM2D_RR_EXCHANGE (P:370-377; one GPU)")
     ap.add_argument("--parent-merge", action="store_true", help="FMM2D_PARENT_MERGE (P:364-370)")
     ap.add_argument("--symmetric-p2p", action="store_true", help="FMM2D_SYMMETRIC_P2P (one GPU)")
+    ap.add_argument("--overlap", action="store_true", help="FMM2D_OVERLAP: expansions concurrent with P2P (one GPU)")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.config]
     if args.n:
@@ -359,6 +360,8 @@ def main():
         shard_kw["parent_merge"] = True
     if args.symmetric_p2p:
         shard_kw["symmetric_p2p"] = True
+    if args.overlap:
+        shard_kw["overlap"] = True
     z = torch.from_numpy(z_np).to(dev)
     m = torch.from_numpy(m_np).to(dev)
     real = cfg.strengths == "real"

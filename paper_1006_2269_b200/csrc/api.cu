@@ -475,7 +475,19 @@ static int eval_impl(fmm2d_plan* const* Ps, int np, const double* m, double* phi
         FMM2D_CUDA_TRY(cudaEventRecord(P0->ev_gather, user));
         FMM2D_CUDA_TRY(cudaStreamWaitEvent(P0->side, P0->ev_gather, 0));
         P0->stream = P0->side;
+        // M2L keeps FMM2D_OVERLAP_M2L_WARPS warps per SM (default 2) so that the P2P CTAs
+        // can co-reside with it
+        {
+            static int wps = [] {
+                const char* e = getenv("FMM2D_OVERLAP_M2L_WARPS");
+                return e ? atoi(e) : 2;
+            }();
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P0->device);
+            P0->m2l_cap = (int64_t)sms * std::max(1, wps);
+        }
         const int rc = expansions();
+        P0->m2l_cap = 0;
         P0->stream = user;
         FMM2D_TRY(rc);
         FMM2D_CUDA_TRY(cudaEventRecord(P0->ev_exp, P0->side));

@@ -81,8 +81,11 @@ __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 
 // children per block of k_m2m / k_l2l (their expansions staged in shared memory, <= 48 KB)
+#ifndef FMM2D_L2L_BLOCK
+#define FMM2D_L2L_BLOCK 128
+#endif
 template <int P>
-__host__ __device__ constexpr int l2l_block() { return (P + 2) * 16 * 128 <= 48 * 1024 ? 128 : 64; }
+__host__ __device__ constexpr int l2l_block() { return (P + 2) * 16 * FMM2D_L2L_BLOCK <= 48 * 1024 ? FMM2D_L2L_BLOCK : 64; }
 
 // ---------------------------------------------------------------- P2M (A4)
 template <int P>
@@ -364,6 +367,39 @@ __global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l(M2LArgs A)
     }
 }
 
+// The same work as k_m2l from a CAPPED grid of single-warp blocks, grid-stride over the warp
+// rounds: used when the expansions run concurrently with the near field (FMM2D_OVERLAP), so
+// that M2L keeps only a few warps per SM and the P2P CTAs fill the rest of each SM.
+template <int P, int NS>
+__global__ void __launch_bounds__(32, 1) k_m2l_gs(M2LArgs A, int64_t nwarps)
+{
+    const int lane = threadIdx.x & 31;
+    constexpr int H = (P + NS) / NS;
+    constexpr int E1 = (2 * H < P + 1) ? 2 * H : P + 1;
+    constexpr int E2 = (3 * H < P + 1) ? 3 * H : P + 1;
+    for (int64_t warp = blockIdx.x; warp < nwarps; warp += gridDim.x) {
+        const int part = (int)(warp % NS);
+        const int64_t w = (warp / NS) * 32 + lane;
+        if (w >= A.pre[A.L + 1]) continue;
+        int lev = 1;
+        while (lev < A.L && w >= A.pre[lev + 1]) ++lev;
+        const int64_t g = A.base[lev] + A.order[w];
+        const int64_t b = g - A.base[lev];
+        const int64_t len = A.woff[lev][b + 1] - A.woff[lev][b] + (A.xoff[lev] ? A.xoff[lev][b + 1] - A.xoff[lev][b] : 0);
+        if (len > FMM2D_M2L_LONG) continue;
+        if constexpr (NS == 1) {
+            m2l_target<P, 0, P + 1>(A, g, lev);
+        } else if constexpr (NS == 2) {
+            if (part == 0) m2l_target<P, 0, H>(A, g, lev);
+            else           m2l_target<P, H, P + 1>(A, g, lev);
+        } else {
+            if (part == 0)      m2l_target<P, 0, H>(A, g, lev);
+            else if (part == 1) m2l_target<P, H, E1>(A, g, lev);
+            else                m2l_target<P, E1, E2>(A, g, lev);
+        }
+    }
+}
+
 // one warp (per coefficient part) per long-list target; long[] holds global box ids
 template <int P, int NS>
 __global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l_long(M2LArgs A, const uint32_t* __restrict__ longs,
@@ -524,7 +560,13 @@ int m2l_p(fmm2d_plan* Pl)
     constexpr int NS = m2l_split<P>();
     const int64_t work = A.pre[L + 1];
     int64_t nthreads = ((work + 31) / 32) * 32 * NS;
-    k_m2l<P, NS><<<grid_for(nthreads, M2L_T), M2L_T, 0, st>>>(A); fmm2d::note_launch();
+    if (Pl->m2l_cap > 0) {                      // concurrent with the near field: a capped grid
+        const int64_t nwarps = nthreads / 32;
+        k_m2l_gs<P, NS><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(Pl->m2l_cap, nwarps)), 32, 0, st>>>(A, nwarps);
+    } else {
+        k_m2l<P, NS><<<grid_for(nthreads, M2L_T), M2L_T, 0, st>>>(A);
+    }
+    fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
     if (Pl->m2l_nlong > 0) {
         k_m2l_long<P, NS><<<grid_for(Pl->m2l_nlong * NS * 32, M2L_T), M2L_T, 0, st>>>(A, Pl->m2l_long,

@@ -133,6 +133,7 @@ struct fmm2d_plan {
     // overlapped eval: the expansion chain on a high-priority side stream while k_near's
     // P2P runs on the plan's stream; k_near_final joins them
     bool overlap = false;
+    int64_t m2l_cap = 0;                // > 0: M2L from this many single-warp blocks (overlap)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_gather = nullptr, ev_exp = nullptr;
     double4* nacc = nullptr;            // [n] P2P sums (leaf order)

@@ -9,8 +9,8 @@
     run is profiles/r02/full_parity_C5.json, tools/full_parity.py); plus sampled outputs
     against the direct sum and properties that hold at any size (perm is a bijection, leaf
     sizes floor/ceil(N/4^L), finite outputs);
-  - C3 (1e6, clusters) and C4 (1e7, curve): tree, discs and lists of every level bit-exact
-    against the oracle, plus sampled outputs against the oracle's long-double direct sum.
+  - C3 (1e6, clusters) and C4 (1e7, curve): the same whole-problem comparison (every level,
+    every output), plus sampled outputs against the oracle's long-double direct sum.
 The direct-sum gate is BJ's: Re Phi (real m) within 1e-6 normwise and Phi' within the
 paper's a-priori law theta^{p+1}/(1-theta)^2 over the sampled targets.
 """
@@ -28,6 +28,16 @@ pytestmark = pytest.mark.gpu
 
 def _nerr(a, b):
     return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+TOL = 1e-12
+
+
+def _assert_whole(r):
+    assert r["levels_compared"] == list(range(r["L"] + 1))
+    for k in ("phi", "dphi"):
+        assert r[k]["norm"] <= TOL, (k, r[k])
+        assert r[k]["point"] <= TOL, (k, r[k])
 
 
 def _run(cfg_name, n=None):
@@ -68,20 +78,25 @@ def _structure_equal(gp, op, L, levels):
             np.testing.assert_array_equal(gi, oi)
 
 
-def test_c3_full_structure_and_sampled(orc):
+def test_c3_whole_problem_and_sampled(orc):
+    """BJ configs[2] (N = 1e6, ten clusters): every level's structure bit-exact, all outputs
+    within 1e-12 of the oracle FMM, sampled outputs within the gate of the direct sum."""
     c, z, m, plan, phi, dphi = _run("C3")
     assert plan.L == orc.nlevels(len(z), c.leaf_target) == 7
-    op = orc.plan(z, c.theta, plan.L)
-    _structure_equal(plan, op, plan.L, range(plan.L + 1))
     _sampled_direct(orc, z, m, phi, dphi, c.theta, c.p, M=64, seed=301)
+    del phi, dphi
+    plan.close()
+    _assert_whole(compare(z, m, c.theta, c.p, 7, real=True))
 
 
-def test_c4_full_structure_and_sampled(orc):
+def test_c4_whole_problem_and_sampled(orc):
+    """BJ configs[3] (N = 1e7 on the curve): as C3 -- all 10 levels, all outputs."""
     c, z, m, plan, phi, dphi = _run("C4")
     assert plan.L == 9
-    op = orc.plan(z, c.theta, plan.L)
-    _structure_equal(plan, op, plan.L, range(plan.L + 1))
     _sampled_direct(orc, z, m, phi, dphi, c.theta, c.p, M=32, seed=401)
+    del phi, dphi
+    plan.close()
+    _assert_whole(compare(z, m, c.theta, c.p, 9, real=True))
 
 
 def test_c5_full_sampled_and_properties(orc):
@@ -94,16 +109,6 @@ def test_c5_full_sampled_and_properties(orc):
     assert sizes.min() == n // 4 ** plan.L and sizes.max() == -(-n // 4 ** plan.L)
     assert torch.isfinite(torch.view_as_real(phi)).all() and torch.isfinite(torch.view_as_real(dphi)).all()
     _sampled_direct(orc, z, m, phi, dphi, c.theta, c.p, M=16, seed=501)
-
-
-TOL = 1e-12
-
-
-def _assert_whole(r):
-    assert r["levels_compared"] == list(range(r["L"] + 1))
-    for k in ("phi", "dphi"):
-        assert r[k]["norm"] <= TOL, (k, r[k])
-        assert r[k]["point"] <= TOL, (k, r[k])
 
 
 def test_c5_recipe_1e7_whole_problem_vs_oracle(orc):
