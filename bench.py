@@ -61,7 +61,7 @@ def p2p_flops_per_pair():
     pair of the library-math pair body (128 at C5-like |dz|).  Falls back to the survey's
     working estimate 105 if the census is missing."""
     c = census().get("libdevice_pair", {})
-    return float(c.get("flops_per_pair", 105.0)), (CENSUS if c else "SURVEY 8(d) working estimate")
+    return float(c.get("flops_per_pair", 105.0)), (os.path.relpath(CENSUS, ROOT) if c else "SURVEY 8(d) working estimate")
 # bounded CPU sample of a workload for the oracle: the C5 recipe at L = 8 (same leaf occupancy,
 # 23.8 points per leaf), build + eval passes repeated up to about 10 s of host work
 CPU_SAMPLE_N = 1_562_500
@@ -438,7 +438,7 @@ def main():
     if kn and "flops_per_pair" in kn:
         ex = pairs * kn["flops_per_pair"] / (near_ms / 1e3) / 1e12
         roof["executed"] = {"flops_per_pair": kn["flops_per_pair"], "tflops": ex, "frac_of_peak": ex / peak,
-                            "fp64_pipe_pct": kn.get("fp64_pipe_pct"), "source": CENSUS,
+                            "fp64_pipe_pct": kn.get("fp64_pipe_pct"), "source": os.path.relpath(CENSUS, ROOT),
                             "note": "the kernel's own executed FP64 flops (table-driven log/Arg/rcp need fewer "
                                     "than libdevice's); the FP64-pipe utilisation is clock-independent"}
     weak_pairs = st.get("weak_pairs", 0.0)
