@@ -93,7 +93,9 @@ extern "C" {
                                       the caller synchronises that stream before reading
                                       phi / dphi (fmm2d_free does).  Lets a caller keep two
                                       problems in flight on two streams (the copies of one
-                                      overlap the kernels of the other)                   */
+                                      overlap the kernels of the other).  On a plan made by
+                                      fmm2d_build_eval it covers that call's evaluation
+                                      only: later fmm2d_eval calls are synchronous      */
 #define FMM2D_TREE_GLOBAL_ONLY 0x10 /* diagnostic: every split step in global memory (no
                                       on-chip finish of the deepest levels; same tree)  */
 

@@ -369,7 +369,11 @@ int fmm2d_build_eval(const double* z, const double* m, int64_t n, const fmm2d_op
         FMM2D_TRY(dev_alloc(P, (void**)&P->phistage, sizeof(double2) * n));
         FMM2D_TRY(dev_alloc(P, (void**)&P->dphistage, sizeof(double2) * n));
         FMM2D_CUDA_TRY(cudaStreamWaitEvent(st, ev_m, 0));
-        return eval_impl(&P, 1, nullptr, phi, dphi, nullptr);   // m == nullptr: already staged
+        const int erc = eval_impl(&P, 1, nullptr, phi, dphi, nullptr);   // m == nullptr: already staged
+        // FMM2D_ASYNC_HOST applies to this call's evaluation only: later fmm2d_eval calls on
+        // the returned host plan are synchronous (their results are in phi / dphi on return)
+        P->flags &= ~FMM2D_ASYNC_HOST;
+        return erc;
     };
     int rc = body();
     if (dz) cudaFreeAsync(dz, bst ? bst : st);

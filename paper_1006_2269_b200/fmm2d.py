@@ -261,6 +261,7 @@ class Fmm2d:
             _check(L.fmm2d_build_eval(ctypes.c_void_p(zp), ctypes.c_void_p(mp), self.n, ctypes.byref(opt),
                                       ctypes.c_void_p(pp), ctypes.c_void_p(dp), ctypes.byref(h)),
                    "fmm2d_build_eval")
+            self.async_host = False             # FMM2D_ASYNC_HOST covered that evaluation only
         self._h = h
         n = ctypes.c_int64()
         nl = ctypes.c_int()
@@ -298,9 +299,10 @@ class Fmm2d:
     def eval(self, m, phi=None, dphi=None, want_phi: bool = True, want_dphi: bool = True):
         """Phi(z_i), Phi'(z_i) in input order.  Device plans: complex128 CUDA tensors,
         asynchronous on the plan's stream.  Host plans: numpy/pinned arrays, synchronous --
-        except with async_host=True (FMM2D_ASYNC_HOST, a property of the plan, also when it
-        came from build_eval), where the call returns once the copies are enqueued and the
-        results are valid after ``plan.stream.synchronize()``."""
+        except for a plan built with async_host=True (FMM2D_ASYNC_HOST), where the call
+        returns once the copies are enqueued and the results are valid after
+        ``plan.stream.synchronize()``.  A plan from build_eval(async_host=True) is async for
+        that call's evaluation only; its later eval calls are synchronous."""
         import torch
         if self._h is None:
             raise RuntimeError("plan freed")

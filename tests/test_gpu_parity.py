@@ -310,6 +310,11 @@ def test_async_host_two_problems_in_flight():
     for (ph, dh), ref in zip(out, (ref1, ref2, ref1)):
         np.testing.assert_array_equal(ph.numpy(), ref[0].numpy())
         np.testing.assert_array_equal(dh.numpy(), ref[1].numpy())
+    # FMM2D_ASYNC_HOST covered build_eval's own evaluation only: a later eval on the host
+    # plan is synchronous (results valid on return, no stream synchronisation)
+    ph2, dh2 = plans[1].eval(m2)
+    np.testing.assert_array_equal(np.asarray(ph2), ref2[0].numpy())
+    np.testing.assert_array_equal(np.asarray(dh2), ref2[1].numpy())
     for p_ in plans:
         p_.close()
 
