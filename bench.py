@@ -78,6 +78,40 @@ def _env_int(k, d):
         return d
 
 
+def hbm_peak():
+    """(GB/s, source): the measured copy bandwidth of MEASURED_PEAKS.json, else the
+    profiling recipe's fallback figure."""
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp["hbm_gbs"]), "MEASURED_PEAKS.json:hbm_gbs"
+    except Exception:
+        return 6544.0, "B200_PROFILING.md fallback"
+
+
+def build_algorithmic_bytes(n, L, weak, strong, nboxes):
+    """Algorithmic DRAM bytes of one fmm2d_build (rows A0-A3) -- what each build kernel must
+    read and write at least, by the data layout of DESIGN 6.1 (records of 8 B, radix sorts
+    of a 4-byte key + 8-byte payload in four 8-bit passes):
+      canonicalise z (16 B in, 16 B out); x / y keys + payloads (16 + 12, 8 + 12 B);
+      two stable radix sorts: 4 onesweep passes x (12 B in + 12 B out) + a 4-byte histogram
+      pass, run fix-up key scans (4 B); y-list + x-list (24 B, one 8-byte bucketing pass of
+      16 B, the scatter 16 B); 2 l0 global split steps of 16 B (8 B record in + out);
+      the on-chip levels (both lists in, the y-list out: 24 B); the final pass (y-list 8,
+      y-rank -> idx 8, coordinates 16 in; perm 4 + source row 32 out); lists: 12 B per
+      CSR entry (slot written + read, CSR written) + 24 B per box (disc)."""
+    l0 = L
+    for l in range(max(0, L - 4), L):
+        if -(-n // 4 ** l) <= 2048:
+            l0 = l
+            break
+    per_pt = {"canon": 32, "keys": 28 + 20, "radix_sorts": 2 * (4 * 24 + 4), "fix_runs": 8,
+              "lists_xy": 24 + 16 + 16, "split_steps": 2 * l0 * 16, "local_levels": 24 if l0 < L else 0,
+              "finish": 68}
+    comp = {k: float(v) * n for k, v in per_pt.items()}
+    comp["connectivity"] = 12.0 * (weak + strong) + 24.0 * nboxes
+    return comp, l0
+
+
 def fp64_peak():
     """(TFLOP/s, source).  MEASURED_PEAKS.json if it has an FP64 entry; else, for a path bound
     by plain FP64 ALU work, the peak derived from the unit counts and clock (B200_PROFILING.md:
@@ -443,6 +477,28 @@ def main():
                                     "than libdevice's); the FP64-pipe utilisation is clock-independent"}
     weak_pairs = st.get("weak_pairs", 0.0)
     m2l_tf = weak_pairs * M2L_FLOPS_PER_PAIR / (phase["m2l_ms"] / 1e3) / 1e12 if phase["m2l_ms"] > 0 else 0.0
+    # the M2L kernel against the same FP64 peak (algorithmic 1450 flop per pair, SURVEY 8(d);
+    # executed flops from the ncu census)
+    roof_m2l = None
+    if phase["m2l_ms"] > 0 and weak_pairs > 0:
+        km = cen.get("k_m2l", {})
+        roof_m2l = {"bound": "alu", "kernel": "k_m2l (M2L, every level)", "unit": "TFLOP/s", "peak": peak,
+                    "achieved": m2l_tf, "frac": m2l_tf / peak, "flops_per_pair": M2L_FLOPS_PER_PAIR,
+                    "pairs_per_launch": weak_pairs, "flop_convention": "4p(p+1) + 12p + 40 at p = 17 (SURVEY 8(d))"}
+        if "flops_per_pair" in km:
+            ex = weak_pairs * km["flops_per_pair"] / (phase["m2l_ms"] / 1e3) / 1e12
+            roof_m2l["executed"] = {"flops_per_pair": km["flops_per_pair"], "tflops": ex, "frac_of_peak": ex / peak,
+                                    "fp64_pipe_pct": km.get("fp64_pipe_pct"), "source": os.path.relpath(CENSUS, ROOT)}
+    # the build (rows A0-A3) against the HBM peak, on its algorithmic bytes
+    hbm, hbm_src = hbm_peak()
+    comp, l0 = build_algorithmic_bytes(cfg.n if world == 1 else cfg.n // world, L, weak_pairs,
+                                       st.get("strong_leaf_pairs", 0.0), st.get("nboxes", 0.0))
+    bbytes = sum(comp.values())
+    build_gbs = bbytes / (phase["build_ms"] / 1e3) / 1e9 if phase["build_ms"] > 0 else 0.0
+    roof_build = {"bound": "hbm", "kernels": "fmm2d_build (A0-A3: presort, split steps, on-chip levels, finish, lists)",
+                  "unit": "GB/s", "achieved": build_gbs, "peak": hbm, "frac": build_gbs / hbm, "peak_source": hbm_src,
+                  "algorithmic_bytes": bbytes, "components_bytes": comp, "global_split_levels": l0,
+                  "traffic": None, "traffic_note": "per-kernel ncu DRAM bytes: DESIGN.md 6.1 table"}
 
     # end to end through the C ABI with host (pinned) buffers
     e2e = None
@@ -475,7 +531,8 @@ def main():
                            "parallelism": f"subtrees{world}" if world > 1 else "single"},
                 "phases_ms": phase, "host_ms_per_step": host_ms / args.steps, "eval_only_points_per_s": cfg.n / (phase["eval_ms"] / 1e3),
                 "m2l_tflops": m2l_tf,
-                "roofline": roof, "gpu_launches": launches_per_step * args.steps,
+                "roofline": roof, "roofline_m2l": roof_m2l, "roofline_build": roof_build,
+                "gpu_launches": launches_per_step * args.steps,
                 "clocks": clk.summary(), "e2e": e2e,
                 "stats": {"weak_pairs": weak_pairs, "p2p_pairs": pairs, "min_leaf": st.get("min_leaf"),
                           "max_leaf": st.get("max_leaf")}}
