@@ -379,6 +379,9 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
+        # one line per rank on stderr (the JSON line stays rank 0's only stdout line)
+        print(f"bench.py: rank {rank} of {world} on cuda:{local_rank} ({torch.cuda.get_device_name(dev)}), "
+              f"NCCL process group up", file=sys.stderr, flush=True)
 
     def barrier():
         if world > 1:
