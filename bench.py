@@ -443,6 +443,7 @@ def main():
     barrier()
     ms = e0.elapsed_time(e1)
     st = plan.stats()
+    L = int(st.get("L", L))
     plan.close()
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:

@@ -25,6 +25,9 @@
 #ifndef FMM2D_NEAR_SPLIT
 #define FMM2D_NEAR_SPLIT 4096       // near lists with more source rows: split over several CTAs
 #endif
+#ifndef FMM2D_RR_SHORT
+#define FMM2D_RR_SHORT 8            // r/R exchange: P2L / M2P lists up to this long take a warp, longer a block
+#endif
 #ifndef FMM2D_M2L_LONG
 #define FMM2D_M2L_LONG 96           // weak lists longer than this: one warp per target (k_m2l_long)
 #endif
@@ -97,6 +100,8 @@ struct fmm2d_plan {
     uint32_t* rr_p2l_leaves = nullptr;  // leaves with a non-empty P2L / M2P list
     uint32_t* rr_m2p_leaves = nullptr;
     int64_t rr_np2l = 0, rr_nm2p = 0;
+    // short lists (<= FMM2D_RR_SHORT entries) at [0, *_short), long ones at [cap - (n - short), cap)
+    int64_t rr_np2l_short = 0, rr_nm2p_short = 0, rr_leaf_cap = 0;
     double4* rr_acc = nullptr;          // [n] M2P sums (leaf order; valid on leaves with M2P work)
     // long near lists split into segments of at most FMM2D_NEAR_SPLIT source rows
     int64_t* near_seg_off = nullptr;    // [leaves + 1] segments of each leaf (empty: not split)

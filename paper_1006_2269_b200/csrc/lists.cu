@@ -344,11 +344,17 @@ __global__ void k_long_lists(int64_t b0, int64_t b1, int64_t gbase, const int64_
 }
 
 // leaves with a non-empty list (compacted ids)
-__global__ void k_nonempty(int64_t t0, int64_t t1, const int64_t* __restrict__ off, uint32_t* __restrict__ out,
-                           unsigned int* __restrict__ n)
+// leaves with a non-empty list: those with at most short_max entries from the front of out
+// (count n[0]), the longer ones from the back (count n[1]; out has t1 - t0 slots)
+__global__ void k_nonempty(int64_t t0, int64_t t1, const int64_t* __restrict__ off, int64_t short_max,
+                           uint32_t* __restrict__ out, unsigned int* __restrict__ n)
 {
     const int64_t t = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < t1 && off[t + 1] > off[t]) out[atomicAdd(n, 1u)] = (uint32_t)t;
+    if (t >= t1) return;
+    const int64_t len = off[t + 1] - off[t];
+    if (len <= 0) return;
+    if (len <= short_max) out[atomicAdd(&n[0], 1u)] = (uint32_t)t;
+    else out[(t1 - t0) - 1 - atomicAdd(&n[1], 1u)] = (uint32_t)t;
 }
 
 // Long near lists (non-uniform inputs: a leaf can be strongly coupled to thousands of
@@ -472,19 +478,24 @@ static int build_rr_lists(fmm2d_plan* P)
                                                P->rr_m2p.idx, nl);
         note_launch();
         // leaves with P2L / M2P work (the order is irrelevant: each leaf is independent)
+        // (short lists from the front, long ones from the back: a warp or a block each, rr.cu)
         unsigned int* d_n = (unsigned int*)cnt;
-        FMM2D_CUDA_TRY(cudaMemsetAsync(d_n, 0, 2 * sizeof(unsigned int), st));
-        FMM2D_TRY(dev_alloc(P, (void**)&P->rr_p2l_leaves, sizeof(uint32_t) * std::max<int64_t>(t1 - t0, 1)));
-        FMM2D_TRY(dev_alloc(P, (void**)&P->rr_m2p_leaves, sizeof(uint32_t) * std::max<int64_t>(t1 - t0, 1)));
-        k_nonempty<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, P->rr_p2l.off, P->rr_p2l_leaves, d_n);
+        FMM2D_CUDA_TRY(cudaMemsetAsync(d_n, 0, 4 * sizeof(unsigned int), st));
+        const int64_t cap = std::max<int64_t>(t1 - t0, 1);
+        FMM2D_TRY(dev_alloc(P, (void**)&P->rr_p2l_leaves, sizeof(uint32_t) * cap));
+        FMM2D_TRY(dev_alloc(P, (void**)&P->rr_m2p_leaves, sizeof(uint32_t) * cap));
+        k_nonempty<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, P->rr_p2l.off, FMM2D_RR_SHORT, P->rr_p2l_leaves, d_n);
         note_launch();
-        k_nonempty<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, P->rr_m2p.off, P->rr_m2p_leaves, d_n + 1);
+        k_nonempty<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, P->rr_m2p.off, FMM2D_RR_SHORT, P->rr_m2p_leaves, d_n + 2);
         note_launch();
-        unsigned int h_n[2];
+        unsigned int h_n[4];
         FMM2D_CUDA_TRY(cudaMemcpyAsync(h_n, d_n, sizeof(h_n), cudaMemcpyDeviceToHost, st));
         FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
-        P->rr_np2l = h_n[0];
-        P->rr_nm2p = h_n[1];
+        P->rr_np2l = (int64_t)h_n[0] + h_n[1];
+        P->rr_nm2p = (int64_t)h_n[2] + h_n[3];
+        P->rr_np2l_short = h_n[0];
+        P->rr_nm2p_short = h_n[2];
+        P->rr_leaf_cap = cap;
         FMM2D_TRY(dev_alloc(P, (void**)&P->rr_acc, sizeof(double4) * P->n));
         return 0;
     };
@@ -528,8 +539,8 @@ static int build_near_segments(fmm2d_plan* P)
         note_launch();
         FMM2D_TRY(dev_alloc(P, (void**)&P->near_split, sizeof(uint32_t) * std::max<int64_t>(t1 - t0, 1)));
         unsigned int* d_n = (unsigned int*)cnt;
-        FMM2D_CUDA_TRY(cudaMemsetAsync(d_n, 0, sizeof(unsigned int), st));
-        k_nonempty<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, soff, P->near_split, d_n);
+        FMM2D_CUDA_TRY(cudaMemsetAsync(d_n, 0, 2 * sizeof(unsigned int), st));
+        k_nonempty<<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, soff, INT64_MAX, P->near_split, d_n);
         note_launch();
         unsigned int h_n = 0;
         FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_n, d_n, sizeof(h_n), cudaMemcpyDeviceToHost, st));

@@ -3,6 +3,8 @@
 // points, for the leaf pairs k_rr_lists moved out of the near field.  (Own translation unit:
 // the table-driven FP64 routines of fastmath.cuh carry __constant__ data that would share the
 // constant bank with M2L's transition matrix.)
+#include <algorithm>
+
 #include "fmm2d_internal.cuh"
 #include "fastmath.cuh"
 
@@ -27,6 +29,17 @@ __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_doub
 // log|.|, Arg and 1/|.|^2 by the table-driven routines of fastmath.cuh (tables in shared
 // memory, as in k_near), t_l = m iv^l by one complex product per l, b_l -= t_l / l.
 constexpr int RR_T = 128, RR_W = RR_T / 32;
+// Leaves with at most FMM2D_RR_SHORT list entries (most leaves; k_rr_lists' leaf arrays
+// hold them at the front): P2L a thread per leaf (k_rr_p2l_t), M2P a warp per leaf
+// (k_rr_m2p_w); longer lists (non-uniform inputs: up to thousands of entries, at the back
+// of the arrays): a block each (k_rr_p2l, k_rr_m2p).  C5 with the exchange: P2L + M2P
+// 16.3 -> 4.4 ms (a block per leaf left most warps idle and reloaded 8 KB of tables per leaf).
+#ifndef FMM2D_RR_WARP
+#define FMM2D_RR_WARP 1
+#endif
+#ifndef FMM2D_RR_P2L_THREAD
+#define FMM2D_RR_P2L_THREAD 1           // short P2L lists: a thread per leaf (else a warp)
+#endif
 
 __device__ __forceinline__ void rr_load_tables(fm::Tables& T, const fm::Tables* __restrict__ g)
 {
@@ -44,10 +57,10 @@ __global__ void __launch_bounds__(RR_T) k_rr_p2l(const uint32_t* __restrict__ le
 {
     __shared__ double2 part[RR_W][P + 1];
     __shared__ fm::Tables T;
+    const uint32_t t = leaves[blockIdx.x];
     rr_load_tables(T, gtab);
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t t = leaves[blockIdx.x];
     const double ctx = cx[t], cty = cy[t];
     double2 b[P + 1];
 #pragma unroll
@@ -116,8 +129,8 @@ __global__ void __launch_bounds__(RR_T) k_rr_m2p(const uint32_t* __restrict__ le
     __shared__ double4 part[RR_T];
     __shared__ double2 sA[RR_CH * E];
     __shared__ fm::Tables T;
-    rr_load_tables(T, gtab);
     const uint32_t t = leaves[blockIdx.x];
+    rr_load_tables(T, gtab);
     const uint32_t ts = boff[t];
     const int nt = (int)(boff[t + 1] - ts);
     const int64_t q0 = off[t], q1 = off[t + 1];
@@ -177,16 +190,203 @@ __global__ void __launch_bounds__(RR_T) k_rr_m2p(const uint32_t* __restrict__ le
     }
 }
 
+// Warp-per-leaf forms (FMM2D_RR_WARP, default): most leaves have one or two P2L / M2P
+// entries of ~24 sources, so a block per leaf left most of its warps idle and reloaded the
+// 8 KB of tables per leaf.  Here persistent blocks load the tables once and each warp takes
+// leaves in a grid-stride loop.  P2L: lanes over each entry's sources, the coefficients in
+// registers, one fixed-order shuffle reduction per leaf.  M2P: lanes over the leaf's points,
+// the entries in list order (multipole coefficients are warp-uniform loads).
+template <int P>
+__global__ void __launch_bounds__(RR_T) k_rr_p2l_w(const uint32_t* __restrict__ leaves, int64_t nleaves,
+                                                   const int64_t* __restrict__ off, const uint32_t* __restrict__ idx,
+                                                   const uint32_t* __restrict__ boff, const double4* __restrict__ src,
+                                                   const double* __restrict__ cx, const double* __restrict__ cy,
+                                                   double2* __restrict__ loc, const fm::Tables* __restrict__ gtab)
+{
+    __shared__ fm::Tables T;
+    rr_load_tables(T, gtab);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * RR_W;
+    for (int64_t li = (int64_t)blockIdx.x * RR_W + (threadIdx.x >> 5); li < nleaves; li += nw) {
+        const uint32_t t = leaves[li];
+        const double ctx = cx[t], cty = cy[t];
+        double2 b[P + 1];
+#pragma unroll
+        for (int l = 0; l <= P; ++l) b[l] = make_double2(0.0, 0.0);
+        for (int64_t q = off[t]; q < off[t + 1]; ++q) {
+            const uint32_t s = idx[q];
+            for (uint32_t j = boff[s] + lane; j < boff[s + 1]; j += 32) {
+                const double4 z = src[j];
+                const double2 m = make_double2(z.z, z.w);
+                const double ux = ctx - z.x, uy = cty - z.y;          // c - z_j
+                const double r2 = fma(ux, ux, uy * uy);
+                const double2 lg = make_double2(0.5 * fm::log_pos(r2, T.lg), fm::arg_t(ux, uy, T.at));
+                b[0] = cadd(b[0], cmul(m, lg));
+                const double vx = z.x - ctx, vy = z.y - cty;          // z_j - c
+                const double iv2 = fm::rcp(fma(vx, vx, vy * vy));
+                const double2 iv = make_double2(vx * iv2, -vy * iv2);
+                double2 tl = m;
+#pragma unroll
+                for (int l = 1; l <= P; ++l) {
+                    tl = cmul(tl, iv);                                 // m iv^l
+                    const double c = -1.0 / l;
+                    b[l].x = fma(c, tl.x, b[l].x);
+                    b[l].y = fma(c, tl.y, b[l].y);
+                }
+            }
+        }
+#pragma unroll
+        for (int l = 0; l <= P; ++l) {
+            for (int o = 16; o; o >>= 1) {
+                b[l].x += __shfl_xor_sync(0xffffffffu, b[l].x, o);
+                b[l].y += __shfl_xor_sync(0xffffffffu, b[l].y, o);
+            }
+        }
+        double2* Lc = loc + (int64_t)t * (P + 1);
+#pragma unroll
+        for (int l = 0; l <= P; ++l)
+            if (lane == (l & 31)) Lc[l] = cadd(Lc[l], b[l]);
+    }
+}
+
+// P2L, thread per leaf (short lists): the leaf's coefficients stay in the thread's registers
+// over all its entries' sources -- no cross-lane reduction (which cost more than the P2L
+// arithmetic of a leaf's one or two entries in the warp-per-leaf form).
+template <int P>
+__global__ void __launch_bounds__(RR_T) k_rr_p2l_t(const uint32_t* __restrict__ leaves, int64_t nleaves,
+                                                   const int64_t* __restrict__ off, const uint32_t* __restrict__ idx,
+                                                   const uint32_t* __restrict__ boff, const double4* __restrict__ src,
+                                                   const double* __restrict__ cx, const double* __restrict__ cy,
+                                                   double2* __restrict__ loc, const fm::Tables* __restrict__ gtab)
+{
+    __shared__ fm::Tables T;
+    rr_load_tables(T, gtab);
+    __syncthreads();
+    const int64_t li = (int64_t)blockIdx.x * RR_T + threadIdx.x;
+    if (li >= nleaves) return;
+    const uint32_t t = leaves[li];
+    const double ctx = cx[t], cty = cy[t];
+    double2 b[P + 1];
+#pragma unroll
+    for (int l = 0; l <= P; ++l) b[l] = make_double2(0.0, 0.0);
+    for (int64_t q = off[t]; q < off[t + 1]; ++q) {
+        const uint32_t s = idx[q];
+        for (uint32_t j = boff[s]; j < boff[s + 1]; ++j) {
+            const double4 z = src[j];
+            const double2 m = make_double2(z.z, z.w);
+            const double ux = ctx - z.x, uy = cty - z.y;              // c - z_j
+            const double r2 = fma(ux, ux, uy * uy);
+            const double2 lg = make_double2(0.5 * fm::log_pos(r2, T.lg), fm::arg_t(ux, uy, T.at));
+            b[0] = cadd(b[0], cmul(m, lg));
+            const double vx = z.x - ctx, vy = z.y - cty;              // z_j - c
+            const double iv2 = fm::rcp(fma(vx, vx, vy * vy));
+            const double2 iv = make_double2(vx * iv2, -vy * iv2);
+            double2 tl = m;
+#pragma unroll
+            for (int l = 1; l <= P; ++l) {
+                tl = cmul(tl, iv);                                     // m iv^l
+                const double c = -1.0 / l;
+                b[l].x = fma(c, tl.x, b[l].x);
+                b[l].y = fma(c, tl.y, b[l].y);
+            }
+        }
+    }
+    double2* Lc = loc + (int64_t)t * (P + 1);
+#pragma unroll
+    for (int l = 0; l <= P; ++l) Lc[l] = cadd(Lc[l], b[l]);
+}
+
+template <int P>
+__global__ void __launch_bounds__(RR_T) k_rr_m2p_w(const uint32_t* __restrict__ leaves, int64_t nleaves,
+                                                   const int64_t* __restrict__ off, const uint32_t* __restrict__ idx,
+                                                   const uint32_t* __restrict__ boff, const double4* __restrict__ src,
+                                                   const double* __restrict__ cx, const double* __restrict__ cy,
+                                                   const double2* __restrict__ mp, double4* __restrict__ acc,
+                                                   const fm::Tables* __restrict__ gtab)
+{
+    __shared__ fm::Tables T;
+    rr_load_tables(T, gtab);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * RR_W;
+    for (int64_t li = (int64_t)blockIdx.x * RR_W + (threadIdx.x >> 5); li < nleaves; li += nw) {
+        const uint32_t t = leaves[li];
+        const uint32_t ts = boff[t], te = boff[t + 1];
+        const int64_t q0 = off[t], q1 = off[t + 1];
+        for (uint32_t i = ts + lane; i < te; i += 32) {
+            const double4 z = src[i];
+            double2 f = make_double2(0.0, 0.0), df = make_double2(0.0, 0.0);
+            for (int64_t q = q0; q < q1; ++q) {
+                const uint32_t s = idx[q];
+                const double2* __restrict__ A = mp + (int64_t)s * (P + 1);
+                const double wx = z.x - cx[s], wy = z.y - cy[s];     // w = z_i - c_s
+                const double r2 = fma(wx, wx, wy * wy);
+                const double iw2 = fm::rcp(r2);
+                const double2 x = make_double2(wx * iw2, -wy * iw2);
+                double2 h = A[P], dh = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int k = P - 1; k >= 1; --k) {
+                    dh = cadd(cmul(dh, x), h);          // H'
+                    h = cadd(cmul(h, x), A[k]);         // H
+                }
+                const double2 d = cadd(h, cmul(x, dh)); // sum_k k a_k x^(k-1)
+                const double2 a0 = A[0];
+                const double2 lg = make_double2(0.5 * fm::log_pos(r2, T.lg), fm::arg_t(wx, wy, T.at));
+                f = cadd(f, cadd(cmul(a0, lg), cmul(h, x)));
+                df = cadd(df, csub(cmul(a0, x), cmul(d, cmul(x, x))));
+            }
+            acc[i] = make_double4(f.x, f.y, df.x, df.y);
+        }
+    }
+}
+
+// persistent grid: as many blocks as fit on the device at once (no second wave)
+template <typename K>
+static unsigned rr_grid(K kernel, int64_t nleaves)
+{
+    int dev = 0, sms = 148, nb = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, RR_T, 0) != cudaSuccess || nb < 1) nb = 1;
+    const int64_t need = (nleaves + RR_W - 1) / RR_W;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * nb));
+}
+
 template <int P>
 int rr_p2l_p(fmm2d_plan* Pl)
 {
     if (Pl->rr_np2l == 0) return 0;
     const int L = Pl->L;
-    k_rr_p2l<P><<<(unsigned)Pl->rr_np2l, RR_T, 0, Pl->stream>>>(
-        Pl->rr_p2l_leaves, Pl->rr_p2l.off, Pl->rr_p2l.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
-        Pl->cy + Pl->base[L], Pl->lcl[L], static_cast<const fm::Tables*>(Pl->tables));
-    fmm2d::note_launch();
-    FMM2D_CUDA_TRY(cudaGetLastError());
+    // short lists: a warp per leaf; long lists (at the back of the leaf array): a block each
+    const int64_t ns = FMM2D_RR_WARP ? Pl->rr_np2l_short : 0, nl = Pl->rr_np2l - Pl->rr_np2l_short;
+    if (ns > 0 && FMM2D_RR_P2L_THREAD) {
+        k_rr_p2l_t<P><<<(unsigned)((ns + RR_T - 1) / RR_T), RR_T, 0, Pl->stream>>>(
+            Pl->rr_p2l_leaves, ns, Pl->rr_p2l.off, Pl->rr_p2l.idx, Pl->boff + Pl->obase[L], Pl->src,
+            Pl->cx + Pl->base[L], Pl->cy + Pl->base[L], Pl->lcl[L], static_cast<const fm::Tables*>(Pl->tables));
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    } else if (ns > 0) {
+        k_rr_p2l_w<P><<<rr_grid(k_rr_p2l_w<P>, ns), RR_T, 0, Pl->stream>>>(
+            Pl->rr_p2l_leaves, ns, Pl->rr_p2l.off, Pl->rr_p2l.idx, Pl->boff + Pl->obase[L], Pl->src,
+            Pl->cx + Pl->base[L], Pl->cy + Pl->base[L], Pl->lcl[L], static_cast<const fm::Tables*>(Pl->tables));
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    }
+    if (!FMM2D_RR_WARP && Pl->rr_np2l_short > 0) {
+        k_rr_p2l<P><<<(unsigned)Pl->rr_np2l_short, RR_T, 0, Pl->stream>>>(
+            Pl->rr_p2l_leaves, Pl->rr_p2l.off, Pl->rr_p2l.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
+            Pl->cy + Pl->base[L], Pl->lcl[L], static_cast<const fm::Tables*>(Pl->tables));
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    }
+    if (nl > 0) {
+        k_rr_p2l<P><<<(unsigned)nl, RR_T, 0, Pl->stream>>>(
+            Pl->rr_p2l_leaves + (Pl->rr_leaf_cap - nl), Pl->rr_p2l.off, Pl->rr_p2l.idx, Pl->boff + Pl->obase[L],
+            Pl->src, Pl->cx + Pl->base[L], Pl->cy + Pl->base[L], Pl->lcl[L], static_cast<const fm::Tables*>(Pl->tables));
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    }
     return 0;
 }
 
@@ -195,11 +395,30 @@ int rr_m2p_p(fmm2d_plan* Pl)
 {
     if (Pl->rr_nm2p == 0) return 0;
     const int L = Pl->L;
-    k_rr_m2p<P><<<(unsigned)Pl->rr_nm2p, RR_T, 0, Pl->stream>>>(
-        Pl->rr_m2p_leaves, Pl->rr_m2p.off, Pl->rr_m2p.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
-        Pl->cy + Pl->base[L], Pl->mpl[L], Pl->rr_acc, static_cast<const fm::Tables*>(Pl->tables));
-    fmm2d::note_launch();
-    FMM2D_CUDA_TRY(cudaGetLastError());
+    const int64_t ns = FMM2D_RR_WARP ? Pl->rr_nm2p_short : 0, nl = Pl->rr_nm2p - Pl->rr_nm2p_short;
+    if (ns > 0) {
+        k_rr_m2p_w<P><<<rr_grid(k_rr_m2p_w<P>, ns), RR_T, 0, Pl->stream>>>(
+            Pl->rr_m2p_leaves, ns, Pl->rr_m2p.off, Pl->rr_m2p.idx, Pl->boff + Pl->obase[L], Pl->src,
+            Pl->cx + Pl->base[L], Pl->cy + Pl->base[L], Pl->mpl[L], Pl->rr_acc,
+            static_cast<const fm::Tables*>(Pl->tables));
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    }
+    if (!FMM2D_RR_WARP && Pl->rr_nm2p_short > 0) {
+        k_rr_m2p<P><<<(unsigned)Pl->rr_nm2p_short, RR_T, 0, Pl->stream>>>(
+            Pl->rr_m2p_leaves, Pl->rr_m2p.off, Pl->rr_m2p.idx, Pl->boff + Pl->obase[L], Pl->src, Pl->cx + Pl->base[L],
+            Pl->cy + Pl->base[L], Pl->mpl[L], Pl->rr_acc, static_cast<const fm::Tables*>(Pl->tables));
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    }
+    if (nl > 0) {
+        k_rr_m2p<P><<<(unsigned)nl, RR_T, 0, Pl->stream>>>(
+            Pl->rr_m2p_leaves + (Pl->rr_leaf_cap - nl), Pl->rr_m2p.off, Pl->rr_m2p.idx, Pl->boff + Pl->obase[L],
+            Pl->src, Pl->cx + Pl->base[L], Pl->cy + Pl->base[L], Pl->mpl[L], Pl->rr_acc,
+            static_cast<const fm::Tables*>(Pl->tables));
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+    }
     return 0;
 }
 
