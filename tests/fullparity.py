@@ -30,7 +30,10 @@ def errors(g, o, floor=PT_FLOOR):
             "point_q50": float(np.quantile(pw, 0.5)), "point_q99": float(np.quantile(pw, 0.99))}
 
 
-def compare(z, m, theta, p, L, real=True, levels=None, evaluate=True, log=print):
+def compare(z, m, theta, p, L, real=True, levels=None, evaluate=True, log=print, rr_exchange=False,
+            parent_merge=False):
+    """rr_exchange / parent_merge: the optional steps (R23, R25) on both
+    sides; their lists (leaf near / P2L / M2P, cross-level weak) are compared bit for bit too."""
     import torch
 
     import oracle
@@ -39,7 +42,8 @@ def compare(z, m, theta, p, L, real=True, levels=None, evaluate=True, log=print)
     n = len(z)
     out = {"n": n, "theta": theta, "p": p, "L": L, "pt_floor": PT_FLOOR}
     t0 = time.time()
-    gp = Fmm2d(torch.from_numpy(z).cuda(), theta=theta, p=p, nlevels=L, real_strengths=real)
+    gp = Fmm2d(torch.from_numpy(z).cuda(), theta=theta, p=p, nlevels=L, real_strengths=real,
+               rr_exchange=rr_exchange, parent_merge=parent_merge)
     if evaluate:
         phi, dphi = gp.eval(torch.from_numpy(m).cuda())
         torch.cuda.synchronize()
@@ -48,7 +52,7 @@ def compare(z, m, theta, p, L, real=True, levels=None, evaluate=True, log=print)
     out["gpu_s"] = time.time() - t0
     log(f"gpu build+eval {out['gpu_s']:.1f} s")
     t0 = time.time()
-    op = oracle.plan(z, theta, L)
+    op = oracle.plan(z, theta, L, rr_exchange=rr_exchange, parent_merge=parent_merge)
     out["oracle_build_s"] = time.time() - t0
     log(f"oracle build {out['oracle_build_s']:.1f} s")
     t0 = time.time()
@@ -62,14 +66,19 @@ def compare(z, m, theta, p, L, real=True, levels=None, evaluate=True, log=print)
         for name, a, b in zip(("cx", "cy", "r"), gp.discs(l), op.discs(l)):
             if not np.array_equal(a, b):
                 raise AssertionError(f"disc {name} differs at level {l}")
-        for kind in ("strong", "weak"):
+        kinds = ["strong", "weak"]
+        if parent_merge and l >= 2:
+            kinds.append("xweak")
+        if rr_exchange and l == L:
+            kinds += ["near", "p2l", "m2p"]
+        for kind in kinds:
             go, gi = gp.list(l, kind)
             oo, oi = op.list(l, kind)
             if not np.array_equal(go, oo):
                 raise AssertionError(f"{kind} offsets differ at level {l}")
             if not np.array_equal(gi, oi):
                 raise AssertionError(f"{kind} entries differ at level {l}")
-            out["entries_compared"][kind] += int(len(oi))
+            out["entries_compared"][kind] = out["entries_compared"].get(kind, 0) + int(len(oi))
             del go, gi, oo, oi
         out["levels_compared"].append(l)
     out["structure_s"] = time.time() - t0

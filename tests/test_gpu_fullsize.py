@@ -130,3 +130,37 @@ def test_c5_whole_problem_vs_oracle(orc):
     L = orc.nlevels(len(z), c.leaf_target)
     assert L == 11
     _assert_whole(compare(z, m, c.theta, c.p, L, real=True))
+
+
+def test_c3_whole_problem_rr_exchange(orc):
+    """C3 at its BJ size (1e6 clusters, where 81 % of the direct pairs qualify) with the r/R
+    exchange (f1, R23) on both sides: every level's lists plus the leaf near / P2L /
+    M2P lists bit-exact, all outputs within 1e-12 of the oracle pass with the same conversions."""
+    c = W.CONFIGS["C3"]
+    z, m = W.make_config("C3")
+    L = orc.nlevels(len(z), c.leaf_target)
+    r = compare(z, m, c.theta, c.p, L, real=True, rr_exchange=True)
+    _assert_whole(r)
+    assert r["entries_compared"]["p2l"] > 0 and r["entries_compared"]["m2p"] > 0
+
+
+def test_c5_recipe_1e7_whole_problem_parent_merge(orc):
+    """The C5 recipe at N = 1e7 with the parent merge (f2, R25) on both sides: the
+    cross-level weak lists of every level bit-exact, all outputs within 1e-12."""
+    c = W.CONFIGS["C5"]
+    z, m = W.make_config("C5", n=10_000_000)
+    L = orc.nlevels(len(z), c.leaf_target)
+    r = compare(z, m, c.theta, c.p, L, real=True, parent_merge=True)
+    _assert_whole(r)
+    assert r["entries_compared"]["xweak"] > 0
+
+
+def test_c5_recipe_1e7_whole_problem_rr_exchange(orc):
+    """The C5 recipe at N = 1e7 with the r/R exchange (f1): short P2L / M2P lists on the
+    thread / warp-per-leaf kernels, every list bit-exact, all outputs within 1e-12."""
+    c = W.CONFIGS["C5"]
+    z, m = W.make_config("C5", n=10_000_000)
+    L = orc.nlevels(len(z), c.leaf_target)
+    r = compare(z, m, c.theta, c.p, L, real=True, rr_exchange=True)
+    _assert_whole(r)
+    assert r["entries_compared"]["p2l"] > 0 and r["entries_compared"]["m2p"] > 0
