@@ -290,19 +290,70 @@ __device__ __forceinline__ bool rr_exchange(double cbx, double cby, double rb, d
     return (r < R) && (d > 0.0) && (__dadd_rn(r, __dmul_rn(theta, R)) <= __dmul_rn(theta, d));
 }
 
-// Split of the leaf strong lists (one warp per leaf, ballot compaction keeps the order):
-// class 0 near (direct), 1 P2L into this smaller leaf, 2 M2P of a smaller leaf here.
+// Split of the leaf strong lists: class 0 near (direct), 1 P2L into this smaller leaf, 2 M2P
+// of a smaller leaf here; the order of each list is the strong list's.  Lists of at most
+// RRL_THREAD entries (every leaf on near-uniform inputs): a thread per leaf (k_rr_lists_t);
+// longer ones (non-uniform inputs) are collected by its count pass and split by a warp per
+// leaf (k_rr_lists, ballot compaction).
+constexpr int64_t RRL_THREAD = 64;
+template <bool FILL>
+__global__ void k_rr_lists_t(int64_t t0, int64_t t1, const double* __restrict__ cx, const double* __restrict__ cy,
+                             const double* __restrict__ r, double theta, const int64_t* __restrict__ soff,
+                             const uint32_t* __restrict__ sidx, int64_t* __restrict__ cnt,   // [3][nl + 1]
+                             const int64_t* __restrict__ o0, const int64_t* __restrict__ o1,
+                             const int64_t* __restrict__ o2, uint32_t* __restrict__ i0, uint32_t* __restrict__ i1,
+                             uint32_t* __restrict__ i2, int64_t nl, uint32_t* __restrict__ longs,
+                             unsigned int* __restrict__ nlong)
+{
+    const int64_t t = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= t1) return;
+    const int64_t qa = soff[t], qb = soff[t + 1];
+    if (qb - qa > RRL_THREAD) {                     // a warp's job (k_rr_lists)
+        if (!FILL) longs[atomicAdd(nlong, 1u)] = (uint32_t)t;
+        return;
+    }
+    const double tx = cx[t], ty = cy[t], tr = r[t];
+    int64_t n0 = 0, n1 = 0, n2 = 0;
+    for (int64_t q = qa; q < qb; ++q) {
+        const uint32_t s = sidx[q];
+        int cls = 0;
+        if (s != (uint32_t)t && rr_exchange(tx, ty, tr, cx[s], cy[s], r[s], theta)) cls = (tr < r[s]) ? 1 : 2;
+        if (FILL) {
+            if (cls == 0) i0[o0[t] + n0] = s;
+            else if (cls == 1) i1[o1[t] + n1] = s;
+            else i2[o2[t] + n2] = s;
+        }
+        n0 += cls == 0;
+        n1 += cls == 1;
+        n2 += cls == 2;
+    }
+    if (!FILL) {
+        cnt[t] = n0;
+        cnt[(nl + 1) + t] = n1;
+        cnt[2 * (nl + 1) + t] = n2;
+    }
+}
+
+// warp per leaf: leaves t0 + w (leaves == nullptr) or leaves[w] (w < nleaves)
 template <bool FILL>
 __global__ void k_rr_lists(int64_t t0, int64_t t1, const double* __restrict__ cx, const double* __restrict__ cy,
                            const double* __restrict__ r, double theta, const int64_t* __restrict__ soff,
                            const uint32_t* __restrict__ sidx, int64_t* __restrict__ cnt,   // [3][nl + 1]
                            const int64_t* __restrict__ o0, const int64_t* __restrict__ o1,
                            const int64_t* __restrict__ o2, uint32_t* __restrict__ i0, uint32_t* __restrict__ i1,
-                           uint32_t* __restrict__ i2, int64_t nl)
+                           uint32_t* __restrict__ i2, int64_t nl, const uint32_t* __restrict__ leaves = nullptr,
+                           int64_t nleaves = 0)
 {
-    const int64_t t = t0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (t >= t1) return;
+    int64_t t;
+    if (leaves) {
+        if (w >= nleaves) return;
+        t = leaves[w];
+    } else {
+        t = t0 + w;
+        if (t >= t1) return;
+    }
     const double tx = cx[t], ty = cy[t], tr = r[t];
     const unsigned lt = (1u << lane) - 1u;
     int64_t n0 = 0, n1 = 0, n2 = 0;
@@ -451,14 +502,29 @@ static int build_rr_lists(fmm2d_plan* P)
     void* scratch = nullptr;
     size_t sb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, sb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(nl + 1), st);
+    uint32_t* longs = nullptr;
+    unsigned int* nlong_d = nullptr;
     FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&cnt, sizeof(int64_t) * 3 * (nl + 1), st));
     FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&scratch, sb, st));
+    FMM2D_CUDA_TRY(fmm2d::pool_malloc((void**)&longs, sizeof(uint32_t) * std::max<int64_t>(nl, 1) + 16, st));
+    nlong_d = reinterpret_cast<unsigned int*>(longs + std::max<int64_t>(nl, 1));
     auto body = [&]() -> int {
         FMM2D_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * 3 * (nl + 1), st));
-        const unsigned grid = grid_for((t1 - t0) * 32, 256);
-        k_rr_lists<false><<<grid, 256, 0, st>>>(t0, t1, cx, cy, r, P->theta, S.off, S.idx, cnt, nullptr, nullptr,
-                                                nullptr, nullptr, nullptr, nullptr, nl);
+        // short lists: a thread per leaf (the long ones collected for a warp each)
+        FMM2D_CUDA_TRY(cudaMemsetAsync(nlong_d, 0, sizeof(unsigned int), st));
+        k_rr_lists_t<false><<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, cx, cy, r, P->theta, S.off, S.idx, cnt,
+                                                                    nullptr, nullptr, nullptr, nullptr, nullptr,
+                                                                    nullptr, nl, longs, nlong_d);
         note_launch();
+        unsigned int nlong = 0;
+        FMM2D_CUDA_TRY(cudaMemcpyAsync(&nlong, nlong_d, sizeof(nlong), cudaMemcpyDeviceToHost, st));
+        FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
+        const unsigned grid = grid_for((int64_t)nlong * 32, 256);
+        if (nlong) {
+            k_rr_lists<false><<<grid, 256, 0, st>>>(t0, t1, cx, cy, r, P->theta, S.off, S.idx, cnt, nullptr, nullptr,
+                                                    nullptr, nullptr, nullptr, nullptr, nl, longs, nlong);
+            note_launch();
+        }
         Csr* C[3] = {&P->near, &P->rr_p2l, &P->rr_m2p};
         int64_t tot[3];
         for (int c = 0; c < 3; ++c) {
@@ -473,10 +539,17 @@ static int build_rr_lists(fmm2d_plan* P)
             C[c]->total = tot[c];
             FMM2D_TRY(dev_alloc(P, (void**)&C[c]->idx, sizeof(uint32_t) * std::max<int64_t>(tot[c], 1)));
         }
-        k_rr_lists<true><<<grid, 256, 0, st>>>(t0, t1, cx, cy, r, P->theta, S.off, S.idx, nullptr, P->near.off,
-                                               P->rr_p2l.off, P->rr_m2p.off, P->near.idx, P->rr_p2l.idx,
-                                               P->rr_m2p.idx, nl);
+        k_rr_lists_t<true><<<grid_for(t1 - t0, 256), 256, 0, st>>>(t0, t1, cx, cy, r, P->theta, S.off, S.idx,
+                                                                   nullptr, P->near.off, P->rr_p2l.off,
+                                                                   P->rr_m2p.off, P->near.idx, P->rr_p2l.idx,
+                                                                   P->rr_m2p.idx, nl, nullptr, nullptr);
         note_launch();
+        if (nlong) {
+            k_rr_lists<true><<<grid, 256, 0, st>>>(t0, t1, cx, cy, r, P->theta, S.off, S.idx, nullptr, P->near.off,
+                                                   P->rr_p2l.off, P->rr_m2p.off, P->near.idx, P->rr_p2l.idx,
+                                                   P->rr_m2p.idx, nl, longs, nlong);
+            note_launch();
+        }
         // leaves with P2L / M2P work (the order is irrelevant: each leaf is independent)
         // (short lists from the front, long ones from the back: a warp or a block each, rr.cu)
         unsigned int* d_n = (unsigned int*)cnt;
@@ -502,6 +575,7 @@ static int build_rr_lists(fmm2d_plan* P)
     const int rc = body();
     cudaFreeAsync(cnt, st);
     cudaFreeAsync(scratch, st);
+    cudaFreeAsync(longs, st);
     return rc;
 }
 
