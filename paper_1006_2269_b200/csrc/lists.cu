@@ -108,6 +108,58 @@ __global__ void k_lists_box(int64_t b0, int64_t b1, const double* __restrict__ c
     }
 }
 
+// One THREAD per box (FMM2D_LISTS_THREAD; short parent lists): the box walks its candidates
+// (the children of its parent's strong list, in order) itself -- siblings sit in adjacent
+// threads, so the candidates' discs are shared through L1 -- and writes its slots in the
+// same order as the ballot compactions of the warp forms (bit-identical lists).
+#ifndef FMM2D_LISTS_THREAD
+#define FMM2D_LISTS_THREAD 1
+#endif
+__global__ void __launch_bounds__(256) k_lists_t(int64_t b0, int64_t b1, const double* __restrict__ cx,
+                                                 const double* __restrict__ cy, const double* __restrict__ r,
+                                                 double theta, const int64_t* __restrict__ poff,
+                                                 const uint32_t* __restrict__ pidx, int64_t* __restrict__ wcnt,
+                                                 int64_t* __restrict__ scnt, uint32_t* __restrict__ wtmp,
+                                                 uint32_t* __restrict__ stmp, bool merge,
+                                                 const double* __restrict__ pcx, const double* __restrict__ pcy,
+                                                 const double* __restrict__ pr, int64_t* __restrict__ xcnt,
+                                                 uint32_t* __restrict__ xtmp)
+{
+    const int64_t b = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= b1) return;
+    const int64_t par = b >> 2;
+    const int64_t o0 = poff[par], nq = poff[par + 1] - o0;
+    const double bx = cx[b], by = cy[b], br = r[b];
+    const int64_t slot = cand_slot(poff, b), xslot = slot / 4;
+    int64_t nw = 0, ns = 0, nx = 0;
+    if (br >= 0.0) {                                // empty box (midpoint tree): no connections
+        for (int64_t k = 0; k < nq; ++k) {
+            const uint32_t q = pidx[o0 + k];
+            bool valid[4], ws[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t c = 4u * q + (uint32_t)j;
+                valid[j] = r[c] >= 0.0;             // empty candidates (midpoint tree) take no part
+                ws[j] = valid[j] && (c != (uint32_t)b) && well_separated(bx, by, br, cx[c], cy[c], r[c], theta);
+            }
+            if (merge && ws[0] && ws[1] && ws[2] && ws[3] && well_separated(bx, by, br, pcx[q], pcy[q], pr[q], theta)) {
+                xtmp[xslot + nx++] = q;
+                continue;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (!valid[j]) continue;
+                const uint32_t c = 4u * q + (uint32_t)j;
+                if (ws[j]) wtmp[slot + nw++] = c;
+                else stmp[slot + ns++] = c;
+            }
+        }
+    }
+    wcnt[b] = nw;
+    scnt[b] = ns;
+    if (merge) xcnt[b] = nx;
+}
+
 #ifndef FMM2D_LISTS_MINB
 #define FMM2D_LISTS_MINB 3            // 80 registers: 3 blocks of 256 per SM (measured best at C5)
 #endif
@@ -713,7 +765,10 @@ int build_lists(fmm2d_plan* P)
             }
             // per parent while the parents' strong lists are short (C5: ~11), per box when long
             const int64_t npar = ((b1 + 3) >> 2) - (b0 >> 2);
-            if (PS.total <= 32 * std::max<int64_t>(npar, 1))
+            if (FMM2D_LISTS_THREAD && PS.total <= 32 * std::max<int64_t>(npar, 1))
+                k_lists_t<<<grid_for(b1 - b0, 256), 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w,
+                                                                  cnt_s, wtmp, stmp, merge, pcx, pcy, pr, cnt_x, xtmp);
+            else if (PS.total <= 32 * std::max<int64_t>(npar, 1))
                 k_lists<<<grid4, 256, 0, st>>>(b0, b1, cx, cy, r, P->theta, PS.off, PS.idx, cnt_w, cnt_s, wtmp, stmp,
                                               merge, pcx, pcy, pr, cnt_x, xtmp);
             else
