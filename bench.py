@@ -346,6 +346,7 @@ def main():
     ap.add_argument("--impl", default="fmm2d", choices=["fmm2d", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-optional", action="store_true", help="skip the optional-steps lines")
     ap.add_argument("--rr-exchange", action="store_true", help="FMM2D_RR_EXCHANGE (P:370-377; one GPU)")
     ap.add_argument("--parent-merge", action="store_true", help="FMM2D_PARENT_MERGE (P:364-370)")
     ap.add_argument("--symmetric-p2p", action="store_true", help="FMM2D_SYMMETRIC_P2P (one GPU)")
@@ -504,6 +505,14 @@ def main():
                   "algorithmic_bytes": bbytes, "components_bytes": comp, "global_split_levels": l0,
                   "traffic": None, "traffic_note": "per-kernel ncu DRAM bytes: DESIGN.md 6.1 table"}
 
+    # the same workload with the paper's two optional steps (r/R exchange P:370-377 and parent
+    # merge P:364-370, off on the headline path by reading R17): device
+    # time per build + eval, same clocking rules, a short run
+    optional = None
+    if world == 1 and not (args.rr_exchange or args.parent_merge or args.overlap or args.symmetric_p2p) \
+            and not args.no_optional:
+        optional = optional_steps(z, m, phi, dphi, cfg, real, stream, steps=3, warmup=2)
+
     # end to end through the C ABI with host (pinned) buffers
     e2e = None
     if not args.no_e2e:
@@ -537,7 +546,7 @@ def main():
                 "m2l_tflops": m2l_tf,
                 "roofline": roof, "roofline_m2l": roof_m2l, "roofline_build": roof_build,
                 "gpu_launches": launches_per_step * args.steps,
-                "clocks": clk.summary(), "e2e": e2e,
+                "clocks": clk.summary(), "e2e": e2e, "optional_steps": optional,
                 "stats": {"weak_pairs": weak_pairs, "p2p_pairs": pairs, "min_leaf": st.get("min_leaf"),
                           "max_leaf": st.get("max_leaf")}}
         line["parity"] = parity_record(args.config == "C5" and not args.n)
@@ -546,6 +555,42 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def optional_steps(z, m, phi, dphi, cfg, real, stream, steps=3, warmup=2):
+    """Points/s of build + eval with the r/R exchange and the parent merge (each alone and
+    both), CUDA events on the launching stream, W untimed steps first."""
+    import torch
+    from paper_1006_2269_b200 import Fmm2d
+    out = {"note": "the paper's optional optimisations (P:364-377), off on the headline path (DESIGN R17); "
+                   "parity: tests/test_gpu_fullsize.py (whole problem with each step)"}
+    for name, kw in (("rr_exchange", {"rr_exchange": True}), ("parent_merge", {"parent_merge": True}),
+                     ("rr_exchange+parent_merge", {"rr_exchange": True, "parent_merge": True})):
+        def step():
+            plan = Fmm2d(z, theta=cfg.theta, p=cfg.p, leaf_target=cfg.leaf_target, real_strengths=real,
+                         stream=stream, **kw)
+            plan.eval(m, phi, dphi)
+            return plan
+        plan = None
+        for _ in range(warmup):
+            if plan is not None:
+                plan.close()
+            plan = step()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            plan.close()
+            plan = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        st = plan.stats()
+        plan.close()
+        out[name] = {"value": cfg.n / (ms / 1e3), "unit": "points/s", "ms_per_step": ms, "steps": steps,
+                     "warmup": warmup, "p2p_pairs": st.get("p2p_pairs"), "weak_pairs": st.get("weak_pairs")}
+    return out
 
 
 def phase_times(z, m, phi, dphi, cfg, real, stream, shard_kw):

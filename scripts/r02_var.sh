@@ -1,7 +1,7 @@
 # time the C5 phases for the in-tree library and each variant library given as arguments
 mkdir -p gpurun_out
 for lib in paper_1006_2269_b200/libfmm2d.so "$@"; do
-  FMM2D_LIB=$PWD/$lib timeout 600 python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-e2e $BENCH_ARGS > gpurun_out/var.log 2>&1
+  FMM2D_LIB=$PWD/$lib timeout 600 python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-e2e --no-optional $BENCH_ARGS > gpurun_out/var.log 2>&1
   python - "$lib" <<'PY'
 import json, sys
 line = [l for l in open("gpurun_out/var.log") if l.startswith("{")]
