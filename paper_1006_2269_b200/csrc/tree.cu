@@ -173,14 +173,10 @@ __global__ void k_keys_y64(const double2* __restrict__ zc, const uint32_t* __res
 // coordinates from zc; idx sits at bit `ishift` of the 64-bit payload).  A run
 // longer than RUN_MAX raises *overflow and is left alone (the caller redoes the axis
 // with 64-bit keys).
-__global__ void k_fix_runs(const uint32_t* __restrict__ key, int64_t n, const double2* __restrict__ zc, int axis,
-                           int ishift, uint64_t* __restrict__ val, int* __restrict__ overflow)
+__device__ __forceinline__ void fix_run(const uint32_t* __restrict__ key, int64_t n, const double2* __restrict__ zc,
+                                        int axis, int ishift, uint64_t* __restrict__ val, int* __restrict__ overflow,
+                                        int64_t k, uint32_t v)
 {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const uint32_t v = key[k];
-    if (k > 0 && key[k - 1] == v) return;            // not a run start
-    if (k + 1 >= n || key[k + 1] != v) return;       // run of one
     int len = 2;
     while (k + len < n && key[k + len] == v && len <= RUN_MAX) ++len;
     if (len > RUN_MAX) {
@@ -207,6 +203,36 @@ __global__ void k_fix_runs(const uint32_t* __restrict__ key, int64_t n, const do
         pv[b] = pl;
     }
     for (int a = 0; a < len; ++a) val[k + a] = pv[a];
+}
+
+// FR keys per thread (vector loads): the run starts among them -- key[k-1] != key[k] ==
+// key[k+1] -- are fixed by fix_run (about 1 % of the points at C5; the scan itself is the
+// cost: one pass over the keys at memory speed instead of three scalar loads per key)
+constexpr int FR = 8;
+__global__ void k_fix_runs(const uint32_t* __restrict__ key, int64_t n, const double2* __restrict__ zc, int axis,
+                           int ishift, uint64_t* __restrict__ val, int* __restrict__ overflow)
+{
+    const int64_t k0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * FR;
+    if (k0 >= n) return;
+    uint32_t kk[FR + 2];                              // key[k0 - 1 .. k0 + FR]
+    if (k0 + FR <= n && ((reinterpret_cast<uintptr_t>(key + k0) & 15) == 0)) {
+        const uint4 a = *reinterpret_cast<const uint4*>(key + k0);
+        const uint4 b = *reinterpret_cast<const uint4*>(key + k0 + 4);
+        kk[1] = a.x; kk[2] = a.y; kk[3] = a.z; kk[4] = a.w;
+        kk[5] = b.x; kk[6] = b.y; kk[7] = b.z; kk[8] = b.w;
+    } else {
+#pragma unroll
+        for (int u = 0; u < FR; ++u) kk[u + 1] = (k0 + u < n) ? key[k0 + u] : 0u;
+    }
+    kk[0] = (k0 > 0) ? key[k0 - 1] : ~kk[1];
+    kk[FR + 1] = (k0 + FR < n) ? key[k0 + FR] : 0u;
+#pragma unroll
+    for (int u = 0; u < FR; ++u) {
+        const int64_t k = k0 + u;
+        if (k + 1 >= n) break;                         // a run needs k + 1 < n
+        const uint32_t v = kk[u + 1];
+        if (kk[u] != v && kk[u + 2] == v) fix_run(key, n, zc, axis, ishift, val, overflow, k, v);
+    }
 }
 
 // y-list and the (local) x-ranks in y order (the key of the sort that inverts them)
@@ -1583,7 +1609,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
                 k_keys_x<false><<<grid_for(m, BS), BS, 0, st>>>(zc, sub, m, bm, k32a, nullptr, v64a);
                 fmm2d::note_launch();
                 FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, v64a, vxm, (int)m, 0, 32, st));
-                k_fix_runs<<<grid_for(m, BS), BS, 0, st>>>(k32b, m, zc, 0, 0, vxm, ovf);
+                k_fix_runs<<<grid_for((m + FR - 1) / FR, BS), BS, 0, st>>>(k32b, m, zc, 0, 0, vxm, ovf);
                 fmm2d::note_launch();
                 FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_ovf[0], ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
                 FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1607,7 +1633,7 @@ int build_tree(fmm2d_plan* P, const double2* z)
                 fmm2d::note_launch();
                 sb = cub_bytes;
                 FMM2D_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scratch, sb, k32a, k32b, v64a, vym, (int)m, 0, 32, st));
-                k_fix_runs<<<grid_for(m, BS), BS, 0, st>>>(k32b, m, zc, 1, 32, vym, ovf + 1);
+                k_fix_runs<<<grid_for((m + FR - 1) / FR, BS), BS, 0, st>>>(k32b, m, zc, 1, 32, vym, ovf + 1);
                 fmm2d::note_launch();
                 FMM2D_CUDA_TRY(cudaMemcpyAsync(&h_ovf[1], ovf + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
                 FMM2D_CUDA_TRY(cudaStreamSynchronize(st));
