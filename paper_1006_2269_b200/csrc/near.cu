@@ -35,6 +35,9 @@ constexpr int NEAR_T = 128;
 #ifndef FMM2D_NEAR_SKIPBAR
 #define FMM2D_NEAR_SKIPBAR 1      // no barrier before the first chunk of a pass
 #endif
+#ifndef FMM2D_NEAR_TMA_TABLES
+#define FMM2D_NEAR_TMA_TABLES 1       // k_near: tables by one cp.async.bulk + mbarrier
+#endif
 #ifndef FMM2D_NEAR_TPT
 #define FMM2D_NEAR_TPT 2          // targets per thread (register blocking)
 #endif
@@ -183,7 +186,25 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
         q0 = sg.qa;
         q1 = sg.qb;
     }
+#if FMM2D_NEAR_TMA_TABLES
+    // the tables by ONE bulk asynchronous copy (TMA engine, completion on an mbarrier) instead
+    // of a copy loop through every thread's registers; waited for just before the first pair
+    __shared__ __align__(8) unsigned long long tbar;
+    const uint32_t tbar_s = (uint32_t)__cvta_generic_to_shared(&tbar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tbar_s) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tbar_s),
+                     "r"((uint32_t)sizeof(fm::Tables)) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"((uint32_t)__cvta_generic_to_shared(&T)), "l"(gtab), "r"((uint32_t)sizeof(fm::Tables)),
+                     "r"(tbar_s) : "memory");
+    }
+    bool tables_ready = false;              // (the mbarrier's init is ordered by the chunk barriers)
+#else
     load_tables(T, gtab);                    // (the first chunk's barriers cover it)
+#endif
     const uint32_t ts = off[t], te = off[t + 1];
     const int nt = (int)(te - ts);
     const int tile = NEAR_T / G;                 // target tuples per pass
@@ -243,6 +264,15 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
             }
             __syncthreads();
             const int total = cstart[nl];
+#if FMM2D_NEAR_TMA_TABLES
+            if (!tables_ready) {                 // first chunk: the tables' bulk copy has landed
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                                 : "=r"(done) : "r"(tbar_s) : "memory");
+                tables_ready = true;
+            }
+#endif
             const int kown = (cinfo[1] >= 0) ? cinfo[1] : total;       // own leaf rows [kown, kown+nt)
             const int kend = min(total, kown + nt);
             if (active) {
