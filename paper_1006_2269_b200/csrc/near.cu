@@ -38,6 +38,9 @@ constexpr int NEAR_T = 128;
 #ifndef FMM2D_NEAR_TMA_TABLES
 #define FMM2D_NEAR_TMA_TABLES 1       // k_near: tables by one cp.async.bulk + mbarrier
 #endif
+#ifndef FMM2D_NEAR_TMA_ROWS
+#define FMM2D_NEAR_TMA_ROWS 1         // k_near: the chunk's source rows by per-leaf cp.async.bulk
+#endif
 #ifndef FMM2D_NEAR_TPT
 #define FMM2D_NEAR_TPT 2          // targets per thread (register blocking)
 #endif
@@ -202,6 +205,17 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                      "r"(tbar_s) : "memory");
     }
     bool tables_ready = false;              // (the mbarrier's init is ordered by the chunk barriers)
+#if FMM2D_NEAR_TMA_ROWS
+    // the chunk's source rows: one bulk copy per leaf (its rows are contiguous), issued by warp 0
+    // right after its scan, completing on rbar (one phase per chunk)
+    __shared__ __align__(8) unsigned long long rbar;
+    const uint32_t rbar_s = (uint32_t)__cvta_generic_to_shared(&rbar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rbar_s) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    uint32_t rphase = 0;
+#endif
 #else
     load_tables(T, gtab);                    // (the first chunk's barriers cover it)
 #endif
@@ -247,9 +261,36 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                 }
                 __syncwarp();
                 if (lane < nl && lf == (uint32_t)t) cinfo[1] = incl - sz;
+#if FMM2D_NEAR_TMA_TABLES && FMM2D_NEAR_TMA_ROWS
+                const int rows = __shfl_sync(0xffffffffu, incl, nl - 1);
+                if (lane == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // after the generic reads of S
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(rbar_s),
+                                 "r"((uint32_t)(rows * sizeof(double4))) : "memory");
+                }
+                __syncwarp();
+                if (lane < nl) {
+                    // own / replicated leaf: rows at its position; halo leaf (sharded plans): in hsrc
+                    const uint32_t hm = lmap ? lmap[lf] : 0xFFFFFFFFu;
+                    const double4* sp = (hm != 0xFFFFFFFFu) ? hsrc + hm : src + off[lf];
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                 ::"r"((uint32_t)__cvta_generic_to_shared(&S[incl - sz])), "l"(sp),
+                                 "r"((uint32_t)(sz * sizeof(double4))), "r"(rbar_s) : "memory");
+                }
+#endif
             }
             __syncthreads();
             const int nl = cinfo[0];
+#if FMM2D_NEAR_TMA_TABLES && FMM2D_NEAR_TMA_ROWS
+            {
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                                 : "=r"(done) : "r"(rbar_s), "r"(rphase) : "memory");
+                rphase ^= 1u;
+            }
+            if (false)
+#endif
             for (int l = warp; l < nl; l += NEAR_T / 32) {
                 const uint32_t lf = sidx[q + l];
                 // own / replicated leaf: rows at its position; halo leaf (sharded plans): in hsrc
@@ -262,7 +303,9 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                 (void)sp; (void)c0; (void)sz;              // timing experiment only: rows not staged
 #endif
             }
+#if !(FMM2D_NEAR_TMA_TABLES && FMM2D_NEAR_TMA_ROWS)
             __syncthreads();
+#endif
             const int total = cstart[nl];
 #if FMM2D_NEAR_TMA_TABLES
             if (!tables_ready) {                 // first chunk: the tables' bulk copy has landed
