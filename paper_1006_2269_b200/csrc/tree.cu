@@ -564,6 +564,9 @@ __global__ void k_seg_prep(const uint32_t* __restrict__ par_off, const uint32_t*
 #ifndef FMM2D_PART_STAGED_OUT
 #define FMM2D_PART_STAGED_OUT 1
 #endif
+#ifndef FMM2D_PART_TMA
+#define FMM2D_PART_TMA 1              // the tile staged by one cp.async.bulk (TMA) + mbarrier
+#endif
 constexpr int PT = FMM2D_PART_PT, PI = FMM2D_PART_PI, PTILE = PT * PI;
 constexpr int PTILE_SHIFT = (PTILE == 1024) ? 10 : (PTILE == 2048) ? 11 : (PTILE == 4096) ? 12 : 13;
 static_assert(PTILE == (1 << PTILE_SHIFT), "tile size");
@@ -594,7 +597,14 @@ __global__ void __launch_bounds__(PT, FMM2D_PART_MINB) k_partition(SplitArgs A)
     typedef cub::BlockScan<uint32_t, PT> Scan;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ uint32_t s_prefix;
+#if FMM2D_PART_TMA
+    // the tile by one bulk asynchronous copy (TMA) from the 16-byte-aligned record at or
+    // before its start (stage0 = the tile's first record)
+    __shared__ __align__(16) uint2 stage_buf[PTILE + 2];
+    __shared__ __align__(8) unsigned long long sbar;
+#else
     __shared__ __align__(16) uint2 stage[PTILE];
+#endif
     __shared__ uint32_t s_off[SEGMAX + 1], s_hi[SEGMAX], s_gp[SEGMAX], s_split[SEGMAX];
 #if FMM2D_PART_STAGED_OUT
     __shared__ uint32_t s_dst[PTILE];
@@ -607,6 +617,21 @@ __global__ void __launch_bounds__(PT, FMM2D_PART_MINB) k_partition(SplitArgs A)
     const uint32_t qhi = (tile + 1 < A.ntiles) ? A.tile_seg[tile + 1] : (A.p1 - A.p0 - 1);
     const int nseg = (int)(qhi - qlo + 1);
     const bool small = nseg <= SEGMAX;
+#if FMM2D_PART_TMA
+    const uint32_t ka = kt & ~1u;                                // 16-byte aligned (uint2 records)
+    const uint32_t nb = (kt + nrec - ka) & ~1u;                  // records copied (even, in range)
+    uint2* stage = stage_buf + (kt - ka);
+    if (tid == 32 && ((kt + nrec - ka) & 1u)) stage[nrec - 1] = A.list[kt + nrec - 1];   // odd tail
+    const uint32_t sbar_s = (uint32_t)__cvta_generic_to_shared(&sbar);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar_s) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar_s), "r"(nb * 8u) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"((uint32_t)__cvta_generic_to_shared(stage_buf)), "l"(A.list + ka), "r"(nb * 8u),
+                     "r"(sbar_s) : "memory");
+    }
+#else
     {   // stage the tile with coalesced 16-byte loads
         const uint4* g = reinterpret_cast<const uint4*>(A.list + kt);
         uint4* sv = reinterpret_cast<uint4*>(stage);
@@ -618,6 +643,7 @@ __global__ void __launch_bounds__(PT, FMM2D_PART_MINB) k_partition(SplitArgs A)
             for (int v = tid; v < nrec; v += PT) stage[v] = A.list[kt + v];
         }
     }
+#endif
     if (small) {
         for (int j = tid; j < nseg; j += PT) {
             const uint32_t q = qlo + j, p = A.p0 + q;
@@ -629,6 +655,14 @@ __global__ void __launch_bounds__(PT, FMM2D_PART_MINB) k_partition(SplitArgs A)
         }
     }
     __syncthreads();
+#if FMM2D_PART_TMA
+    {
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done) : "r"(sbar_s) : "memory");
+    }
+#endif
     uint2 r[PI];
     uint32_t seg[PI], f[PI];
     uint32_t cnt = 0;
