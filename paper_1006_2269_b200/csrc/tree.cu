@@ -618,7 +618,8 @@ __global__ void __launch_bounds__(PT, FMM2D_PART_MINB) k_partition(SplitArgs A)
     const int nseg = (int)(qhi - qlo + 1);
     const bool small = nseg <= SEGMAX;
 #if FMM2D_PART_TMA
-    const uint32_t ka = kt & ~1u;                                // 16-byte aligned (uint2 records)
+    // (the list may be a virtual base: alignment from the address, not the index)
+    const uint32_t ka = kt - (uint32_t)((reinterpret_cast<uintptr_t>(A.list + kt) >> 3) & 1u);   // 16-byte aligned
     const uint32_t nb = (kt + nrec - ka) & ~1u;                  // records copied (even, in range)
     uint2* stage = stage_buf + (kt - ka);
     if (tid == 32 && ((kt + nrec - ka) & 1u)) stage[nrec - 1] = A.list[kt + nrec - 1];   // odd tail
