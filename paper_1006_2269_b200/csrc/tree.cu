@@ -815,7 +815,7 @@ struct LocalArgs {
 };
 
 struct LocalSmem {
-    uint2 buf[3][LMAX];
+    uint2 buf[3][LMAX + 2];                          // (+2: a TMA load may start one record early)
     uint32_t segs[2 * LSEG + 1];                     // segment starts (local positions)
     uint32_t subs[4 * LSEG + 1];                     // sub-segment starts
     uint32_t split[2 * LSEG], gp[2 * LSEG];
@@ -832,6 +832,9 @@ __device__ __forceinline__ uint32_t local_seg(const uint32_t* __restrict__ O, in
     return (uint32_t)lo;
 }
 
+#ifndef FMM2D_LOCAL_TMA
+#define FMM2D_LOCAL_TMA 1                 // k_tree_local: both lists by cp.async.bulk (TMA)
+#endif
 #ifndef FMM2D_LOCAL_MINB
 #define FMM2D_LOCAL_MINB 3
 #endif
@@ -849,10 +852,43 @@ __global__ void __launch_bounds__(LT, FMM2D_LOCAL_MINB) k_tree_local(LocalArgs A
     uint2* X = S.buf[0];
     uint2* Y = S.buf[1];
     uint2* T = S.buf[2];
+#if FMM2D_LOCAL_TMA
+    {   // both lists by two bulk asynchronous copies (TMA) from 16-byte-aligned starts
+        __shared__ __align__(8) unsigned long long lbar;
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&lbar);
+        const uint32_t mx = (uint32_t)((reinterpret_cast<uintptr_t>(A.xl + s0) >> 3) & 1u);
+        const uint32_t my = (uint32_t)((reinterpret_cast<uintptr_t>(A.yl + s0) >> 3) & 1u);
+        const uint32_t nbx = ((uint32_t)n + mx) & ~1u, nby = ((uint32_t)n + my) & ~1u;
+        X = S.buf[0] + mx;
+        Y = S.buf[1] + my;
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((nbx + nby) * 8u)
+                         : "memory");
+            if (nbx)
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"((uint32_t)__cvta_generic_to_shared(S.buf[0])), "l"(A.xl + s0 - mx), "r"(nbx * 8u),
+                             "r"(bar) : "memory");
+            if (nby)
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"((uint32_t)__cvta_generic_to_shared(S.buf[1])), "l"(A.yl + s0 - my), "r"(nby * 8u),
+                             "r"(bar) : "memory");
+        }
+        if (tid == 32 && (((uint32_t)n + mx) & 1u)) X[n - 1] = A.xl[s0 + n - 1];    // odd tails
+        if (tid == 64 && (((uint32_t)n + my) & 1u)) Y[n - 1] = A.yl[s0 + n - 1];
+        __syncthreads();                              // (mbarrier init before the waits; tails)
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done) : "r"(bar) : "memory");
+    }
+#else
     for (int k = tid; k < n; k += LT) {
         X[k] = A.xl[s0 + k];
         Y[k] = A.yl[s0 + k];
     }
+#endif
     for (int l = A.l0; l < A.L; ++l) {
         const int64_t nb = (int64_t)1 << (2 * (l - A.l0));         // level-l boxes of this CTA
         const int64_t gb = b * nb;                                  // first one, level-local id
