@@ -18,4 +18,4 @@ ncu -i /tmp/prof_$K.ncu-rep --page source --csv --print-source sass > gpurun_out
 done
 # FP64 census of k_near / k_m2l (executed DFMA/DADD/DMUL per pair, FP64 pipe) for profiles/r02/fp64_census.json
 M=sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__inst_executed.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,gpu__time_duration.sum,smsp__thread_inst_executed.sum
-timeout 900 ncu --metrics $M --csv -k regex:"k_near|k_m2l" -c 2 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-optional > gpurun_out/ncu_census_c5.csv 2>&1
+timeout 900 ncu --metrics $M --csv --kernel-name-base demangled -k "regex:k_near<|k_m2l<" -c 2 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-optional > gpurun_out/ncu_census_c5.csv 2>&1
