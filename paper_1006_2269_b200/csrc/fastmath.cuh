@@ -8,11 +8,17 @@
 //   log r2 = e ln2 + L_j + log1p(u),  u = f ic_j - 1, f in [1,2) the mantissa of r2,
 //            j = its top 8 bits, ic_j ~ 1/(1 + (j+1/2)/256), L_j = -log(ic_j) exactly
 //            rounded for the ROUNDED ic_j (f >= 1.5 is taken as 2 (f/2), L_j absorbing
-//            the ln 2, so log r2 ~ 0 does not cancel), |u| < 2^-9, degree-6 series;
+//            the ln 2, so log r2 ~ 0 does not cancel), |u| < 2^-9, degree-6 series.
+//            The mantissa is never extracted: with E' = exponent + [f >= 1.5] (one add
+//            and one mask on the high word), u = r2 (ic_j 2^-E') - 1 where the table
+//            entry's exponent field is lowered by E' (one integer add; the table holds
+//            2 ic_j for f >= 1.5, so the product is f ic_j exactly), and e comes from
+//            the double {hi 0x43300000, lo E' << 20} = 2^52 + E' 2^20 by one subtraction;
 //   Arg    = octant reduction a = atan(mn/mx), mn <= mx; c = mn/mx rounded to a
 //            multiple of 1/256 (22-bit estimate + magic-number rounding, no int<->fp
 //            conversion); atan(mn/mx) = atan(c) + atan(t), t = (mn - c mx)/(mx + c mn),
-//            |t| < 2^-8, degree-5 series; octant / sign fixes by selects and a sign-bit OR;
+//            |t| < 2^-8, degree-5 series; octant: base + s a as one FMA with {base, s}
+//            read from the table by (swap, dx < 0), sign of dy by a sign-bit OR;
 //   1/x    = MUFU.RCP64H estimate + one cubic Newton step.
 // Polynomial coefficients and constants sit in __constant__ memory (a warp-uniform
 // DFMA operand).  Error (tests/test_fastmath.py, host build against long double):
@@ -57,17 +63,17 @@ struct Tables {
 };
 
 // [0..3] log1p series -1/6, 1/5, -1/4, 1/3, [4] -1/2, [5] unused, [6..7] atan series 1/5, -1/3,
-// [8] ln2 * 2^-32 (exact scaling of the double nearest ln 2), [9] unused, [10] pi/2, [11] unused,
-// [12] pi, [13] unused, [14] 2^52 + 1023 * 2^32 (exponent extraction), [15] 1.5 * 2^44
+// [8] ln2 * 2^-20 (exact scaling of the double nearest ln 2), [9] unused, [10] pi/2, [11] unused,
+// [12] pi, [13] unused, [14] 2^52 + 1023 * 2^20 (exponent extraction), [15] 1.5 * 2^44
 // (rounding to a multiple of 1/256), [16..17] asin series 3/40, 1/6, [18] 1.5 * 2^52 (rounding
 // to an integer), [19] 3/8, [20] 1/2
 FM_CONST double kC[21] = {
     -1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -0.5, 0.0,
     1.0 / 5.0, -1.0 / 3.0,
-    6.931471805599453094e-01 / 4294967296.0, 0.0,
+    6.931471805599453094e-01 / 1048576.0, 0.0,
     1.5707963267948966192e+00, 0.0,
     3.141592653589793116e+00, 0.0,
-    4503599627370496.0 + 1023.0 * 4294967296.0, 1.5 * 17592186044416.0};
+    4503599627370496.0 + 1023.0 * 1048576.0, 1.5 * 17592186044416.0};
 
 FM_HD int64_t as_bits(double x)
 {
@@ -98,6 +104,17 @@ FM_HD double fma_(double a, double b, double c)
 #endif
 }
 
+FM_HD int hi_word(double x) { return (int)(as_bits(x) >> 32); }
+FM_HD int lo_word(double x) { return (int)as_bits(x); }
+FM_HD double make_double(int hi, int lo)
+{
+#ifdef __CUDA_ARCH__
+    return __hiloint2double(hi, lo);
+#else
+    return from_bits((int64_t)(((uint64_t)(uint32_t)hi << 32) | (uint32_t)lo));
+#endif
+}
+
 // coarse reciprocal (~2^-22 relative) and the refined one (~1 ulp)
 FM_HD double rcp_approx(double x)
 {
@@ -106,7 +123,11 @@ FM_HD double rcp_approx(double x)
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     return r;
 #else
+#ifdef FM_HOST_RCP_PERTURB             // worst case of the device estimate (2^-22 relative), for the accuracy test
+    return (double)(float)(1.0 / x) * (1.0 + FM_HOST_RCP_PERTURB * 2.384185791015625e-07);
+#else
     return (double)(float)(1.0 / x);      // host stand-in with a comparable error
+#endif
 #endif
 }
 FM_HD double rcp(double x)
@@ -116,49 +137,51 @@ FM_HD double rcp(double x)
     return fma_(r, fma_(e, e, e), r);      // cubic step: err^3
 }
 
+// The reduction shared by log_pos / log_pos5 (header comment): j = the top 8 mantissa bits,
+// hw = (exponent + [f >= 1.5]) << 20 = E' << 20, u = r2 (ic_j 2^-E') - 1 = f ic_j - 1 exactly
+// as before (power-of-two scalings), e20 = (E' - 1023) 2^20.  Normal r2 < 2^1021.
+FM_HD void log_reduce(double r2, const double2* __restrict__ tab, double& u, double& e20, double& Lj)
+{
+    const int hi = hi_word(r2);
+    // row j = the top LOG_BITS mantissa bits, as a byte offset (16-byte rows)
+    const uint32_t jb = ((uint32_t)hi >> (20 - LOG_BITS - 4)) & (uint32_t)((LOG_N - 1) << 4);
+    const int hw = (int)(((uint32_t)hi + 0x00080000u) & 0xFFF00000u);
+    const double2 T = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab) + jb);
+    const double ics = make_double(hi_word(T.x) - hw + 0x3FF00000, lo_word(T.x));
+    u = fma_(r2, ics, -1.0);
+    e20 = make_double(0x43300000, hw) - kC[14];
+    Lj = T.y;
+}
+
 // log(r2) with a degree-5 series (|u| < 2^-9: truncation < 2^-54 / 6 absolute), used
 // by the near-field kernel where only the absolute error of each term matters.  No
 // special case for r2 == 0 (coincident distinct points): there arg_t gives NaN, so
 // the pair's Phi and Phi' are non-finite anyway.
 FM_HD double log_pos5(double r2, const double2* __restrict__ tab)
 {
-    const int64_t b = as_bits(r2);
-    const int hi = (int)(b >> 32);
-    const int j = (hi >> (20 - LOG_BITS)) & (LOG_N - 1);
-    const int eb = (hi >> 20) + (j >> (LOG_BITS - 1));
-    const double e32 = from_bits((int64_t)(0x43300000 | eb) << 32) - kC[14];
-    const double f = from_bits((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
-    const double2 T = tab[j];
-    const double u = fma_(f, T.x, -1.0);
+    double u, e20, Lj;
+    log_reduce(r2, tab, u, e20, Lj);
     // log1p(u) = u - u^2/2 + u^3/3 - u^4/4 + u^5/5
     double p = fma_(kC[1], u, kC[2]);
     p = fma_(p, u, kC[3]);
     p = fma_(p, u, kC[4]);
     const double lp = fma_(p, u * u, u);
-    const double r = fma_(e32, kC[8], T.y + lp);
+    const double r = fma_(e20, kC[8], Lj + lp);
     return r;                    // r2 == 0 gives a finite value; Arg(0) is NaN (see k_near)
 }
 
 // log(r2) for r2 > 0 normal; -inf for r2 == 0.
 FM_HD double log_pos(double r2, const double2* __restrict__ tab)
 {
-    const int64_t b = as_bits(r2);
-    const int hi = (int)(b >> 32);
-    const int j = (hi >> (20 - LOG_BITS)) & (LOG_N - 1);
-    // exponent (+1 when f >= 1.5) as a double scaled by 2^32, without a conversion:
-    // bits 0x43300000:E:00000000 = 2^52 + E 2^32
-    const int eb = (hi >> 20) + (j >> (LOG_BITS - 1));
-    const double e32 = from_bits((int64_t)(0x43300000 | eb) << 32) - kC[14];
-    const double f = from_bits((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
-    const double2 T = tab[j];
-    const double u = fma_(f, T.x, -1.0);
+    double u, e20, Lj;
+    log_reduce(r2, tab, u, e20, Lj);
     // log1p(u) = u - u^2/2 + u^3/3 - u^4/4 + u^5/5 - u^6/6   (|u| < 2^-9: trunc. 2^-66)
     double p = fma_(kC[0], u, kC[1]);
     p = fma_(p, u, kC[2]);
     p = fma_(p, u, kC[3]);
     p = fma_(p, u, kC[4]);
     const double lp = fma_(p, u * u, u);
-    const double r = fma_(e32, kC[8], T.y + lp);      // e ln2 in one rounding (|e| ln2 error < 0.3 ulp)
+    const double r = fma_(e20, kC[8], Lj + lp);       // e ln2 in one rounding (|e| ln2 error < 0.3 ulp)
     return (r2 == 0.0) ? -HUGE_VAL : r;
 }
 
@@ -199,20 +222,22 @@ FM_HD double arg(double dx, double dy, const double2* __restrict__ tab)
     return octant_fix(a, swap, hx < 0, (int64_t)(uint32_t)(hy & (int)0x80000000u) << 32);
 }
 
-// arg with the octant base read from the table (rows OCT_ROW, OCT_ROW+1 = {0, pi},
-// {pi/2, pi/2} indexed by 2 swap + neg) instead of selects; same result bit for bit.
+// arg with the octant placement as ONE FMA: rows OCT_ROW + 2 swap + neg of the table hold
+// {base, s} = {0, 1}, {pi, -1}, {pi/2, -1}, {pi/2, 1}, and res = s a + base (s a is exact, so
+// this is base +- a in one rounding: the same result as arg() bit for bit).  The table index
+// is the low word of q0 + 1.5 2^44 itself (no mask: the unsigned clamp covers NaN).
 constexpr int OCT_ROW = ATAN_N + 4;
 FM_HD double arg_t(double dx, double dy, const double2* __restrict__ tab)
 {
-    const int hx = (int)(as_bits(dx) >> 32), hy = (int)(as_bits(dy) >> 32);
+    const int hx = hi_word(dx), hy = hi_word(dy);
     const bool swap = fabs(dy) > fabs(dx);
     const double mns = swap ? dx : dy;
     const double mxs = swap ? dy : dx;
     const double mn = fabs(mns), mx = fabs(mxs);
     const double q0 = fabs(mns * rcp_approx(mxs));
     const double y = q0 + kC[15];
-    const int jr = (int)as_bits(y) & (2 * ATAN_N - 1);
-    const int j = jr < ATAN_N ? jr : ATAN_N;
+    const uint32_t jr = (uint32_t)lo_word(y);
+    const int j = (int)(jr < (uint32_t)ATAN_N ? jr : (uint32_t)ATAN_N);
     const double c = y - kC[15];
     const double num = fma_(-c, mx, mn);
     const double den = fma_(c, mn, mx);
@@ -223,9 +248,45 @@ FM_HD double arg_t(double dx, double dy, const double2* __restrict__ tab)
     const double2 T = tab[j];
     const double a = T.x + (at + T.y);
     const bool neg = hx < 0;
-    const double base = reinterpret_cast<const double*>(tab + OCT_ROW)[2 * (int)swap + (int)neg];
-    const double sa = from_bits(as_bits(a) ^ ((int64_t)(swap != neg) << 63));
-    const double res = base + sa;
+    const double2 O = (tab + OCT_ROW)[2 * (int)swap + (int)neg];
+    const double res = fma_(a, O.y, O.x);
+    return from_bits(as_bits(res) | ((int64_t)(uint32_t)(hy & (int)0x80000000u) << 32));
+}
+
+// The near field's Arg (k_near): as arg_t, with the quotient t = num/den from the COARSE
+// reciprocal and one residual correction (t0 = num r0, t = t0 + (num - den t0) r0: relative
+// error 2^-44 of |t| < 2^-8, i.e. < 2^-52 ABSOLUTE -- one FP64 operation fewer than the refined
+// reciprocal, and a shorter dependent chain).  Each term m Arg enters Phi with its absolute
+// error, like the log term (log_pos5); tests/test_fastmath.py bounds it in units of 2^-52.
+FM_HD double arg_n(double dx, double dy, const double2* __restrict__ tab)
+{
+    const int hx = hi_word(dx), hy = hi_word(dy);
+    const bool swap = fabs(dy) > fabs(dx);
+    const double mns = swap ? dx : dy;
+    const double mxs = swap ? dy : dx;
+    const double mn = fabs(mns), mx = fabs(mxs);
+    const double q0 = fabs(mns * rcp_approx(mxs));
+    const double y = q0 + kC[15];
+    const uint32_t jr = (uint32_t)lo_word(y);
+    const int j = (int)(jr < (uint32_t)ATAN_N ? jr : (uint32_t)ATAN_N);
+    const double c = y - kC[15];
+    const double num = fma_(-c, mx, mn);
+    const double den = fma_(c, mn, mx);
+    const double r0 = rcp_approx(den);
+    const double t0 = num * r0;
+    const double t = fma_(fma_(-den, t0, num), r0, t0);
+    const double t2 = t * t;
+    const double p = fma_(kC[6], t2, kC[7]);
+    const double at = fma_(p * t2, t, t);
+    const double2 T = tab[j];
+#ifdef FMM2D_ARG_NOLO
+    const double a = T.x + at;
+#else
+    const double a = T.x + (at + T.y);
+#endif
+    const bool neg = hx < 0;
+    const double2 O = (tab + OCT_ROW)[2 * (int)swap + (int)neg];
+    const double res = fma_(a, O.y, O.x);
     return from_bits(as_bits(res) | ((int64_t)(uint32_t)(hy & (int)0x80000000u) << 32));
 }
 
@@ -262,7 +323,7 @@ static inline void make_tables(Tables* T)
     for (int j = 0; j < LOG_N; ++j) {
         long double c = 1.0L + ((long double)j + 0.5L) / (long double)LOG_N;
         double ic = (double)(1.0L / c);
-        T->lg[j].x = ic;
+        T->lg[j].x = (j >= LOG_N / 2 ? 2.0 : 1.0) * ic;        // 2 ic_j for f >= 1.5 (log_reduce)
         // -log(ic) for f in [1, 1.5); -log(2 ic) = log(f/2) offset for f in [1.5, 2)
         T->lg[j].y = (double)(-logl((long double)ic * (j >= LOG_N / 2 ? 2.0L : 1.0L)));
     }
@@ -272,11 +333,16 @@ static inline void make_tables(Tables* T)
         T->at[j].x = hi;
         T->at[j].y = (double)(th - (long double)hi);
     }
-    // octant bases for arg_t (rows never reached by the clamped index j <= ATAN_N)
-    T->at[OCT_ROW].x = 0.0;
-    T->at[OCT_ROW].y = kC[12];
-    T->at[OCT_ROW + 1].x = kC[10];
-    T->at[OCT_ROW + 1].y = kC[10];
+    // octant rows {base, s} for arg_t / arg_n (never reached by the clamped index j <= ATAN_N),
+    // indexed by 2 swap + (dx < 0)
+    T->at[OCT_ROW + 0].x = 0.0;
+    T->at[OCT_ROW + 0].y = 1.0;
+    T->at[OCT_ROW + 1].x = kC[12];
+    T->at[OCT_ROW + 1].y = -1.0;
+    T->at[OCT_ROW + 2].x = kC[10];
+    T->at[OCT_ROW + 2].y = -1.0;
+    T->at[OCT_ROW + 3].x = kC[10];
+    T->at[OCT_ROW + 3].y = 1.0;
 }
 
 }  // namespace fm

@@ -52,6 +52,9 @@ constexpr int NEAR_UNROLL = FMM2D_NEAR_UNROLL;
 #ifndef FMM2D_NEAR_LOG5
 #define FMM2D_NEAR_LOG5 1         // degree-5 log1p (absolute error < 2^-52: tests/test_fastmath.py)
 #endif
+#ifndef FMM2D_NEAR_ARGN
+#define FMM2D_NEAR_ARGN 1         // Arg by fm::arg_n (coarse reciprocal + residual correction)
+#endif
 constexpr int NEAR_CHUNK = FMM2D_NEAR_CHUNK;    // >= 256: the chunk buffer doubles as reduction space
 static_assert(NEAR_CHUNK >= 2 * NEAR_T, "chunk buffer too small for the reduction");
 
@@ -93,7 +96,11 @@ __device__ __forceinline__ void pair(PairAcc& a, double dx, double dy, double mr
 #else
     const double l2 = fm::log_pos(r2, T.lg);
 #endif
-    const double th = fm::arg_t(dx, dy, T.at);                        // Arg dz
+#if FMM2D_NEAR_ARGN
+    const double th = fm::arg_n(dx, dy, T.at);                        // Arg dz (absolute error < 2^-51)
+#else
+    const double th = fm::arg_t(dx, dy, T.at);                        // Arg dz (<= 2 ulp)
+#endif
     const double ir2 = fm::rcp(r2);
     const double mr2 = mr * ir2;
     a.ar = fma(mr, l2, a.ar);

@@ -23,7 +23,7 @@ int main()
     std::uniform_real_distribution<double> U(-1.0, 1.0);
     std::uniform_real_distribution<double> E(-60.0, 60.0);
     double mlog = 0, marg = 0, mabs_log = 0, margn = 0;
-    double mlog5_abs = 0;
+    double mlog5_abs = 0, margn_abs = 0, margn_small_rel = 0;
     long pair_mismatch = 0;
     long n = 0;
     for (long k = 0; k < 4000000; ++k) {
@@ -55,10 +55,17 @@ int main()
         double lg5 = 0.5 * log_pos5(r2, T.lg);
         double sc = std::fmax(1.0, (double)fabsl(rl)) * 2.220446049250313e-16;
         mlog5_abs = std::fmax(mlog5_abs, (double)(fabsl((long double)lg5 - rl) / sc));
+        // near-field Arg (arg_n: coarse reciprocal + one residual correction): absolute error in
+        // units of 2^-52 max(1, |Arg|), and the relative error where |Arg| is small
+        double an = arg_n(dx, dy, T.at);
+        double sa = std::fmax(1.0, (double)fabsl(ra)) * 2.220446049250313e-16;
+        margn_abs = std::fmax(margn_abs, (double)(fabsl((long double)an - ra) / sa));
+        if (ra != 0.0L) margn_small_rel = std::fmax(margn_small_rel, (double)(fabsl(((long double)an - ra) / ra)));
+        if ((an < 0) != (a < 0) || (an == 0.0) != (a == 0.0)) pair_mismatch++;
         ++n;
     }
     double zero = log_pos(0.0, T.lg);
-    printf("{\"log5_max_abs_eps\": %.3f, ", mlog5_abs);
+    printf("{\"log5_max_abs_eps\": %.3f, \"argn_max_abs_eps\": %.3f, \"argn_max_rel\": %.3e, ", mlog5_abs, margn_abs, margn_small_rel);
     printf("\"n\": %ld, \"log_max_ulp\": %.3f, \"log_max_abs\": %.3e, \"arg_max_ulp\": %.3f, \"argneg_max_ulp\": %.3f, "
            "\"pair_mismatch\": %ld, \"log0_is_neg_inf\": %d, \"arg_pi\": %d, \"arg_zero\": %d}\n",
            n, mlog, mabs_log, marg, margn, pair_mismatch, (int)(std::isinf(zero) && zero < 0),
