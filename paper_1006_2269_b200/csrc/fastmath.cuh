@@ -62,6 +62,33 @@ struct Tables {
     double2 at[ATAN_N + 8];
 };
 
+// The near field's own tables (k_near, k_near_wide): the P2P loop is bound by shared-memory
+// wavefronts -- 32 lanes reading random 16-byte rows collide in the 8 bank groups (ncu: 9.4
+// wavefronts per LDS.128 against 4 ideal, the shared pipe 73 % busy) -- so
+//  - the atan table holds ONE double per row (atan(j/256) rounded; the low part is dropped, an
+//    absolute error < 2^-54): 8-byte rows, half the bytes per lookup;
+//  - both tables can be REPLICATED: copy k = lane mod R of row j sits at [j R + k], so each copy
+//    owns its own banks and only the lanes sharing a copy can collide.
+#ifndef FMM2D_NEAR_RL
+#define FMM2D_NEAR_RL 1            // copies of the log table (power of two)
+#endif
+#ifndef FMM2D_NEAR_RA
+#define FMM2D_NEAR_RA 1            // copies of the atan table (power of two)
+#endif
+constexpr int NRL = FMM2D_NEAR_RL, NRA = FMM2D_NEAR_RA;
+constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
+constexpr int LRL = ilog2c(NRL), LRA = ilog2c(NRA);
+static_assert((1 << LRL) == NRL && (1 << LRA) == NRA, "replication factors are powers of two");
+struct TablesN {
+    double2 lg[LOG_N * NRL];                       // {ic_j (2 ic_j for f >= 1.5), L_j}
+    double th[((ATAN_N + 1) * NRA + 1) & ~1];      // atan(j/256), j = 0..256
+    double2 oct[4];                                // {base, s} by 2 swap + (dx < 0)
+};
+struct AllTables {
+    Tables t;
+    TablesN n;
+};
+
 // [0..3] log1p series -1/6, 1/5, -1/4, 1/3, [4] -1/2, [5] unused, [6..7] atan series 1/5, -1/3,
 // [8] ln2 * 2^-20 (exact scaling of the double nearest ln 2), [9] unused, [10] pi/2, [11] unused,
 // [12] pi, [13] unused, [14] 2^52 + 1023 * 2^20 (exponent extraction), [15] 1.5 * 2^44
@@ -137,19 +164,35 @@ FM_HD double rcp(double x)
     return fma_(r, fma_(e, e, e), r);      // cubic step: err^3
 }
 
+// Operand forms matter on B200: an FP64 instruction with three distinct register operands
+// occupies the FP64 pipe for 3 cycles instead of 2 (register-file bandwidth; tools/fp64_mix.cu:
+// 0.66 against 0.91 of the nominal rate), so the near-field routines keep their constants out of
+// the register file -- literal constants (uniform registers / immediates) instead of loads from
+// __constant__ arrays, the small high-order coefficients as SHORT immediates (high word only:
+// 1/5 enters log1p and atan below 2^-40, so 20 mantissa bits are plenty) -- and are written so
+// that no FMA needs three different registers (q = p u, then q u + u).
+constexpr double K_FIFTH_SHORT = 0.20000004768371582;        // 0x3FC9999A00000000
+constexpr double K_THIRD = 1.0 / 3.0;
+constexpr double K_LN2_20 = 6.931471805599453094e-01 / 1048576.0;
+constexpr double K_MAGIC_E = 4503599627370496.0 + 1023.0 * 1048576.0;
+constexpr double K_MAGIC_Q = 1.5 * 17592186044416.0;
+
 // The reduction shared by log_pos / log_pos5 (header comment): j = the top 8 mantissa bits,
 // hw = (exponent + [f >= 1.5]) << 20 = E' << 20, u = r2 (ic_j 2^-E') - 1 = f ic_j - 1 exactly
 // as before (power-of-two scalings), e20 = (E' - 1023) 2^20.  Normal r2 < 2^1021.
+// LR: log2 of the row stride in rows (the near field's replicated table, TablesN: row j of copy k
+// at [j 2^LR + k], tab pointing at copy k's row 0).
+template <int LR = 0>
 FM_HD void log_reduce(double r2, const double2* __restrict__ tab, double& u, double& e20, double& Lj)
 {
     const int hi = hi_word(r2);
     // row j = the top LOG_BITS mantissa bits, as a byte offset (16-byte rows)
-    const uint32_t jb = ((uint32_t)hi >> (20 - LOG_BITS - 4)) & (uint32_t)((LOG_N - 1) << 4);
+    const uint32_t jb = ((uint32_t)hi >> (20 - LOG_BITS - 4 - LR)) & (uint32_t)((LOG_N - 1) << (4 + LR));
     const int hw = (int)(((uint32_t)hi + 0x00080000u) & 0xFFF00000u);
     const double2 T = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab) + jb);
     const double ics = make_double(hi_word(T.x) - hw + 0x3FF00000, lo_word(T.x));
     u = fma_(r2, ics, -1.0);
-    e20 = make_double(0x43300000, hw) - kC[14];
+    e20 = make_double(0x43300000, hw) - K_MAGIC_E;
     Lj = T.y;
 }
 
@@ -157,16 +200,18 @@ FM_HD void log_reduce(double r2, const double2* __restrict__ tab, double& u, dou
 // by the near-field kernel where only the absolute error of each term matters.  No
 // special case for r2 == 0 (coincident distinct points): there arg_t gives NaN, so
 // the pair's Phi and Phi' are non-finite anyway.
+template <int LR = 0>
 FM_HD double log_pos5(double r2, const double2* __restrict__ tab)
 {
     double u, e20, Lj;
-    log_reduce(r2, tab, u, e20, Lj);
-    // log1p(u) = u - u^2/2 + u^3/3 - u^4/4 + u^5/5
-    double p = fma_(kC[1], u, kC[2]);
-    p = fma_(p, u, kC[3]);
-    p = fma_(p, u, kC[4]);
-    const double lp = fma_(p, u * u, u);
-    const double r = fma_(e20, kC[8], Lj + lp);
+    log_reduce<LR>(r2, tab, u, e20, Lj);
+    // log1p(u) = u - u^2/2 + u^3/3 - u^4/4 + u^5/5 = u + u (u p(u))
+    double p = fma_(u, K_FIFTH_SHORT, -0.25);
+    p = fma_(p, u, K_THIRD);
+    p = fma_(p, u, -0.5);
+    const double q = p * u;
+    const double lp = fma_(q, u, u);
+    const double r = fma_(e20, K_LN2_20, Lj + lp);
     return r;                    // r2 == 0 gives a finite value; Arg(0) is NaN (see k_near)
 }
 
@@ -254,11 +299,12 @@ FM_HD double arg_t(double dx, double dy, const double2* __restrict__ tab)
 }
 
 // The near field's Arg (k_near): as arg_t, with the quotient t = num/den from the COARSE
-// reciprocal and one residual correction (t0 = num r0, t = t0 + (num - den t0) r0: relative
-// error 2^-44 of |t| < 2^-8, i.e. < 2^-52 ABSOLUTE -- one FP64 operation fewer than the refined
-// reciprocal, and a shorter dependent chain).  Each term m Arg enters Phi with its absolute
+// reciprocal and one correction (t0 = num r0, e = 1 - den r0, t = t0 + t0 e: relative error
+// e^2 < 2^-44 of |t| < 2^-8, i.e. < 2^-52 ABSOLUTE -- one FP64 operation fewer than the refined
+// reciprocal, e and t0 independent, no FMA with three different registers).  Each term m Arg enters Phi with its absolute
 // error, like the log term (log_pos5); tests/test_fastmath.py bounds it in units of 2^-52.
-FM_HD double arg_n(double dx, double dy, const double2* __restrict__ tab)
+// The table is TablesN's single-double atan(j/256) (no low part).
+FM_HD double arg_n(double dx, double dy, const double* __restrict__ th, const double2* __restrict__ oct)
 {
     const int hx = hi_word(dx), hy = hi_word(dy);
     const bool swap = fabs(dy) > fabs(dx);
@@ -266,26 +312,23 @@ FM_HD double arg_n(double dx, double dy, const double2* __restrict__ tab)
     const double mxs = swap ? dy : dx;
     const double mn = fabs(mns), mx = fabs(mxs);
     const double q0 = fabs(mns * rcp_approx(mxs));
-    const double y = q0 + kC[15];
+    const double y = q0 + K_MAGIC_Q;
     const uint32_t jr = (uint32_t)lo_word(y);
     const int j = (int)(jr < (uint32_t)ATAN_N ? jr : (uint32_t)ATAN_N);
-    const double c = y - kC[15];
+    const double c = y - K_MAGIC_Q;
     const double num = fma_(-c, mx, mn);
     const double den = fma_(c, mn, mx);
+    // t = num/den = t0 (1 + e + e^2 + ...), t0 = num r0, e = 1 - den r0 (|e| < 2^-22): t0 + t0 e
     const double r0 = rcp_approx(den);
+    const double e = fma_(-den, r0, 1.0);
     const double t0 = num * r0;
-    const double t = fma_(fma_(-den, t0, num), r0, t0);
+    const double t = fma_(t0, e, t0);
     const double t2 = t * t;
-    const double p = fma_(kC[6], t2, kC[7]);
+    const double p = fma_(t2, K_FIFTH_SHORT, -K_THIRD);
     const double at = fma_(p * t2, t, t);
-    const double2 T = tab[j];
-#ifdef FMM2D_ARG_NOLO
-    const double a = T.x + at;
-#else
-    const double a = T.x + (at + T.y);
-#endif
+    const double a = th[j * NRA] + at;                        // th: the lane's copy (TablesN)
     const bool neg = hx < 0;
-    const double2 O = (tab + OCT_ROW)[2 * (int)swap + (int)neg];
+    const double2 O = oct[2 * (int)swap + (int)neg];
     const double res = fma_(a, O.y, O.x);
     return from_bits(as_bits(res) | ((int64_t)(uint32_t)(hy & (int)0x80000000u) << 32));
 }
@@ -343,6 +386,18 @@ static inline void make_tables(Tables* T)
     T->at[OCT_ROW + 2].y = -1.0;
     T->at[OCT_ROW + 3].x = kC[10];
     T->at[OCT_ROW + 3].y = 1.0;
+}
+
+static inline void make_tables_n(TablesN* N)
+{
+    static Tables T;
+    make_tables(&T);
+    for (int j = 0; j < LOG_N; ++j)
+        for (int k = 0; k < NRL; ++k) N->lg[j * NRL + k] = T.lg[j];
+    for (size_t i = 0; i < sizeof(N->th) / sizeof(double); ++i) N->th[i] = 0.0;
+    for (int j = 0; j <= ATAN_N; ++j)
+        for (int k = 0; k < NRA; ++k) N->th[j * NRA + k] = (double)atanl((long double)j / (long double)ATAN_N);
+    for (int i = 0; i < 4; ++i) N->oct[i] = T.at[OCT_ROW + i];
 }
 
 }  // namespace fm

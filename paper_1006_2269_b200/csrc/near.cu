@@ -52,9 +52,6 @@ constexpr int NEAR_UNROLL = FMM2D_NEAR_UNROLL;
 #ifndef FMM2D_NEAR_LOG5
 #define FMM2D_NEAR_LOG5 1         // degree-5 log1p (absolute error < 2^-52: tests/test_fastmath.py)
 #endif
-#ifndef FMM2D_NEAR_ARGN
-#define FMM2D_NEAR_ARGN 1         // Arg by fm::arg_n (coarse reciprocal + residual correction)
-#endif
 constexpr int NEAR_CHUNK = FMM2D_NEAR_CHUNK;    // >= 256: the chunk buffer doubles as reduction space
 static_assert(NEAR_CHUNK >= 2 * NEAR_T, "chunk buffer too small for the reduction");
 
@@ -86,26 +83,53 @@ struct PairAcc {
 };
 
 // one ordered pair: Phi_i += m Log(dz), Phi'_i += m / dz  (REAL: Im m = 0)
+// the lane's view of the near-field tables (fm::TablesN in shared memory): its copy of each
+struct NearTab {
+    const double2* lg;
+    const double* th;
+    const double2* oct;
+    __device__ __forceinline__ NearTab(const fm::TablesN& N, int lane)
+        : lg(N.lg + (lane & (fm::NRL - 1))), th(N.th + (lane & (fm::NRA - 1))), oct(N.oct) {}
+};
+
 template <bool REAL>
 __device__ __forceinline__ void pair(PairAcc& a, double dx, double dy, double mr, double mi,
-                                     const fm::Tables& T)
+                                     const NearTab& T)
 {
     const double r2 = fma(dx, dx, dy * dy);
 #if FMM2D_NEAR_LOG5
-    const double l2 = fm::log_pos5(r2, T.lg);                         // log |dz|^2
+    const double l2 = fm::log_pos5<fm::LRL>(r2, T.lg);                // log |dz|^2
 #else
-    const double l2 = fm::log_pos(r2, T.lg);
+#error "k_near uses the degree-5 near-field log"
 #endif
-#if FMM2D_NEAR_ARGN
-    const double th = fm::arg_n(dx, dy, T.at);                        // Arg dz (absolute error < 2^-51)
-#else
-    const double th = fm::arg_t(dx, dy, T.at);                        // Arg dz (<= 2 ulp)
-#endif
+    const double th = fm::arg_n(dx, dy, T.th, T.oct);                 // Arg dz (absolute error < 2^-51)
     const double ir2 = fm::rcp(r2);
     const double mr2 = mr * ir2;
     a.ar = fma(mr, l2, a.ar);
     a.br = fma(mr, th, a.br);
     a.dr = fma(mr2, dx, a.dr);                                        // m conj(dz) / |dz|^2
+    a.di = fma(-mr2, dy, a.di);
+    if (!REAL) {
+        const double mi2 = mi * ir2;
+        a.ai = fma(mi, l2, a.ai);
+        a.bi = fma(mi, th, a.bi);
+        a.dr = fma(mi2, dy, a.dr);
+        a.di = fma(mi2, dx, a.di);
+    }
+}
+
+// the same with the general-purpose routines on fm::Tables (symmetric kernel's own leaf)
+template <bool REAL>
+__device__ __forceinline__ void pair_t(PairAcc& a, double dx, double dy, double mr, double mi, const fm::Tables& T)
+{
+    const double r2 = fma(dx, dx, dy * dy);
+    const double l2 = fm::log_pos5(r2, T.lg);
+    const double th = fm::arg_t(dx, dy, T.at);
+    const double ir2 = fm::rcp(r2);
+    const double mr2 = mr * ir2;
+    a.ar = fma(mr, l2, a.ar);
+    a.br = fma(mr, th, a.br);
+    a.dr = fma(mr2, dx, a.dr);
     a.di = fma(-mr2, dy, a.di);
     if (!REAL) {
         const double mi2 = mi * ir2;
@@ -145,11 +169,13 @@ __device__ __forceinline__ void l2p(const double2* __restrict__ B, int p, double
     }
 }
 
-__device__ __forceinline__ void load_tables(fm::Tables& T, const fm::Tables* __restrict__ g)
+template <class TT>
+__device__ __forceinline__ void load_tables(TT& T, const TT* __restrict__ g)
 {
+    static_assert(sizeof(TT) % 16 == 0, "tables are copied in 16-byte pieces");
     const double2* gs = (const double2*)g;
     double2* ss = (double2*)&T;
-    for (int k = threadIdx.x; k < (int)(sizeof(fm::Tables) / 16); k += blockDim.x) ss[k] = gs[k];
+    for (int k = threadIdx.x; k < (int)(sizeof(TT) / 16); k += blockDim.x) ss[k] = gs[k];
 }
 
 // first k >= b with k == g (mod G)
@@ -171,18 +197,19 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                                                  const int64_t* __restrict__ soff, const uint32_t* __restrict__ sidx,
                                                  const double4* __restrict__ src, const double* __restrict__ cx,
                                                  const double* __restrict__ cy, const double2* __restrict__ loc,
-                                                 const uint32_t* __restrict__ perm, const fm::Tables* __restrict__ gtab,
+                                                 const uint32_t* __restrict__ perm, const fm::TablesN* __restrict__ gtab,
                                                  double2* __restrict__ phi, double2* __restrict__ dphi,
                                                  const int64_t* __restrict__ m2p_off, const double4* __restrict__ m2p_acc,
                                                  double4* __restrict__ nacc, const uint32_t* __restrict__ lmap,
                                                  const double4* __restrict__ hsrc)
 {
     __shared__ double4 S[(NEAR_CHUNK > NEAR_TPT * NEAR_T) ? NEAR_CHUNK : NEAR_TPT * NEAR_T];
-    __shared__ fm::Tables T;
+    __shared__ fm::TablesN T;
     double4(*red)[NEAR_T] = reinterpret_cast<double4(*)[NEAR_T]>(S);   // after the last chunk
     __shared__ int cstart[33];
     __shared__ int cinfo[2];                 // [0] leaves in chunk, [1] chunk row of leaf t (-1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const NearTab NT(T, lane);
     int64_t t, q0, q1, segi = -1;
     if ((int64_t)blockIdx.x < nmain) {
         t = t0 + blockIdx.x;
@@ -206,9 +233,9 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tbar_s),
-                     "r"((uint32_t)sizeof(fm::Tables)) : "memory");
+                     "r"((uint32_t)sizeof(fm::TablesN)) : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"((uint32_t)__cvta_generic_to_shared(&T)), "l"(gtab), "r"((uint32_t)sizeof(fm::Tables)),
+                     ::"r"((uint32_t)__cvta_generic_to_shared(&T)), "l"(gtab), "r"((uint32_t)sizeof(fm::TablesN)),
                      "r"(tbar_s) : "memory");
     }
     bool tables_ready = false;              // (the mbarrier's init is ordered by the chunk barriers)
@@ -331,13 +358,13 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                 for (int k = g; k < kown; k += G) {
                     const double4 s = S[k];
 #pragma unroll
-                    for (int u = 0; u < NEAR_TPT; ++u) pair<REAL>(acc[u], A[u].x - s.x, A[u].y - s.y, s.z, s.w, T);
+                    for (int u = 0; u < NEAR_TPT; ++u) pair<REAL>(acc[u], A[u].x - s.x, A[u].y - s.y, s.z, s.w, NT);
                 }
 #pragma unroll NEAR_UNROLL
                 for (int k = first_in_class(kend, g, G); k < total; k += G) {
                     const double4 s = S[k];
 #pragma unroll
-                    for (int u = 0; u < NEAR_TPT; ++u) pair<REAL>(acc[u], A[u].x - s.x, A[u].y - s.y, s.z, s.w, T);
+                    for (int u = 0; u < NEAR_TPT; ++u) pair<REAL>(acc[u], A[u].x - s.x, A[u].y - s.y, s.z, s.w, NT);
                 }
                 // own leaf: neutralise j == i
                 for (int k = first_in_class(kown, g, G); k < kend; k += G) {
@@ -346,7 +373,7 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
                     for (int u = 0; u < NEAR_TPT; ++u) {
                         const bool x = (k == kown + i0 + la[u]);
                         pair<REAL>(acc[u], x ? 1.0 : A[u].x - s.x, x ? 0.0 : A[u].y - s.y, x ? 0.0 : s.z,
-                                   x ? 0.0 : s.w, T);
+                                   x ? 0.0 : s.w, NT);
                     }
                 }
             }
@@ -486,15 +513,16 @@ __global__ void __launch_bounds__(NEAR_T) k_near_wide(int p, int64_t t0, const u
                                                       const double4* __restrict__ src, const double* __restrict__ cx,
                                                       const double* __restrict__ cy, const double2* __restrict__ loc,
                                                       const uint32_t* __restrict__ perm,
-                                                      const fm::Tables* __restrict__ gtab, double2* __restrict__ phi,
+                                                      const fm::TablesN* __restrict__ gtab, double2* __restrict__ phi,
                                                       double2* __restrict__ dphi, const int64_t* __restrict__ m2p_off,
                                                       const double4* __restrict__ m2p_acc,
                                                       const uint32_t* __restrict__ lmap,
                                                       const double4* __restrict__ hsrc)
 {
-    __shared__ fm::Tables T;
+    __shared__ fm::TablesN T;
     load_tables(T, gtab);
     __syncthreads();
+    const NearTab NT(T, threadIdx.x & 31);
     const int64_t t = t0 + blockIdx.x;
     const uint32_t ts = off[t], te = off[t + 1];
     for (uint32_t i = ts + threadIdx.x; i < te; i += NEAR_T) {
@@ -508,7 +536,7 @@ __global__ void __launch_bounds__(NEAR_T) k_near_wide(int p, int64_t t0, const u
                 const double4 s = sp[j];
                 const bool self = (j == i) && (hm == 0xFFFFFFFFu);
                 pair<REAL>(acc, self ? 1.0 : me.x - s.x, self ? 0.0 : me.y - s.y, self ? 0.0 : s.z,
-                           self ? 0.0 : s.w, T);
+                           self ? 0.0 : s.w, NT);
             }
         }
         double fr, fi, gr, gi;
@@ -630,8 +658,8 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_SYM_MINB) k_near_sym(SymArgs A)
             for (int k = g; k < nt; k += G) {
                 const double4 s = S[k];
                 const bool xa = (k == sa), xb = (k == sb);
-                pair<REAL>(aa, xa ? 1.0 : PA.x - s.x, xa ? 0.0 : PA.y - s.y, xa ? 0.0 : s.z, xa ? 0.0 : s.w, T);
-                pair<REAL>(ab, xb ? 1.0 : PB.x - s.x, xb ? 0.0 : PB.y - s.y, xb ? 0.0 : s.z, xb ? 0.0 : s.w, T);
+                pair_t<REAL>(aa, xa ? 1.0 : PA.x - s.x, xa ? 0.0 : PA.y - s.y, xa ? 0.0 : s.z, xa ? 0.0 : s.w, T);
+                pair_t<REAL>(ab, xb ? 1.0 : PB.x - s.x, xb ? 0.0 : PB.y - s.y, xb ? 0.0 : s.z, xb ? 0.0 : s.w, T);
             }
         }
         // ---- upper leaves s > t: symmetric
@@ -781,9 +809,9 @@ __global__ void k_sym_index(int64_t nl, const int64_t* __restrict__ soff, const 
 inline unsigned grid_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
 // per-device table copy (built once on the host, long double evaluation)
-const fm::Tables* device_tables(int dev, int* rc)
+const fm::AllTables* device_tables(int dev, int* rc)
 {
-    static const fm::Tables* cache[64] = {nullptr};
+    static const fm::AllTables* cache[64] = {nullptr};
     static std::mutex mu;                            // plans may be built from several threads
     *rc = 0;
     if (dev < 0 || dev >= 64) {
@@ -792,10 +820,11 @@ const fm::Tables* device_tables(int dev, int* rc)
     }
     std::lock_guard<std::mutex> lk(mu);
     if (cache[dev]) return cache[dev];
-    static fm::Tables h;
-    fm::make_tables(&h);
-    fm::Tables* d = nullptr;
-    cudaError_t e = cudaMalloc((void**)&d, sizeof(fm::Tables));
+    static fm::AllTables h;
+    fm::make_tables(&h.t);
+    fm::make_tables_n(&h.n);
+    fm::AllTables* d = nullptr;
+    cudaError_t e = cudaMalloc((void**)&d, sizeof(fm::AllTables));
     if (e == cudaSuccess) e = cudaMemcpy(d, &h, sizeof(h), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         fmm2d_set_last_cuda_error(e, "device_tables", __FILE__, __LINE__);
@@ -901,7 +930,9 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi, int mode)
     const double2* loc = P->lcl[L];
     const uint32_t* off = P->boff + P->obase[L];
     const bool real = (P->flags & FMM2D_REAL_STRENGTHS) != 0;
-    const fm::Tables* tab = (const fm::Tables*)P->tables;
+    // P->tables: fm::AllTables {Tables t (rr.cu, symmetric kernel), TablesN n (k_near, k_near_wide)}
+    const fm::Tables* tab = &((const fm::AllTables*)P->tables)->t;
+    const fm::TablesN* tabn = &((const fm::AllTables*)P->tables)->n;
     const int64_t* m2p_off = (P->rr_nm2p > 0) ? P->rr_m2p.off : nullptr;     // r/R exchange
     double4* nacc = (mode == 1) ? P->nacc : nullptr;
     if (mode == 2) {
@@ -952,12 +983,12 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi, int mode)
         if (real)
             k_near<true><<<grid, NEAR_T, 0, P->stream>>>(G, P->p, t0, nl, P->near_seg_off, P->near_segs,
                                                         P->near_part, P->stats.max_leaf, off, P->near.off,
-                                                        P->near.idx, P->src, cx, cy, loc, P->perm, tab, phi, dphi,
+                                                        P->near.idx, P->src, cx, cy, loc, P->perm, tabn, phi, dphi,
                                                         m2p_off, P->rr_acc, nacc, P->lmap, P->hsrc);
         else
             k_near<false><<<grid, NEAR_T, 0, P->stream>>>(G, P->p, t0, nl, P->near_seg_off, P->near_segs,
                                                          P->near_part, P->stats.max_leaf, off, P->near.off,
-                                                         P->near.idx, P->src, cx, cy, loc, P->perm, tab, phi, dphi,
+                                                         P->near.idx, P->src, cx, cy, loc, P->perm, tabn, phi, dphi,
                                                          m2p_off, P->rr_acc, nacc, P->lmap, P->hsrc);
         if (P->near_nsplit > 0) {
             fmm2d::note_launch();
@@ -969,11 +1000,11 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi, int mode)
     } else {
         if (real)
             k_near_wide<true><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, t0, off, P->near.off, P->near.idx,
-                                                                     P->src, cx, cy, loc, P->perm, tab, phi, dphi,
+                                                                     P->src, cx, cy, loc, P->perm, tabn, phi, dphi,
                                                                      m2p_off, P->rr_acc, P->lmap, P->hsrc);
         else
             k_near_wide<false><<<(unsigned)nl, NEAR_T, 0, P->stream>>>(P->p, t0, off, P->near.off, P->near.idx,
-                                                                      P->src, cx, cy, loc, P->perm, tab, phi, dphi,
+                                                                      P->src, cx, cy, loc, P->perm, tabn, phi, dphi,
                                                                       m2p_off, P->rr_acc, P->lmap, P->hsrc);
     }
     fmm2d::note_launch();

@@ -19,6 +19,8 @@ int main()
 {
     Tables T;
     make_tables(&T);
+    static TablesN N;
+    make_tables_n(&N);
     std::mt19937_64 g(12345);
     std::uniform_real_distribution<double> U(-1.0, 1.0);
     std::uniform_real_distribution<double> E(-60.0, 60.0);
@@ -52,12 +54,12 @@ int main()
         if (arg_t(dx, dy, T.at) != a) pair_mismatch++;       // table-based octant: bit-identical
         margn = std::fmax(margn, ulp_err(thn, rn));
         // near-field log: degree-5 series, absolute error in units of 2^-52 max(1, |log|)
-        double lg5 = 0.5 * log_pos5(r2, T.lg);
+        double lg5 = 0.5 * log_pos5<LRL>(r2, N.lg);
         double sc = std::fmax(1.0, (double)fabsl(rl)) * 2.220446049250313e-16;
         mlog5_abs = std::fmax(mlog5_abs, (double)(fabsl((long double)lg5 - rl) / sc));
         // near-field Arg (arg_n: coarse reciprocal + one residual correction): absolute error in
         // units of 2^-52 max(1, |Arg|), and the relative error where |Arg| is small
-        double an = arg_n(dx, dy, T.at);
+        double an = arg_n(dx, dy, N.th, N.oct);
         double sa = std::fmax(1.0, (double)fabsl(ra)) * 2.220446049250313e-16;
         margn_abs = std::fmax(margn_abs, (double)(fabsl((long double)an - ra) / sa));
         if (ra != 0.0L) margn_small_rel = std::fmax(margn_small_rel, (double)(fabsl(((long double)an - ra) / ra)));
