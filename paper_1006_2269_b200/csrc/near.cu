@@ -18,6 +18,7 @@
 // result is stored at the input position perm[i].
 // Leaves larger than NEAR_CHUNK (only when nlevels forces a shallow tree) take
 // k_near_wide, which reads sources straight from global memory.
+#include <cstdlib>
 #include <mutex>
 #include <cub/cub.cuh>
 
@@ -97,11 +98,7 @@ __device__ __forceinline__ void pair(PairAcc& a, double dx, double dy, double mr
                                      const NearTab& T)
 {
     const double r2 = fma(dx, dx, dy * dy);
-#if FMM2D_NEAR_LOG5
-    const double l2 = fm::log_pos5<fm::LRL>(r2, T.lg);                // log |dz|^2
-#else
-#error "k_near uses the degree-5 near-field log"
-#endif
+    const double l2 = fm::log_pos5<fm::LRL>(r2, T.lg);                // log |dz|^2 (absolute error < 2^-52)
     const double th = fm::arg_n(dx, dy, T.th, T.oct);                 // Arg dz (absolute error < 2^-51)
     const double ir2 = fm::rcp(r2);
     const double mr2 = mr * ir2;
@@ -255,7 +252,7 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
 #endif
     const uint32_t ts = off[t], te = off[t + 1];
     const int nt = (int)(te - ts);
-    const int tile = NEAR_T / G;                 // target tuples per pass
+    const int tile = (int)blockDim.x / G;        // target tuples per pass (the launch picks the block size)
     for (int i0 = 0; i0 < nt; i0 += NEAR_TPT * tile) {
         const int tp = tid % tile;
         const int g = tid / tile;
@@ -325,7 +322,7 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
             }
             if (false)
 #endif
-            for (int l = warp; l < nl; l += NEAR_T / 32) {
+            for (int l = warp; l < nl; l += (int)blockDim.x / 32) {
                 const uint32_t lf = sidx[q + l];
                 // own / replicated leaf: rows at its position; halo leaf (sharded plans): in hsrc
                 const uint32_t hm = lmap ? lmap[lf] : 0xFFFFFFFFu;
@@ -384,7 +381,7 @@ __global__ void __launch_bounds__(NEAR_T, FMM2D_NEAR_MINB) k_near(int G, int p, 
         for (int u = 0; u < NEAR_TPT; ++u) red[u][tid] = pack(acc[u]);
         __syncthreads();
         // finalize: NEAR_TPT*tile targets, thread k < ni handles target k (tuple k/TPT, slot k%TPT)
-        for (int kk = tid; kk < ni; kk += NEAR_T) {
+        for (int kk = tid; kk < ni; kk += (int)blockDim.x) {
             const int ptp = kk / NEAR_TPT, slot = kk % NEAR_TPT;
             double4 acc = red[slot][ptp];
             for (int gg = 1; gg < G; ++gg) {
@@ -977,16 +974,34 @@ int run_near(fmm2d_plan* P, double2* phi, double2* dphi, int mode)
     if (P->stats.max_leaf <= NEAR_CHUNK) {
         // target tuples per leaf, groups so that tuples * G <= 128
         const int pairs = (std::max(1, P->stats.max_leaf) + NEAR_TPT - 1) / NEAR_TPT;
-        int G = NEAR_T / std::min(pairs, NEAR_T);
-        if (G < 1) G = 1;
+        // block size 64 / 96 / 128: the one whose G = T / tuples groups leave the fewest idle lanes
+        // (C5: 12 tuples -> 96 threads, 8 groups, every lane busy; 128 threads would idle 8)
+        int T = NEAR_T, G = 1;
+        double best = -1.0;
+        for (int cand = NEAR_T; cand >= 64; cand -= 32) {
+            const int g = std::max(1, cand / std::min(pairs, cand));
+            const double util = (double)std::min(pairs, cand) * g / cand;
+            if (util > best + 1e-9) {
+                best = util;
+                T = cand;
+                G = g;
+            }
+        }
+        if (const char* e = getenv("FMM2D_NEAR_THREADS")) {      // tuning / tests: force the block size
+            const int v = atoi(e);
+            if (v == 64 || v == 96 || v == 128) {
+                T = v;
+                G = std::max(1, T / std::min(pairs, T));
+            }
+        }
         const unsigned grid = (unsigned)(nl + P->near_nseg);
         if (real)
-            k_near<true><<<grid, NEAR_T, 0, P->stream>>>(G, P->p, t0, nl, P->near_seg_off, P->near_segs,
+            k_near<true><<<grid, T, 0, P->stream>>>(G, P->p, t0, nl, P->near_seg_off, P->near_segs,
                                                         P->near_part, P->stats.max_leaf, off, P->near.off,
                                                         P->near.idx, P->src, cx, cy, loc, P->perm, tabn, phi, dphi,
                                                         m2p_off, P->rr_acc, nacc, P->lmap, P->hsrc);
         else
-            k_near<false><<<grid, NEAR_T, 0, P->stream>>>(G, P->p, t0, nl, P->near_seg_off, P->near_segs,
+            k_near<false><<<grid, T, 0, P->stream>>>(G, P->p, t0, nl, P->near_seg_off, P->near_segs,
                                                          P->near_part, P->stats.max_leaf, off, P->near.off,
                                                          P->near.idx, P->src, cx, cy, loc, P->perm, tabn, phi, dphi,
                                                          m2p_off, P->rr_acc, nacc, P->lmap, P->hsrc);
