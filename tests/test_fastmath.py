@@ -9,11 +9,15 @@ import subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_fastmath_ulps(tmp_path):
+def _run(tmp_path, *flags):
     exe = tmp_path / "test_fastmath"
-    subprocess.check_call(["g++", "-O2", "-ffp-contract=off", "-o", str(exe),
+    subprocess.check_call(["g++", "-O2", "-ffp-contract=off", *flags, "-o", str(exe),
                            os.path.join(ROOT, "tools", "test_fastmath.cpp")])
-    r = json.loads(subprocess.check_output([str(exe)]).decode())
+    return json.loads(subprocess.check_output([str(exe)]).decode())
+
+
+def test_fastmath_ulps(tmp_path):
+    r = _run(tmp_path)
     assert r["n"] > 3_000_000
     assert r["log_max_ulp"] <= 2.0
     assert r["log_max_abs"] <= 1e-14          # |log|dz|| up to ~42 here: < 1 ulp
@@ -23,3 +27,16 @@ def test_fastmath_ulps(tmp_path):
     # near-field log (k_near): each term enters Phi with its ABSOLUTE error, so the bar is
     # in units of eps = 2^-52 of max(1, |value|)
     assert r["log5_max_abs_eps"] <= 1.0           # degree-5 log1p, |u| < 2^-9
+    # near-field Arg (arg_n: coarse reciprocal + one correction, single-double atan table): absolute
+    # error in the same units, and small angles keep a relative error far below the 1e-12 parity bar
+    assert r["argn_max_abs_eps"] <= 2.0 and r["argn_max_rel"] <= 2e-13
+
+
+def test_fastmath_near_field_worst_case_reciprocal(tmp_path):
+    """The device's reciprocal estimate (MUFU.RCP64H) is only ~2^-22 accurate; the host stand-in
+    is perturbed by +-2^-22 on top of its float rounding, and by the replicated-table layout."""
+    for sign in ("(1.0)", "(-1.0)"):
+        r = _run(tmp_path, f"-DFM_HOST_RCP_PERTURB={sign}", "-DFMM2D_NEAR_RL=2", "-DFMM2D_NEAR_RA=4")
+        assert r["argn_max_abs_eps"] <= 2.0 and r["argn_max_rel"] <= 2e-13
+        assert r["log5_max_abs_eps"] <= 1.0 and r["pair_mismatch"] == 0
+        assert r["log_max_ulp"] <= 2.0 and r["arg_max_ulp"] <= 2.0
