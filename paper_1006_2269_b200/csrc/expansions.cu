@@ -232,26 +232,50 @@ __device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, const doub
         if (k < P) wk = cmul(wk, w);
     }
     const double2 a0 = M[0];
+#if FMM2D_M2L_LB > 0
+    // The contraction in blocks of FMM2D_M2L_LB output coefficients, k outermost inside a block:
+    // 2 LB independent FMA chains, so consecutive FMAs of one chain are 2 LB instructions apart
+    // (the shared FP64 pipe's dependent-issue latency is ~28 cycles).
+    double2 beta[L1 - L0];
+#pragma unroll
+    for (int lb = L0; lb < L1; lb += FMM2D_M2L_LB) {
+#pragma unroll
+        for (int l = lb; l < lb + FMM2D_M2L_LB && l < L1; ++l) beta[l - L0] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 1; k <= P; ++k) {
+#pragma unroll
+            for (int l = lb; l < lb + FMM2D_M2L_LB && l < L1; ++l) {
+                const double c = c_m2l[l * M2L_CS + k - 1 + M2L_KOFF];
+                beta[l - L0].x = fma(c, al[k].x, beta[l - L0].x);
+                beta[l - L0].y = fma(c, al[k].y, beta[l - L0].y);
+            }
+        }
+    }
+#endif
     double2 izl = make_double2(1.0, 0.0);
 #pragma unroll
     for (int l = 0; l < L1; ++l) {
         if (l >= 1) izl = cmul(izl, iz);            // z0^-l
         if (l < L0) continue;
-        double2 beta = make_double2(0.0, 0.0);
+#if FMM2D_M2L_LB > 0
+        const double2 bl = beta[l - L0];
+#else
+        double2 bl = make_double2(0.0, 0.0);
 #pragma unroll
         for (int k = 1; k <= P; ++k) {
             const double c = c_m2l[l * M2L_CS + k - 1 + M2L_KOFF];
-            beta.x = fma(c, al[k].x, beta.x);
-            beta.y = fma(c, al[k].y, beta.y);
+            bl.x = fma(c, al[k].x, bl.x);
+            bl.y = fma(c, al[k].y, bl.y);
         }
+#endif
         double2 v;
         if (l == 0) {
             // a_0 Log(c_t - c_s), componentwise difference (DESIGN R2)
             const double tx = ctx - csx, ty = cty - csy;
             const double2 lg = make_double2(0.5 * log(r2), atan2(ty, tx));
-            v = cadd(cmul(a0, lg), beta);
+            v = cadd(cmul(a0, lg), bl);
         } else {
-            const double2 t = csub(beta, cscale(a0, 1.0 / l));
+            const double2 t = csub(bl, cscale(a0, 1.0 / l));
             v = cmul(t, izl);
         }
         acc[l - L0] = cadd(acc[l - L0], v);
@@ -335,6 +359,9 @@ __device__ __forceinline__ void m2l_target_warp(const M2LArgs& A, int64_t g, int
     }
 }
 
+#ifndef FMM2D_M2L_LB
+#define FMM2D_M2L_LB 0            // 0: one output coefficient at a time (the compiler interleaves)
+#endif
 #ifndef FMM2D_M2L_PREFETCH
 #define FMM2D_M2L_PREFETCH 1   // next entry's box index loaded one pair ahead (M2L 19.26 -> 19.02 ms at C5)
 #endif
