@@ -189,6 +189,16 @@ __global__ void __launch_bounds__(128) k_m2m(int64_t b0, int64_t b1, const doubl
 }
 
 // ---------------------------------------------------------------- M2L (A6/A7)
+// compile-time options of the M2L pair body (defaults: measured best at C5)
+#ifndef FMM2D_M2L_POW2
+#define FMM2D_M2L_POW2 0          // bit 0: pre-scale powers by doubling, bit 1: post-scale powers
+#endif
+#ifndef FMM2D_M2L_LB
+#define FMM2D_M2L_LB 18           // 0: one output coefficient at a time; 18: C5 M2L 19.26 -> 17.40 ms
+#endif
+#ifndef FMM2D_M2L_PREFETCH
+#define FMM2D_M2L_PREFETCH 1   // next entry's box index loaded one pair ahead (M2L 19.26 -> 19.02 ms at C5)
+#endif
 struct M2LArgs {
     const int64_t* woff[FMM2D_MAXL + 1];
     const uint32_t* widx[FMM2D_MAXL + 1];
@@ -225,12 +235,29 @@ __device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, const doub
     const double2 w = make_double2(-iz.x, -iz.y);
     // pre-scale: alpha_k = a_k (-1/z0)^k
     double2 al[P + 1];
+#if FMM2D_M2L_POW2 & 1
+    {   // powers by doubling: w^k = w^h w^(k-h), h the largest power of two below k -- a
+        // dependent chain of <= 5 complex products instead of P - 1 (the FP64 pipe's
+        // dependent-issue latency is ~28 cycles)
+        double2 pw[P + 1];
+        pw[1] = w;
+#pragma unroll
+        for (int k = 2; k <= P; ++k) {
+            int h = 1;
+            while (2 * h < k) h *= 2;
+            pw[k] = cmul(pw[h], pw[k - h]);
+        }
+#pragma unroll
+        for (int k = 1; k <= P; ++k) al[k] = cmul(M[k], pw[k]);
+    }
+#else
     double2 wk = w;
 #pragma unroll
     for (int k = 1; k <= P; ++k) {
         al[k] = cmul(M[k], wk);
         if (k < P) wk = cmul(wk, w);
     }
+#endif
     const double2 a0 = M[0];
 #if FMM2D_M2L_LB > 0
     // The contraction in blocks of FMM2D_M2L_LB output coefficients, k outermost inside a block:
@@ -252,10 +279,25 @@ __device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, const doub
         }
     }
 #endif
+#if FMM2D_M2L_POW2 & 2
+    double2 ipw[L1 > 2 ? L1 : 2];
+    ipw[0] = make_double2(1.0, 0.0);
+    ipw[1] = iz;
+#pragma unroll
+    for (int l = 2; l < L1; ++l) {
+        int h = 1;
+        while (2 * h < l) h *= 2;
+        ipw[l] = cmul(ipw[h], ipw[l - h]);
+    }
+#endif
     double2 izl = make_double2(1.0, 0.0);
 #pragma unroll
     for (int l = 0; l < L1; ++l) {
+#if FMM2D_M2L_POW2 & 2
+        izl = ipw[l];
+#else
         if (l >= 1) izl = cmul(izl, iz);            // z0^-l
+#endif
         if (l < L0) continue;
 #if FMM2D_M2L_LB > 0
         const double2 bl = beta[l - L0];
@@ -359,12 +401,6 @@ __device__ __forceinline__ void m2l_target_warp(const M2LArgs& A, int64_t g, int
     }
 }
 
-#ifndef FMM2D_M2L_LB
-#define FMM2D_M2L_LB 0            // 0: one output coefficient at a time (the compiler interleaves)
-#endif
-#ifndef FMM2D_M2L_PREFETCH
-#define FMM2D_M2L_PREFETCH 1   // next entry's box index loaded one pair ahead (M2L 19.26 -> 19.02 ms at C5)
-#endif
 #ifndef FMM2D_M2L_MINB
 #define FMM2D_M2L_MINB 2
 #endif
