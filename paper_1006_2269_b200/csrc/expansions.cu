@@ -190,6 +190,9 @@ __global__ void __launch_bounds__(128) k_m2m(int64_t b0, int64_t b1, const doubl
 
 // ---------------------------------------------------------------- M2L (A6/A7)
 // compile-time options of the M2L pair body (defaults: measured best at C5)
+#ifndef FMM2D_M2L_RCP
+#define FMM2D_M2L_RCP 1            // 1 / r2 by MUFU + one cubic Newton step (C5 M2L 16.53 -> 15.84 ms)
+#endif
 #ifndef FMM2D_M2L_POW2
 #define FMM2D_M2L_POW2 0          // bit 0: pre-scale powers by doubling, bit 1: post-scale powers
 #endif
@@ -230,7 +233,19 @@ __device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, const doub
     // z0 = c_s - c_t and 1/z0
     const double dx = csx - ctx, dy = csy - cty;
     const double r2 = dx * dx + dy * dy;
+#if FMM2D_M2L_RCP
+    // 1 / r2 by the reciprocal estimate and one cubic Newton step (~1 ulp) instead of the IEEE
+    // division's longer dependent chain: everything in the pair waits for it
+    double ir2;
+    {
+        double r0;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(r2));
+        const double e = fma(-r2, r0, 1.0);
+        ir2 = fma(r0, fma(e, e, e), r0);
+    }
+#else
     const double ir2 = 1.0 / r2;
+#endif
     const double2 iz = make_double2(dx * ir2, -dy * ir2);
     const double2 w = make_double2(-iz.x, -iz.y);
     // pre-scale: alpha_k = a_k (-1/z0)^k
