@@ -190,6 +190,9 @@ __global__ void __launch_bounds__(128) k_m2m(int64_t b0, int64_t b1, const doubl
 
 // ---------------------------------------------------------------- M2L (A6/A7)
 // compile-time options of the M2L pair body (defaults: measured best at C5)
+#ifndef FMM2D_M2L_LOGSPLIT
+#define FMM2D_M2L_LOGSPLIT 1       // the a_0 Log term of coefficient 0 in its own kernel (rr.cu: k_m2l_log)
+#endif
 #ifndef FMM2D_M2L_RCP
 #define FMM2D_M2L_RCP 1            // 1 / r2 by MUFU + one cubic Newton step (C5 M2L 16.53 -> 15.84 ms)
 #endif
@@ -202,30 +205,12 @@ __global__ void __launch_bounds__(128) k_m2m(int64_t b0, int64_t b1, const doubl
 #ifndef FMM2D_M2L_PREFETCH
 #define FMM2D_M2L_PREFETCH 1   // next entry's box index loaded one pair ahead (M2L 19.26 -> 19.02 ms at C5)
 #endif
-struct M2LArgs {
-    const int64_t* woff[FMM2D_MAXL + 1];
-    const uint32_t* widx[FMM2D_MAXL + 1];
-    const int64_t* xoff[FMM2D_MAXL + 1];     // cross-level entries (parent merge) or nullptr
-    const uint32_t* xidx[FMM2D_MAXL + 1];
-    int64_t base[FMM2D_MAXL + 2];
-    int64_t lo[FMM2D_MAXL + 1];       // target boxes of level l: [lo[l], lo[l] + (pre[l+1] - pre[l]))
-    int64_t pre[FMM2D_MAXL + 2];      // work prefix over levels 1..L
-    const uint32_t* order;            // [pre[L+1]] target box of each work item (level-local id)
-    int L;
-    const double* cx;
-    const double* cy;
-    // per level: stored expansions (level-local box b at mpl[l] + b (p+1)) and the stored
-    // range [slo, shi) -- one GPU: every box; other sources are imported (mhalo + hmap)
-    const double2* mpl[FMM2D_MAXL + 1];
-    double2* lcl[FMM2D_MAXL + 1];
-    int64_t slo[FMM2D_MAXL + 1], shi[FMM2D_MAXL + 1];
-    const double2* mhalo;
-    const uint32_t* hmap;             // [global box id] import slot
-};
+// (struct M2LArgs: fmm2d_internal.cuh -- shared with the log-term kernel in rr.cu)
 
 // One weak pair: the multipole M of source box s (global id, for its centre) into
 // coefficients l in [L0, L1) of the local about (ctx, cty), accumulated into acc.
-template <int P, int L0, int L1>
+// LOGT = false leaves out the a_0 Log(c_t - c_s) term of coefficient 0 (k_m2l_log adds it).
+template <int P, int L0, int L1, bool LOGT = true>
 __device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, const double2* __restrict__ M, double ctx,
                                          double cty, double2 (&acc)[L1 - L0])
 {
@@ -327,10 +312,14 @@ __device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, const doub
 #endif
         double2 v;
         if (l == 0) {
-            // a_0 Log(c_t - c_s), componentwise difference (DESIGN R2)
-            const double tx = ctx - csx, ty = cty - csy;
-            const double2 lg = make_double2(0.5 * log(r2), atan2(ty, tx));
-            v = cadd(cmul(a0, lg), bl);
+            if (LOGT) {
+                // a_0 Log(c_t - c_s), componentwise difference (DESIGN R2)
+                const double tx = ctx - csx, ty = cty - csy;
+                const double2 lg = make_double2(0.5 * log(r2), atan2(ty, tx));
+                v = cadd(cmul(a0, lg), bl);
+            } else {
+                v = bl;
+            }
         } else {
             const double2 t = csub(bl, cscale(a0, 1.0 / l));
             v = cmul(t, izl);
@@ -342,7 +331,7 @@ __device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, const doub
 // Output coefficients l in [L0, L1) of target box g (level lev, level-local b), summed
 // over the entries j = ja, ja + js, ... < jb of its weak list followed by its cross-level
 // (parent merge) list.
-template <int P, int L0, int L1>
+template <int P, int L0, int L1, bool LOGT = true>
 __device__ __forceinline__ void m2l_accum(const M2LArgs& A, int64_t g, int lev, int64_t b, int64_t ja, int64_t js,
                                           double2 (&acc)[L1 - L0])
 {
@@ -374,19 +363,19 @@ __device__ __forceinline__ void m2l_accum(const M2LArgs& A, int64_t g, int lev, 
         // stored multipole (own / replicated box), or an imported one (sharded plans' halo)
         const double2* M = (bs >= A.slo[sl] && bs < A.shi[sl]) ? A.mpl[sl] + (int64_t)bs * (P + 1)
                                                               : A.mhalo + (int64_t)A.hmap[s] * (P + 1);
-        m2l_pair<P, L0, L1>(A, s, M, ctx, cty, acc);
+        m2l_pair<P, L0, L1, LOGT>(A, s, M, ctx, cty, acc);
     }
 }
 
 // One thread computes output coefficients l in [L0, L1) of one target box.
-template <int P, int L0, int L1>
+template <int P, int L0, int L1, bool LOGT = true>
 __device__ __forceinline__ void m2l_target(const M2LArgs& A, int64_t g, int lev)
 {
     const int64_t b = g - A.base[lev];
     double2 acc[L1 - L0];
 #pragma unroll
     for (int l = 0; l < L1 - L0; ++l) acc[l] = make_double2(0.0, 0.0);
-    m2l_accum<P, L0, L1>(A, g, lev, b, 0, 1, acc);
+    m2l_accum<P, L0, L1, LOGT>(A, g, lev, b, 0, 1, acc);
     double2* out = A.lcl[lev] + b * (P + 1);
 #pragma unroll
     for (int l = L0; l < L1; ++l) out[l] = acc[l - L0];
@@ -449,7 +438,7 @@ __global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l(M2LArgs A)
     constexpr int E1 = (2 * H < P + 1) ? 2 * H : P + 1;
     constexpr int E2 = (3 * H < P + 1) ? 3 * H : P + 1;
     if constexpr (NS == 1) {
-        m2l_target<P, 0, P + 1>(A, g, lev);
+        m2l_target<P, 0, P + 1, !FMM2D_M2L_LOGSPLIT>(A, g, lev);     // (k_m2l_log adds the log terms)
     } else if constexpr (NS == 2) {
         if (part == 0) m2l_target<P, 0, H>(A, g, lev);
         else           m2l_target<P, H, P + 1>(A, g, lev);
@@ -614,6 +603,16 @@ template <int P>
 #endif
 constexpr int m2l_split() { return P <= FMM2D_M2L_SPLIT_P ? 1 : (P <= 26 ? 2 : 3); }
 
+template <int P, int NS>
+int m2l_long_p(fmm2d_plan* Pl, const M2LArgs& A)
+{
+    k_m2l_long<P, NS><<<grid_for(Pl->m2l_nlong * NS * 32, M2L_T), M2L_T, 0, Pl->stream>>>(A, Pl->m2l_long,
+                                                                                        Pl->m2l_nlong);
+    fmm2d::note_launch();
+    FMM2D_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
 template <int P>
 int m2l_p(fmm2d_plan* Pl)
 {
@@ -659,16 +658,14 @@ int m2l_p(fmm2d_plan* Pl)
         k_m2l_gs<P, NS><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(Pl->m2l_cap, nwarps)), 32, 0, st>>>(A, nwarps);
     } else {
         k_m2l<P, NS><<<grid_for(nthreads, M2L_T), M2L_T, 0, st>>>(A);
+        fmm2d::note_launch();
+        FMM2D_CUDA_TRY(cudaGetLastError());
+        if (NS == 1 && FMM2D_M2L_LOGSPLIT) FMM2D_TRY(m2l_log_terms(Pl, A, P + 1));
+        return Pl->m2l_nlong > 0 ? m2l_long_p<P, NS>(Pl, A) : 0;
     }
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
-    if (Pl->m2l_nlong > 0) {
-        k_m2l_long<P, NS><<<grid_for(Pl->m2l_nlong * NS * 32, M2L_T), M2L_T, 0, st>>>(A, Pl->m2l_long,
-                                                                                  Pl->m2l_nlong);
-        fmm2d::note_launch();
-        FMM2D_CUDA_TRY(cudaGetLastError());
-    }
-    return 0;
+    return Pl->m2l_nlong > 0 ? m2l_long_p<P, NS>(Pl, A) : 0;
 }
 
 template <int P>

@@ -178,6 +178,29 @@ int prepare_near_sym(fmm2d_plan* P);
 int gather_strengths(fmm2d_plan* P, const double2* m);
 int run_upward_top(fmm2d_plan* P);
 int run_rr_p2l(fmm2d_plan* P);
+// M2L kernel arguments (expansions.cu) and the log-term kernel (rr.cu, beside the table-driven
+// log / Arg): adds sum_s a_0(s) Log(c_t - c_s) to coefficient 0 of every short-list target
+struct M2LArgs {
+    const int64_t* woff[FMM2D_MAXL + 1];
+    const uint32_t* widx[FMM2D_MAXL + 1];
+    const int64_t* xoff[FMM2D_MAXL + 1];     // cross-level entries (parent merge) or nullptr
+    const uint32_t* xidx[FMM2D_MAXL + 1];
+    int64_t base[FMM2D_MAXL + 2];
+    int64_t lo[FMM2D_MAXL + 1];       // target boxes of level l: [lo[l], lo[l] + (pre[l+1] - pre[l]))
+    int64_t pre[FMM2D_MAXL + 2];      // work prefix over levels 1..L
+    const uint32_t* order;            // [pre[L+1]] target box of each work item (level-local id)
+    int L;
+    const double* cx;
+    const double* cy;
+    // per level: stored expansions (level-local box b at mpl[l] + b (p+1)) and the stored
+    // range [slo, shi) -- one GPU: every box; other sources are imported (mhalo + hmap)
+    const double2* mpl[FMM2D_MAXL + 1];
+    double2* lcl[FMM2D_MAXL + 1];
+    int64_t slo[FMM2D_MAXL + 1], shi[FMM2D_MAXL + 1];
+    const double2* mhalo;
+    const uint32_t* hmap;             // [global box id] import slot
+};
+int m2l_log_terms(fmm2d_plan* P, const M2LArgs& A, int p1);
 int run_rr_m2p(fmm2d_plan* P);
 // sharding (shard.cu)
 int64_t box_start_host(int64_t n, int l, int64_t b);

@@ -422,7 +422,63 @@ int rr_m2p_p(fmm2d_plan* Pl)
     return 0;
 }
 
+
+// ---------------------------------------------------------------- M2L: the log terms
+// Coefficient 0 of the M2L shift carries a_0 Log(c_t - c_s) (DESIGN R2: the
+// componentwise difference).  k_m2l (255 registers, 2 warps per sub-partition) leaves it out; here
+// one thread per target box walks the same weak (+ cross-level) list with the table-driven
+// log / Arg (<= 2 ulp) at full occupancy and adds the sum to the stored coefficient.  Same work
+// order as k_m2l; long-list targets are k_m2l_long's (which keeps the term).
+__global__ void __launch_bounds__(128) k_m2l_log(M2LArgs A, int p1, const fm::Tables* __restrict__ gtab)
+{
+    __shared__ fm::Tables T;
+    rr_load_tables(T, gtab);
+    __syncthreads();
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= A.pre[A.L + 1]) return;
+    int lev = 1;
+    while (lev < A.L && w >= A.pre[lev + 1]) ++lev;
+    const int64_t b = A.order[w];
+    const int64_t g = A.base[lev] + b;
+    const int64_t w0 = A.woff[lev][b], nw = A.woff[lev][b + 1] - w0;
+    const int64_t x0 = A.xoff[lev] ? A.xoff[lev][b] : 0;
+    const int64_t jb = nw + (A.xoff[lev] ? A.xoff[lev][b + 1] - x0 : 0);
+    if (jb > FMM2D_M2L_LONG || jb == 0) return;
+    const uint32_t* __restrict__ widx = A.widx[lev];
+    const uint32_t* __restrict__ xidx = A.xidx[lev];
+    const int64_t wbase = A.base[lev], xbase = lev > 0 ? A.base[lev - 1] : 0;
+    const double ctx = A.cx[g], cty = A.cy[g];
+    double sr = 0.0, si = 0.0;
+    for (int64_t j = 0; j < jb; ++j) {
+        const bool cross = j >= nw;
+        const int sl = cross ? lev - 1 : lev;
+        const uint32_t bs = cross ? xidx[x0 + (j - nw)] : widx[w0 + j];
+        const int64_t s = (cross ? xbase : wbase) + bs;
+        const double2* M = (bs >= A.slo[sl] && bs < A.shi[sl]) ? A.mpl[sl] + (int64_t)bs * p1
+                                                              : A.mhalo + (int64_t)A.hmap[s] * p1;
+        const double2 a0 = M[0];
+        const double tx = ctx - A.cx[s], ty = cty - A.cy[s];
+        const double r2 = fma(tx, tx, ty * ty);
+        const double lr = 0.5 * fm::log_pos(r2, T.lg), li = fm::arg_t(tx, ty, T.at);
+        sr += a0.x * lr - a0.y * li;
+        si += a0.x * li + a0.y * lr;
+    }
+    double2* out = A.lcl[lev] + b * p1;
+    const double2 o = out[0];
+    out[0] = make_double2(o.x + sr, o.y + si);
+}
+
 }  // namespace
+
+int m2l_log_terms(fmm2d_plan* P, const M2LArgs& A, int p1)
+{
+    const int64_t work = A.pre[A.L + 1];
+    if (work <= 0) return 0;
+    k_m2l_log<<<(unsigned)((work + 127) / 128), 128, 0, P->stream>>>(A, p1, static_cast<const fm::Tables*>(P->tables));
+    fmm2d::note_launch();
+    FMM2D_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
 
 #define FMM2D_P_CASES(F)                                                                      \
     case 1: return F<1>(P); case 2: return F<2>(P); case 3: return F<3>(P);                   \
