@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(128) k_m2m(int64_t b0, int64_t b1, const doubl
 // ---------------------------------------------------------------- M2L (A6/A7)
 // compile-time options of the M2L pair body (defaults: measured best at C5)
 #ifndef FMM2D_M2L_LOGSPLIT
-#define FMM2D_M2L_LOGSPLIT 1       // the a_0 Log term of coefficient 0 in its own kernel (rr.cu: k_m2l_log)
+#define FMM2D_M2L_LOGSPLIT 0       // 1: the a_0 Log term of coefficient 0 in its own kernel (rr.cu: k_m2l_log) -- measured: k_m2l without the term compiles to 242 registers, no spills, and runs 31 ms instead of 15.8
 #endif
 #ifndef FMM2D_M2L_RCP
 #define FMM2D_M2L_RCP 1            // 1 / r2 by MUFU + one cubic Newton step (C5 M2L 16.53 -> 15.84 ms)
