@@ -480,6 +480,18 @@ def main():
                             "fp64_pipe_pct": kn.get("fp64_pipe_pct"), "source": os.path.relpath(CENSUS, ROOT),
                             "note": "the kernel's own executed FP64 flops (table-driven log/Arg/rcp need fewer "
                                     "than libdevice's); the FP64-pipe utilisation is clock-independent"}
+    if roof["frac"] > 1.0:
+        roof["frac_note"] = ("above 1 under the survey's convention: the kernel's table-driven pair body does the "
+                             "libdevice-equivalent work of a pair in fewer executed FP64 operations; see 'executed' "
+                             "(the kernel's own flops against the same peak) and 'pipe_limits'")
+    try:       # what the FP64 pipe delivers per operand form (tools/fp64_mix.cu, measured on this pool's B200)
+        mix = json.load(open(os.path.join(ROOT, "profiles", "r02", "fp64_mix.json")))["fp64_rate_fraction_of_nominal"]
+        roof["pipe_limits"] = {"dfma_shared_operands": mix["dfma_shared_operands"],
+                               "dfma_three_distinct_registers": mix["dfma_distinct_operands"],
+                               "source": "profiles/r02/fp64_mix.json (fraction of the nominal FP64 rate; k_near's "
+                                         "operand mix sits between the two, DESIGN.md 6.4)"}
+    except (OSError, KeyError, ValueError):
+        pass
     weak_pairs = st.get("weak_pairs", 0.0)
     m2l_tf = weak_pairs * M2L_FLOPS_PER_PAIR / (phase["m2l_ms"] / 1e3) / 1e12 if phase["m2l_ms"] > 0 else 0.0
     # the M2L kernel against the same FP64 peak (algorithmic 1450 flop per pair, SURVEY 8(d);
