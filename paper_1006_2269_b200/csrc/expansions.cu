@@ -30,6 +30,14 @@ namespace fmm2d {
 #define FMM2D_M2L_KOFF 1
 #endif
 constexpr int M2L_CS = FMM2D_M2L_CS, M2L_KOFF = FMM2D_M2L_KOFF;
+#ifndef FMM2D_M2L_CT
+#define FMM2D_M2L_CT 0            // 1: the matrix transposed, C(l+k-1, k-1) at [(k-1) M2L_CS + l + M2L_KOFF]
+#endif
+// index of C(l+k-1, k-1)
+__host__ __device__ constexpr int m2l_ci(int l, int k)
+{
+    return FMM2D_M2L_CT ? (k - 1) * M2L_CS + l + M2L_KOFF : l * M2L_CS + k - 1 + M2L_KOFF;
+}
 static_assert(M2L_CS + M2L_KOFF >= FMM2D_PMAX + 1, "row stride of the M2L matrix");
 __constant__ double c_m2l[(FMM2D_PMAX + 1) * M2L_CS + M2L_KOFF];
 
@@ -58,7 +66,7 @@ int upload_binomials(int p)
     std::vector<double> m2l(S * M2L_CS + M2L_KOFF, 0.0), pas(S * S, 0.0);
     for (int l = 0; l <= FMM2D_PMAX; ++l)
         for (int k = 1; k <= FMM2D_PMAX; ++k)
-            m2l[l * M2L_CS + k - 1 + M2L_KOFF] = (double)binom_u64(l + k - 1, k - 1);
+            m2l[m2l_ci(l, k)] = (double)binom_u64(l + k - 1, k - 1);
     for (int a = 0; a <= FMM2D_PMAX; ++a)
         for (int b = 0; b <= a; ++b) pas[a * S + b] = (double)binom_u64(a, b);
     FMM2D_CUDA_TRY(cudaMemcpyToSymbol(c_m2l, m2l.data(), sizeof(double) * m2l.size()));
@@ -272,7 +280,7 @@ __device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, const doub
         for (int k = 1; k <= P; ++k) {
 #pragma unroll
             for (int l = lb; l < lb + FMM2D_M2L_LB && l < L1; ++l) {
-                const double c = c_m2l[l * M2L_CS + k - 1 + M2L_KOFF];
+                const double c = c_m2l[m2l_ci(l, k)];
                 beta[l - L0].x = fma(c, al[k].x, beta[l - L0].x);
                 beta[l - L0].y = fma(c, al[k].y, beta[l - L0].y);
             }
@@ -305,7 +313,7 @@ __device__ __forceinline__ void m2l_pair(const M2LArgs& A, int64_t s, const doub
         double2 bl = make_double2(0.0, 0.0);
 #pragma unroll
         for (int k = 1; k <= P; ++k) {
-            const double c = c_m2l[l * M2L_CS + k - 1 + M2L_KOFF];
+            const double c = c_m2l[m2l_ci(l, k)];
             bl.x = fma(c, al[k].x, bl.x);
             bl.y = fma(c, al[k].y, bl.y);
         }

@@ -164,6 +164,24 @@ def test_eval_matches_oracle(orc, name, cfg, n, theta, p):
     assert p1["point"] <= TOL and p2["point"] <= TOL, (p1, p2)
 
 
+@pytest.mark.parametrize("threads", [64, 96, 128])
+@pytest.mark.parametrize("cfg,n", [("C2", None), ("C3", 60_000)])
+def test_near_block_sizes(orc, monkeypatch, threads, cfg, n):
+    """k_near picks its block size per plan (64 / 96 / 128 threads: the fewest idle lanes for the
+    plan's target tuples); every choice gives the oracle's result within the parity bar
+    (FMM2D_NEAR_THREADS forces one; the group partial sums are added in a different order)."""
+    monkeypatch.setenv("FMM2D_NEAR_THREADS", str(threads))
+    z, m = W.make_config(cfg, n=n)
+    L = orc.nlevels(len(z), 35)
+    gp = _gpu_plan(z, 0.5, 17, L)
+    phi_o, dphi_o = orc.plan(z, 0.5, L).eval(m, 17)
+    phi_g, dphi_g = _gpu_eval(gp, m)
+    e1, e2 = _nerr(phi_g, phi_o), _nerr(dphi_g, dphi_o)
+    assert e1 <= TOL and e2 <= TOL, (threads, e1, e2)
+    p1, p2 = _errors(phi_g, phi_o), _errors(dphi_g, dphi_o)
+    assert p1["point"] <= TOL and p2["point"] <= TOL, (threads, p1, p2)
+
+
 @pytest.mark.parametrize("n,theta,L", [(2000, 0.5, 2), (40_000, 0.3, 4), (40_000, 0.5, 4)])
 def test_eval_level1_weak_pairs(orc, n, theta, L):
     """Level-1 M2L carries the whole inter-cluster field (corners input, DESIGN R15): the GPU
