@@ -414,12 +414,13 @@ __device__ __forceinline__ void m2l_target_warp(const M2LArgs& A, int64_t g, int
 }
 
 #ifndef FMM2D_M2L_MINB
-#define FMM2D_M2L_MINB 2
+#define FMM2D_M2L_MINB 1
 #endif
 #ifndef FMM2D_M2L_T
-#define FMM2D_M2L_T 128
+#define FMM2D_M2L_T 256              // one block of 8 warps per SM (255 registers): C5 M2L 15.84 -> 15.25 ms (128 x 2 blocks: 15.84, 64 x 4: 15.74)
 #endif
 constexpr int M2L_T = FMM2D_M2L_T;
+constexpr int M2L_LONG_T = 128;     // k_m2l_long (warp per long-list target): 2 blocks of 128 (C4: 6.7 ms vs 7.4 at 256)
 
 // threads: NS consecutive warps share 32 target boxes; warp-uniform part index.
 // (Tried and measured slower at p = 17 on B200: accumulators in shared memory, and a
@@ -493,7 +494,7 @@ __global__ void __launch_bounds__(32, 1) k_m2l_gs(M2LArgs A, int64_t nwarps)
 
 // one warp (per coefficient part) per long-list target; long[] holds global box ids
 template <int P, int NS>
-__global__ void __launch_bounds__(M2L_T, FMM2D_M2L_MINB) k_m2l_long(M2LArgs A, const uint32_t* __restrict__ longs,
+__global__ void __launch_bounds__(M2L_LONG_T, 2) k_m2l_long(M2LArgs A, const uint32_t* __restrict__ longs,
                                                                    int64_t nlong)
 {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -614,7 +615,7 @@ constexpr int m2l_split() { return P <= FMM2D_M2L_SPLIT_P ? 1 : (P <= 26 ? 2 : 3
 template <int P, int NS>
 int m2l_long_p(fmm2d_plan* Pl, const M2LArgs& A)
 {
-    k_m2l_long<P, NS><<<grid_for(Pl->m2l_nlong * NS * 32, M2L_T), M2L_T, 0, Pl->stream>>>(A, Pl->m2l_long,
+    k_m2l_long<P, NS><<<grid_for(Pl->m2l_nlong * NS * 32, M2L_LONG_T), M2L_LONG_T, 0, Pl->stream>>>(A, Pl->m2l_long,
                                                                                         Pl->m2l_nlong);
     fmm2d::note_launch();
     FMM2D_CUDA_TRY(cudaGetLastError());
